@@ -1,0 +1,977 @@
+// C ABI and device context of the B200 PPPM mesh core (see include/pppm_b200.h).
+//
+// The context owns every device buffer of one mesh geometry (the B200 analogue
+// of driver.SolverContext, driver.py:213-228): the influence function in the
+// R2C half-spectrum layout, ik vectors, stencil table, mesh / spectrum /
+// field buffers, cuFFT plans and the atom binning scratch.  Host-pointer calls
+// copy in, run, and copy out on the context stream; device-resident calls
+// leave everything in HBM.
+#include <cufft.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <utility>
+
+#include "../../include/pppm_b200.h"
+#include "pppm_kernels.cuh"
+
+using namespace pppm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+const char* fft_name(cufftResult r) {
+  switch (r) {
+    case CUFFT_SUCCESS: return "CUFFT_SUCCESS";
+    case CUFFT_INVALID_PLAN: return "CUFFT_INVALID_PLAN";
+    case CUFFT_ALLOC_FAILED: return "CUFFT_ALLOC_FAILED";
+    case CUFFT_INVALID_VALUE: return "CUFFT_INVALID_VALUE";
+    case CUFFT_INTERNAL_ERROR: return "CUFFT_INTERNAL_ERROR";
+    case CUFFT_EXEC_FAILED: return "CUFFT_EXEC_FAILED";
+    case CUFFT_SETUP_FAILED: return "CUFFT_SETUP_FAILED";
+    case CUFFT_INVALID_SIZE: return "CUFFT_INVALID_SIZE";
+    default: return "CUFFT_ERROR";
+  }
+}
+
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(PPPM_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define FFT(x)                                                                             \
+  do {                                                                                     \
+    cufftResult r_ = (x);                                                                  \
+    if (r_ != CUFFT_SUCCESS) return fail(PPPM_ERR_CUFFT, std::string(#x) + ": " + fft_name(r_)); \
+  } while (0)
+
+#define TRY(x)                     \
+  do {                             \
+    int s_ = (x);                  \
+    if (s_ != PPPM_OK) return s_;  \
+  } while (0)
+
+#define LAUNCH_CHECK() CU(cudaPeekAtLastError())
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t b) {
+    if (b <= bytes) return PPPM_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (b == 0) return PPPM_OK;
+    CU(cudaMalloc(&p, b));
+    bytes = b;
+    return PPPM_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <typename F> int with_order(int s, F&& f) {
+  switch (s) {
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    default: return fail(PPPM_ERR_CONFIG, "stencil order must be one of (3, 4, 5, 6, 7)");
+  }
+}
+
+template <typename F> int with_bool(bool b, F&& f) {
+  return b ? f(std::true_type{}) : f(std::false_type{});
+}
+
+int grid_for(int64_t n, int threads = kThreads) {
+  int64_t g = (n + threads - 1) / threads;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+  return (int)g;
+}
+
+}  // namespace
+
+enum SubPhase { SP_BIN = 0, SP_SPREAD, SP_FFT_FWD, SP_GREEN, SP_FFT_BWD, SP_GATHER, SP_COUNT };
+
+struct pppm_ctx {
+  int device = 0;
+  Geom g{};
+  Bricks bk{};
+  int order = 5, mode = PPPM_MODE_IK, prec = PPPM_PREC_FP64;
+  double alpha = 0.0, cscale = 1.0;
+  int n_points = 0;  // 0 => exact rows
+  int green_kind = -1;  // -1: none or uploaded from a foreign plan
+  double green_floor = 1e-10;
+  int64_t M = 0, half = 0;
+  int nxh = 0;
+  cudaStream_t stream = nullptr;
+  cufftHandle fwd = 0, bwd = 0;
+  bool plans = false;
+  bool have_green = false, have_rho = false, have_fields = false, binned = false;
+
+  DevBuf rho, rho_fix, rho_hat, ework, fields, green, ikc, ik64, tab;
+  DevBuf pos_stage, q_stage, out_stage, node_stage;
+  DevBuf counts, start, abin, aslot, rec, perm;
+  DevBuf partial, scal, err, flush;
+  DevBuf res_pos, res_q, res_force;
+  int64_t n_res = 0;
+  int res_dtype = PPPM_F64;
+  int* h_err = nullptr;
+  double* h_scal = nullptr;
+  cudaEvent_t ev[SP_COUNT + 1] = {};
+  int launches = 0;
+
+  bool fp64() const { return prec == PPPM_PREC_FP64; }
+  size_t real_size() const { return fp64() ? sizeof(double) : sizeof(float); }
+  int nfields() const { return mode == PPPM_MODE_IK ? 3 : 1; }
+};
+
+// ---------------------------------------------------------------------------
+// internal helpers
+
+static int activate(pppm_ctx* c) {
+  CU(cudaSetDevice(c->device));
+  return PPPM_OK;
+}
+
+static int check_err_flag(pppm_ctx* c) {
+  CU(cudaMemcpyAsync(c->h_err, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (*c->h_err) {
+    *c->h_err = 0;
+    CU(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
+    return fail(PPPM_ERR_RUNTIME, "positions must be wrapped into the box before mapping");
+  }
+  return PPPM_OK;
+}
+
+static int ensure_plans(pppm_ctx* c) {
+  if (c->plans) return PPPM_OK;
+  int n[3] = {c->g.nz, c->g.ny, c->g.nx};
+  const bool d = c->fp64();
+  FFT(cufftPlanMany(&c->fwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, d ? CUFFT_D2Z : CUFFT_R2C, 1));
+  FFT(cufftPlanMany(&c->bwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, d ? CUFFT_Z2D : CUFFT_C2R,
+                    c->nfields()));
+  FFT(cufftSetStream(c->fwd, c->stream));
+  FFT(cufftSetStream(c->bwd, c->stream));
+  c->plans = true;
+  return PPPM_OK;
+}
+
+// stage host or device atoms into device pointers of their own dtype
+static int stage_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem,
+                       const void** dpos, const void** dq) {
+  if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
+  if (dtype != PPPM_F64 && dtype != PPPM_F32) return fail(PPPM_ERR_VALUE, "unknown dtype");
+  const size_t es = dtype == PPPM_F64 ? 8 : 4;
+  if (mem == PPPM_DEVICE) {
+    *dpos = pos;
+    *dq = q;
+    return PPPM_OK;
+  }
+  TRY(c->pos_stage.ensure(3 * n * es));
+  CU(cudaMemcpyAsync(c->pos_stage.p, pos, 3 * n * es, cudaMemcpyHostToDevice, c->stream));
+  *dpos = c->pos_stage.p;
+  if (q) {
+    TRY(c->q_stage.ensure(n * es));
+    CU(cudaMemcpyAsync(c->q_stage.p, q, n * es, cudaMemcpyHostToDevice, c->stream));
+    *dq = c->q_stage.p;
+  } else {
+    *dq = nullptr;
+  }
+  return PPPM_OK;
+}
+
+static int ensure_bins(pppm_ctx* c, int64_t n) {
+  const int nb = c->bk.count();
+  TRY(c->counts.ensure(sizeof(int) * nb));
+  TRY(c->start.ensure(sizeof(int) * (nb + 1)));
+  TRY(c->abin.ensure(sizeof(int) * n));
+  TRY(c->aslot.ensure(sizeof(int) * n));
+  TRY(c->rec.ensure(sizeof(float4) * n));
+  TRY(c->perm.ensure(sizeof(int) * n));
+  return PPPM_OK;
+}
+
+static void rec_event(pppm_ctx* c, int idx, bool timing) {
+  if (timing) cudaEventRecord(c->ev[idx], c->stream);
+}
+
+// make_rho on device atoms -----------------------------------------------------
+static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
+  TRY(ensure_bins(c, n));
+  const int nb = c->bk.count();
+  CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int) * nb, c->stream));
+  const int grid = grid_for(n);
+  int st = with_order(c->order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    if (dtype == PPPM_F64)
+      k_bin_count<S, double, true><<<grid, kThreads, 0, c->stream>>>(
+          (const double*)pos, n, c->g, c->bk, c->counts.as<int>(), c->abin.as<int>(), c->aslot.as<int>(),
+          c->err.as<int>());
+    else
+      k_bin_count<S, float, true><<<grid, kThreads, 0, c->stream>>>(
+          (const float*)pos, n, c->g, c->bk, c->counts.as<int>(), c->abin.as<int>(), c->aslot.as<int>(),
+          c->err.as<int>());
+    return PPPM_OK;
+  });
+  TRY(st);
+  LAUNCH_CHECK();
+  k_scan_bricks<<<1, 1024, 0, c->stream>>>(c->counts.as<int>(), nb, c->start.as<int>());
+  LAUNCH_CHECK();
+  if (dtype == PPPM_F64)
+    k_bin_scatter<double><<<grid, kThreads, 0, c->stream>>>(
+        (const double*)pos, (const double*)q, n, c->abin.as<int>(), c->aslot.as<int>(), c->start.as<int>(),
+        c->rec.as<float4>(), c->perm.as<int>());
+  else
+    k_bin_scatter<float><<<grid, kThreads, 0, c->stream>>>(
+        (const float*)pos, (const float*)q, n, c->abin.as<int>(), c->aslot.as<int>(), c->start.as<int>(),
+        c->rec.as<float4>(), c->perm.as<int>());
+  LAUNCH_CHECK();
+  c->launches += 3;
+  c->binned = true;
+  return PPPM_OK;
+}
+
+static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
+  const int grid = grid_for(n);
+  if (c->fp64()) {
+    double* sc = c->scal.as<double>();
+    unsigned long long* qmax = reinterpret_cast<unsigned long long*>(sc + 4);
+    CU(cudaMemsetAsync(c->rho_fix.p, 0, sizeof(unsigned long long) * c->M, c->stream));
+    CU(cudaMemsetAsync(qmax, 0, sizeof(unsigned long long), c->stream));
+    k_absmax_charge<<<grid, kThreads, 0, c->stream>>>(q, dtype == PPPM_F64 ? 0 : 1, n, qmax);
+    LAUNCH_CHECK();
+    k_fix_scale<<<1, 1, 0, c->stream>>>(qmax, n, sc + 1, sc + 2);
+    LAUNCH_CHECK();
+    int st = with_order(c->order, [&](auto S_) -> int {
+      constexpr int S = decltype(S_)::value;
+      return with_bool(c->n_points > 0, [&](auto T_) -> int {
+        constexpr bool TAB = decltype(T_)::value;
+        if (dtype == PPPM_F64)
+          k_spread_fix64<S, TAB, double, false><<<grid, kThreads, 0, c->stream>>>(
+              (const double*)pos, (const double*)q, n, c->g, c->tab.as<double>(), c->n_points, sc + 1,
+              c->rho_fix.as<unsigned long long>(), c->err.as<int>());
+        else
+          k_spread_fix64<S, TAB, float, false><<<grid, kThreads, 0, c->stream>>>(
+              (const float*)pos, (const float*)q, n, c->g, c->tab.as<double>(), c->n_points, sc + 1,
+              c->rho_fix.as<unsigned long long>(), c->err.as<int>());
+        return PPPM_OK;
+      });
+    });
+    TRY(st);
+    LAUNCH_CHECK();
+    const double vcell = c->g.hx * c->g.hy * c->g.hz;
+    k_fix64_to_real<double><<<grid_for(c->M), kThreads, 0, c->stream>>>(
+        c->rho_fix.as<unsigned long long>(), c->M, sc + 2, vcell, c->rho.as<double>());
+    LAUNCH_CHECK();
+    c->launches += 4;
+  } else {
+    CU(cudaMemsetAsync(c->rho.p, 0, sizeof(float) * c->M, c->stream));
+    const float inv_vcell = (float)(1.0 / (c->g.hx * c->g.hy * c->g.hz));
+    int st = with_order(c->order, [&](auto S_) -> int {
+      constexpr int S = decltype(S_)::value;
+      return with_bool(c->n_points > 0, [&](auto T_) -> int {
+        constexpr bool TAB = decltype(T_)::value;
+        k_spread_brick<S, TAB><<<c->bk.count(), kThreads, 0, c->stream>>>(
+            c->rec.as<float4>(), c->start.as<int>(), c->g, c->bk, c->tab.as<float>(), c->n_points,
+            inv_vcell, c->rho.as<float>());
+        return PPPM_OK;
+      });
+    });
+    TRY(st);
+    LAUNCH_CHECK();
+    c->launches += 1;
+  }
+  c->have_rho = true;
+  return PPPM_OK;
+}
+
+// Poisson ----------------------------------------------------------------------
+static int run_fft_fwd(pppm_ctx* c) {
+  TRY(ensure_plans(c));
+  if (c->fp64())
+    FFT(cufftExecD2Z(c->fwd, c->rho.as<double>(), c->rho_hat.as<cufftDoubleComplex>()));
+  else
+    FFT(cufftExecR2C(c->fwd, c->rho.as<float>(), c->rho_hat.as<cufftComplex>()));
+  c->launches += 1;
+  return PPPM_OK;
+}
+
+static int run_green(pppm_ctx* c, bool fields) {
+  if (!c->have_green) return fail(PPPM_ERR_STATE, "influence function not built");
+  double* sc = c->scal.as<double>();
+  const double vol = c->g.lx * c->g.ly * c->g.lz;
+  const double vcell = vol / (double)c->M;
+  const double pref = c->cscale * vcell * vcell / (2.0 * vol);
+  auto go = [&](auto T_, auto MODE_, auto FIELDS_) {
+    using T = decltype(T_);
+    constexpr int MODE = decltype(MODE_)::value;
+    constexpr bool FL = decltype(FIELDS_)::value;
+    using C = typename Cplx<T>::C;
+    const T* ik = c->ikc.as<T>();
+    k_green<T, MODE, FL><<<kGreenBlocks, kThreads, 0, c->stream>>>(
+        c->rho_hat.as<C>(), c->green.as<T>(), c->g.nx, c->g.ny, c->g.nz, ik, ik + c->g.nx,
+        ik + c->g.nx + c->g.ny, (T)(1.0 / (double)c->M), c->ework.as<C>(), c->partial.as<double>());
+  };
+  auto by_mode = [&](auto T_) {
+    if (c->mode == PPPM_MODE_IK) {
+      if (fields) go(T_, std::integral_constant<int, 0>{}, std::true_type{});
+      else go(T_, std::integral_constant<int, 0>{}, std::false_type{});
+    } else {
+      if (fields) go(T_, std::integral_constant<int, 1>{}, std::true_type{});
+      else go(T_, std::integral_constant<int, 1>{}, std::false_type{});
+    }
+  };
+  if (c->fp64()) by_mode(double{});
+  else by_mode(float{});
+  LAUNCH_CHECK();
+  k_energy_final<<<1, 32, 0, c->stream>>>(c->partial.as<double>(), kGreenBlocks, pref, sc);
+  LAUNCH_CHECK();
+  c->launches += 2;
+  return PPPM_OK;
+}
+
+static int run_fft_bwd(pppm_ctx* c) {
+  TRY(ensure_plans(c));
+  if (c->fp64())
+    FFT(cufftExecZ2D(c->bwd, c->ework.as<cufftDoubleComplex>(), c->fields.as<double>()));
+  else
+    FFT(cufftExecC2R(c->bwd, c->ework.as<cufftComplex>(), c->fields.as<float>()));
+  c->launches += 1;
+  c->have_fields = true;
+  return PPPM_OK;
+}
+
+// fieldforce ---------------------------------------------------------------------
+// out: device buffer of (n, 3) fp64 (out_f64) or fp32
+static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, void* out,
+                      bool out_f64) {
+  if (!c->have_fields) return fail(PPPM_ERR_STATE, "no field grids on the device");
+  if (c->fp64()) {
+    const double* f = c->fields.as<double>();
+    const int grid = grid_for(n);
+    int st = with_order(c->order, [&](auto S_) -> int {
+      constexpr int S = decltype(S_)::value;
+      return with_bool(c->n_points > 0, [&](auto T_) -> int {
+        constexpr bool TAB = decltype(T_)::value;
+        auto go = [&](auto MODE_) {
+          constexpr int MODE = decltype(MODE_)::value;
+          const double* ta = c->tab.as<double>();
+          const double* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
+          if (dtype == PPPM_F64)
+            k_gather_direct<S, TAB, MODE, double, false><<<grid, kThreads, 0, c->stream>>>(
+                (const double*)pos, (const double*)q, n, c->g, ta, td, c->n_points, f, f + c->M,
+                f + 2 * c->M, c->cscale, (double*)out, c->err.as<int>());
+          else
+            k_gather_direct<S, TAB, MODE, float, false><<<grid, kThreads, 0, c->stream>>>(
+                (const float*)pos, (const float*)q, n, c->g, ta, td, c->n_points, f, f + c->M,
+                f + 2 * c->M, c->cscale, (double*)out, c->err.as<int>());
+        };
+        if (c->mode == PPPM_MODE_IK) go(std::integral_constant<int, 0>{});
+        else go(std::integral_constant<int, 1>{});
+        return PPPM_OK;
+      });
+    });
+    TRY(st);
+  } else {
+    if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
+    int st = with_order(c->order, [&](auto S_) -> int {
+      constexpr int S = decltype(S_)::value;
+      return with_bool(c->n_points > 0, [&](auto T_) -> int {
+        constexpr bool TAB = decltype(T_)::value;
+        auto go = [&](auto MODE_, auto OUT_) {
+          constexpr int MODE = decltype(MODE_)::value;
+          using TO = decltype(OUT_);
+          const float* ta = c->tab.as<float>();
+          const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
+          k_gather_brick<S, TAB, MODE, TO><<<c->bk.count(), kThreads, 0, c->stream>>>(
+              c->rec.as<float4>(), c->perm.as<int>(), c->start.as<int>(), c->g, c->bk, ta, td,
+              c->n_points, c->fields.as<float>(), c->M, (float)c->cscale, (TO*)out);
+        };
+        if (c->mode == PPPM_MODE_IK) {
+          if (out_f64) go(std::integral_constant<int, 0>{}, double{});
+          else go(std::integral_constant<int, 0>{}, float{});
+        } else {
+          if (out_f64) go(std::integral_constant<int, 1>{}, double{});
+          else go(std::integral_constant<int, 1>{}, float{});
+        }
+        return PPPM_OK;
+      });
+    });
+    TRY(st);
+  }
+  LAUNCH_CHECK();
+  c->launches += 1;
+  return PPPM_OK;
+}
+
+static int mesh_to_host(pppm_ctx* c, const void* dev, double* host, int64_t count) {
+  if (c->fp64()) {
+    CU(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    TRY(c->out_stage.ensure(sizeof(double) * count));
+    k_convert<float, double><<<grid_for(count), kThreads, 0, c->stream>>>((const float*)dev,
+                                                                          c->out_stage.as<double>(), count);
+    LAUNCH_CHECK();
+    CU(cudaMemcpyAsync(host, c->out_stage.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return PPPM_OK;
+}
+
+static int mesh_from_host(pppm_ctx* c, void* dev, const double* host, int64_t count) {
+  if (c->fp64()) {
+    CU(cudaMemcpyAsync(dev, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    TRY(c->out_stage.ensure(sizeof(double) * count));
+    CU(cudaMemcpyAsync(c->out_stage.p, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+    k_convert<double, float><<<grid_for(count), kThreads, 0, c->stream>>>(c->out_stage.as<double>(),
+                                                                          (float*)dev, count);
+    LAUNCH_CHECK();
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return PPPM_OK;
+}
+
+static int do_make_rho(pppm_ctx* c, const void* dpos, const void* dq, int64_t n, int dtype) {
+  c->binned = false;
+  if (!c->fp64()) TRY(run_bin(c, dpos, dq, n, dtype));
+  return run_spread(c, dpos, dq, n, dtype);
+}
+
+static int do_fieldforce(pppm_ctx* c, const void* dpos, const void* dq, int64_t n, int dtype,
+                         bool rebin, void* out, bool out_f64) {
+  if (!c->fp64() && rebin) TRY(run_bin(c, dpos, dq, n, dtype));
+  return run_gather(c, dpos, dq, n, dtype, out, out_f64);
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int pppm_abi_version(void) { return PPPM_ABI_VERSION; }
+
+const char* pppm_last_error(void) { return g_err.c_str(); }
+
+int pppm_device_count(int* count) {
+  CU(cudaGetDeviceCount(count));
+  return PPPM_OK;
+}
+
+void* pppm_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void pppm_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int pppm_weight_rows(int device, int order, const double* t, int64_t n, double* assign, double* deriv) {
+  if (n < 0) return fail(PPPM_ERR_VALUE, "negative count");
+  if (n == 0) return PPPM_OK;
+  CU(cudaSetDevice(device));
+  double *dt = nullptr, *da = nullptr;
+  CU(cudaMalloc(&dt, sizeof(double) * n));
+  CU(cudaMalloc(&da, sizeof(double) * n * kRowPad * 2));
+  CU(cudaMemcpy(dt, t, sizeof(double) * n, cudaMemcpyHostToDevice));
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    k_weight_rows<S><<<(int)((n + 255) / 256), 256>>>(dt, n, da, da + n * kRowPad);
+    return PPPM_OK;
+  });
+  if (st == PPPM_OK) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(assign, da, sizeof(double) * n * kRowPad, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(deriv, da + n * kRowPad, sizeof(double) * n * kRowPad, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(PPPM_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(dt);
+  cudaFree(da);
+  return st;
+}
+
+int pppm_table_rows(int device, int order, int n_points, double* assign, double* deriv) {
+  if (n_points < 2) return fail(PPPM_ERR_VALUE, "n_points must be >= 2");
+  CU(cudaSetDevice(device));
+  double* da = nullptr;
+  CU(cudaMalloc(&da, sizeof(double) * n_points * kRowPad * 2));
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    k_table_rows<S><<<(n_points + 255) / 256, 256>>>(n_points, da, da + (int64_t)n_points * kRowPad);
+    return PPPM_OK;
+  });
+  if (st == PPPM_OK) {
+    cudaError_t e = cudaGetLastError();
+    const size_t b = sizeof(double) * n_points * kRowPad;
+    if (e == cudaSuccess) e = cudaMemcpy(assign, da, b, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(deriv, da + (int64_t)n_points * kRowPad, b, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(PPPM_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(da);
+  return st;
+}
+
+int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
+                    int order, int mode, int precision, double alpha, double coulomb_constant,
+                    double dielectric) {
+  if (!out) return fail(PPPM_ERR_VALUE, "null output pointer");
+  *out = nullptr;
+  if (order < 3 || order > 7) return fail(PPPM_ERR_CONFIG, "stencil order must be one of (3, 4, 5, 6, 7)");
+  if (nx < order || ny < order || nz < order)
+    return fail(PPPM_ERR_CONFIG, "grid dimensions must be >= the stencil order");
+  if (!(lx > 0 && ly > 0 && lz > 0)) return fail(PPPM_ERR_VALUE, "box edge lengths must be strictly positive");
+  if (mode != PPPM_MODE_IK && mode != PPPM_MODE_AD) return fail(PPPM_ERR_CONFIG, "mode must be IK or AD");
+  if (precision != PPPM_PREC_FP64 && precision != PPPM_PREC_MIXED)
+    return fail(PPPM_ERR_CONFIG, "precision must be fp64 or mixed");
+  if (!(alpha > 0.0)) return fail(PPPM_ERR_CONFIG, "alpha must be positive");
+  if (!(dielectric > 0.0)) return fail(PPPM_ERR_CONFIG, "dielectric must be positive");
+  CU(cudaSetDevice(device));
+  pppm_ctx* c = new pppm_ctx();
+  c->device = device;
+  c->g.nx = nx; c->g.ny = ny; c->g.nz = nz;
+  c->g.lx = lx; c->g.ly = ly; c->g.lz = lz;
+  c->g.hx = lx / nx; c->g.hy = ly / ny; c->g.hz = lz / nz;   // gridmap.py:83
+  c->bk.nbx = (nx + kBrick - 1) / kBrick;
+  c->bk.nby = (ny + kBrick - 1) / kBrick;
+  c->bk.nbz = (nz + kBrick - 1) / kBrick;
+  c->order = order; c->mode = mode; c->prec = precision;
+  c->alpha = alpha;
+  c->cscale = coulomb_constant / dielectric;  // model.py:244-247
+  c->M = (int64_t)nx * ny * nz;
+  c->nxh = nx / 2 + 1;
+  c->half = (int64_t)c->nxh * ny * nz;
+  auto cleanup = [&](int st) {
+    pppm_ctx_destroy(c);
+    return st;
+  };
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(PPPM_ERR_CUDA, "stream creation failed"));
+  const size_t rs = c->real_size();
+  const size_t cs = 2 * rs;
+  int st = PPPM_OK;
+  if (st == PPPM_OK) st = c->rho.ensure(rs * c->M);
+  if (st == PPPM_OK && c->fp64()) st = c->rho_fix.ensure(8 * c->M);
+  if (st == PPPM_OK) st = c->rho_hat.ensure(cs * c->half);
+  if (st == PPPM_OK) st = c->ework.ensure(cs * c->half * c->nfields());
+  if (st == PPPM_OK) st = c->fields.ensure(rs * c->M * c->nfields());
+  if (st == PPPM_OK) st = c->green.ensure(rs * c->half);
+  if (st == PPPM_OK) st = c->ikc.ensure(rs * (nx + ny + nz));
+  if (st == PPPM_OK) st = c->ik64.ensure(8 * (nx + ny + nz));
+  if (st == PPPM_OK) st = c->partial.ensure(8 * kGreenBlocks);
+  if (st == PPPM_OK) st = c->scal.ensure(64);
+  if (st == PPPM_OK) st = c->err.ensure(sizeof(int));
+  if (st != PPPM_OK) return cleanup(st);
+  if (cudaHostAlloc(&c->h_err, sizeof(int), 0) != cudaSuccess ||
+      cudaHostAlloc(&c->h_scal, 64, 0) != cudaSuccess)
+    return cleanup(fail(PPPM_ERR_CUDA, "pinned allocation failed"));
+  *c->h_err = 0;
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(PPPM_ERR_CUDA, "event creation failed"));
+  if (cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->scal.p, 0, 64, c->stream) != cudaSuccess)
+    return cleanup(fail(PPPM_ERR_CUDA, "memset failed"));
+  // ik vectors in fp64, then the compute-type copy
+  double* ik = c->ik64.as<double>();
+  k_ik_vectors<<<(std::max(nx, std::max(ny, nz)) + 255) / 256, 256, 0, c->stream>>>(
+      nx, ny, nz, lx, ly, lz, ik, ik + nx, ik + nx + ny);
+  if (c->fp64()) {
+    cudaMemcpyAsync(c->ikc.p, ik, 8 * (nx + ny + nz), cudaMemcpyDeviceToDevice, c->stream);
+  } else {
+    k_convert<double, float><<<1, 256, 0, c->stream>>>(ik, c->ikc.as<float>(), nx + ny + nz);
+  }
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return cleanup(fail(PPPM_ERR_CUDA, "context setup kernels failed"));
+  *out = c;
+  return PPPM_OK;
+}
+
+int pppm_ctx_destroy(pppm_ctx* c) {
+  if (!c) return PPPM_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->plans) {
+    cufftDestroy(c->fwd);
+    cufftDestroy(c->bwd);
+  }
+  DevBuf* bufs[] = {&c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
+                    &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
+                    &c->counts, &c->start, &c->abin, &c->aslot, &c->rec, &c->perm, &c->partial,
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force};
+  for (DevBuf* b : bufs) b->release();
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->h_scal) cudaFreeHost(c->h_scal);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return PPPM_OK;
+}
+
+int pppm_ctx_set_table(pppm_ctx* c, int n_points, const double* assign, const double* deriv) {
+  TRY(activate(c));
+  if (n_points == 0) {
+    c->n_points = 0;
+    return PPPM_OK;
+  }
+  if (n_points < 2) return fail(PPPM_ERR_CONFIG, "table_points must be >= 2 when the table is enabled");
+  const int64_t cnt = (int64_t)n_points * kRowPad;
+  TRY(c->tab.ensure(c->real_size() * cnt * 2));
+  if (c->fp64()) {
+    CU(cudaMemcpyAsync(c->tab.p, assign, 8 * cnt, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->tab.as<double>() + cnt, deriv, 8 * cnt, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    TRY(c->out_stage.ensure(8 * cnt * 2));
+    CU(cudaMemcpyAsync(c->out_stage.p, assign, 8 * cnt, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->out_stage.as<double>() + cnt, deriv, 8 * cnt, cudaMemcpyHostToDevice, c->stream));
+    k_convert<double, float><<<grid_for(2 * cnt), kThreads, 0, c->stream>>>(c->out_stage.as<double>(),
+                                                                            c->tab.as<float>(), 2 * cnt);
+    LAUNCH_CHECK();
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  c->n_points = n_points;
+  return PPPM_OK;
+}
+
+int pppm_ctx_build_table(pppm_ctx* c, int n_points) {
+  TRY(activate(c));
+  if (n_points == 0) {
+    c->n_points = 0;
+    return PPPM_OK;
+  }
+  if (n_points < 2) return fail(PPPM_ERR_CONFIG, "table_points must be >= 2 when the table is enabled");
+  const int64_t cnt = (int64_t)n_points * kRowPad;
+  TRY(c->out_stage.ensure(8 * cnt * 2));
+  double* rows = c->out_stage.as<double>();
+  int st = with_order(c->order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    k_table_rows<S><<<(n_points + 255) / 256, 256, 0, c->stream>>>(n_points, rows, rows + cnt);
+    return PPPM_OK;
+  });
+  TRY(st);
+  LAUNCH_CHECK();
+  TRY(c->tab.ensure(c->real_size() * cnt * 2));
+  if (c->fp64())
+    CU(cudaMemcpyAsync(c->tab.p, rows, 16 * cnt, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    k_convert<double, float><<<grid_for(2 * cnt), kThreads, 0, c->stream>>>(rows, c->tab.as<float>(), 2 * cnt);
+  LAUNCH_CHECK();
+  CU(cudaStreamSynchronize(c->stream));
+  c->n_points = n_points;
+  return PPPM_OK;
+}
+
+int pppm_ctx_build_influence(pppm_ctx* c, int kind, double deconv_floor) {
+  TRY(activate(c));
+  if (kind != PPPM_INFLUENCE_PME && kind != PPPM_INFLUENCE_OPTIMAL)
+    return fail(PPPM_ERR_CONFIG, "unknown influence variant");
+  GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, deconv_floor,
+              kind == PPPM_INFLUENCE_OPTIMAL};
+  const int grid = grid_for(c->half);
+  if (c->fp64())
+    k_influence<double><<<grid, kThreads, 0, c->stream>>>(s, c->green.as<double>(), nullptr);
+  else
+    k_influence<float><<<grid, kThreads, 0, c->stream>>>(s, c->green.as<float>(), nullptr);
+  LAUNCH_CHECK();
+  CU(cudaStreamSynchronize(c->stream));
+  c->have_green = true;
+  c->green_kind = kind;
+  c->green_floor = deconv_floor;
+  return PPPM_OK;
+}
+
+int pppm_ctx_set_influence(pppm_ctx* c, const double* g_full) {
+  TRY(activate(c));
+  // upload the full grid, keep the R2C half (valid: G is even in kx, kspace.py:139-196)
+  TRY(c->out_stage.ensure(8 * c->M));
+  CU(cudaMemcpy2DAsync(c->out_stage.p, 8 * c->nxh, g_full, 8 * c->g.nx, 8 * c->nxh,
+                       (size_t)c->g.ny * c->g.nz, cudaMemcpyHostToDevice, c->stream));
+  if (c->fp64())
+    CU(cudaMemcpyAsync(c->green.p, c->out_stage.p, 8 * c->half, cudaMemcpyDeviceToDevice, c->stream));
+  else {
+    k_convert<double, float><<<grid_for(c->half), kThreads, 0, c->stream>>>(c->out_stage.as<double>(),
+                                                                            c->green.as<float>(), c->half);
+    LAUNCH_CHECK();
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  c->have_green = true;
+  c->green_kind = -1;
+  return PPPM_OK;
+}
+
+int pppm_ctx_get_influence(pppm_ctx* c, double* g_full) {
+  TRY(activate(c));
+  if (c->green_kind < 0) return fail(PPPM_ERR_STATE, "influence function was not built on the device");
+  // the full (nz, ny, nx) grid, evaluated on the device in fp64
+  GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, c->green_floor,
+              c->green_kind == PPPM_INFLUENCE_OPTIMAL};
+  TRY(c->out_stage.ensure(8 * c->M));
+  k_influence<double><<<grid_for(c->M), kThreads, 0, c->stream>>>(s, nullptr, c->out_stage.as<double>());
+  LAUNCH_CHECK();
+  CU(cudaMemcpyAsync(g_full, c->out_stage.p, 8 * c->M, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return PPPM_OK;
+}
+
+int pppm_ctx_get_ik(pppm_ctx* c, double* ikx, double* iky, double* ikz) {
+  TRY(activate(c));
+  const double* ik = c->ik64.as<double>();
+  CU(cudaMemcpy(ikx, ik, 8 * c->g.nx, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(iky, ik + c->g.nx, 8 * c->g.ny, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(ikz, ik + c->g.nx + c->g.ny, 8 * c->g.nz, cudaMemcpyDeviceToHost));
+  return PPPM_OK;
+}
+
+int pppm_particle_map(pppm_ctx* c, const void* pos, int64_t n, int dtype, int mem, int32_t* nodes) {
+  TRY(activate(c));
+  const void *dpos, *dq;
+  TRY(stage_atoms(c, pos, nullptr, n, dtype, mem, &dpos, &dq));
+  TRY(c->node_stage.ensure(sizeof(int32_t) * 3 * n));
+  const bool r32 = !c->fp64();
+  int st = with_order(c->order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    const int grid = grid_for(n);
+    int32_t* nd = c->node_stage.as<int32_t>();
+    if (dtype == PPPM_F64) {
+      if (r32) k_particle_map<S, double, true><<<grid, kThreads, 0, c->stream>>>((const double*)dpos, n, c->g, nd, c->err.as<int>());
+      else k_particle_map<S, double, false><<<grid, kThreads, 0, c->stream>>>((const double*)dpos, n, c->g, nd, c->err.as<int>());
+    } else {
+      k_particle_map<S, float, false><<<grid, kThreads, 0, c->stream>>>((const float*)dpos, n, c->g, nd, c->err.as<int>());
+    }
+    return PPPM_OK;
+  });
+  TRY(st);
+  LAUNCH_CHECK();
+  CU(cudaMemcpyAsync(nodes, c->node_stage.p, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  return check_err_flag(c);
+}
+
+int pppm_make_rho(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, double* rho_out) {
+  TRY(activate(c));
+  const void *dpos, *dq;
+  TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
+  TRY(do_make_rho(c, dpos, dq, n, dtype));
+  TRY(check_err_flag(c));
+  if (rho_out) TRY(mesh_to_host(c, c->rho.p, rho_out, c->M));
+  return PPPM_OK;
+}
+
+int pppm_set_rho(pppm_ctx* c, const double* rho) {
+  TRY(activate(c));
+  TRY(mesh_from_host(c, c->rho.p, rho, c->M));
+  c->have_rho = true;
+  return PPPM_OK;
+}
+
+int pppm_get_rho(pppm_ctx* c, double* rho) {
+  TRY(activate(c));
+  if (!c->have_rho) return fail(PPPM_ERR_STATE, "no charge grid on the device");
+  return mesh_to_host(c, c->rho.p, rho, c->M);
+}
+
+int pppm_poisson(pppm_ctx* c, int want_fields, double* energy) {
+  TRY(activate(c));
+  if (!c->have_rho) return fail(PPPM_ERR_STATE, "no charge grid on the device");
+  TRY(run_fft_fwd(c));
+  TRY(run_green(c, want_fields != 0));
+  if (want_fields) TRY(run_fft_bwd(c));
+  if (energy) {
+    CU(cudaMemcpyAsync(c->h_scal, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *energy = c->h_scal[0];
+  } else {
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  return PPPM_OK;
+}
+
+int pppm_get_fields(pppm_ctx* c, double* f0, double* f1, double* f2) {
+  TRY(activate(c));
+  if (!c->have_fields) return fail(PPPM_ERR_STATE, "no field grids on the device");
+  const size_t rs = c->real_size();
+  double* outs[3] = {f0, f1, f2};
+  for (int f = 0; f < c->nfields(); ++f)
+    if (outs[f]) TRY(mesh_to_host(c, (char*)c->fields.p + rs * c->M * f, outs[f], c->M));
+  return PPPM_OK;
+}
+
+int pppm_set_fields(pppm_ctx* c, const double* f0, const double* f1, const double* f2) {
+  TRY(activate(c));
+  const size_t rs = c->real_size();
+  const double* ins[3] = {f0, f1, f2};
+  for (int f = 0; f < c->nfields(); ++f) {
+    if (!ins[f]) return fail(PPPM_ERR_VALUE, "missing field grid");
+    TRY(mesh_from_host(c, (char*)c->fields.p + rs * c->M * f, ins[f], c->M));
+  }
+  c->have_fields = true;
+  return PPPM_OK;
+}
+
+int pppm_fieldforce(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, double* forces) {
+  TRY(activate(c));
+  const void *dpos, *dq;
+  TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
+  TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
+  TRY(do_fieldforce(c, dpos, dq, n, dtype, true, c->out_stage.p, true));
+  TRY(check_err_flag(c));
+  CU(cudaMemcpyAsync(forces, c->out_stage.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return PPPM_OK;
+}
+
+int pppm_compute(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, double* forces,
+                 double* energy) {
+  TRY(activate(c));
+  const void *dpos, *dq;
+  TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
+  TRY(do_make_rho(c, dpos, dq, n, dtype));
+  TRY(run_fft_fwd(c));
+  TRY(run_green(c, true));
+  TRY(run_fft_bwd(c));
+  TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
+  TRY(do_fieldforce(c, dpos, dq, n, dtype, false, c->out_stage.p, true));
+  CU(cudaMemcpyAsync(forces, c->out_stage.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(c->h_scal, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_err_flag(c));
+  if (energy) *energy = c->h_scal[0];
+  return PPPM_OK;
+}
+
+int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
+  TRY(activate(c));
+  if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
+  const size_t es = dtype == PPPM_F64 ? 8 : 4;
+  TRY(c->res_pos.ensure(3 * n * es));
+  TRY(c->res_q.ensure(n * es));
+  TRY(c->res_force.ensure(3 * n * (c->fp64() ? 8 : 4)));
+  CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * n * es, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->res_q.p, q, n * es, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  c->n_res = n;
+  c->res_dtype = dtype;
+  return PPPM_OK;
+}
+
+static int step_phases(pppm_ctx* c, int phases, bool timing) {
+  const int64_t n = c->n_res;
+  const void* p = c->res_pos.p;
+  const void* q = c->res_q.p;
+  if (phases & PPPM_PHASE_MAKE_RHO) {
+    c->binned = false;
+    rec_event(c, SP_BIN, timing);
+    if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype));
+    rec_event(c, SP_SPREAD, timing);
+    TRY(run_spread(c, p, q, n, c->res_dtype));
+  }
+  if (phases & PPPM_PHASE_POISSON) {
+    rec_event(c, SP_FFT_FWD, timing);
+    TRY(run_fft_fwd(c));
+    rec_event(c, SP_GREEN, timing);
+    TRY(run_green(c, true));
+    rec_event(c, SP_FFT_BWD, timing);
+    TRY(run_fft_bwd(c));
+  }
+  if (phases & PPPM_PHASE_FIELDFORCE) {
+    rec_event(c, SP_GATHER, timing);
+    TRY(do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64()));
+  }
+  rec_event(c, SP_COUNT, timing);
+  return PPPM_OK;
+}
+
+int pppm_ctx_step(pppm_ctx* c, int phases) {
+  TRY(activate(c));
+  if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  return step_phases(c, phases, false);
+}
+
+int pppm_ctx_synchronize(pppm_ctx* c) {
+  TRY(activate(c));
+  return check_err_flag(c);
+}
+
+int pppm_ctx_get_forces(pppm_ctx* c, double* forces) {
+  TRY(activate(c));
+  const int64_t cnt = 3 * c->n_res;
+  if (c->fp64()) {
+    CU(cudaMemcpyAsync(forces, c->res_force.p, 8 * cnt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return PPPM_OK;
+  }
+  return mesh_to_host(c, c->res_force.p, forces, cnt);
+}
+
+int pppm_ctx_get_energy(pppm_ctx* c, double* energy) {
+  TRY(activate(c));
+  CU(cudaMemcpyAsync(c->h_scal, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  *energy = c->h_scal[0];
+  return PPPM_OK;
+}
+
+int pppm_ctx_time_steps(pppm_ctx* c, int steps, int warmup, int flush_l2, double* ms) {
+  TRY(activate(c));
+  if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  const size_t flush_bytes = (size_t)256 << 20;
+  if (flush_l2) TRY(c->flush.ensure(flush_bytes));
+  for (int i = 0; i <= SP_COUNT; ++i) ms[i] = 0.0;
+  cudaEvent_t t0, t1;
+  CU(cudaEventCreate(&t0));
+  CU(cudaEventCreate(&t1));
+  for (int w = 0; w < warmup; ++w) {
+    if (flush_l2) CU(cudaMemsetAsync(c->flush.p, w & 0xff, flush_bytes, c->stream));
+    TRY(step_phases(c, PPPM_PHASE_ALL, false));
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  TRY(check_err_flag(c));
+  CU(cudaEventRecord(t0, c->stream));
+  for (int s = 0; s < steps; ++s) {
+    if (flush_l2) CU(cudaMemsetAsync(c->flush.p, (s + 1) & 0xff, flush_bytes, c->stream));
+    TRY(step_phases(c, PPPM_PHASE_ALL, true));
+    CU(cudaEventSynchronize(c->ev[SP_COUNT]));
+    for (int k = 0; k < SP_COUNT; ++k) {
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, c->ev[k], c->ev[k + 1]));
+      ms[k] += t;
+    }
+  }
+  CU(cudaEventRecord(t1, c->stream));
+  CU(cudaEventSynchronize(t1));
+  float tot = 0.f;
+  CU(cudaEventElapsedTime(&tot, t0, t1));
+  ms[SP_COUNT] = tot;
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  return check_err_flag(c);
+}
+
+int pppm_ctx_launches_per_step(pppm_ctx* c, int* launches) {
+  TRY(activate(c));
+  if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  const int before = c->launches;
+  TRY(step_phases(c, PPPM_PHASE_ALL, false));
+  CU(cudaStreamSynchronize(c->stream));
+  *launches = c->launches - before;
+  return PPPM_OK;
+}
+
+}  // extern "C"

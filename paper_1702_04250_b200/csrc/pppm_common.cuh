@@ -1,0 +1,143 @@
+// Shared device helpers for the B200 PPPM mesh path.
+//
+// particle_map and the B-spline weight rows (compute_rho1d / compute_drho1d)
+// live here so every kernel evaluates them identically.  The fp64 variants use
+// explicit round-to-nearest intrinsics (__dadd_rn / __dmul_rn / __ddiv_rn) so
+// the compiler cannot contract them into FMAs: that reproduces the reference's
+// numpy arithmetic op for op, which makes node indices, table bins and fp64
+// weight rows bitwise identical to the reference (stencil.py:38-77,
+// stencil.py:123-126, gridmap.py:103-109).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pppm {
+
+constexpr int kRowPad = 8;           // stencil.py:23
+constexpr int kMaxOrder = 7;
+constexpr double kHalfBelow = 0.49999999999999994;  // nextafter(0.5, 0)
+
+// ---------------------------------------------------------------------------
+// arithmetic policies: Exact (fp64, no contraction) and Fast (fp32, FMA ok)
+
+struct ExactF64 {
+  using T = double;
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double divi(double a, int d) { return __ddiv_rn(a, (double)d); }
+};
+
+struct FastF32 {
+  using T = float;
+  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+  static __device__ __forceinline__ float divi(float a, int d) {
+    // exact for d in {1, 2, 4}; <= 1 ulp otherwise (fp32 path tolerance 1e-5)
+    return a * (1.0f / (float)d);
+  }
+};
+
+template <typename T> struct PolicyOf;
+template <> struct PolicyOf<double> { using P = ExactF64; };
+template <> struct PolicyOf<float> { using P = FastF32; };
+
+// ---------------------------------------------------------------------------
+// particle_map: one coordinate, fp64, bit-exact with gridmap.py:103-109.
+// Odd S: node = floor(u + 1/2), t = u - node.  Even S (extension, not in the
+// reference): node = floor(u), t = (u - node) - 1/2.  t is clipped to
+// [-1/2, nextafter(1/2, 0)].  node is pre-wrap and may equal n.
+
+template <int S>
+__device__ __forceinline__ void particle_map_1d(double x, double h, int& node, double& t) {
+  const double u = __ddiv_rn(x, h);
+  double nd, tt;
+  if (S & 1) {
+    nd = floor(__dadd_rn(u, 0.5));
+    tt = __dsub_rn(u, nd);
+  } else {
+    nd = floor(u);
+    tt = __dsub_rn(__dsub_rn(u, nd), 0.5);
+  }
+  tt = fmin(fmax(tt, -0.5), kHalfBelow);
+  node = (int)nd;
+  t = tt;
+}
+
+// lowest stencil node relative to `node` (gridmap.py:124 half = (S-1)//2)
+template <int S> struct Stencil {
+  static constexpr int lo = (S - 1) / 2;   // ghost planes below
+  static constexpr int hi = S - 1 - lo;    // ghost planes above
+};
+
+// table bin of offset t: clip(floor((t + 1/2) * n), 0, n-1)   (stencil.py:123-126)
+__device__ __forceinline__ int table_bin(double t, int n_points) {
+  const double v = floor(__dmul_rn(__dadd_rn(t, 0.5), (double)n_points));
+  int k = (int)fmax(fmin(v, (double)(n_points - 1)), 0.0);
+  return k;
+}
+
+// ---------------------------------------------------------------------------
+// B-spline rows by the triangular recurrence on M_m(w + k), w = t + 1/2
+// (stencil.py:50-76).  a[i], d[i]: node i, lowest grid index first.
+
+template <typename P, int S>
+__device__ __forceinline__ void bspline_rows(typename P::T t, typename P::T (&a)[S],
+                                             typename P::T (&d)[S]) {
+  using T = typename P::T;
+  const T w = P::add(t, (T)0.5);
+  T s[S];
+  T ds[S];
+  s[0] = (T)1;
+#pragma unroll
+  for (int k = 1; k < S; ++k) s[k] = (T)0;
+#pragma unroll
+  for (int m = 2; m <= S; ++m) {
+    if (m == S) {
+      ds[0] = s[0];
+#pragma unroll
+      for (int k = 1; k < S - 1; ++k) ds[k] = P::sub(s[k], s[k - 1]);
+      ds[S - 1] = -s[S - 2];
+    }
+    T nx[S];
+    nx[0] = P::divi(P::mul(w, s[0]), m - 1);
+#pragma unroll
+    for (int k = 1; k < m - 1; ++k) {
+      const T left = P::mul(P::add(w, (T)k), s[k]);
+      const T right = P::mul(P::sub(P::sub((T)m, w), (T)k), s[k - 1]);
+      nx[k] = P::divi(P::add(left, right), m - 1);
+    }
+    nx[m - 1] = P::divi(P::mul(P::sub(P::sub((T)m, w), (T)(m - 1)), s[m - 2]), m - 1);
+#pragma unroll
+    for (int k = 0; k < m; ++k) s[k] = nx[k];
+  }
+  if (S == 1) ds[0] = (T)0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    a[i] = s[S - 1 - i];
+    d[i] = ds[S - 1 - i];
+  }
+}
+
+// assignment row only (cheaper: no derivative samples kept live)
+template <typename P, int S>
+__device__ __forceinline__ void bspline_assign(typename P::T t, typename P::T (&a)[S]) {
+  typename P::T d[S];
+  bspline_rows<P, S>(t, a, d);
+}
+
+__device__ __forceinline__ int wrap_index(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+// warp/block reductions -----------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace pppm

@@ -1,0 +1,58 @@
+"""Rebind the reference package's hot-path names to this package's operators.
+
+The reference has no plugin registry: ``compute_forces`` and the CLI use the
+names bound at import time in ``pppm/driver.py:32-33`` and re-exported in
+``pppm/__init__.py:32-41``.  ``install(pppm)`` rebinds them in
+``pppm``, ``pppm.driver``, ``pppm.gridmap``, ``pppm.kspace`` and
+``pppm.stencil``, and makes this package return the reference's own result
+types and raise its ConfigurationError.  Call it before modules that do
+``from pppm import map_charge`` are imported (e.g. from a pytest plugin).
+"""
+
+from __future__ import annotations
+
+from . import _native as nat
+from . import _runtime as rt
+from . import gridmap, kspace, stencil
+
+HOT_PATH = {
+    "gridmap": ("map_charge", "distribute_force_ik", "distribute_force_ad"),
+    "kspace": ("build_plan", "poisson_ik", "poisson_ad", "kspace_energy"),
+    "stencil": ("build_table",),
+}
+_SOURCES = {"gridmap": gridmap, "kspace": kspace, "stencil": stencil}
+_saved = {}
+
+
+def install(pppm_module):
+    """Point the reference's hot-path names at the B200 operators."""
+    import importlib
+
+    mods = {name: importlib.import_module(f"{pppm_module.__name__}.{name}")
+            for name in ("gridmap", "kspace", "stencil", "driver", "model")}
+    T = rt.types()
+    T.DiffMode = mods["model"].DiffMode
+    T.ChargeGrid = mods["gridmap"].ChargeGrid
+    T.FieldGrids = mods["gridmap"].FieldGrids
+    T.StencilTable = mods["stencil"].StencilTable
+    T.KSpacePlan = mods["kspace"].KSpacePlan
+    nat.ERRORS.config = mods["model"].ConfigurationError
+    for modname, names in HOT_PATH.items():
+        for name in names:
+            new = getattr(_SOURCES[modname], name)
+            for target in (pppm_module, mods[modname], mods["driver"]):
+                if hasattr(target, name):
+                    _saved.setdefault((target.__name__, name), (target, getattr(target, name)))
+                    setattr(target, name, new)
+    return sorted({name for names in HOT_PATH.values() for name in names})
+
+
+def uninstall():
+    """Restore every name ``install`` rebound."""
+    for (_, name), (target, old) in list(_saved.items()):
+        setattr(target, name, old)
+    _saved.clear()
+    rt.types().reset()
+    from .model import ConfigurationError
+
+    nat.ERRORS.config = ConfigurationError
