@@ -1,0 +1,340 @@
+"""Benchmark of the B200 PPPM mesh core (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--mode ik|ad]
+
+A step is one PPPM long-range evaluation of BASELINE config 3 (1,048,576 point
+charges, 128^3 mesh, order 5, ik, mixed precision) on atoms already resident
+in HBM: bin + make_rho -> R2C -> Green/ik multiply (+energy) -> 3x C2R ->
+fieldforce.  ``value`` is the metric BASELINE.json names: atom-steps/s of
+make_rho + fieldforce (binning included in make_rho), from CUDA events on the
+context stream; L2 (126 MB) is flushed with a 256 MiB memset before every
+step.  ``e2e`` is the same workload through the C ABI with pinned host
+buffers (H2D of positions/charges, full step, D2H of forces and energy).
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own config-3
+system (weak scaling, independent replicas; the z-slab decomposition is
+not in this round), barrier + device sync around the timed region, max
+time over ranks.
+
+``--impl reference`` times the CPU oracle port of the reference algorithm
+(oracle/pppm_oracle.py, numpy, all host threads for make_rho) on bounded
+samples of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPPM atom-steps/s (make_rho+fieldforce) at order 5; achieved HBM GB/s vs peak"
+UNIT = "atom-steps/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--mode", default=None, choices=(None, "ik", "ad"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        pg = dist
+    return rank, local, world, pg
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def max_over_ranks(pg, value):
+    if pg is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(pg, value):
+    if pg is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64)
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic(config, mode):
+    """ncu dram bytes per launch of the dominant kernel, committed under profiles/."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"config{config}_{mode}")
+    except Exception:
+        return None
+
+
+def cpu_sample_rate(pos, q, lengths, dims, order, mode, sample, workers, reps=1):
+    """Oracle make_rho + fieldforce on the first ``sample`` atoms: atom-steps/s."""
+    from oracle import pppm_oracle as orc
+
+    p = np.ascontiguousarray(pos[:sample], dtype=np.float64)
+    qq = np.ascontiguousarray(q[:sample], dtype=np.float64)
+    nx, ny, nz = dims
+    fields = [np.random.default_rng(0).standard_normal((nz, ny, nx)) for _ in range(3 if mode == "ik" else 1)]
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.map_charge(p, qq, lengths, dims, order, workers=workers)
+        if mode == "ik":
+            orc.fieldforce_ik(fields, p, qq, lengths, dims, order)
+        else:
+            orc.fieldforce_ad(fields[0], p, qq, lengths, dims, order)
+        times.append(time.perf_counter() - t0)
+    return sample / min(times), times
+
+
+def run_reference(args, cfg, rank, pg):
+    if rank != 0:
+        return
+    from paper_1702_04250_b200 import scenarios  # noqa: F401
+
+    mode = args.mode or cfg.mode
+    pos, q, lengths = cfg.build()
+    cores = len(os.sched_getaffinity(0))
+    sample = 16384
+    for _ in range(max(args.warmup, 0)):
+        cpu_sample_rate(pos, q, lengths, cfg.dims, cfg.order, mode, 4096, cores)
+    times = []
+    for s in range(args.steps):
+        _, t = cpu_sample_rate(pos, q, lengths, cfg.dims, cfg.order, mode, sample, cores)
+        times.append(t[0])
+    mean = sum(times) / len(times)
+    value = sample / mean
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{cfg.index}: {cfg.n_atoms} atoms, mesh {cfg.dims}, order {cfg.order}, "
+                               f"{mode}; each step a {sample}-atom sample", "mode": mode},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"make_rho(workers={cores}) + fieldforce_{mode} on {sample} atoms of config "
+                                   f"{cfg.index} per step (numpy oracle port of the reference, fp64)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_1702_04250_b200 import scenarios
+
+    cfg = scenarios.CONFIGS[args.config]
+    rank, local, world, pg = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, pg)
+        return
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_1702_04250_b200 as pb
+    from paper_1702_04250_b200 import _native as nat
+
+    mode = args.mode or cfg.mode
+    pos, q, lengths = cfg.build(seed=cfg.index + 1000 * rank)
+    n = pos.shape[0]
+    fp32 = cfg.precision != "fp64"
+    posd = pos.astype(np.float32) if fp32 else pos
+    qd = q.astype(np.float32) if fp32 else q
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision=cfg.precision,
+                         alpha=cfg.alpha, device=local)
+    ctx.load_atoms(posd, qd)
+    launches = ctx.launches_per_step()
+
+    barrier(pg)
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_wall = time.perf_counter()
+    ms = ctx.time_steps(args.steps, args.warmup, flush_l2=True)
+    t_wall = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    barrier(pg)
+
+    k = args.steps
+    t_mf = (ms["bin"] + ms["spread"] + ms["gather"]) / 1e3        # make_rho + fieldforce, s
+    t_step = (ms["bin"] + ms["spread"] + ms["fft_fwd"] + ms["green"] + ms["fft_bwd"] + ms["gather"]) / 1e3
+    t_mf_max = max_over_ranks(pg, t_mf)
+    t_step_max = max_over_ranks(pg, t_step)
+    atoms_total = sum_over_ranks(pg, float(n))
+    value = atoms_total * k / t_mf_max
+
+    # roofline of the dominant kernel: algorithmic bytes per launch / mean launch time
+    p = 4 if fp32 else 8
+    M = int(np.prod(cfg.dims))
+    nf = 3 if mode == "ik" else 1
+    alg = {
+        "spread": n * (3 * p + p) + M * p,                       # make_rho: atoms in, mesh out
+        "gather": n * (3 * p + p) + nf * M * p + 3 * n * p,      # fieldforce: atoms + fields in, forces out
+        "bin": n * (3 * p + p) * 2 + n * 4 * 4,                  # counting sort passes (scratch)
+    }
+    per_kernel = {}
+    for key in ("bin", "spread", "gather"):
+        t = ms[key] / 1e3 / k
+        per_kernel[key] = {"ms": t * 1e3, "alg_bytes": alg[key], "gbs": alg[key] / t / 1e9}
+    dom = max(("spread", "gather"), key=lambda kk: per_kernel[kk]["ms"])
+    peak, peak_kind = peaks()
+    achieved = per_kernel[dom]["gbs"]
+    mf_bytes = alg["spread"] + alg["gather"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": load_traffic(args.config, mode), "kernel": "k_spread_brick" if dom == "spread" else "k_gather_brick",
+                "peak_kind": peak_kind,
+                "make_rho_fieldforce_gbs": mf_bytes / (t_mf / k) / 1e9,
+                "make_rho_fieldforce_frac": mf_bytes / (t_mf / k) / 1e9 / peak}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
+        "ms_per_step": t_step_max / k * 1e3, "ms_make_rho_fieldforce": t_mf_max / k * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if fp32 else "f64", "data": "synthetic",
+        "config": {"workload": f"config{cfg.index}: {n} point charges per GPU, mesh {cfg.dims[0]}^3, order {cfg.order}, "
+                               f"{mode}, {cfg.precision}", "n_atoms_per_gpu": n, "mesh": list(cfg.dims),
+                   "order": cfg.order, "mode": mode, "precision": cfg.precision,
+                   "l2": "flushed before every step (256 MiB memset, outside the phase intervals)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "phases_ms_per_step": {kk: v / k for kk, v in ms.items()},
+        "whole_step_atom_steps_per_s": atoms_total * k / t_step_max,
+        "kernels": per_kernel, "roofline": roofline, "clocks": clocks, "gpu_launches": launches * k,
+        "wall_s_timed_region": t_wall,
+    }
+
+    if not args.no_e2e:
+        # end to end through the C ABI: pinned host fp32 inputs -> H2D -> full step -> D2H forces (fp64) + energy
+        hp = pb.PinnedArray(posd.shape, posd.dtype)
+        hq = pb.PinnedArray(qd.shape, qd.dtype)
+        hp.array[...] = posd
+        hq.array[...] = qd
+        for _ in range(max(2, args.warmup)):
+            ctx.compute(hp.array, hq.array)
+        barrier(pg)
+        times = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            ctx.compute(hp.array, hq.array)
+            times.append(time.perf_counter() - t0)
+        t_e2e = max_over_ranks(pg, sum(times))
+        line["e2e"] = {"value": atoms_total * k / t_e2e, "unit": UNIT,
+                       "h2d_bytes_per_step": int(posd.nbytes + qd.nbytes), "d2h_bytes_per_step": int(n * 3 * 8 + 8),
+                       "what": "pppm_compute: H2D pos+q (pinned), make_rho, poisson, fieldforce, D2H forces+energy; "
+                               "wall clock per synchronous call"}
+        hp.free()
+        hq.free()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        sample = 65536
+        rate, times = cpu_sample_rate(pos.astype(np.float64), q, lengths, cfg.dims, cfg.order, mode, sample, cores)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"make_rho(workers={cores}) + fieldforce_{mode} on the first {sample} atoms "
+                                          f"of config {cfg.index} (numpy oracle port, fp64), {times[0]:.1f} s"}
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

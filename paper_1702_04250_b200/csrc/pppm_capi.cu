@@ -310,7 +310,6 @@ static int run_fft_fwd(pppm_ctx* c) {
     FFT(cufftExecD2Z(c->fwd, c->rho.as<double>(), c->rho_hat.as<cufftDoubleComplex>()));
   else
     FFT(cufftExecR2C(c->fwd, c->rho.as<float>(), c->rho_hat.as<cufftComplex>()));
-  c->launches += 1;
   return PPPM_OK;
 }
 
@@ -354,7 +353,6 @@ static int run_fft_bwd(pppm_ctx* c) {
     FFT(cufftExecZ2D(c->bwd, c->ework.as<cufftDoubleComplex>(), c->fields.as<double>()));
   else
     FFT(cufftExecC2R(c->bwd, c->ework.as<cufftComplex>(), c->fields.as<float>()));
-  c->launches += 1;
   c->have_fields = true;
   return PPPM_OK;
 }

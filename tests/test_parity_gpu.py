@@ -167,7 +167,8 @@ def test_influence_optimal_and_ik(pb):
     box = pb.SimulationBox(g["lengths"])
     dims = tuple(int(d) for d in g["dims"])
     opt = pb.build_plan(dims, box, float(g["alpha"]), int(g["order"]), influence="optimal")
-    assert np.allclose(opt.influence, g["optimal"], rtol=1e-12, atol=0)
+    # alias sums partially cancel: compare against the grid's scale
+    assert np.abs(opt.influence - g["optimal"]).max() <= 1e-12 * np.abs(g["optimal"]).max()
     pme = pb.build_plan(dims, box, float(g["alpha"]), int(g["order"]))
     assert np.allclose(pme.influence, g["pme"], rtol=1e-13, atol=0)
     for k in ("ik_x", "ik_y", "ik_z"):
