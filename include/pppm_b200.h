@@ -119,6 +119,10 @@ int pppm_ctx_get_energy(pppm_ctx* ctx, double* energy);
  * 256 MiB buffer before each step (outside the phase intervals).
  * ms[0..6]: bin, spread, fft_fwd, green, fft_bwd, gather, total (summed over steps) */
 int pppm_ctx_time_steps(pppm_ctx* ctx, int steps, int warmup, int flush_l2, double* ms);
+/* kernel variants for A/B measurement: kernel 0 = fp32 make_rho
+ * (0: float CAS shared atomics, 1: int32 fixed-point shared atomics [default]),
+ * kernel 1 = fp32 fieldforce (0: bucket order, 1: cell-sorted in shared memory [default]) */
+int pppm_ctx_set_variant(pppm_ctx* ctx, int kernel, int variant);
 /* kernels launched by one step (for the bench's gpu_launches claim) */
 int pppm_ctx_launches_per_step(pppm_ctx* ctx, int* launches);
 

@@ -1,51 +1,21 @@
-// sm_100a kernels of the PPPM particle-mesh path.
+// Setup, particle_map, fp64 make_rho, Poisson multiply and fp64 fieldforce
+// kernels of the B200 PPPM mesh path, with their launchers.
 //
-//   particle_map        k_particle_map            (gridmap.py:92-119)
+//   particle_map        k_particle_map              (gridmap.py:92-119)
 //   table rows          k_table_rows / k_weight_rows (stencil.py:38-77, 129-139)
-//   make_rho  fp64      k_spread_fix64 + k_fix64_to_real  (gridmap.py:141-213)
-//   make_rho  fp32      k_bin_count / k_scan_bricks / k_bin_scatter / k_spread_brick
-//   influence           k_influence (kspace.py:139-196)
+//   make_rho  fp64      k_spread_fix64 + k_fix64_to_real (gridmap.py:141-213)
+//   influence           k_influence                 (kspace.py:139-196)
 //   Poisson multiply    k_green (kspace.py:271-317) with fused energy (kspace.py:320-337)
-//   fieldforce fp64     k_gather_direct (gridmap.py:236-312)
-//   fieldforce fp32     k_gather_brick
+//   fieldforce fp64     k_gather_direct             (gridmap.py:236-312)
 //
 // The fp64 path is deterministic: charges are accumulated as 64-bit fixed
 // point (integer adds are associative), every per-atom gather sums in a fixed
 // order, and the energy reduction uses a fixed grid with an ordered final sum.
-#pragma once
-
 #include <cuComplex.h>
 
-#include "pppm_common.cuh"
+#include "pppm_device.cuh"
 
 namespace pppm {
-
-constexpr int kBrick = 8;          // owned cells per brick edge (fp32 path)
-constexpr int kGreenBlocks = 592;  // 4 x 148 SMs: fixed grid => deterministic energy order
-constexpr int kThreads = 256;
-
-// ---------------------------------------------------------------------------
-// input loads: positions are AoS (N, 3), charges (N,), fp64 or fp32.  When the
-// context runs in mixed precision, fp64 inputs are rounded to fp32 first (the
-// oracle is fed the same rounded values).
-
-template <typename TIn, bool R32>
-__device__ __forceinline__ double load_real(const TIn* p, int64_t k) {
-  double v = (double)p[k];
-  if (R32) v = (double)(float)v;
-  return v;
-}
-
-struct Geom {
-  int nx, ny, nz;
-  double hx, hy, hz;
-  double lx, ly, lz;
-};
-
-__device__ __forceinline__ bool outside(double x, double len) { return !(x >= 0.0 && x < len); }
-
-// ---------------------------------------------------------------------------
-// particle_map
 
 template <int S, typename TIn, bool R32>
 __global__ void k_particle_map(const TIn* __restrict__ pos, int64_t n, Geom g,
@@ -66,9 +36,6 @@ __global__ void k_particle_map(const TIn* __restrict__ pos, int64_t n, Geom g,
     nodes[2 * n + i] = nd;
   }
 }
-
-// ---------------------------------------------------------------------------
-// stencil rows on the device (build_table / assignment_weights)
 
 template <int S>
 __global__ void k_table_rows(int n_points, double* __restrict__ assign, double* __restrict__ deriv) {
@@ -96,27 +63,6 @@ __global__ void k_weight_rows(const double* __restrict__ tv, int64_t n, double* 
   for (int j = 0; j < kRowPad; ++j) {
     assign[k * kRowPad + j] = j < S ? a[j < S ? j : 0] : 0.0;
     deriv[k * kRowPad + j] = j < S ? d[j < S ? j : 0] : 0.0;
-  }
-}
-
-// per-dimension weights for one coordinate, exact recurrence or table lookup
-template <typename P, int S, bool TAB, bool DERIV>
-__device__ __forceinline__ void weights_1d(double t, const typename P::T* __restrict__ ta,
-                                           const typename P::T* __restrict__ td, int n_points,
-                                           typename P::T (&a)[S], typename P::T (&d)[S]) {
-  using T = typename P::T;
-  if (TAB) {
-    const int k = table_bin(t, n_points);
-    const T* ra = ta + (int64_t)k * kRowPad;
-#pragma unroll
-    for (int j = 0; j < S; ++j) a[j] = ra[j];
-    if (DERIV) {
-      const T* rd = td + (int64_t)k * kRowPad;
-#pragma unroll
-      for (int j = 0; j < S; ++j) d[j] = rd[j];
-    }
-  } else {
-    bspline_rows<P, S>((T)t, a, d);
   }
 }
 
@@ -219,160 +165,6 @@ __global__ void k_fix64_to_real(const unsigned long long* __restrict__ acc, int6
 }
 
 // ---------------------------------------------------------------------------
-// make_rho, fp32: counting sort of atoms into 8^3-cell bricks, then one CTA
-// per brick accumulates its atoms' S^3 stencils in a shared-memory tile that
-// carries an (S-1)-cell halo, and adds the tile to the mesh with red.global.
-
-struct Bricks {
-  int nbx, nby, nbz;
-  __host__ __device__ __forceinline__ int count() const { return nbx * nby * nbz; }
-};
-
-template <int S>
-__device__ __forceinline__ void brick_of(double x, double y, double z, const Geom& g, const Bricks& bk,
-                                         int& b) {
-  int n0, n1, n2;
-  double t;
-  particle_map_1d<S>(x, g.hx, n0, t);
-  particle_map_1d<S>(y, g.hy, n1, t);
-  particle_map_1d<S>(z, g.hz, n2, t);
-  n0 = n0 >= g.nx ? n0 - g.nx : n0;
-  n1 = n1 >= g.ny ? n1 - g.ny : n1;
-  n2 = n2 >= g.nz ? n2 - g.nz : n2;
-  b = ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
-}
-
-template <int S, typename TIn, bool R32>
-__global__ void __launch_bounds__(kThreads) k_bin_count(
-    const TIn* __restrict__ pos, int64_t n, Geom g, Bricks bk, int* __restrict__ counts,
-    int* __restrict__ abin, int* __restrict__ aslot, int* __restrict__ err) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_real<TIn, true>(pos, 3 * i + 0);
-    const double y = load_real<TIn, true>(pos, 3 * i + 1);
-    const double z = load_real<TIn, true>(pos, 3 * i + 2);
-    if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
-      atomicOr(err, 1);
-      abin[i] = -1;
-      continue;
-    }
-    int b;
-    brick_of<S>(x, y, z, g, bk, b);
-    abin[i] = b;
-    aslot[i] = atomicAdd(counts + b, 1);
-  }
-}
-
-// exclusive scan of brick counts, one CTA (nb <= a few 10^5)
-__global__ void __launch_bounds__(1024) k_scan_bricks(const int* __restrict__ counts, int nb,
-                                                      int* __restrict__ start) {
-  __shared__ int warp_tot[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < nb; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int v = i < nb ? counts[i] : 0;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      int w = warp_tot[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      warp_tot[lane] = w;
-    }
-    __syncthreads();
-    const int excl = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - v;
-    if (i < nb) start[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) start[nb] = carry;
-}
-
-template <typename TIn>
-__global__ void __launch_bounds__(kThreads) k_bin_scatter(
-    const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, const int* __restrict__ abin,
-    const int* __restrict__ aslot, const int* __restrict__ start, float4* __restrict__ rec,
-    int* __restrict__ perm) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = abin[i];
-    if (b < 0) continue;
-    const int dst = start[b] + aslot[i];
-    rec[dst] = make_float4((float)pos[3 * i], (float)pos[3 * i + 1], (float)pos[3 * i + 2], (float)qv[i]);
-    perm[dst] = (int)i;
-  }
-}
-
-template <int S>
-struct Tile {
-  static constexpr int D = kBrick + S - 1;  // tile edge: brick + halo
-  static constexpr int N = D * D * D;
-};
-
-template <int S, bool TAB>
-__global__ void __launch_bounds__(kThreads) k_spread_brick(
-    const float4* __restrict__ rec, const int* __restrict__ start, Geom g, Bricks bk,
-    const float* __restrict__ ta, int n_points, float inv_vcell, float* __restrict__ rho) {
-  constexpr int D = Tile<S>::D, TN = Tile<S>::N, lo = Stencil<S>::lo;
-  __shared__ float tile[TN];
-  for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0.f;
-  __syncthreads();
-  const int b = blockIdx.x;
-  const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-  const int j0 = start[b], j1 = start[b + 1];
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-    const float4 r = rec[j];
-    int n0, n1, n2;
-    double tx, ty, tz;
-    particle_map_1d<S>((double)r.x, g.hx, n0, tx);
-    particle_map_1d<S>((double)r.y, g.hy, n1, ty);
-    particle_map_1d<S>((double)r.z, g.hz, n2, tz);
-    const int lx = (n0 >= g.nx ? n0 - g.nx : n0) - bx * kBrick;
-    const int ly = (n1 >= g.ny ? n1 - g.ny : n1) - by * kBrick;
-    const int lz = (n2 >= g.nz ? n2 - g.nz : n2) - bz * kBrick;
-    float wx[S], wy[S], wz[S], dd[S];
-    weights_1d<FastF32, S, TAB, false>(tx, ta, ta, n_points, wx, dd);
-    weights_1d<FastF32, S, TAB, false>(ty, ta, ta, n_points, wy, dd);
-    weights_1d<FastF32, S, TAB, false>(tz, ta, ta, n_points, wz, dd);
-    const float qv = r.w * inv_vcell;
-#pragma unroll
-    for (int a = 0; a < S; ++a) {
-      const float qa = qv * wz[a];
-#pragma unroll
-      for (int bb = 0; bb < S; ++bb) {
-        const float qab = qa * wy[bb];
-        float* row = tile + ((lz + a) * D + (ly + bb)) * D + lx;
-#pragma unroll
-        for (int c = 0; c < S; ++c) atomicAdd(row + c, qab * wx[c]);
-      }
-    }
-  }
-  __syncthreads();
-  const int ox = bx * kBrick - lo, oy = by * kBrick - lo, oz = bz * kBrick - lo;
-  for (int k = threadIdx.x; k < TN; k += blockDim.x) {
-    const float v = tile[k];
-    if (v == 0.f) continue;
-    const int tx_ = k % D, ty_ = (k / D) % D, tz_ = k / (D * D);
-    const int gx = wrap_index(ox + tx_, g.nx), gy = wrap_index(oy + ty_, g.ny),
-              gz = wrap_index(oz + tz_, g.nz);
-    atomicAdd(rho + ((int64_t)gz * g.ny + gy) * g.nx + gx, v);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // influence function (kspace.py:139-196), fp64, any grid subset
 
 __device__ __forceinline__ double mode_number(int i, int n) { return (double)(i <= (n - 1) / 2 ? i : i - n); }
@@ -386,12 +178,6 @@ __device__ __forceinline__ double ipow(double v, int s) {
   for (int i = 0; i < s; ++i) r *= v;
   return r;
 }
-
-struct GreenSpec {
-  int nx, ny, nz, order;
-  double lx, ly, lz, alpha, floor;
-  int optimal;
-};
 
 __device__ double influence_at(const GreenSpec& s, int ix, int iy, int iz) {
   const double two_pi = 2.0 * M_PI;
@@ -433,7 +219,7 @@ __device__ double influence_at(const GreenSpec& s, int ix, int iy, int iz) {
 
 // half spectrum (nz, ny, nx/2+1) in the compute type, plus optional full grid in fp64
 template <typename T>
-__global__ void k_influence(GreenSpec s, T* __restrict__ g_half, double* __restrict__ g_full) {
+__global__ void __launch_bounds__(kThreads) k_influence(GreenSpec s, T* __restrict__ g_half, double* __restrict__ g_full) {
   const int nxh = s.nx / 2 + 1;
   const int64_t total = g_full ? (int64_t)s.nx * s.ny * s.nz : (int64_t)nxh * s.ny * s.nz;
   const int width = g_full ? s.nx : nxh;
@@ -528,7 +314,7 @@ __global__ void k_energy_final(const double* __restrict__ partial, int nparts, d
 }
 
 // ---------------------------------------------------------------------------
-// fieldforce, fp64, one thread per atom (original order), fixed summation order.
+// fieldforce, fp64, one thread per atom (input order), fixed summation order.
 // ik: F_d = (C/eps) q sum wz wy wx E_d          (gridmap.py:236-267)
 // ad: F_d = -(C/eps) q sum_d / h_d, sum_x = sum az ay dx phi, ...  (gridmap.py:270-312)
 
@@ -618,106 +404,154 @@ __global__ void __launch_bounds__(kThreads) k_gather_direct(
   }
 }
 
-// ---------------------------------------------------------------------------
-// fieldforce, fp32: one CTA per brick, the field tile (brick + halo) staged in
-// shared memory, one thread per atom, forces scattered back to input order.
-
-template <int S, bool TAB, int MODE, typename TOut>
-__global__ void __launch_bounds__(kThreads) k_gather_brick(
-    const float4* __restrict__ rec, const int* __restrict__ perm, const int* __restrict__ start, Geom g,
-    Bricks bk, const float* __restrict__ ta, const float* __restrict__ td, int n_points,
-    const float* __restrict__ fields, int64_t mesh, float cscale, TOut* __restrict__ force) {
-  constexpr int D = Tile<S>::D, TN = Tile<S>::N, lo = Stencil<S>::lo;
-  constexpr int F = MODE == 0 ? 3 : 1;
-  __shared__ float tile[F * TN];
-  const int b = blockIdx.x;
-  const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-  const int j0 = start[b], j1 = start[b + 1];
-  if (j0 == j1) return;
-  const int ox = bx * kBrick - lo, oy = by * kBrick - lo, oz = bz * kBrick - lo;
-  for (int k = threadIdx.x; k < TN; k += blockDim.x) {
-    const int tx_ = k % D, ty_ = (k / D) % D, tz_ = k / (D * D);
-    const int gx = wrap_index(ox + tx_, g.nx), gy = wrap_index(oy + ty_, g.ny),
-              gz = wrap_index(oz + tz_, g.nz);
-    const int64_t gi = ((int64_t)gz * g.ny + gy) * g.nx + gx;
-#pragma unroll
-    for (int f = 0; f < F; ++f) tile[f * TN + k] = __ldg(fields + f * mesh + gi);
-  }
-  __syncthreads();
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-    const float4 r = rec[j];
-    int n0, n1, n2;
-    double tx, ty, tz;
-    particle_map_1d<S>((double)r.x, g.hx, n0, tx);
-    particle_map_1d<S>((double)r.y, g.hy, n1, ty);
-    particle_map_1d<S>((double)r.z, g.hz, n2, tz);
-    const int lx = (n0 >= g.nx ? n0 - g.nx : n0) - bx * kBrick;
-    const int ly = (n1 >= g.ny ? n1 - g.ny : n1) - by * kBrick;
-    const int lz = (n2 >= g.nz ? n2 - g.nz : n2) - bz * kBrick;
-    float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
-    weights_1d<FastF32, S, TAB, MODE == 1>(tx, ta, td, n_points, ax, dx);
-    weights_1d<FastF32, S, TAB, MODE == 1>(ty, ta, td, n_points, ay, dy);
-    weights_1d<FastF32, S, TAB, MODE == 1>(tz, ta, td, n_points, az, dz);
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int a = 0; a < S; ++a) {
-      float r0 = 0.f, r1 = 0.f, r2 = 0.f;
-#pragma unroll
-      for (int bb = 0; bb < S; ++bb) {
-        const float* row = tile + ((lz + a) * D + (ly + bb)) * D + lx;
-        if (MODE == 0) {
-          float e0 = 0.f, e1 = 0.f, e2 = 0.f;
-#pragma unroll
-          for (int c = 0; c < S; ++c) {
-            e0 = fmaf(ax[c], row[c], e0);
-            e1 = fmaf(ax[c], row[TN + c], e1);
-            e2 = fmaf(ax[c], row[2 * TN + c], e2);
-          }
-          r0 = fmaf(ay[bb], e0, r0);
-          r1 = fmaf(ay[bb], e1, r1);
-          r2 = fmaf(ay[bb], e2, r2);
-        } else {
-          float pd = 0.f, pa = 0.f;
-#pragma unroll
-          for (int c = 0; c < S; ++c) {
-            pd = fmaf(dx[c], row[c], pd);
-            pa = fmaf(ax[c], row[c], pa);
-          }
-          r0 = fmaf(ay[bb], pd, r0);
-          r1 = fmaf(dy[bb], pa, r1);
-          r2 = fmaf(ay[bb], pa, r2);
-        }
-      }
-      if (MODE == 0) {
-        s0 = fmaf(az[a], r0, s0);
-        s1 = fmaf(az[a], r1, s1);
-        s2 = fmaf(az[a], r2, s2);
-      } else {
-        s0 = fmaf(az[a], r0, s0);
-        s1 = fmaf(az[a], r1, s1);
-        s2 = fmaf(dz[a], r2, s2);
-      }
-    }
-    const float sc = cscale * r.w;
-    const int i = perm[j];
-    if (MODE == 0) {
-      force[3 * (int64_t)i + 0] = (TOut)(sc * s0);
-      force[3 * (int64_t)i + 1] = (TOut)(sc * s1);
-      force[3 * (int64_t)i + 2] = (TOut)(sc * s2);
-    } else {
-      force[3 * (int64_t)i + 0] = (TOut)(-sc * s0 / (float)g.hx);
-      force[3 * (int64_t)i + 1] = (TOut)(-sc * s1 / (float)g.hy);
-      force[3 * (int64_t)i + 2] = (TOut)(-sc * s2 / (float)g.hz);
-    }
-  }
-}
-
 // real-mesh conversions for the host boundary
 template <typename TA, typename TB>
 __global__ void k_convert(const TA* __restrict__ a, TB* __restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (TB)a[i];
+}
+
+
+// ---------------------------------------------------------------------------
+// launchers
+
+int launch_particle_map(int order, bool r32, const AtomsIn& a, const Geom& g, int32_t* nodes, int* err,
+                        cudaStream_t s) {
+  const int grid = grid_for(a.n);
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    if (!a.f32) {
+      if (r32) k_particle_map<S, double, true><<<grid, kThreads, 0, s>>>((const double*)a.pos, a.n, g, nodes, err);
+      else k_particle_map<S, double, false><<<grid, kThreads, 0, s>>>((const double*)a.pos, a.n, g, nodes, err);
+    } else {
+      k_particle_map<S, float, false><<<grid, kThreads, 0, s>>>((const float*)a.pos, a.n, g, nodes, err);
+    }
+    return 0;
+  });
+  return st ? st : launch_status();
+}
+
+int launch_table_rows(int order, int n_points, double* assign, double* deriv, cudaStream_t s) {
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    k_table_rows<S><<<(n_points + 255) / 256, 256, 0, s>>>(n_points, assign, deriv);
+    return 0;
+  });
+  return st ? st : launch_status();
+}
+
+int launch_weight_rows(int order, const double* t, int64_t n, double* assign, double* deriv, cudaStream_t s) {
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    k_weight_rows<S><<<(int)((n + 255) / 256), 256, 0, s>>>(t, n, assign, deriv);
+    return 0;
+  });
+  return st ? st : launch_status();
+}
+
+// scal: [0] energy, [1] scale, [2] inv_scale, [4] qmax bits
+int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, const double* ta, int n_points,
+                        double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s) {
+  const int grid = grid_for(a.n);
+  const int64_t M = (int64_t)g.nx * g.ny * g.nz;
+  unsigned long long* qmax = reinterpret_cast<unsigned long long*>(scal + 4);
+  if (cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * M, s) != cudaSuccess ||
+      cudaMemsetAsync(qmax, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    return launch_status();
+  k_absmax_charge<<<grid, kThreads, 0, s>>>(a.q, a.f32, a.n, qmax);
+  k_fix_scale<<<1, 1, 0, s>>>(qmax, a.n, scal + 1, scal + 2);
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    return with_bool(tab, [&](auto T_) -> int {
+      constexpr bool TAB = decltype(T_)::value;
+      if (!a.f32)
+        k_spread_fix64<S, TAB, double, false><<<grid, kThreads, 0, s>>>(
+            (const double*)a.pos, (const double*)a.q, a.n, g, ta, n_points, scal + 1, acc, err);
+      else
+        k_spread_fix64<S, TAB, float, false><<<grid, kThreads, 0, s>>>(
+            (const float*)a.pos, (const float*)a.q, a.n, g, ta, n_points, scal + 1, acc, err);
+      return 0;
+    });
+  });
+  if (st) return st;
+  const double vcell = g.hx * g.hy * g.hz;
+  k_fix64_to_real<double><<<grid_for(M), kThreads, 0, s>>>(acc, M, scal + 2, vcell, rho);
+  return launch_status();
+}
+
+int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
+                         const double* td, int n_points, const double* f, int64_t mesh, double cscale,
+                         double* force, int* err, cudaStream_t s) {
+  const int grid = grid_for(a.n);
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    return with_bool(tab, [&](auto T_) -> int {
+      constexpr bool TAB = decltype(T_)::value;
+      auto go = [&](auto MODE_) {
+        constexpr int MODE = decltype(MODE_)::value;
+        if (!a.f32)
+          k_gather_direct<S, TAB, MODE, double, false><<<grid, kThreads, 0, s>>>(
+              (const double*)a.pos, (const double*)a.q, a.n, g, ta, td, n_points, f, f + mesh, f + 2 * mesh,
+              cscale, force, err);
+        else
+          k_gather_direct<S, TAB, MODE, float, false><<<grid, kThreads, 0, s>>>(
+              (const float*)a.pos, (const float*)a.q, a.n, g, ta, td, n_points, f, f + mesh, f + 2 * mesh,
+              cscale, force, err);
+      };
+      if (mode == 0) go(std::integral_constant<int, 0>{});
+      else go(std::integral_constant<int, 1>{});
+      return 0;
+    });
+  });
+  return st ? st : launch_status();
+}
+
+int launch_influence(bool f64, const GreenSpec& gs, void* g_half, double* g_full, cudaStream_t s) {
+  const int64_t total = g_full ? (int64_t)gs.nx * gs.ny * gs.nz : (int64_t)(gs.nx / 2 + 1) * gs.ny * gs.nz;
+  const int grid = grid_for(total);
+  if (f64) k_influence<double><<<grid, kThreads, 0, s>>>(gs, (double*)g_half, g_full);
+  else k_influence<float><<<grid, kThreads, 0, s>>>(gs, (float*)g_half, g_full);
+  return launch_status();
+}
+
+int launch_ik_vectors(const Geom& g, double* ik, cudaStream_t s) {
+  const int n = g.nx > g.ny ? (g.nx > g.nz ? g.nx : g.nz) : (g.ny > g.nz ? g.ny : g.nz);
+  k_ik_vectors<<<(n + 255) / 256, 256, 0, s>>>(g.nx, g.ny, g.nz, g.lx, g.ly, g.lz, ik, ik + g.nx, ik + g.nx + g.ny);
+  return launch_status();
+}
+
+int launch_green(bool f64, int mode, bool fields, const void* rho_hat, const void* green, const Geom& g,
+                 const void* ik, double inv_m, void* out, double* partial, double prefactor, double* energy,
+                 cudaStream_t s) {
+  auto go = [&](auto T_, auto MODE_, auto FIELDS_) {
+    using T = decltype(T_);
+    constexpr int MODE = decltype(MODE_)::value;
+    constexpr bool FL = decltype(FIELDS_)::value;
+    using C = typename Cplx<T>::C;
+    const T* k = (const T*)ik;
+    k_green<T, MODE, FL><<<kGreenBlocks, kThreads, 0, s>>>((const C*)rho_hat, (const T*)green, g.nx, g.ny, g.nz, k,
+                                                           k + g.nx, k + g.nx + g.ny, (T)inv_m, (C*)out, partial);
+  };
+  auto by_mode = [&](auto T_) {
+    if (mode == 0) {
+      if (fields) go(T_, std::integral_constant<int, 0>{}, std::true_type{});
+      else go(T_, std::integral_constant<int, 0>{}, std::false_type{});
+    } else {
+      if (fields) go(T_, std::integral_constant<int, 1>{}, std::true_type{});
+      else go(T_, std::integral_constant<int, 1>{}, std::false_type{});
+    }
+  };
+  if (f64) by_mode(double{});
+  else by_mode(float{});
+  k_energy_final<<<1, 32, 0, s>>>(partial, kGreenBlocks, prefactor, energy);
+  return launch_status();
+}
+
+int launch_convert(bool to_f64, const void* src, void* dst, int64_t n, cudaStream_t s) {
+  if (to_f64) k_convert<float, double><<<grid_for(n), kThreads, 0, s>>>((const float*)src, (double*)dst, n);
+  else k_convert<double, float><<<grid_for(n), kThreads, 0, s>>>((const double*)src, (float*)dst, n);
+  return launch_status();
 }
 
 }  // namespace pppm

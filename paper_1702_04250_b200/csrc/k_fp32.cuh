@@ -1,0 +1,216 @@
+// fp32 (mixed precision) mapping kernels: binning, make_rho, fieldforce (templates;
+// instantiated by k_bin.cu, k_spread32.cu, k_gather32_ik.cu, k_gather32_ad.cu).
+//
+// Layout in HBM: atoms are binned into 8^3-cell bricks with a
+// single pass into fixed-capacity buckets (bucket b holds slots
+// [b*cap, b*cap + min(count_b, cap)); atoms beyond a full bucket go to an
+// overflow list handled by extra CTAs of the same launches).  A bucket slot
+// stores what the mapping kernels need, computed once by particle_map in the
+// binning pass: float4 {tx, ty, tz, q} (offsets, or table bins in table mode),
+// the brick-local cell (9 bits) and the input index.
+//
+// make_rho (gridmap.py:156-213): one CTA per brick.  The brick's atoms are
+// staged in shared memory and counting-sorted by cell (consecutive lanes get
+// neighbouring cells: fewer bank conflicts), each thread scatters its atom's
+// S^3 stencil into a shared tile of (8+S-1)^3 cells, and the tile is added to
+// the mesh with red.global.add.f32.  The shared tile accumulates in int32 fixed
+// point (native ATOMS.ADD; a float atomicAdd on shared memory is a CAS loop on
+// sm_100a) with a per-brick power-of-two scale chosen from sum|q| so no cell can
+// overflow.
+//
+// fieldforce (gridmap.py:236-312): one CTA per brick; the (8+S-1)^3 field tile
+// (3 fields for ik, 1 for ad) is staged in shared memory, atoms are sorted the
+// same way, one thread per atom, forces scattered to the input order.
+#pragma once
+
+#include "pppm_device.cuh"
+
+namespace pppm {
+
+constexpr int kCapMax = 1024;      // bucket capacity limit (4 atoms per thread)
+constexpr int kPer = kCapMax / kThreads;
+constexpr int kOvfBlocks = 64;     // extra CTAs per launch for overflow atoms
+
+template <int S> struct Tile {
+  static constexpr int D = kBrick + S - 1;  // brick + halo
+  static constexpr int N = D * D * D;
+};
+
+// largest 1D weight of the order-S spline (t = 0 for odd S, w = 0 for even S)
+template <int S> struct WMax;
+template <> struct WMax<3> { static constexpr float v = 0.75f; };
+template <> struct WMax<4> { static constexpr float v = 0.6666667f; };
+template <> struct WMax<5> { static constexpr float v = 0.5989584f; };
+template <> struct WMax<6> { static constexpr float v = 0.55f; };
+template <> struct WMax<7> { static constexpr float v = 0.5110244f; };
+
+template <typename K>
+inline void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// ---------------------------------------------------------------------------
+// binning
+
+template <int S, bool TAB, typename TIn>
+__global__ void __launch_bounds__(kThreads) k_bin_fixed(
+    const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
+    int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
+    int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
+    int* __restrict__ err) {
+  const double ihx = 1.0 / g.hx, ihy = 1.0 / g.hy, ihz = 1.0 / g.hz;
+  int* ovf_count = counts + bk.count();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = load_real<TIn, true>(pos, 3 * i + 0);
+    const double y = load_real<TIn, true>(pos, 3 * i + 1);
+    const double z = load_real<TIn, true>(pos, 3 * i + 2);
+    const float q = (float)qv[i];
+    if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
+      atomicOr(err, 1);
+      continue;
+    }
+    int n0, n1, n2;
+    double tx, ty, tz;
+    particle_map_fast<S>(x, g.hx, ihx, n0, tx);
+    particle_map_fast<S>(y, g.hy, ihy, n1, ty);
+    particle_map_fast<S>(z, g.hz, ihz, n2, tz);
+    n0 = n0 >= g.nx ? n0 - g.nx : n0;
+    n1 = n1 >= g.ny ? n1 - g.ny : n1;
+    n2 = n2 >= g.nz ? n2 - g.nz : n2;
+    const int b = ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
+    const int lc = (((n2 % kBrick) * kBrick) + (n1 % kBrick)) * kBrick + (n0 % kBrick);
+    const int slot = atomicAdd(counts + b, 1);
+    if (slot < cap) {
+      const int64_t k = (int64_t)b * cap + slot;
+      float4 r;
+      if (TAB) {
+        r.x = __int_as_float(table_bin(tx, n_points));
+        r.y = __int_as_float(table_bin(ty, n_points));
+        r.z = __int_as_float(table_bin(tz, n_points));
+      } else {
+        r.x = (float)tx;
+        r.y = (float)ty;
+        r.z = (float)tz;
+      }
+      r.w = q;
+      rec[k] = r;
+      rcell[k] = lc;
+      perm[k] = (int)i;
+    } else {
+      // overflow record: same payload, wrapped global node packed 10+10+10 bits (dims <= 1024)
+      const int o = atomicAdd(ovf_count, 1);
+      float4 r;
+      r.x = TAB ? __int_as_float(table_bin(tx, n_points)) : (float)tx;
+      r.y = TAB ? __int_as_float(table_bin(ty, n_points)) : (float)ty;
+      r.z = TAB ? __int_as_float(table_bin(tz, n_points)) : (float)tz;
+      r.w = q;
+      ovf_rec[o] = r;
+      ovf_cell[o] = n0 | (n1 << 10) | (n2 << 20);
+      ovf_perm[o] = (int)i;
+    }
+  }
+}
+
+// weights of one dimension from a stored offset (exact) or table bin
+template <int S, bool TAB, bool DERIV>
+__device__ __forceinline__ void rows_f32(float v, const float* __restrict__ ta, const float* __restrict__ td,
+                                         float (&a)[S], float (&d)[S]) {
+  if (TAB) {
+    const int k = __float_as_int(v);
+    const float* ra = ta + (int64_t)k * kRowPad;
+#pragma unroll
+    for (int j = 0; j < S; ++j) a[j] = __ldg(ra + j);
+    if (DERIV) {
+      const float* rd = td + (int64_t)k * kRowPad;
+#pragma unroll
+      for (int j = 0; j < S; ++j) d[j] = __ldg(rd + j);
+    }
+  } else {
+    bspline_rows<FastF32, S>(v, a, d);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// in-CTA staging: the brick's atoms into shared memory, counting-sorted by
+// brick-local cell.  Returns the atom count; fills s_r / s_c (/ s_p) in
+// sorted order and (optionally) the block sum of |q|.
+
+struct StageSmem {
+  float4* r;
+  int* c;
+  int* p;
+  int* hist;    // kBrick^3 + 1
+  float* red;   // kThreads / 32
+};
+
+template <bool PERM, bool QSUM>
+__device__ __forceinline__ int stage_sorted(const float4* __restrict__ rec, const int* __restrict__ rcell,
+                                            const int* __restrict__ perm, int64_t base, int cnt,
+                                            StageSmem sm, float& qsum) {
+  constexpr int NC = kBrick * kBrick * kBrick;
+  for (int k = threadIdx.x; k < NC; k += blockDim.x) sm.hist[k] = 0;
+  __syncthreads();
+  float4 r[kPer];
+  int c[kPer], rk[kPer], p[kPer];
+  float qa = 0.f;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int j = threadIdx.x + k * kThreads;
+    if (j < cnt) {
+      r[k] = rec[base + j];
+      c[k] = rcell[base + j];
+      if (PERM) p[k] = perm[base + j];
+      rk[k] = atomicAdd(sm.hist + c[k], 1);
+      if (QSUM) qa += fabsf(r[k].w);
+    }
+  }
+  if (QSUM) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qa += __shfl_xor_sync(0xffffffffu, qa, o);
+    if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = qa;
+  }
+  __syncthreads();
+  // exclusive scan of NC = 512 counters, two per thread
+  {
+    const int i0 = 2 * threadIdx.x;
+    const int a0 = sm.hist[i0], a1 = sm.hist[i0 + 1];
+    int x = a0 + a1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __shared__ int wsum[kThreads / 32];
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    int off = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) off += w < wid ? wsum[w] : 0;
+    const int excl = off + x - a0 - a1;
+    sm.hist[i0] = excl;
+    sm.hist[i0 + 1] = excl + a0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int j = threadIdx.x + k * kThreads;
+    if (j < cnt) {
+      const int dst = sm.hist[c[k]] + rk[k];
+      sm.r[dst] = r[k];
+      sm.c[dst] = c[k];
+      if (PERM) sm.p[dst] = p[k];
+    }
+  }
+  if (QSUM) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += sm.red[w];
+    qsum = t;
+  }
+  __syncthreads();
+  return cnt;
+}
+
+}  // namespace pppm

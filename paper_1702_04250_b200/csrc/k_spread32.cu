@@ -1,0 +1,127 @@
+// make_rho, fp32 path (gridmap.py:156-213): one CTA per brick, cell-sorted
+// atoms, S^3 stencils accumulated in a shared (8+S-1)^3 tile (int32 fixed
+// point with a per-brick power-of-two scale, or float CAS atomics), tile added
+// to the mesh with red.global.add.f32.  CTAs past the brick count handle the
+// overflow atoms of full buckets straight into the mesh.
+#include "k_fp32.cuh"
+
+namespace pppm {
+
+template <int S, bool TAB, bool FIX>
+__global__ void __launch_bounds__(kThreads) k_spread_sorted(
+    const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
+    Geom g, Bricks bk, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
+    const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
+  constexpr int D = Tile<S>::D, TN = Tile<S>::N, lo = Stencil<S>::lo;
+  constexpr int NC = kBrick * kBrick * kBrick;
+  const int nb = bk.count();
+  if ((int)blockIdx.x >= nb) {
+    const int novf = counts[nb];
+    for (int k = (blockIdx.x - nb) * blockDim.x + threadIdx.x; k < novf; k += (gridDim.x - nb) * blockDim.x) {
+      const float4 r = ovf_rec[k];
+      const int cc = ovf_cell[k];
+      const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
+      float wx[S], wy[S], wz[S], dd[S];
+      rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+      rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+      rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+      const float q = r.w * inv_vcell;
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        const int iz = wrap_index(n2 - lo + a, g.nz);
+#pragma unroll
+        for (int b = 0; b < S; ++b) {
+          const int iy = wrap_index(n1 - lo + b, g.ny);
+          const float p = q * wz[a] * wy[b];
+          float* row = rho + ((int64_t)iz * g.ny + iy) * g.nx;
+#pragma unroll
+          for (int c = 0; c < S; ++c) atomicAdd(row + wrap_index(n0 - lo + c, g.nx), p * wx[c]);
+        }
+      }
+    }
+    return;
+  }
+  extern __shared__ float4 dyn[];
+  __shared__ int tile[TN];
+  __shared__ int hist[NC + 1];
+  __shared__ float red[kThreads / 32];
+  const int b = blockIdx.x;
+  int cnt = counts[b];
+  cnt = cnt < cap ? cnt : cap;
+  if (cnt == 0) return;
+  for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
+  StageSmem sm{dyn, (int*)(dyn + cap), nullptr, hist, red};
+  float qsum = 0.f;
+  stage_sorted<false, FIX>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm, qsum);
+  float scale = inv_vcell, inv_scale = 1.f;
+  if (FIX) {
+    // |cell| <= sum|q| * wmax^3 < 2^30 / scale  (+1% margin for fp32 rounding)
+    const float bound = qsum * (WMax<S>::v * WMax<S>::v * WMax<S>::v) * 1.01f;
+    int e = 0;
+    frexpf(bound > 0.f ? bound : 1.f, &e);  // bound < 2^e
+    scale = ldexpf(1.f, 30 - e);
+    inv_scale = ldexpf(1.f, e - 30) * inv_vcell;
+  }
+  float* ftile = reinterpret_cast<float*>(tile);
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    const float4 r = sm.r[j];
+    const int cc = sm.c[j];
+    const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+    float wx[S], wy[S], wz[S], dd[S];
+    rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+    rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+    rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+    const float qs = r.w * scale;
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      const float qa = qs * wz[a];
+#pragma unroll
+      for (int bb = 0; bb < S; ++bb) {
+        const float qab = qa * wy[bb];
+        const int row = ((lz + a) * D + (ly + bb)) * D + lx;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+          if (FIX) atomicAdd(tile + row + c, __float2int_rn(qab * wx[c]));
+          else atomicAdd(ftile + row + c, qab * wx[c]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+  const int ox = bx * kBrick - lo, oy = by * kBrick - lo, oz = bz * kBrick - lo;
+  for (int k = threadIdx.x; k < TN; k += blockDim.x) {
+    const int v = tile[k];
+    if (v == 0) continue;
+    const float val = FIX ? (float)v * inv_scale : __int_as_float(v);
+    const int tx_ = k % D, ty_ = (k / D) % D, tz_ = k / (D * D);
+    const int gx = wrap_index(ox + tx_, g.nx), gy = wrap_index(oy + ty_, g.ny), gz = wrap_index(oz + tz_, g.nz);
+    atomicAdd(rho + ((int64_t)gz * g.ny + gy) * g.nx + gx, val);
+  }
+}
+
+int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
+                        int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
+                        const float* ta, float* rho, cudaStream_t s) {
+  const int64_t M = (int64_t)g.nx * g.ny * g.nz;
+  if (cudaMemsetAsync(rho, 0, sizeof(float) * M, s) != cudaSuccess) return launch_status();
+  const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
+  const size_t dyn = (size_t)cap * (sizeof(float4) + sizeof(int));
+  int st = with_order(order, [&](auto S_) -> int {
+    constexpr int S = decltype(S_)::value;
+    return with_bool(tab, [&](auto T_) -> int {
+      constexpr bool TAB = decltype(T_)::value;
+      return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
+        constexpr bool FIX = decltype(F_)::value;
+        auto k = k_spread_sorted<S, TAB, FIX>;
+        allow_smem(k, dyn);
+        k<<<bk.count() + kOvfBlocks, kThreads, dyn, s>>>(rec, rcell, counts, cap, g, bk, ta, inv_vcell, rho, ovf_rec,
+                                                           ovf_cell);
+        return 0;
+      });
+    });
+  });
+  return st ? st : launch_status();
+}
+
+}  // namespace pppm

@@ -10,19 +10,29 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
 #include <utility>
 
 #include "../../include/pppm_b200.h"
-#include "pppm_kernels.cuh"
+#include "pppm_types.h"
 
 using namespace pppm;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
+
+namespace pppm {
+void set_error(int code, const char* msg) {
+  (void)code;
+  g_err = msg ? msg : "";
+}
+}  // namespace pppm
+
+namespace {
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -84,26 +94,6 @@ struct DevBuf {
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
-template <typename F> int with_order(int s, F&& f) {
-  switch (s) {
-    case 3: return f(std::integral_constant<int, 3>{});
-    case 4: return f(std::integral_constant<int, 4>{});
-    case 5: return f(std::integral_constant<int, 5>{});
-    case 6: return f(std::integral_constant<int, 6>{});
-    case 7: return f(std::integral_constant<int, 7>{});
-    default: return fail(PPPM_ERR_CONFIG, "stencil order must be one of (3, 4, 5, 6, 7)");
-  }
-}
-
-template <typename F> int with_bool(bool b, F&& f) {
-  return b ? f(std::true_type{}) : f(std::false_type{});
-}
-
-int grid_for(int64_t n, int threads = kThreads) {
-  int64_t g = (n + threads - 1) / threads;
-  g = std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
-  return (int)g;
-}
 
 }  // namespace
 
@@ -127,7 +117,9 @@ struct pppm_ctx {
 
   DevBuf rho, rho_fix, rho_hat, ework, fields, green, ikc, ik64, tab;
   DevBuf pos_stage, q_stage, out_stage, node_stage;
-  DevBuf counts, start, abin, aslot, rec, perm;
+  DevBuf counts, rec, rcell, perm, ovf_rec, ovf_cell, ovf_perm;
+  int cap = 0;
+  int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SORTED;
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force;
   int64_t n_res = 0;
@@ -198,14 +190,30 @@ static int stage_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, i
   return PPPM_OK;
 }
 
+static AtomsIn atoms_in(const void* pos, const void* q, int64_t n, int dtype) {
+  return AtomsIn{pos, q, n, dtype == PPPM_F32 ? 1 : 0};
+}
+
+// bucket capacity: twice the mean brick occupancy plus slack, in [128, 1024]
+static int bucket_cap(pppm_ctx* c, int64_t n) {
+  const int64_t nb = c->bk.count();
+  int64_t cap = 2 * ((n + nb - 1) / nb) + 64;
+  cap = (cap + 31) / 32 * 32;
+  cap = std::max<int64_t>(128, std::min<int64_t>(cap, 1024));
+  return (int)cap;
+}
+
 static int ensure_bins(pppm_ctx* c, int64_t n) {
   const int nb = c->bk.count();
-  TRY(c->counts.ensure(sizeof(int) * nb));
-  TRY(c->start.ensure(sizeof(int) * (nb + 1)));
-  TRY(c->abin.ensure(sizeof(int) * n));
-  TRY(c->aslot.ensure(sizeof(int) * n));
-  TRY(c->rec.ensure(sizeof(float4) * n));
-  TRY(c->perm.ensure(sizeof(int) * n));
+  c->cap = bucket_cap(c, n);
+  const int64_t slots = (int64_t)nb * c->cap;
+  TRY(c->counts.ensure(sizeof(int) * (nb + 1)));
+  TRY(c->rec.ensure(sizeof(float4) * slots));
+  TRY(c->rcell.ensure(sizeof(int) * slots));
+  TRY(c->perm.ensure(sizeof(int) * slots));
+  TRY(c->ovf_rec.ensure(sizeof(float4) * n));
+  TRY(c->ovf_cell.ensure(sizeof(int) * n));
+  TRY(c->ovf_perm.ensure(sizeof(int) * n));
   return PPPM_OK;
 }
 
@@ -216,87 +224,26 @@ static void rec_event(pppm_ctx* c, int idx, bool timing) {
 // make_rho on device atoms -----------------------------------------------------
 static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
   TRY(ensure_bins(c, n));
-  const int nb = c->bk.count();
-  CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int) * nb, c->stream));
-  const int grid = grid_for(n);
-  int st = with_order(c->order, [&](auto S_) -> int {
-    constexpr int S = decltype(S_)::value;
-    if (dtype == PPPM_F64)
-      k_bin_count<S, double, true><<<grid, kThreads, 0, c->stream>>>(
-          (const double*)pos, n, c->g, c->bk, c->counts.as<int>(), c->abin.as<int>(), c->aslot.as<int>(),
-          c->err.as<int>());
-    else
-      k_bin_count<S, float, true><<<grid, kThreads, 0, c->stream>>>(
-          (const float*)pos, n, c->g, c->bk, c->counts.as<int>(), c->abin.as<int>(), c->aslot.as<int>(),
-          c->err.as<int>());
-    return PPPM_OK;
-  });
-  TRY(st);
-  LAUNCH_CHECK();
-  k_scan_bricks<<<1, 1024, 0, c->stream>>>(c->counts.as<int>(), nb, c->start.as<int>());
-  LAUNCH_CHECK();
-  if (dtype == PPPM_F64)
-    k_bin_scatter<double><<<grid, kThreads, 0, c->stream>>>(
-        (const double*)pos, (const double*)q, n, c->abin.as<int>(), c->aslot.as<int>(), c->start.as<int>(),
-        c->rec.as<float4>(), c->perm.as<int>());
-  else
-    k_bin_scatter<float><<<grid, kThreads, 0, c->stream>>>(
-        (const float*)pos, (const float*)q, n, c->abin.as<int>(), c->aslot.as<int>(), c->start.as<int>(),
-        c->rec.as<float4>(), c->perm.as<int>());
-  LAUNCH_CHECK();
-  c->launches += 3;
+  TRY(launch_bin(c->order, c->n_points > 0, atoms_in(pos, q, n, dtype), c->g, c->bk, c->cap, c->n_points,
+                 c->counts.as<int>(), c->rec.as<float4>(), c->rcell.as<int>(), c->perm.as<int>(),
+                 c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->err.as<int>(), c->stream));
+  c->launches += 1;
   c->binned = true;
   return PPPM_OK;
 }
 
 static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
-  const int grid = grid_for(n);
+  const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
-    double* sc = c->scal.as<double>();
-    unsigned long long* qmax = reinterpret_cast<unsigned long long*>(sc + 4);
-    CU(cudaMemsetAsync(c->rho_fix.p, 0, sizeof(unsigned long long) * c->M, c->stream));
-    CU(cudaMemsetAsync(qmax, 0, sizeof(unsigned long long), c->stream));
-    k_absmax_charge<<<grid, kThreads, 0, c->stream>>>(q, dtype == PPPM_F64 ? 0 : 1, n, qmax);
-    LAUNCH_CHECK();
-    k_fix_scale<<<1, 1, 0, c->stream>>>(qmax, n, sc + 1, sc + 2);
-    LAUNCH_CHECK();
-    int st = with_order(c->order, [&](auto S_) -> int {
-      constexpr int S = decltype(S_)::value;
-      return with_bool(c->n_points > 0, [&](auto T_) -> int {
-        constexpr bool TAB = decltype(T_)::value;
-        if (dtype == PPPM_F64)
-          k_spread_fix64<S, TAB, double, false><<<grid, kThreads, 0, c->stream>>>(
-              (const double*)pos, (const double*)q, n, c->g, c->tab.as<double>(), c->n_points, sc + 1,
-              c->rho_fix.as<unsigned long long>(), c->err.as<int>());
-        else
-          k_spread_fix64<S, TAB, float, false><<<grid, kThreads, 0, c->stream>>>(
-              (const float*)pos, (const float*)q, n, c->g, c->tab.as<double>(), c->n_points, sc + 1,
-              c->rho_fix.as<unsigned long long>(), c->err.as<int>());
-        return PPPM_OK;
-      });
-    });
-    TRY(st);
-    LAUNCH_CHECK();
-    const double vcell = c->g.hx * c->g.hy * c->g.hz;
-    k_fix64_to_real<double><<<grid_for(c->M), kThreads, 0, c->stream>>>(
-        c->rho_fix.as<unsigned long long>(), c->M, sc + 2, vcell, c->rho.as<double>());
-    LAUNCH_CHECK();
+    TRY(launch_spread_fix64(c->order, c->n_points > 0, a, c->g, c->tab.as<double>(), c->n_points,
+                            c->scal.as<double>(), c->rho_fix.as<unsigned long long>(), c->rho.as<double>(),
+                            c->err.as<int>(), c->stream));
     c->launches += 4;
   } else {
-    CU(cudaMemsetAsync(c->rho.p, 0, sizeof(float) * c->M, c->stream));
-    const float inv_vcell = (float)(1.0 / (c->g.hx * c->g.hy * c->g.hz));
-    int st = with_order(c->order, [&](auto S_) -> int {
-      constexpr int S = decltype(S_)::value;
-      return with_bool(c->n_points > 0, [&](auto T_) -> int {
-        constexpr bool TAB = decltype(T_)::value;
-        k_spread_brick<S, TAB><<<c->bk.count(), kThreads, 0, c->stream>>>(
-            c->rec.as<float4>(), c->start.as<int>(), c->g, c->bk, c->tab.as<float>(), c->n_points,
-            inv_vcell, c->rho.as<float>());
-        return PPPM_OK;
-      });
-    });
-    TRY(st);
-    LAUNCH_CHECK();
+    if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
+    TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
+                            c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
+                            c->bk, c->tab.as<float>(), c->rho.as<float>(), c->stream));
     c->launches += 1;
   }
   c->have_rho = true;
@@ -319,30 +266,8 @@ static int run_green(pppm_ctx* c, bool fields) {
   const double vol = c->g.lx * c->g.ly * c->g.lz;
   const double vcell = vol / (double)c->M;
   const double pref = c->cscale * vcell * vcell / (2.0 * vol);
-  auto go = [&](auto T_, auto MODE_, auto FIELDS_) {
-    using T = decltype(T_);
-    constexpr int MODE = decltype(MODE_)::value;
-    constexpr bool FL = decltype(FIELDS_)::value;
-    using C = typename Cplx<T>::C;
-    const T* ik = c->ikc.as<T>();
-    k_green<T, MODE, FL><<<kGreenBlocks, kThreads, 0, c->stream>>>(
-        c->rho_hat.as<C>(), c->green.as<T>(), c->g.nx, c->g.ny, c->g.nz, ik, ik + c->g.nx,
-        ik + c->g.nx + c->g.ny, (T)(1.0 / (double)c->M), c->ework.as<C>(), c->partial.as<double>());
-  };
-  auto by_mode = [&](auto T_) {
-    if (c->mode == PPPM_MODE_IK) {
-      if (fields) go(T_, std::integral_constant<int, 0>{}, std::true_type{});
-      else go(T_, std::integral_constant<int, 0>{}, std::false_type{});
-    } else {
-      if (fields) go(T_, std::integral_constant<int, 1>{}, std::true_type{});
-      else go(T_, std::integral_constant<int, 1>{}, std::false_type{});
-    }
-  };
-  if (c->fp64()) by_mode(double{});
-  else by_mode(float{});
-  LAUNCH_CHECK();
-  k_energy_final<<<1, 32, 0, c->stream>>>(c->partial.as<double>(), kGreenBlocks, pref, sc);
-  LAUNCH_CHECK();
+  TRY(launch_green(c->fp64(), c->mode, fields, c->rho_hat.p, c->green.p, c->g, c->ikc.p, 1.0 / (double)c->M,
+                   c->ework.p, c->partial.as<double>(), pref, sc, c->stream));
   c->launches += 2;
   return PPPM_OK;
 }
@@ -362,60 +287,21 @@ static int run_fft_bwd(pppm_ctx* c) {
 static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, void* out,
                       bool out_f64) {
   if (!c->have_fields) return fail(PPPM_ERR_STATE, "no field grids on the device");
+  const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
-    const double* f = c->fields.as<double>();
-    const int grid = grid_for(n);
-    int st = with_order(c->order, [&](auto S_) -> int {
-      constexpr int S = decltype(S_)::value;
-      return with_bool(c->n_points > 0, [&](auto T_) -> int {
-        constexpr bool TAB = decltype(T_)::value;
-        auto go = [&](auto MODE_) {
-          constexpr int MODE = decltype(MODE_)::value;
-          const double* ta = c->tab.as<double>();
-          const double* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
-          if (dtype == PPPM_F64)
-            k_gather_direct<S, TAB, MODE, double, false><<<grid, kThreads, 0, c->stream>>>(
-                (const double*)pos, (const double*)q, n, c->g, ta, td, c->n_points, f, f + c->M,
-                f + 2 * c->M, c->cscale, (double*)out, c->err.as<int>());
-          else
-            k_gather_direct<S, TAB, MODE, float, false><<<grid, kThreads, 0, c->stream>>>(
-                (const float*)pos, (const float*)q, n, c->g, ta, td, c->n_points, f, f + c->M,
-                f + 2 * c->M, c->cscale, (double*)out, c->err.as<int>());
-        };
-        if (c->mode == PPPM_MODE_IK) go(std::integral_constant<int, 0>{});
-        else go(std::integral_constant<int, 1>{});
-        return PPPM_OK;
-      });
-    });
-    TRY(st);
+    const double* ta = c->tab.as<double>();
+    const double* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
+    TRY(launch_gather_direct(c->order, c->n_points > 0, c->mode, a, c->g, ta, td, c->n_points,
+                             c->fields.as<double>(), c->M, c->cscale, (double*)out, c->err.as<int>(), c->stream));
   } else {
     if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
-    int st = with_order(c->order, [&](auto S_) -> int {
-      constexpr int S = decltype(S_)::value;
-      return with_bool(c->n_points > 0, [&](auto T_) -> int {
-        constexpr bool TAB = decltype(T_)::value;
-        auto go = [&](auto MODE_, auto OUT_) {
-          constexpr int MODE = decltype(MODE_)::value;
-          using TO = decltype(OUT_);
-          const float* ta = c->tab.as<float>();
-          const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
-          k_gather_brick<S, TAB, MODE, TO><<<c->bk.count(), kThreads, 0, c->stream>>>(
-              c->rec.as<float4>(), c->perm.as<int>(), c->start.as<int>(), c->g, c->bk, ta, td,
-              c->n_points, c->fields.as<float>(), c->M, (float)c->cscale, (TO*)out);
-        };
-        if (c->mode == PPPM_MODE_IK) {
-          if (out_f64) go(std::integral_constant<int, 0>{}, double{});
-          else go(std::integral_constant<int, 0>{}, float{});
-        } else {
-          if (out_f64) go(std::integral_constant<int, 1>{}, double{});
-          else go(std::integral_constant<int, 1>{}, float{});
-        }
-        return PPPM_OK;
-      });
-    });
-    TRY(st);
+    const float* ta = c->tab.as<float>();
+    const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
+    TRY(launch_gather_brick(c->gather_variant, c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
+                            c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
+                            c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, ta,
+                            td, c->fields.as<float>(), c->M, (float)c->cscale, out, c->stream));
   }
-  LAUNCH_CHECK();
   c->launches += 1;
   return PPPM_OK;
 }
@@ -425,9 +311,7 @@ static int mesh_to_host(pppm_ctx* c, const void* dev, double* host, int64_t coun
     CU(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
   } else {
     TRY(c->out_stage.ensure(sizeof(double) * count));
-    k_convert<float, double><<<grid_for(count), kThreads, 0, c->stream>>>((const float*)dev,
-                                                                          c->out_stage.as<double>(), count);
-    LAUNCH_CHECK();
+    TRY(launch_convert(true, dev, c->out_stage.p, count, c->stream));
     CU(cudaMemcpyAsync(host, c->out_stage.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
@@ -440,9 +324,7 @@ static int mesh_from_host(pppm_ctx* c, void* dev, const double* host, int64_t co
   } else {
     TRY(c->out_stage.ensure(sizeof(double) * count));
     CU(cudaMemcpyAsync(c->out_stage.p, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
-    k_convert<double, float><<<grid_for(count), kThreads, 0, c->stream>>>(c->out_stage.as<double>(),
-                                                                          (float*)dev, count);
-    LAUNCH_CHECK();
+    TRY(launch_convert(false, c->out_stage.p, dev, count, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   return PPPM_OK;
@@ -492,11 +374,7 @@ int pppm_weight_rows(int device, int order, const double* t, int64_t n, double* 
   CU(cudaMalloc(&dt, sizeof(double) * n));
   CU(cudaMalloc(&da, sizeof(double) * n * kRowPad * 2));
   CU(cudaMemcpy(dt, t, sizeof(double) * n, cudaMemcpyHostToDevice));
-  int st = with_order(order, [&](auto S_) -> int {
-    constexpr int S = decltype(S_)::value;
-    k_weight_rows<S><<<(int)((n + 255) / 256), 256>>>(dt, n, da, da + n * kRowPad);
-    return PPPM_OK;
-  });
+  int st = launch_weight_rows(order, dt, n, da, da + n * kRowPad, 0);
   if (st == PPPM_OK) {
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpy(assign, da, sizeof(double) * n * kRowPad, cudaMemcpyDeviceToHost);
@@ -513,11 +391,7 @@ int pppm_table_rows(int device, int order, int n_points, double* assign, double*
   CU(cudaSetDevice(device));
   double* da = nullptr;
   CU(cudaMalloc(&da, sizeof(double) * n_points * kRowPad * 2));
-  int st = with_order(order, [&](auto S_) -> int {
-    constexpr int S = decltype(S_)::value;
-    k_table_rows<S><<<(n_points + 255) / 256, 256>>>(n_points, da, da + (int64_t)n_points * kRowPad);
-    return PPPM_OK;
-  });
+  int st = launch_table_rows(order, n_points, da, da + (int64_t)n_points * kRowPad, 0);
   if (st == PPPM_OK) {
     cudaError_t e = cudaGetLastError();
     const size_t b = sizeof(double) * n_points * kRowPad;
@@ -590,16 +464,25 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
     return cleanup(fail(PPPM_ERR_CUDA, "memset failed"));
   // ik vectors in fp64, then the compute-type copy
   double* ik = c->ik64.as<double>();
-  k_ik_vectors<<<(std::max(nx, std::max(ny, nz)) + 255) / 256, 256, 0, c->stream>>>(
-      nx, ny, nz, lx, ly, lz, ik, ik + nx, ik + nx + ny);
+  launch_ik_vectors(c->g, ik, c->stream);
   if (c->fp64()) {
     cudaMemcpyAsync(c->ikc.p, ik, 8 * (nx + ny + nz), cudaMemcpyDeviceToDevice, c->stream);
   } else {
-    k_convert<double, float><<<1, 256, 0, c->stream>>>(ik, c->ikc.as<float>(), nx + ny + nz);
+    launch_convert(false, ik, c->ikc.p, nx + ny + nz, c->stream);
   }
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess)
     return cleanup(fail(PPPM_ERR_CUDA, "context setup kernels failed"));
+  if (const char* v = getenv("PPPM_B200_SPREAD")) c->spread_variant = atoi(v);
+  if (const char* v = getenv("PPPM_B200_GATHER")) c->gather_variant = atoi(v);
   *out = c;
+  return PPPM_OK;
+}
+
+int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
+  if (!c) return fail(PPPM_ERR_VALUE, "null context");
+  if (kernel == 0 && (variant == SPREAD_CAS_F32 || variant == SPREAD_FIX32)) c->spread_variant = variant;
+  else if (kernel == 1 && (variant == GATHER_PLAIN || variant == GATHER_SORTED)) c->gather_variant = variant;
+  else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
   return PPPM_OK;
 }
 
@@ -613,7 +496,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   }
   DevBuf* bufs[] = {&c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
-                    &c->counts, &c->start, &c->abin, &c->aslot, &c->rec, &c->perm, &c->partial,
+                    &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
                     &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)
@@ -641,9 +524,7 @@ int pppm_ctx_set_table(pppm_ctx* c, int n_points, const double* assign, const do
     TRY(c->out_stage.ensure(8 * cnt * 2));
     CU(cudaMemcpyAsync(c->out_stage.p, assign, 8 * cnt, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(c->out_stage.as<double>() + cnt, deriv, 8 * cnt, cudaMemcpyHostToDevice, c->stream));
-    k_convert<double, float><<<grid_for(2 * cnt), kThreads, 0, c->stream>>>(c->out_stage.as<double>(),
-                                                                            c->tab.as<float>(), 2 * cnt);
-    LAUNCH_CHECK();
+    TRY(launch_convert(false, c->out_stage.p, c->tab.p, 2 * cnt, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   c->n_points = n_points;
@@ -660,19 +541,12 @@ int pppm_ctx_build_table(pppm_ctx* c, int n_points) {
   const int64_t cnt = (int64_t)n_points * kRowPad;
   TRY(c->out_stage.ensure(8 * cnt * 2));
   double* rows = c->out_stage.as<double>();
-  int st = with_order(c->order, [&](auto S_) -> int {
-    constexpr int S = decltype(S_)::value;
-    k_table_rows<S><<<(n_points + 255) / 256, 256, 0, c->stream>>>(n_points, rows, rows + cnt);
-    return PPPM_OK;
-  });
-  TRY(st);
-  LAUNCH_CHECK();
+  TRY(launch_table_rows(c->order, n_points, rows, rows + cnt, c->stream));
   TRY(c->tab.ensure(c->real_size() * cnt * 2));
   if (c->fp64())
     CU(cudaMemcpyAsync(c->tab.p, rows, 16 * cnt, cudaMemcpyDeviceToDevice, c->stream));
   else
-    k_convert<double, float><<<grid_for(2 * cnt), kThreads, 0, c->stream>>>(rows, c->tab.as<float>(), 2 * cnt);
-  LAUNCH_CHECK();
+    TRY(launch_convert(false, rows, c->tab.p, 2 * cnt, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   c->n_points = n_points;
   return PPPM_OK;
@@ -684,12 +558,7 @@ int pppm_ctx_build_influence(pppm_ctx* c, int kind, double deconv_floor) {
     return fail(PPPM_ERR_CONFIG, "unknown influence variant");
   GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, deconv_floor,
               kind == PPPM_INFLUENCE_OPTIMAL};
-  const int grid = grid_for(c->half);
-  if (c->fp64())
-    k_influence<double><<<grid, kThreads, 0, c->stream>>>(s, c->green.as<double>(), nullptr);
-  else
-    k_influence<float><<<grid, kThreads, 0, c->stream>>>(s, c->green.as<float>(), nullptr);
-  LAUNCH_CHECK();
+  TRY(launch_influence(c->fp64(), s, c->green.p, nullptr, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   c->have_green = true;
   c->green_kind = kind;
@@ -706,9 +575,7 @@ int pppm_ctx_set_influence(pppm_ctx* c, const double* g_full) {
   if (c->fp64())
     CU(cudaMemcpyAsync(c->green.p, c->out_stage.p, 8 * c->half, cudaMemcpyDeviceToDevice, c->stream));
   else {
-    k_convert<double, float><<<grid_for(c->half), kThreads, 0, c->stream>>>(c->out_stage.as<double>(),
-                                                                            c->green.as<float>(), c->half);
-    LAUNCH_CHECK();
+    TRY(launch_convert(false, c->out_stage.p, c->green.p, c->half, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   c->have_green = true;
@@ -723,8 +590,7 @@ int pppm_ctx_get_influence(pppm_ctx* c, double* g_full) {
   GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, c->green_floor,
               c->green_kind == PPPM_INFLUENCE_OPTIMAL};
   TRY(c->out_stage.ensure(8 * c->M));
-  k_influence<double><<<grid_for(c->M), kThreads, 0, c->stream>>>(s, nullptr, c->out_stage.as<double>());
-  LAUNCH_CHECK();
+  TRY(launch_influence(true, s, nullptr, c->out_stage.as<double>(), c->stream));
   CU(cudaMemcpyAsync(g_full, c->out_stage.p, 8 * c->M, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return PPPM_OK;
@@ -745,20 +611,8 @@ int pppm_particle_map(pppm_ctx* c, const void* pos, int64_t n, int dtype, int me
   TRY(stage_atoms(c, pos, nullptr, n, dtype, mem, &dpos, &dq));
   TRY(c->node_stage.ensure(sizeof(int32_t) * 3 * n));
   const bool r32 = !c->fp64();
-  int st = with_order(c->order, [&](auto S_) -> int {
-    constexpr int S = decltype(S_)::value;
-    const int grid = grid_for(n);
-    int32_t* nd = c->node_stage.as<int32_t>();
-    if (dtype == PPPM_F64) {
-      if (r32) k_particle_map<S, double, true><<<grid, kThreads, 0, c->stream>>>((const double*)dpos, n, c->g, nd, c->err.as<int>());
-      else k_particle_map<S, double, false><<<grid, kThreads, 0, c->stream>>>((const double*)dpos, n, c->g, nd, c->err.as<int>());
-    } else {
-      k_particle_map<S, float, false><<<grid, kThreads, 0, c->stream>>>((const float*)dpos, n, c->g, nd, c->err.as<int>());
-    }
-    return PPPM_OK;
-  });
-  TRY(st);
-  LAUNCH_CHECK();
+  TRY(launch_particle_map(c->order, r32, atoms_in(dpos, nullptr, n, dtype), c->g, c->node_stage.as<int32_t>(),
+                          c->err.as<int>(), c->stream));
   CU(cudaMemcpyAsync(nodes, c->node_stage.p, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
   return check_err_flag(c);
 }

@@ -12,9 +12,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
+#include "pppm_types.h"
+
 namespace pppm {
 
-constexpr int kRowPad = 8;           // stencil.py:23
 constexpr int kMaxOrder = 7;
 constexpr double kHalfBelow = 0.49999999999999994;  // nextafter(0.5, 0)
 
@@ -138,6 +141,92 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// ---------------------------------------------------------------------------
+// input loads: positions are AoS (N, 3), charges (N,), fp64 or fp32.  In mixed
+// precision fp64 inputs are rounded to fp32 first (the oracle is fed the same
+// rounded values).
+
+template <typename TIn, bool R32>
+__device__ __forceinline__ double load_real(const TIn* p, int64_t k) {
+  double v = (double)p[k];
+  if (R32) v = (double)(float)v;
+  return v;
+}
+
+__device__ __forceinline__ bool outside(double x, double len) { return !(x >= 0.0 && x < len); }
+
+// particle_map with a multiply instead of the division, bit-exact anyway:
+// |x * (1/h) - x / h| is a few ulp of u, so floor() can only differ when
+// u (+1/2) lies within 1e-6 of an integer; those rare atoms take the exact
+// division.  Returns the node and the offset t (from the approximate u,
+// within 1e-15 of the exact t; the fp32 kernels round it to fp32 anyway).
+template <int S>
+__device__ __forceinline__ void particle_map_fast(double x, double h, double inv_h, int& node, double& t) {
+  double u = x * inv_h;
+  const double v = (S & 1) ? u + 0.5 : u;
+  const double fl = floor(v);
+  const double fr = v - fl;
+  if (fr < 1e-6 || fr > 1.0 - 1e-6) {
+    particle_map_1d<S>(x, h, node, t);
+    return;
+  }
+  node = (int)fl;
+  t = (S & 1) ? u - fl : (u - fl) - 0.5;
+  t = fmin(fmax(t, -0.5), kHalfBelow);
+}
+
+// per-dimension weights for one coordinate, exact recurrence or table lookup
+template <typename P, int S, bool TAB, bool DERIV>
+__device__ __forceinline__ void weights_1d(double t, const typename P::T* __restrict__ ta,
+                                           const typename P::T* __restrict__ td, int n_points,
+                                           typename P::T (&a)[S], typename P::T (&d)[S]) {
+  using T = typename P::T;
+  if (TAB) {
+    const int k = table_bin(t, n_points);
+    const T* ra = ta + (int64_t)k * kRowPad;
+#pragma unroll
+    for (int j = 0; j < S; ++j) a[j] = ra[j];
+    if (DERIV) {
+      const T* rd = td + (int64_t)k * kRowPad;
+#pragma unroll
+      for (int j = 0; j < S; ++j) d[j] = rd[j];
+    }
+  } else {
+    bspline_rows<P, S>((T)t, a, d);
+  }
+}
+
+template <typename F> int with_order(int s, F&& f) {
+  switch (s) {
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    default: set_error(1, "stencil order must be one of (3, 4, 5, 6, 7)"); return 1;
+  }
+}
+
+template <typename F> int with_bool(bool b, F&& f) {
+  return b ? f(std::true_type{}) : f(std::false_type{});
+}
+
+inline int grid_for(int64_t n, int threads = kThreads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+inline int launch_status() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    set_error(4, cudaGetErrorString(e));
+    return 4;
+  }
+  return 0;
 }
 
 }  // namespace pppm

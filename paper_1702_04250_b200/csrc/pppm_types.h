@@ -1,0 +1,73 @@
+// POD types and launcher declarations shared by the host context
+// (pppm_capi.cu) and the kernel translation units (k_*.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pppm {
+
+constexpr int kBrick = 8;          // owned cells per brick edge (fp32 path)
+constexpr int kGreenBlocks = 592;  // 4 x 148 SMs: fixed grid => deterministic energy order
+constexpr int kThreads = 256;
+constexpr int kRowPad = 8;         // stencil.py:23
+
+struct Geom {
+  int nx, ny, nz;
+  double hx, hy, hz;
+  double lx, ly, lz;
+};
+
+struct Bricks {
+  int nbx, nby, nbz;
+  __host__ __device__ __forceinline__ int count() const { return nbx * nby * nbz; }
+};
+
+struct GreenSpec {
+  int nx, ny, nz, order;
+  double lx, ly, lz, alpha, floor;
+  int optimal;
+};
+
+// device atoms as handed to the context: AoS (N, 3) positions, (N,) charges
+struct AtomsIn {
+  const void* pos;
+  const void* q;
+  int64_t n;
+  int f32;  // 0: fp64 elements, 1: fp32 elements
+};
+
+// kernel variants (selectable per context for A/B measurement)
+enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1 };
+enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1 };
+
+// launchers: return 0, or a pppm_status code with the message set via set_error()
+void set_error(int code, const char* msg);
+int launch_particle_map(int order, bool r32, const AtomsIn& a, const Geom& g, int32_t* nodes, int* err,
+                        cudaStream_t s);
+int launch_table_rows(int order, int n_points, double* assign, double* deriv, cudaStream_t s);
+int launch_weight_rows(int order, const double* t, int64_t n, double* assign, double* deriv, cudaStream_t s);
+int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, const double* ta, int n_points,
+                        double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s);
+int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
+               int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
+               int* err, cudaStream_t s);
+int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
+                        int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
+                        const float* ta, float* rho, cudaStream_t s);
+int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
+                         const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
+                         double* force, int* err, cudaStream_t s);
+int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64, const float4* rec,
+                        const int* rcell, const int* perm, const int* counts, int cap, const float4* ovf_rec,
+                        const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const float* ta,
+                        const float* td, const float* fields, int64_t mesh, float cscale, void* force,
+                        cudaStream_t s);
+int launch_influence(bool f64, const GreenSpec& gs, void* g_half, double* g_full, cudaStream_t s);
+int launch_ik_vectors(const Geom& g, double* ik, cudaStream_t s);
+int launch_green(bool f64, int mode, bool fields, const void* rho_hat, const void* green, const Geom& g,
+                 const void* ik, double inv_m, void* out, double* partial, double prefactor, double* energy,
+                 cudaStream_t s);
+int launch_convert(bool to_f64, const void* src, void* dst, int64_t n, cudaStream_t s);
+
+}  // namespace pppm
