@@ -53,12 +53,11 @@ inline void allow_smem(K kernel, size_t bytes) {
 // binning
 
 template <int S, bool TAB, typename TIn>
-__global__ void __launch_bounds__(kThreads) k_bin_fixed(
+__global__ void __launch_bounds__(kThreads, 8) k_bin_fixed(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
     int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
     int* __restrict__ err) {
-  const double ihx = 1.0 / g.hx, ihy = 1.0 / g.hy, ihz = 1.0 / g.hz;
   int* ovf_count = counts + bk.count();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -72,9 +71,9 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
     }
     int n0, n1, n2;
     double tx, ty, tz;
-    particle_map_fast<S>(x, g.hx, ihx, n0, tx);
-    particle_map_fast<S>(y, g.hy, ihy, n1, ty);
-    particle_map_fast<S>(z, g.hz, ihz, n2, tz);
+    particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
+    particle_map_fast<S>(y, g.hy, g.ihy, n1, ty);
+    particle_map_fast<S>(z, g.hz, g.ihz, n2, tz);
     n0 = n0 >= g.nx ? n0 - g.nx : n0;
     n1 = n1 >= g.ny ? n1 - g.ny : n1;
     n2 = n2 >= g.nz ? n2 - g.nz : n2;
@@ -141,19 +140,19 @@ struct StageSmem {
   int* c;
   int* p;
   int* hist;    // kBrick^3 + 1
-  float* red;   // kThreads / 32
+  float* red;   // 2 * kThreads / 32
 };
 
 template <bool PERM, bool QSUM>
 __device__ __forceinline__ int stage_sorted(const float4* __restrict__ rec, const int* __restrict__ rcell,
                                             const int* __restrict__ perm, int64_t base, int cnt,
-                                            StageSmem sm, float& qsum) {
+                                            StageSmem sm, float& qsum, float& qmax) {
   constexpr int NC = kBrick * kBrick * kBrick;
   for (int k = threadIdx.x; k < NC; k += blockDim.x) sm.hist[k] = 0;
   __syncthreads();
   float4 r[kPer];
   int c[kPer], rk[kPer], p[kPer];
-  float qa = 0.f;
+  float qa = 0.f, qm = 0.f;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int j = threadIdx.x + k * kThreads;
@@ -162,13 +161,22 @@ __device__ __forceinline__ int stage_sorted(const float4* __restrict__ rec, cons
       c[k] = rcell[base + j];
       if (PERM) p[k] = perm[base + j];
       rk[k] = atomicAdd(sm.hist + c[k], 1);
-      if (QSUM) qa += fabsf(r[k].w);
+      if (QSUM) {
+        qa += fabsf(r[k].w);
+        qm = fmaxf(qm, fabsf(r[k].w));
+      }
     }
   }
   if (QSUM) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) qa += __shfl_xor_sync(0xffffffffu, qa, o);
-    if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = qa;
+    for (int o = 16; o > 0; o >>= 1) {
+      qa += __shfl_xor_sync(0xffffffffu, qa, o);
+      qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sm.red[threadIdx.x >> 5] = qa;
+      sm.red[kThreads / 32 + (threadIdx.x >> 5)] = qm;
+    }
   }
   __syncthreads();
   // exclusive scan of NC = 512 counters, two per thread
@@ -204,10 +212,14 @@ __device__ __forceinline__ int stage_sorted(const float4* __restrict__ rec, cons
     }
   }
   if (QSUM) {
-    float t = 0.f;
+    float t = 0.f, m = 0.f;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) t += sm.red[w];
+    for (int w = 0; w < kThreads / 32; ++w) {
+      t += sm.red[w];
+      m = fmaxf(m, sm.red[kThreads / 32 + w]);
+    }
     qsum = t;
+    qmax = m;
   }
   __syncthreads();
   return cnt;

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_sorted(
   constexpr int NC = kBrick * kBrick * kBrick;
   constexpr int F = MODE == 0 ? 3 : 1;
   const int nb = bk.count();
-  const float ihx = (float)(1.0 / g.hx), ihy = (float)(1.0 / g.hy), ihz = (float)(1.0 / g.hz);
+  const float ihx = (float)g.ihx, ihy = (float)g.ihy, ihz = (float)g.ihz;
   if ((int)blockIdx.x >= nb) {
     const int novf = counts[nb];
     for (int k = (blockIdx.x - nb) * blockDim.x + threadIdx.x; k < novf; k += (gridDim.x - nb) * blockDim.x) {
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_sorted(
   extern __shared__ float4 dyn[];
   __shared__ float tile[F * TN];
   __shared__ int hist[NC + 1];
-  __shared__ float red[kThreads / 32];
+  __shared__ float red[2 * kThreads / 32];
   const int b = blockIdx.x;
   int cnt = counts[b];
   cnt = cnt < cap ? cnt : cap;
@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(kThreads) k_gather_sorted(
   }
   const int64_t base = (int64_t)b * cap;
   StageSmem sm{dyn, (int*)(dyn + cap), (int*)(dyn + cap) + cap, hist, red};
-  float unused = 0.f;
-  if (sort) stage_sorted<true, false>(rec, rcell, perm, base, cnt, sm, unused);
+  float unused = 0.f, unused2 = 0.f;
+  if (sort) stage_sorted<true, false>(rec, rcell, perm, base, cnt, sm, unused, unused2);
   else __syncthreads();
   for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
     const float4 r = sort ? sm.r[j] : rec[base + j];

@@ -11,7 +11,7 @@ template <int S, bool TAB, bool FIX>
 __global__ void __launch_bounds__(kThreads) k_spread_sorted(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
-    const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
+    const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell, bool sort) {
   constexpr int D = Tile<S>::D, TN = Tile<S>::N, lo = Stencil<S>::lo;
   constexpr int NC = kBrick * kBrick * kBrick;
   const int nb = bk.count();
@@ -44,28 +44,61 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
   extern __shared__ float4 dyn[];
   __shared__ int tile[TN];
   __shared__ int hist[NC + 1];
-  __shared__ float red[kThreads / 32];
+  __shared__ float red[2 * kThreads / 32];
   const int b = blockIdx.x;
   int cnt = counts[b];
   cnt = cnt < cap ? cnt : cap;
   if (cnt == 0) return;
   for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
+  const int64_t base = (int64_t)b * cap;
   StageSmem sm{dyn, (int*)(dyn + cap), nullptr, hist, red};
-  float qsum = 0.f;
-  stage_sorted<false, FIX>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm, qsum);
+  float qsum = 0.f, qmax = 0.f;
+  if (sort) {
+    stage_sorted<false, FIX>(rec, rcell, nullptr, base, cnt, sm, qsum, qmax);
+  } else if (FIX) {
+    float qa = 0.f, qm = 0.f;
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const float q = fabsf(rec[base + j].w);
+      qa += q;
+      qm = fmaxf(qm, q);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      qa += __shfl_xor_sync(0xffffffffu, qa, o);
+      qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5] = qa;
+      red[kThreads / 32 + (threadIdx.x >> 5)] = qm;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      qsum += red[w];
+      qmax = fmaxf(qmax, red[kThreads / 32 + w]);
+    }
+  } else {
+    __syncthreads();
+  }
   float scale = inv_vcell, inv_scale = 1.f;
   if (FIX) {
-    // |cell| <= sum|q| * wmax^3 < 2^30 / scale  (+1% margin for fp32 rounding)
-    const float bound = qsum * (WMax<S>::v * WMax<S>::v * WMax<S>::v) * 1.01f;
-    int e = 0;
-    frexpf(bound > 0.f ? bound : 1.f, &e);  // bound < 2^e
-    scale = ldexpf(1.f, 30 - e);
-    inv_scale = ldexpf(1.f, e - 30) * inv_vcell;
+    // int32 fixed point with a power-of-two scale: every cell sum stays below
+    // 2^30 (|cell| <= sum|q| wmax^3) and every single contribution below 2^22,
+    // so the float->int conversion is one FFMA with the 1.5*2^23 magic number
+    // (round to nearest) instead of an F2I on the quarter-rate conversion pipe.
+    const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
+    int e_sum = 0, e_one = 0;
+    frexpf(qsum > 0.f ? qsum * w3 : 1.f, &e_sum);  // qsum w3 < 2^e_sum
+    frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);
+    const int s = min(30 - e_sum, 22 - e_one);
+    scale = ldexpf(1.f, s);
+    inv_scale = ldexpf(1.f, -s) * inv_vcell;
   }
   float* ftile = reinterpret_cast<float*>(tile);
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-    const float4 r = sm.r[j];
-    const int cc = sm.c[j];
+    const float4 r = sort ? sm.r[j] : rec[base + j];
+    const int cc = sort ? sm.c[j] : rcell[base + j];
     const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
     float wx[S], wy[S], wz[S], dd[S];
     rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
@@ -81,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
         const int row = ((lz + a) * D + (ly + bb)) * D + lx;
 #pragma unroll
         for (int c = 0; c < S; ++c) {
-          if (FIX) atomicAdd(tile + row + c, __float2int_rn(qab * wx[c]));
+          if (FIX) atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
           else atomicAdd(ftile + row + c, qab * wx[c]);
         }
       }
@@ -100,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
   }
 }
 
-int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
+int launch_spread_brick(int variant, bool sort, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
                         const float* ta, float* rho, cudaStream_t s) {
   const int64_t M = (int64_t)g.nx * g.ny * g.nz;
@@ -116,7 +149,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         auto k = k_spread_sorted<S, TAB, FIX>;
         allow_smem(k, dyn);
         k<<<bk.count() + kOvfBlocks, kThreads, dyn, s>>>(rec, rcell, counts, cap, g, bk, ta, inv_vcell, rho, ovf_rec,
-                                                           ovf_cell);
+                                                           ovf_cell, sort);
         return 0;
       });
     });

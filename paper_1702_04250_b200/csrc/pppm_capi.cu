@@ -241,7 +241,7 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     c->launches += 4;
   } else {
     if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
-    TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
+    TRY(launch_spread_brick(c->spread_variant & 1, (c->spread_variant & 2) != 0, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
                             c->bk, c->tab.as<float>(), c->rho.as<float>(), c->stream));
     c->launches += 1;
@@ -423,6 +423,7 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
   c->g.nx = nx; c->g.ny = ny; c->g.nz = nz;
   c->g.lx = lx; c->g.ly = ly; c->g.lz = lz;
   c->g.hx = lx / nx; c->g.hy = ly / ny; c->g.hz = lz / nz;   // gridmap.py:83
+  c->g.ihx = 1.0 / c->g.hx; c->g.ihy = 1.0 / c->g.hy; c->g.ihz = 1.0 / c->g.hz;
   c->bk.nbx = (nx + kBrick - 1) / kBrick;
   c->bk.nby = (ny + kBrick - 1) / kBrick;
   c->bk.nbz = (nz + kBrick - 1) / kBrick;
@@ -480,7 +481,7 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
 
 int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
-  if (kernel == 0 && (variant == SPREAD_CAS_F32 || variant == SPREAD_FIX32)) c->spread_variant = variant;
+  if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
   else if (kernel == 1 && (variant == GATHER_PLAIN || variant == GATHER_SORTED)) c->gather_variant = variant;
   else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
   return PPPM_OK;

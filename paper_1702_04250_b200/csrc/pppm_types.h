@@ -16,6 +16,7 @@ struct Geom {
   int nx, ny, nz;
   double hx, hy, hz;
   double lx, ly, lz;
+  double ihx, ihy, ihz;  // 1/h, host-computed (particle_map_fast)
 };
 
 struct Bricks {
@@ -38,7 +39,7 @@ struct AtomsIn {
 };
 
 // kernel variants (selectable per context for A/B measurement)
-enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1 };
+enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1 };  // + 2: same, cell-sorted in shared memory
 enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1 };
 
 // launchers: return 0, or a pppm_status code with the message set via set_error()
@@ -52,7 +53,7 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, cudaStream_t s);
-int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
+int launch_spread_brick(int variant, bool sort, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
                         const float* ta, float* rho, cudaStream_t s);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
