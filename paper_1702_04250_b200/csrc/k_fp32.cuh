@@ -52,62 +52,91 @@ inline void allow_smem(K kernel, size_t bytes) {
 // ---------------------------------------------------------------------------
 // binning
 
+constexpr int kBinUnroll = 4;  // atoms per thread in flight (latency of the slot atomics)
+
+// One pass: particle_map (bit-exact nodes) -> brick, slot = atomicAdd(count),
+// record into the bucket (or the overflow list).  Also the global max |q|
+// (as float bits, counts[nb + 1]) for the make_rho fixed-point scale.
 template <int S, bool TAB, typename TIn>
-__global__ void __launch_bounds__(kThreads, 8) k_bin_fixed(
+__global__ void __launch_bounds__(kThreads) k_bin_fixed(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
     int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
     int* __restrict__ err) {
-  int* ovf_count = counts + bk.count();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_real<TIn, true>(pos, 3 * i + 0);
-    const double y = load_real<TIn, true>(pos, 3 * i + 1);
-    const double z = load_real<TIn, true>(pos, 3 * i + 2);
-    const float q = (float)qv[i];
-    if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
-      atomicOr(err, 1);
-      continue;
-    }
-    int n0, n1, n2;
-    double tx, ty, tz;
-    particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
-    particle_map_fast<S>(y, g.hy, g.ihy, n1, ty);
-    particle_map_fast<S>(z, g.hz, g.ihz, n2, tz);
-    n0 = n0 >= g.nx ? n0 - g.nx : n0;
-    n1 = n1 >= g.ny ? n1 - g.ny : n1;
-    n2 = n2 >= g.nz ? n2 - g.nz : n2;
-    const int b = ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
-    const int lc = (((n2 % kBrick) * kBrick) + (n1 % kBrick)) * kBrick + (n0 % kBrick);
-    const int slot = atomicAdd(counts + b, 1);
-    if (slot < cap) {
-      const int64_t k = (int64_t)b * cap + slot;
-      float4 r;
-      if (TAB) {
-        r.x = __int_as_float(table_bin(tx, n_points));
-        r.y = __int_as_float(table_bin(ty, n_points));
-        r.z = __int_as_float(table_bin(tz, n_points));
-      } else {
-        r.x = (float)tx;
-        r.y = (float)ty;
-        r.z = (float)tz;
+  const int nb = bk.count();
+  int* ovf_count = counts + nb;
+  float qmax = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += stride * kBinUnroll) {
+    float4 r[kBinUnroll];
+    int b[kBinUnroll], lc[kBinUnroll], slot[kBinUnroll], pk[kBinUnroll];
+#pragma unroll
+    for (int u = 0; u < kBinUnroll; ++u) {
+      const int64_t i = i0 + u * stride;
+      b[u] = -1;
+      if (i >= n) continue;
+      const double x = load_real<TIn, true>(pos, 3 * i + 0);
+      const double y = load_real<TIn, true>(pos, 3 * i + 1);
+      const double z = load_real<TIn, true>(pos, 3 * i + 2);
+      const float q = (float)qv[i];
+      if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
+        atomicOr(err, 1);
+        continue;
       }
-      r.w = q;
-      rec[k] = r;
-      rcell[k] = lc;
-      perm[k] = (int)i;
-    } else {
-      // overflow record: same payload, wrapped global node packed 10+10+10 bits (dims <= 1024)
-      const int o = atomicAdd(ovf_count, 1);
-      float4 r;
-      r.x = TAB ? __int_as_float(table_bin(tx, n_points)) : (float)tx;
-      r.y = TAB ? __int_as_float(table_bin(ty, n_points)) : (float)ty;
-      r.z = TAB ? __int_as_float(table_bin(tz, n_points)) : (float)tz;
-      r.w = q;
-      ovf_rec[o] = r;
-      ovf_cell[o] = n0 | (n1 << 10) | (n2 << 20);
-      ovf_perm[o] = (int)i;
+      qmax = fmaxf(qmax, fabsf(q));
+      int n0, n1, n2;
+      double tx, ty, tz;
+      particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
+      particle_map_fast<S>(y, g.hy, g.ihy, n1, ty);
+      particle_map_fast<S>(z, g.hz, g.ihz, n2, tz);
+      n0 = n0 >= g.nx ? n0 - g.nx : n0;
+      n1 = n1 >= g.ny ? n1 - g.ny : n1;
+      n2 = n2 >= g.nz ? n2 - g.nz : n2;
+      b[u] = ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
+      lc[u] = (((n2 % kBrick) * kBrick) + (n1 % kBrick)) * kBrick + (n0 % kBrick);
+      pk[u] = n0 | (n1 << 10) | (n2 << 20);
+      if (TAB) {
+        r[u].x = __int_as_float(table_bin(tx, n_points));
+        r[u].y = __int_as_float(table_bin(ty, n_points));
+        r[u].z = __int_as_float(table_bin(tz, n_points));
+      } else {
+        r[u].x = (float)tx;
+        r[u].y = (float)ty;
+        r[u].z = (float)tz;
+      }
+      r[u].w = q;
     }
+#pragma unroll
+    for (int u = 0; u < kBinUnroll; ++u)
+      if (b[u] >= 0) slot[u] = atomicAdd(counts + b[u], 1);
+#pragma unroll
+    for (int u = 0; u < kBinUnroll; ++u) {
+      if (b[u] < 0) continue;
+      const int64_t i = i0 + u * stride;
+      if (slot[u] < cap) {
+        const int64_t k = (int64_t)b[u] * cap + slot[u];
+        rec[k] = r[u];
+        rcell[k] = lc[u];
+        perm[k] = (int)i;
+      } else {
+        // overflow record: same payload, wrapped global node packed 10+10+10 bits (dims <= 1024)
+        const int o = atomicAdd(ovf_count, 1);
+        ovf_rec[o] = r[u];
+        ovf_cell[o] = pk[u];
+        ovf_perm[o] = (int)i;
+      }
+    }
+  }
+  // block max |q| -> one atomicMax per block (non-negative float bits order as ints)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) qmax = fmaxf(qmax, __shfl_xor_sync(0xffffffffu, qmax, o));
+  __shared__ float wmax[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = qmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) m = fmaxf(m, wmax[w]);
+    atomicMax(counts + nb + 1, __float_as_int(m));
   }
 }
 

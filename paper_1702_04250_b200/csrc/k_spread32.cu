@@ -7,12 +7,28 @@
 
 namespace pppm {
 
+// shared tile: x spans [bx*8 - 4, bx*8 + 12) (16 cells, quad-aligned so the
+// flush can use red.global.add.v4.f32), row pitch 20 words (16B aligned rows,
+// 8 consecutive rows hit distinct bank quads); y, z span brick + halo.
+template <int S> struct STile {
+  static constexpr int D = kBrick + S - 1;
+  static constexpr int TX = 20;
+  static constexpr int N = D * D * TX;
+  static constexpr int XOFF = 4 - Stencil<S>::lo;  // tile x of the lowest stencil node of local cell 0
+};
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 template <int S, bool TAB, bool FIX>
 __global__ void __launch_bounds__(kThreads) k_spread_sorted(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
     const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell, bool sort) {
-  constexpr int D = Tile<S>::D, TN = Tile<S>::N, lo = Stencil<S>::lo;
+  using T = STile<S>;
+  constexpr int D = T::D, TX = T::TX, TN = T::N, lo = Stencil<S>::lo;
   constexpr int NC = kBrick * kBrick * kBrick;
   const int nb = bk.count();
   if ((int)blockIdx.x >= nb) {
@@ -42,7 +58,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
     return;
   }
   extern __shared__ float4 dyn[];
-  __shared__ int tile[TN];
+  __shared__ __align__(16) int tile[TN];
   __shared__ int hist[NC + 1];
   __shared__ float red[2 * kThreads / 32];
   const int b = blockIdx.x;
@@ -53,42 +69,19 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
   const int64_t base = (int64_t)b * cap;
   StageSmem sm{dyn, (int*)(dyn + cap), nullptr, hist, red};
   float qsum = 0.f, qmax = 0.f;
-  if (sort) {
-    stage_sorted<false, FIX>(rec, rcell, nullptr, base, cnt, sm, qsum, qmax);
-  } else if (FIX) {
-    float qa = 0.f, qm = 0.f;
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const float q = fabsf(rec[base + j].w);
-      qa += q;
-      qm = fmaxf(qm, q);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      qa += __shfl_xor_sync(0xffffffffu, qa, o);
-      qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      red[threadIdx.x >> 5] = qa;
-      red[kThreads / 32 + (threadIdx.x >> 5)] = qm;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
-      qsum += red[w];
-      qmax = fmaxf(qmax, red[kThreads / 32 + w]);
-    }
-  } else {
-    __syncthreads();
-  }
+  if (sort) stage_sorted<false, false>(rec, rcell, nullptr, base, cnt, sm, qsum, qmax);
+  else __syncthreads();
   float scale = inv_vcell, inv_scale = 1.f;
   if (FIX) {
     // int32 fixed point with a power-of-two scale: every cell sum stays below
-    // 2^30 (|cell| <= sum|q| wmax^3) and every single contribution below 2^22,
-    // so the float->int conversion is one FFMA with the 1.5*2^23 magic number
-    // (round to nearest) instead of an F2I on the quarter-rate conversion pipe.
+    // 2^30 (|cell| <= count * max|q| * wmax^3) and every single contribution
+    // below 2^22, so the float->int conversion is one FFMA with the 1.5*2^23
+    // magic number (round to nearest) instead of an F2I on the quarter-rate
+    // conversion pipe.  max|q| is the global one from the binning pass.
     const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
+    qmax = __int_as_float(counts[nb + 1]);
     int e_sum = 0, e_one = 0;
-    frexpf(qsum > 0.f ? qsum * w3 : 1.f, &e_sum);  // qsum w3 < 2^e_sum
+    frexpf(qmax > 0.f ? (float)cnt * qmax * w3 : 1.f, &e_sum);
     frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);
     const int s = min(30 - e_sum, 22 - e_one);
     scale = ldexpf(1.f, s);
@@ -111,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
 #pragma unroll
       for (int bb = 0; bb < S; ++bb) {
         const float qab = qa * wy[bb];
-        const int row = ((lz + a) * D + (ly + bb)) * D + lx;
+        const int row = ((lz + a) * D + (ly + bb)) * TX + lx + T::XOFF;
 #pragma unroll
         for (int c = 0; c < S; ++c) {
           if (FIX) atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
@@ -122,14 +115,29 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
   }
   __syncthreads();
   const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-  const int ox = bx * kBrick - lo, oy = by * kBrick - lo, oz = bz * kBrick - lo;
-  for (int k = threadIdx.x; k < TN; k += blockDim.x) {
-    const int v = tile[k];
-    if (v == 0) continue;
-    const float val = FIX ? (float)v * inv_scale : __int_as_float(v);
-    const int tx_ = k % D, ty_ = (k / D) % D, tz_ = k / (D * D);
-    const int gx = wrap_index(ox + tx_, g.nx), gy = wrap_index(oy + ty_, g.ny), gz = wrap_index(oz + tz_, g.nz);
-    atomicAdd(rho + ((int64_t)gz * g.ny + gy) * g.nx + gx, val);
+  const int ox = bx * kBrick - 4, oy = by * kBrick - lo, oz = bz * kBrick - lo;
+  const bool vec = (g.nx & 3) == 0;
+  for (int k = threadIdx.x; k < D * D * 4; k += blockDim.x) {
+    const int qx = k & 3, ty_ = (k >> 2) % D, tz_ = (k >> 2) / D;
+    const int4 v = *reinterpret_cast<const int4*>(tile + (tz_ * D + ty_) * TX + 4 * qx);
+    if ((v.x | v.y | v.z | v.w) == 0) continue;
+    float4 f;
+    if (FIX) {
+      f = make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
+    } else {
+      f = make_float4(__int_as_float(v.x), __int_as_float(v.y), __int_as_float(v.z), __int_as_float(v.w));
+    }
+    const int gy = wrap_index(oy + ty_, g.ny), gz = wrap_index(oz + tz_, g.nz);
+    float* row = rho + ((int64_t)gz * g.ny + gy) * g.nx;
+    const int x0 = ox + 4 * qx;
+    if (vec) {
+      red_add_v4(row + wrap_index(x0, g.nx), f.x, f.y, f.z, f.w);
+    } else {
+      const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (fv[e] != 0.f) atomicAdd(row + wrap_index(x0 + e, g.nx), fv[e]);
+    }
   }
 }
 
