@@ -6,7 +6,7 @@ namespace pppm {
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, cudaStream_t s) {
-  if (cudaMemsetAsync(counts, 0, sizeof(int) * (bk.count() + 2), s) != cudaSuccess) return launch_status();
+  if (cudaMemsetAsync(counts, 0, sizeof(int) * (bk.count() + 2) * kCountStride, s) != cudaSuccess) return launch_status();
   const int grid = grid_for((a.n + kBinUnroll - 1) / kBinUnroll);
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
     int* __restrict__ err) {
   const int nb = bk.count();
-  int* ovf_count = counts + nb;
+  int* ovf_count = counts + (int64_t)nb * kCountStride;
   float qmax = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += stride * kBinUnroll) {
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
     }
 #pragma unroll
     for (int u = 0; u < kBinUnroll; ++u)
-      if (b[u] >= 0) slot[u] = atomicAdd(counts + b[u], 1);
+      if (b[u] >= 0) slot[u] = atomicAdd(counts + (int64_t)b[u] * kCountStride, 1);
 #pragma unroll
     for (int u = 0; u < kBinUnroll; ++u) {
       if (b[u] < 0) continue;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
   if (threadIdx.x == 0) {
     float m = 0.f;
     for (int w = 0; w < kThreads / 32; ++w) m = fmaxf(m, wmax[w]);
-    atomicMax(counts + nb + 1, __float_as_int(m));
+    atomicMax(counts + ((int64_t)nb + 1) * kCountStride, __float_as_int(m));
   }
 }
 

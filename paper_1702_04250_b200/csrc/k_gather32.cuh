@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_sorted(
   const int nb = bk.count();
   const float ihx = (float)g.ihx, ihy = (float)g.ihy, ihz = (float)g.ihz;
   if ((int)blockIdx.x >= nb) {
-    const int novf = counts[nb];
+    const int novf = counts[(int64_t)nb * kCountStride];
     for (int k = (blockIdx.x - nb) * blockDim.x + threadIdx.x; k < novf; k += (gridDim.x - nb) * blockDim.x) {
       const float4 r = ovf_rec[k];
       const int cc = ovf_cell[k];
@@ -75,23 +75,30 @@ __global__ void __launch_bounds__(kThreads) k_gather_sorted(
   __shared__ int hist[NC + 1];
   __shared__ float red[2 * kThreads / 32];
   const int b = blockIdx.x;
-  int cnt = counts[b];
+  int cnt = counts[(int64_t)b * kCountStride];
   cnt = cnt < cap ? cnt : cap;
   if (cnt == 0) return;
   const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
   const int ox = bx * kBrick - lo, oy = by * kBrick - lo, oz = bz * kBrick - lo;
+  // field tile: asynchronous global->shared copies (cp.async, no register
+  // round trip), overlapped with the atom staging / sort below
   for (int k = threadIdx.x; k < TN; k += blockDim.x) {
     const int tx_ = k % D, ty_ = (k / D) % D, tz_ = k / (D * D);
     const int gx = wrap_index(ox + tx_, g.nx), gy = wrap_index(oy + ty_, g.ny), gz = wrap_index(oz + tz_, g.nz);
     const int64_t gi = ((int64_t)gz * g.ny + gy) * g.nx + gx;
 #pragma unroll
-    for (int f = 0; f < F; ++f) tile[f * TN + k] = __ldg(fields + f * mesh + gi);
+    for (int f = 0; f < F; ++f) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + f * TN + k);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(fields + f * mesh + gi) : "memory");
+    }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   const int64_t base = (int64_t)b * cap;
   StageSmem sm{dyn, (int*)(dyn + cap), (int*)(dyn + cap) + cap, hist, red};
   float unused = 0.f, unused2 = 0.f;
   if (sort) stage_sorted<true, false>(rec, rcell, perm, base, cnt, sm, unused, unused2);
-  else __syncthreads();
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
     const float4 r = sort ? sm.r[j] : rec[base + j];
     const int cc = sort ? sm.c[j] : rcell[base + j];

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
   constexpr int NC = kBrick * kBrick * kBrick;
   const int nb = bk.count();
   if ((int)blockIdx.x >= nb) {
-    const int novf = counts[nb];
+    const int novf = counts[(int64_t)nb * kCountStride];
     for (int k = (blockIdx.x - nb) * blockDim.x + threadIdx.x; k < novf; k += (gridDim.x - nb) * blockDim.x) {
       const float4 r = ovf_rec[k];
       const int cc = ovf_cell[k];
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
   __shared__ int hist[NC + 1];
   __shared__ float red[2 * kThreads / 32];
   const int b = blockIdx.x;
-  int cnt = counts[b];
+  int cnt = counts[(int64_t)b * kCountStride];
   cnt = cnt < cap ? cnt : cap;
   if (cnt == 0) return;
   for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_sorted(
     // magic number (round to nearest) instead of an F2I on the quarter-rate
     // conversion pipe.  max|q| is the global one from the binning pass.
     const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
-    qmax = __int_as_float(counts[nb + 1]);
+    qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
     int e_sum = 0, e_one = 0;
     frexpf(qmax > 0.f ? (float)cnt * qmax * w3 : 1.f, &e_sum);
     frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);

@@ -207,7 +207,7 @@ static int ensure_bins(pppm_ctx* c, int64_t n) {
   const int nb = c->bk.count();
   c->cap = bucket_cap(c, n);
   const int64_t slots = (int64_t)nb * c->cap;
-  TRY(c->counts.ensure(sizeof(int) * (nb + 2)));
+  TRY(c->counts.ensure(sizeof(int) * (nb + 2) * kCountStride));
   TRY(c->rec.ensure(sizeof(float4) * slots));
   TRY(c->rcell.ensure(sizeof(int) * slots));
   TRY(c->perm.ensure(sizeof(int) * slots));

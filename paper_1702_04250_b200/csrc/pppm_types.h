@@ -11,6 +11,7 @@ constexpr int kBrick = 8;          // owned cells per brick edge (fp32 path)
 constexpr int kGreenBlocks = 592;  // 4 x 148 SMs: fixed grid => deterministic energy order
 constexpr int kThreads = 256;
 constexpr int kRowPad = 8;         // stencil.py:23
+constexpr int kCountStride = 32;   // brick counters padded to 128 B (L2 atomics serialise per line)
 
 struct Geom {
   int nx, ny, nz;
