@@ -132,8 +132,15 @@ __device__ __forceinline__ void bspline_assign(typename P::T t, typename P::T (&
 }
 
 __device__ __forceinline__ int wrap_index(int i, int n) {
-  i %= n;
-  return i < 0 ? i + n : i;
+  // fast path for i in [-n, 2n) (every stencil / tile index on meshes >= 16),
+  // integer modulo otherwise
+  int r = i < 0 ? i + n : i;
+  r = r >= n ? r - n : r;
+  if ((unsigned)r >= (unsigned)n) {
+    r = i % n;
+    r = r < 0 ? r + n : r;
+  }
+  return r;
 }
 
 // warp/block reductions -----------------------------------------------------
