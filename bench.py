@@ -156,13 +156,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def load_traffic(config, mode):
-    """ncu dram bytes per launch of the dominant kernel, committed under profiles/."""
+KERNEL_NAMES = {"spread": "k_spread_sorted", "gather": "k_gather_sorted", "bin": "k_bin_fixed"}
+
+
+def load_traffic(config, mode, kernel):
+    """ncu DRAM bytes (read + write) per launch of ``kernel``, from the committed
+    profiles/traffic.json (tools/launch_summary.py --traffic), else None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"config{config}_{mode}")
+        return d.get(f"config{config}_{mode}", {}).get(KERNEL_NAMES[kernel])
     except Exception:
         return None
 
@@ -284,7 +288,7 @@ def main():
     achieved = per_kernel[dom]["gbs"]
     mf_bytes = alg["spread"] + alg["gather"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(args.config, mode), "kernel": "k_spread_brick" if dom == "spread" else "k_gather_brick",
+                "traffic": load_traffic(args.config, mode, dom), "kernel": KERNEL_NAMES[dom],
                 "peak_kind": peak_kind,
                 "make_rho_fieldforce_gbs": mf_bytes / (t_mf / k) / 1e9,
                 "make_rho_fieldforce_frac": mf_bytes / (t_mf / k) / 1e9 / peak}
