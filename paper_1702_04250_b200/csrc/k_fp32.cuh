@@ -31,6 +31,12 @@ constexpr int kCapMax = 1024;      // bucket capacity limit (4 atoms per thread)
 constexpr int kPer = kCapMax / kThreads;
 constexpr int kOvfBlocks = 64;     // extra CTAs per launch for overflow atoms
 
+template <int S> struct TmaTile {
+  static constexpr int D = kBrick + S - 1;         // brick + stencil halo (y, z)
+  static constexpr int TXB = (D + 3) / 4 * 4;      // box x extent (16-byte rows)
+  static constexpr int N = TXB * D * D;
+};
+
 template <int S> struct Tile {
   static constexpr int D = kBrick + S - 1;  // brick + halo
   static constexpr int N = D * D * D;

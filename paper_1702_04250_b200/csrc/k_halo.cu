@@ -1,0 +1,148 @@
+// Halo handling of the padded fp32 meshes (see Pad in pppm_types.h).
+//
+// make_rho adds each brick tile (brick + stencil halo) into the padded charge
+// mesh with one TMA reduce-add; the periodic wrap is then a fold of the halo
+// shell into its periodic images, one axis at a time (x over every padded row,
+// then y, then z over the interior), so no cell receives two adds in one pass.
+// The field grids come out of the C2R transforms in the padded interior and
+// the halo is filled from periodic images before the fieldforce TMA loads.
+#include "pppm_device.cuh"
+
+namespace pppm {
+
+// x: rows over the whole padded (y, z) range; 2H halo cells per row
+__global__ void k_fold_x(Geom g, Pad p, float* __restrict__ rho) {
+  const int64_t rows = (int64_t)p.py * p.pz;
+  const int per = 2 * p.H;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < rows * per;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = k / per;
+    const int h = (int)(k % per);
+    float* r = rho + row * p.px;
+    const int src = h < p.H ? h : g.nx + h;   // left halo [0, H) / right halo [nx + H, nx + 2H)
+    const int dst = h < p.H ? h + g.nx : h;   // periodic image in [H, nx + H)
+    r[dst] += r[src];
+    r[src] = 0.f;
+  }
+}
+
+// y: for every padded z, interior x
+__global__ void k_fold_y(Geom g, Pad p, float* __restrict__ rho) {
+  const int per = 2 * p.H;
+  const int64_t total = (int64_t)p.pz * per * g.nx;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(k % g.nx) + p.H;
+    const int64_t r2 = k / g.nx;
+    const int h = (int)(r2 % per);
+    const int z = (int)(r2 / per);
+    const int ys = h < p.H ? h : g.ny + h;
+    const int yd = h < p.H ? h + g.ny : h;
+    float* base = rho + (int64_t)z * p.py * p.px + x;
+    base[(int64_t)yd * p.px] += base[(int64_t)ys * p.px];
+    base[(int64_t)ys * p.px] = 0.f;
+  }
+}
+
+// z: interior x, y
+__global__ void k_fold_z(Geom g, Pad p, float* __restrict__ rho) {
+  const int per = 2 * p.H;
+  const int64_t total = (int64_t)per * g.ny * g.nx;
+  const int64_t plane = (int64_t)p.py * p.px;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(k % g.nx) + p.H;
+    const int64_t r2 = k / g.nx;
+    const int y = (int)(r2 % g.ny) + p.H;
+    const int h = (int)(r2 / g.ny);
+    const int zs = h < p.H ? h : g.nz + h;
+    const int zd = h < p.H ? h + g.nz : h;
+    float* base = rho + (int64_t)y * p.px + x;
+    base[zd * plane] += base[zs * plane];
+    base[zs * plane] = 0.f;
+  }
+}
+
+// halo fill: every cell of [0, nx+2H) x [0, ny+2H) x [0, nz+2H) outside the
+// interior takes the value of its periodic image, for `nf` fields
+__global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
+  const int ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H, per = 2 * p.H;
+  const int64_t ra = (int64_t)per * ey * ex;       // z halo planes
+  const int64_t rb = (int64_t)g.nz * per * ex;     // y halo rows, interior z
+  const int64_t rc = (int64_t)g.nz * g.ny * per;   // x halo cells, interior y, z
+  const int64_t total = ra + rb + rc;
+  const int64_t mesh = p.count();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    int x, y, z;
+    if (k < ra) {
+      x = (int)(k % ex);
+      y = (int)((k / ex) % ey);
+      const int h = (int)(k / ((int64_t)ex * ey));
+      z = h < p.H ? h : g.nz + h;
+    } else if (k < ra + rb) {
+      const int64_t q = k - ra;
+      x = (int)(q % ex);
+      const int h = (int)((q / ex) % per);
+      y = h < p.H ? h : g.ny + h;
+      z = (int)(q / ((int64_t)ex * per)) + p.H;
+    } else {
+      const int64_t q = k - ra - rb;
+      const int h = (int)(q % per);
+      x = h < p.H ? h : g.nx + h;
+      y = (int)((q / per) % g.ny) + p.H;
+      z = (int)(q / ((int64_t)per * g.ny)) + p.H;
+    }
+    const int ix = wrap_index(x - p.H, g.nx) + p.H;
+    const int iy = wrap_index(y - p.H, g.ny) + p.H;
+    const int iz = wrap_index(z - p.H, g.nz) + p.H;
+    const int64_t dst = ((int64_t)z * p.py + y) * p.px + x;
+    const int64_t src = ((int64_t)iz * p.py + iy) * p.px + ix;
+    for (int fi = 0; fi < nf; ++fi) f[fi * mesh + dst] = f[fi * mesh + src];
+  }
+}
+
+__global__ void k_unpad(Geom g, Pad p, const float* __restrict__ src, double* __restrict__ dst) {
+  const int64_t total = (int64_t)g.nx * g.ny * g.nz;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(k % g.nx);
+    const int y = (int)((k / g.nx) % g.ny);
+    const int z = (int)(k / ((int64_t)g.nx * g.ny));
+    dst[k] = (double)src[p.at(x, y, z)];
+  }
+}
+
+__global__ void k_pad_in(Geom g, Pad p, const double* __restrict__ src, float* __restrict__ dst) {
+  const int64_t total = (int64_t)g.nx * g.ny * g.nz;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(k % g.nx);
+    const int y = (int)((k / g.nx) % g.ny);
+    const int z = (int)(k / ((int64_t)g.nx * g.ny));
+    dst[p.at(x, y, z)] = (float)src[k];
+  }
+}
+
+int launch_fold_halo(const Geom& g, const Pad& p, float* rho, cudaStream_t s) {
+  if (p.H == 0) return 0;
+  k_fold_x<<<grid_for((int64_t)p.py * p.pz * 2 * p.H), kThreads, 0, s>>>(g, p, rho);
+  k_fold_y<<<grid_for((int64_t)p.pz * 2 * p.H * g.nx), kThreads, 0, s>>>(g, p, rho);
+  k_fold_z<<<grid_for((int64_t)2 * p.H * g.ny * g.nx), kThreads, 0, s>>>(g, p, rho);
+  return launch_status();
+}
+
+int launch_fill_halo(const Geom& g, const Pad& p, float* f, int nf, cudaStream_t s) {
+  if (p.H == 0) return 0;
+  const int64_t ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H;
+  const int64_t total = 2 * p.H * ey * ex + (int64_t)g.nz * 2 * p.H * ex + (int64_t)g.nz * g.ny * 2 * p.H;
+  k_fill<<<grid_for(total), kThreads, 0, s>>>(g, p, f, nf);
+  return launch_status();
+}
+
+int launch_unpad(const Geom& g, const Pad& p, const float* src, double* dst, cudaStream_t s) {
+  k_unpad<<<grid_for((int64_t)g.nx * g.ny * g.nz), kThreads, 0, s>>>(g, p, src, dst);
+  return launch_status();
+}
+
+int launch_pad_in(const Geom& g, const Pad& p, const double* src, float* dst, cudaStream_t s) {
+  k_pad_in<<<grid_for((int64_t)g.nx * g.ny * g.nz), kThreads, 0, s>>>(g, p, src, dst);
+  return launch_status();
+}
+
+}  // namespace pppm

@@ -1,168 +1,143 @@
-// make_rho, fp32 path (gridmap.py:156-213): one CTA per brick, cell-sorted
-// atoms, S^3 stencils accumulated in a shared (8+S-1)^3 tile (int32 fixed
-// point with a per-brick power-of-two scale, or float CAS atomics), tile added
-// to the mesh with red.global.add.f32.  CTAs past the brick count handle the
-// overflow atoms of full buckets straight into the mesh.
+// make_rho, fp32 path (gridmap.py:156-213): persistent CTAs over bricks,
+// S^3 stencils accumulated in a shared (8+S-1)^3 tile (int32 fixed point with a
+// per-brick power-of-two scale, or float CAS atomics), the tile added to the
+// halo-padded mesh with one TMA reduce-add, then the halo folded back.
+#include <algorithm>
+
 #include "k_fp32.cuh"
+#include "tma.cuh"
 
 namespace pppm {
 
-// shared tile: x spans [bx*8 - 4, bx*8 + 12) (16 cells, quad-aligned so the
-// flush can use red.global.add.v4.f32), row pitch 20 words (16B aligned rows,
-// 8 consecutive rows hit distinct bank quads); y, z span brick + halo.
-template <int S> struct STile {
-  static constexpr int D = kBrick + S - 1;
-  static constexpr int TX = 20;
-  static constexpr int N = D * D * TX;
-  static constexpr int XOFF = 4 - Stencil<S>::lo;  // tile x of the lowest stencil node of local cell 0
-};
-
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-
+// make_rho, persistent CTAs: bricks b = blockIdx.x, += gridDim.x.  Per brick the
+// int32 fixed-point tile is accumulated with shared atomics, converted to fp32
+// in place and added to the padded mesh with ONE TMA reduce-add of the
+// (TXB, D, D) box at the brick origin - lo (always in bounds: the mesh carries
+// an H-cell halo, folded back periodically by k_halo.cu afterwards).
 template <int S, bool TAB, bool FIX>
-__global__ void __launch_bounds__(kThreads) k_spread_sorted(
+__global__ void __launch_bounds__(kThreads) k_spread_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
-    Geom g, Bricks bk, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
-    const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell, bool sort) {
-  using T = STile<S>;
-  constexpr int D = T::D, TX = T::TX, TN = T::N, lo = Stencil<S>::lo;
-  constexpr int NC = kBrick * kBrick * kBrick;
+    Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
+    const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
+  using T = TmaTile<S>;
+  constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
+  __shared__ __align__(128) int tile[TN];
   const int nb = bk.count();
-  if ((int)blockIdx.x >= nb) {
-    const int novf = counts[(int64_t)nb * kCountStride];
-    for (int k = (blockIdx.x - nb) * blockDim.x + threadIdx.x; k < novf; k += (gridDim.x - nb) * blockDim.x) {
-      const float4 r = ovf_rec[k];
-      const int cc = ovf_cell[k];
-      const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
+  const float qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
+  const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
+  float* ftile = reinterpret_cast<float*>(tile);
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    int cnt = counts[(int64_t)b * kCountStride];
+    cnt = cnt < cap ? cnt : cap;
+    if (cnt == 0) continue;
+    // the previous brick's reduce must have finished reading the tile
+    if (threadIdx.x == 0) bulk_wait_read<0>();
+    __syncthreads();
+    for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
+    __syncthreads();
+    float scale = inv_vcell, inv_scale = 1.f;
+    if (FIX) {
+      // int32 fixed point, power-of-two scale: every cell sum below 2^30
+      // (|cell| <= count * max|q| * wmax^3) and every contribution below 2^22,
+      // so float->int is one FFMA with the 1.5*2^23 magic number (round to
+      // nearest) instead of an F2I on the quarter-rate conversion pipe.
+      int e_sum = 0, e_one = 0;
+      frexpf(qmax > 0.f ? (float)cnt * qmax * w3 : 1.f, &e_sum);
+      frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);
+      const int sc = min(30 - e_sum, 22 - e_one);
+      scale = ldexpf(1.f, sc);
+      inv_scale = ldexpf(1.f, -sc) * inv_vcell;
+    }
+    const int64_t base = (int64_t)b * cap;
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const float4 r = rec[base + j];
+      const int cc = rcell[base + j];
+      const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float wx[S], wy[S], wz[S], dd[S];
       rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
       rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
       rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
-      const float q = r.w * inv_vcell;
+      const float qs = r.w * scale;
 #pragma unroll
       for (int a = 0; a < S; ++a) {
-        const int iz = wrap_index(n2 - lo + a, g.nz);
+        const float qa = qs * wz[a];
 #pragma unroll
-        for (int b = 0; b < S; ++b) {
-          const int iy = wrap_index(n1 - lo + b, g.ny);
-          const float p = q * wz[a] * wy[b];
-          float* row = rho + ((int64_t)iz * g.ny + iy) * g.nx;
+        for (int bb = 0; bb < S; ++bb) {
+          const float qab = qa * wy[bb];
+          const int row = ((lz + a) * D + (ly + bb)) * TXB + lx;
 #pragma unroll
-          for (int c = 0; c < S; ++c) atomicAdd(row + wrap_index(n0 - lo + c, g.nx), p * wx[c]);
+          for (int c = 0; c < S; ++c) {
+            if (FIX) atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
+            else atomicAdd(ftile + row + c, qab * wx[c]);
+          }
         }
       }
     }
-    return;
+    __syncthreads();
+    if (FIX)
+      for (int k = threadIdx.x; k < TN; k += blockDim.x) ftile[k] = (float)tile[k] * inv_scale;
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+      tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.H, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
+      bulk_commit();
+    }
   }
-  extern __shared__ float4 dyn[];
-  __shared__ __align__(16) int tile[TN];
-  __shared__ int hist[NC + 1];
-  __shared__ float red[2 * kThreads / 32];
-  const int b = blockIdx.x;
-  int cnt = counts[(int64_t)b * kCountStride];
-  cnt = cnt < cap ? cnt : cap;
-  if (cnt == 0) return;
-  for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
-  const int64_t base = (int64_t)b * cap;
-  StageSmem sm{dyn, (int*)(dyn + cap), nullptr, hist, red};
-  float qsum = 0.f, qmax = 0.f;
-  if (sort) stage_sorted<false, false>(rec, rcell, nullptr, base, cnt, sm, qsum, qmax);
-  else __syncthreads();
-  float scale = inv_vcell, inv_scale = 1.f;
-  if (FIX) {
-    // int32 fixed point with a power-of-two scale: every cell sum stays below
-    // 2^30 (|cell| <= count * max|q| * wmax^3) and every single contribution
-    // below 2^22, so the float->int conversion is one FFMA with the 1.5*2^23
-    // magic number (round to nearest) instead of an F2I on the quarter-rate
-    // conversion pipe.  max|q| is the global one from the binning pass.
-    const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
-    qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
-    int e_sum = 0, e_one = 0;
-    frexpf(qmax > 0.f ? (float)cnt * qmax * w3 : 1.f, &e_sum);
-    frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);
-    const int s = min(30 - e_sum, 22 - e_one);
-    scale = ldexpf(1.f, s);
-    inv_scale = ldexpf(1.f, -s) * inv_vcell;
-  }
-  float* ftile = reinterpret_cast<float*>(tile);
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-    const float4 r = sort ? sm.r[j] : rec[base + j];
-    const int cc = sort ? sm.c[j] : rcell[base + j];
-    const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+  if (threadIdx.x == 0) bulk_wait_read<0>();
+  // overflow atoms (full buckets): straight into the padded interior
+  const int novf = counts[(int64_t)nb * kCountStride];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
+    const float4 r = ovf_rec[k];
+    const int cc = ovf_cell[k];
+    const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
     float wx[S], wy[S], wz[S], dd[S];
     rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
     rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
     rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
-    const float qs = r.w * scale;
+    const float q = r.w * inv_vcell;
 #pragma unroll
     for (int a = 0; a < S; ++a) {
-      const float qa = qs * wz[a];
+      const int iz = wrap_index(n2 - lo + a, g.nz);
 #pragma unroll
       for (int bb = 0; bb < S; ++bb) {
-        const float qab = qa * wy[bb];
-        const int row = ((lz + a) * D + (ly + bb)) * TX + lx + T::XOFF;
+        const int iy = wrap_index(n1 - lo + bb, g.ny);
+        const float p = q * wz[a] * wy[bb];
 #pragma unroll
-        for (int c = 0; c < S; ++c) {
-          if (FIX) atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
-          else atomicAdd(ftile + row + c, qab * wx[c]);
-        }
+        for (int c = 0; c < S; ++c) atomicAdd(rho + pd.at(wrap_index(n0 - lo + c, g.nx), iy, iz), p * wx[c]);
       }
-    }
-  }
-  __syncthreads();
-  const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-  const int ox = bx * kBrick - 4, oy = by * kBrick - lo, oz = bz * kBrick - lo;
-  const bool vec = (g.nx & 3) == 0;
-  for (int k = threadIdx.x; k < D * D * 4; k += blockDim.x) {
-    const int qx = k & 3, ty_ = (k >> 2) % D, tz_ = (k >> 2) / D;
-    const int4 v = *reinterpret_cast<const int4*>(tile + (tz_ * D + ty_) * TX + 4 * qx);
-    if ((v.x | v.y | v.z | v.w) == 0) continue;
-    float4 f;
-    if (FIX) {
-      f = make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
-    } else {
-      f = make_float4(__int_as_float(v.x), __int_as_float(v.y), __int_as_float(v.z), __int_as_float(v.w));
-    }
-    const int gy = wrap_index(oy + ty_, g.ny), gz = wrap_index(oz + tz_, g.nz);
-    float* row = rho + ((int64_t)gz * g.ny + gy) * g.nx;
-    const int x0 = ox + 4 * qx;
-    if (vec) {
-      red_add_v4(row + wrap_index(x0, g.nx), f.x, f.y, f.z, f.w);
-    } else {
-      const float fv[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (fv[e] != 0.f) atomicAdd(row + wrap_index(x0 + e, g.nx), fv[e]);
     }
   }
 }
 
-int launch_spread_brick(int variant, bool sort, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
+int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
-                        const float* ta, float* rho, cudaStream_t s) {
-  const int64_t M = (int64_t)g.nx * g.ny * g.nz;
-  if (cudaMemsetAsync(rho, 0, sizeof(float) * M, s) != cudaSuccess) return launch_status();
+                        const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, cudaStream_t s) {
+  if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
-  const size_t dyn = (size_t)cap * (sizeof(float4) + sizeof(int));
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
-        auto k = k_spread_sorted<S, TAB, FIX>;
-        allow_smem(k, dyn);
-        k<<<bk.count() + kOvfBlocks, kThreads, dyn, s>>>(rec, rcell, counts, cap, g, bk, ta, inv_vcell, rho, ovf_rec,
-                                                           ovf_cell, sort);
+        auto k = k_spread_tma<S, TAB, FIX>;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+        k<<<grid, kThreads, 0, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
         return 0;
       });
     });
   });
-  return st ? st : launch_status();
+  if (st) return st;
+  st = launch_status();
+  if (st) return st;
+  return launch_fold_halo(g, pd, rho, s);
 }
 
 }  // namespace pppm

@@ -6,6 +6,8 @@
 // field buffers, cuFFT plans and the atom binning scratch.  Host-pointer calls
 // copy in, run, and copy out on the context stream; device-resident calls
 // leave everything in HBM.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cufft.h>
 
 #include <algorithm>
@@ -109,6 +111,8 @@ struct pppm_ctx {
   int green_kind = -1;  // -1: none or uploaded from a foreign plan
   double green_floor = 1e-10;
   int64_t M = 0, half = 0;
+  Pad pd{};                          // fp32: halo-padded meshes; fp64: H = 0 (dense)
+  CUtensorMap rho_map{}, field_map{};  // TMA descriptors of the padded fp32 meshes
   int nxh = 0;
   cudaStream_t stream = nullptr;
   cufftHandle fwd = 0, bwd = 0;
@@ -156,13 +160,56 @@ static int check_err_flag(pppm_ctx* c) {
 static int ensure_plans(pppm_ctx* c) {
   if (c->plans) return PPPM_OK;
   int n[3] = {c->g.nz, c->g.ny, c->g.nx};
+  int real_emb[3] = {c->pd.pz, c->pd.py, c->pd.px};   // padded real meshes (interior at pd.interior())
+  int cplx_emb[3] = {c->g.nz, c->g.ny, c->nxh};
   const bool d = c->fp64();
-  FFT(cufftPlanMany(&c->fwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, d ? CUFFT_D2Z : CUFFT_R2C, 1));
-  FFT(cufftPlanMany(&c->bwd, 3, n, nullptr, 1, 0, nullptr, 1, 0, d ? CUFFT_Z2D : CUFFT_C2R,
-                    c->nfields()));
+  FFT(cufftPlanMany(&c->fwd, 3, n, real_emb, 1, (int)c->pd.count(), cplx_emb, 1, (int)c->half,
+                    d ? CUFFT_D2Z : CUFFT_R2C, 1));
+  FFT(cufftPlanMany(&c->bwd, 3, n, cplx_emb, 1, (int)c->half, real_emb, 1, (int)c->pd.count(),
+                    d ? CUFFT_Z2D : CUFFT_C2R, c->nfields()));
   FFT(cufftSetStream(c->fwd, c->stream));
   FFT(cufftSetStream(c->bwd, c->stream));
   c->plans = true;
+  return PPPM_OK;
+}
+
+// TMA descriptors of the padded fp32 meshes (driver entry point fetched at
+// run time, so the library does not link libcuda)
+static int encode_maps(pppm_ctx* c) {
+  using Encode = PFN_cuTensorMapEncodeTiled_v12000;
+  static Encode fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    fn = reinterpret_cast<Encode>(p);
+  }
+  const int D = kBrick + c->order - 1;
+  const int txb = (D + 3) / 4 * 4;
+  const cuuint64_t row = (cuuint64_t)c->pd.px * 4, plane = row * c->pd.py, vol = plane * c->pd.pz;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)c->pd.px, (cuuint64_t)c->pd.py, (cuuint64_t)c->pd.pz};
+    cuuint64_t strides[2] = {row, plane};
+    cuuint32_t box[3] = {(cuuint32_t)txb, (cuuint32_t)D, (cuuint32_t)D};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(&c->rho_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->rho.p, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (rho) failed");
+  }
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)c->pd.px, (cuuint64_t)c->pd.py, (cuuint64_t)c->pd.pz,
+                          (cuuint64_t)c->nfields()};
+    cuuint64_t strides[3] = {row, plane, vol};
+    cuuint32_t box[4] = {(cuuint32_t)txb, (cuuint32_t)D, (cuuint32_t)D, (cuuint32_t)c->nfields()};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = fn(&c->field_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->fields.p, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (fields) failed");
+  }
   return PPPM_OK;
 }
 
@@ -241,10 +288,10 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     c->launches += 4;
   } else {
     if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
-    TRY(launch_spread_brick(c->spread_variant & 1, (c->spread_variant & 2) != 0, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
+    TRY(launch_spread_brick(c->spread_variant & 1, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
-                            c->bk, c->tab.as<float>(), c->rho.as<float>(), c->stream));
-    c->launches += 1;
+                            c->bk, c->pd, c->rho_map, c->tab.as<float>(), c->rho.as<float>(), c->stream));
+    c->launches += 4;  // spread + 3 halo folds
   }
   c->have_rho = true;
   return PPPM_OK;
@@ -254,9 +301,9 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
 static int run_fft_fwd(pppm_ctx* c) {
   TRY(ensure_plans(c));
   if (c->fp64())
-    FFT(cufftExecD2Z(c->fwd, c->rho.as<double>(), c->rho_hat.as<cufftDoubleComplex>()));
+    FFT(cufftExecD2Z(c->fwd, c->rho.as<double>() + c->pd.interior(), c->rho_hat.as<cufftDoubleComplex>()));
   else
-    FFT(cufftExecR2C(c->fwd, c->rho.as<float>(), c->rho_hat.as<cufftComplex>()));
+    FFT(cufftExecR2C(c->fwd, c->rho.as<float>() + c->pd.interior(), c->rho_hat.as<cufftComplex>()));
   return PPPM_OK;
 }
 
@@ -275,9 +322,11 @@ static int run_green(pppm_ctx* c, bool fields) {
 static int run_fft_bwd(pppm_ctx* c) {
   TRY(ensure_plans(c));
   if (c->fp64())
-    FFT(cufftExecZ2D(c->bwd, c->ework.as<cufftDoubleComplex>(), c->fields.as<double>()));
+    FFT(cufftExecZ2D(c->bwd, c->ework.as<cufftDoubleComplex>(), c->fields.as<double>() + c->pd.interior()));
   else
-    FFT(cufftExecC2R(c->bwd, c->ework.as<cufftComplex>(), c->fields.as<float>()));
+    FFT(cufftExecC2R(c->bwd, c->ework.as<cufftComplex>(), c->fields.as<float>() + c->pd.interior()));
+    TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), c->nfields(), c->stream));
+    c->launches += 1;
   c->have_fields = true;
   return PPPM_OK;
 }
@@ -299,14 +348,15 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
     TRY(launch_gather_brick(c->gather_variant, c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
-                            c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, ta,
-                            td, c->fields.as<float>(), c->M, (float)c->cscale, out, c->stream));
+                            c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
+                            c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out, c->stream));
   }
   c->launches += 1;
   return PPPM_OK;
 }
 
-static int mesh_to_host(pppm_ctx* c, const void* dev, double* host, int64_t count) {
+// flat device array (count reals of the context type) -> host fp64
+static int flat_to_host(pppm_ctx* c, const void* dev, double* host, int64_t count) {
   if (c->fp64()) {
     CU(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
   } else {
@@ -318,13 +368,27 @@ static int mesh_to_host(pppm_ctx* c, const void* dev, double* host, int64_t coun
   return PPPM_OK;
 }
 
-static int mesh_from_host(pppm_ctx* c, void* dev, const double* host, int64_t count) {
+// one (padded) device mesh -> dense host fp64 (nz, ny, nx)
+static int mesh_to_host(pppm_ctx* c, const void* dev, double* host) {
   if (c->fp64()) {
-    CU(cudaMemcpyAsync(dev, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(host, dev, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->stream));
   } else {
-    TRY(c->out_stage.ensure(sizeof(double) * count));
-    CU(cudaMemcpyAsync(c->out_stage.p, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
-    TRY(launch_convert(false, c->out_stage.p, dev, count, c->stream));
+    TRY(c->out_stage.ensure(sizeof(double) * c->M));
+    TRY(launch_unpad(c->g, c->pd, (const float*)dev, c->out_stage.as<double>(), c->stream));
+    CU(cudaMemcpyAsync(host, c->out_stage.p, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return PPPM_OK;
+}
+
+// dense host fp64 mesh -> (padded) device mesh interior
+static int mesh_from_host(pppm_ctx* c, void* dev, const double* host) {
+  if (c->fp64()) {
+    CU(cudaMemcpyAsync(dev, host, sizeof(double) * c->M, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    TRY(c->out_stage.ensure(sizeof(double) * c->M));
+    CU(cudaMemcpyAsync(c->out_stage.p, host, sizeof(double) * c->M, cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_pad_in(c->g, c->pd, c->out_stage.as<double>(), (float*)dev, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   return PPPM_OK;
@@ -431,6 +495,12 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
   c->alpha = alpha;
   c->cscale = coulomb_constant / dielectric;  // model.py:244-247
   c->M = (int64_t)nx * ny * nz;
+  if (precision == PPPM_PREC_FP64) {
+    c->pd = Pad{0, nx, ny, nz, 0};
+  } else {
+    const int lo = (order - 1) / 2, hi = order - 1 - lo, H = lo > hi ? lo : hi;
+    c->pd = Pad{H, (nx + 2 * H + 3) / 4 * 4, ny + 2 * H, nz + 2 * H, (kBrick + order - 1 + 3) / 4 * 4};
+  }
   c->nxh = nx / 2 + 1;
   c->half = (int64_t)c->nxh * ny * nz;
   auto cleanup = [&](int st) {
@@ -442,11 +512,15 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
   const size_t rs = c->real_size();
   const size_t cs = 2 * rs;
   int st = PPPM_OK;
-  if (st == PPPM_OK) st = c->rho.ensure(rs * c->M);
+  if (st == PPPM_OK) st = c->rho.ensure(rs * c->pd.count());
   if (st == PPPM_OK && c->fp64()) st = c->rho_fix.ensure(8 * c->M);
   if (st == PPPM_OK) st = c->rho_hat.ensure(cs * c->half);
   if (st == PPPM_OK) st = c->ework.ensure(cs * c->half * c->nfields());
-  if (st == PPPM_OK) st = c->fields.ensure(rs * c->M * c->nfields());
+  if (st == PPPM_OK) st = c->fields.ensure(rs * c->pd.count() * c->nfields());
+  if (st == PPPM_OK && !c->fp64()) {
+    cudaMemset(c->fields.p, 0, rs * c->pd.count() * c->nfields());
+    st = encode_maps(c);
+  }
   if (st == PPPM_OK) st = c->green.ensure(rs * c->half);
   if (st == PPPM_OK) st = c->ikc.ensure(rs * (nx + ny + nz));
   if (st == PPPM_OK) st = c->ik64.ensure(8 * (nx + ny + nz));
@@ -624,13 +698,14 @@ int pppm_make_rho(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dt
   TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
   TRY(do_make_rho(c, dpos, dq, n, dtype));
   TRY(check_err_flag(c));
-  if (rho_out) TRY(mesh_to_host(c, c->rho.p, rho_out, c->M));
+  if (rho_out) TRY(mesh_to_host(c, c->rho.p, rho_out));
   return PPPM_OK;
 }
 
 int pppm_set_rho(pppm_ctx* c, const double* rho) {
   TRY(activate(c));
-  TRY(mesh_from_host(c, c->rho.p, rho, c->M));
+  if (!c->fp64()) CU(cudaMemsetAsync(c->rho.p, 0, sizeof(float) * c->pd.count(), c->stream));
+  TRY(mesh_from_host(c, c->rho.p, rho));
   c->have_rho = true;
   return PPPM_OK;
 }
@@ -638,7 +713,7 @@ int pppm_set_rho(pppm_ctx* c, const double* rho) {
 int pppm_get_rho(pppm_ctx* c, double* rho) {
   TRY(activate(c));
   if (!c->have_rho) return fail(PPPM_ERR_STATE, "no charge grid on the device");
-  return mesh_to_host(c, c->rho.p, rho, c->M);
+  return mesh_to_host(c, c->rho.p, rho);
 }
 
 int pppm_poisson(pppm_ctx* c, int want_fields, double* energy) {
@@ -663,7 +738,7 @@ int pppm_get_fields(pppm_ctx* c, double* f0, double* f1, double* f2) {
   const size_t rs = c->real_size();
   double* outs[3] = {f0, f1, f2};
   for (int f = 0; f < c->nfields(); ++f)
-    if (outs[f]) TRY(mesh_to_host(c, (char*)c->fields.p + rs * c->M * f, outs[f], c->M));
+    if (outs[f]) TRY(mesh_to_host(c, (char*)c->fields.p + rs * c->pd.count() * f, outs[f]));
   return PPPM_OK;
 }
 
@@ -673,7 +748,11 @@ int pppm_set_fields(pppm_ctx* c, const double* f0, const double* f1, const doubl
   const double* ins[3] = {f0, f1, f2};
   for (int f = 0; f < c->nfields(); ++f) {
     if (!ins[f]) return fail(PPPM_ERR_VALUE, "missing field grid");
-    TRY(mesh_from_host(c, (char*)c->fields.p + rs * c->M * f, ins[f], c->M));
+    TRY(mesh_from_host(c, (char*)c->fields.p + rs * c->pd.count() * f, ins[f]));
+  }
+  if (!c->fp64()) {
+    TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), c->nfields(), c->stream));
+    CU(cudaStreamSynchronize(c->stream));
   }
   c->have_fields = true;
   return PPPM_OK;
@@ -770,7 +849,7 @@ int pppm_ctx_get_forces(pppm_ctx* c, double* forces) {
     CU(cudaStreamSynchronize(c->stream));
     return PPPM_OK;
   }
-  return mesh_to_host(c, c->res_force.p, forces, cnt);
+  return flat_to_host(c, c->res_force.p, forces, cnt);
 }
 
 int pppm_ctx_get_energy(pppm_ctx* c, double* energy) {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace pppm {
@@ -31,6 +32,20 @@ struct GreenSpec {
   int optimal;
 };
 
+// Halo-padded mesh of the fp32 path: interior cell (x, y, z) lives at padded
+// ((z + H) * py + (y + H)) * px + (x + H).  H = max(ghost below, ghost above)
+// of the stencil; px is rounded to a multiple of 4 (16-byte rows for TMA).
+// Every brick tile (brick + halo) is then an in-bounds TMA box: no wrap in the
+// mapping kernels; halo contributions are folded back (make_rho) or filled
+// from their periodic images (fields) by k_halo.cu.
+struct Pad {
+  int H, px, py, pz;
+  int txb;  // tile/box x extent: 8 + S - 1 rounded up to a multiple of 4
+  __host__ __device__ int64_t count() const { return (int64_t)px * py * pz; }
+  __host__ __device__ int64_t interior() const { return ((int64_t)H * py + H) * px + H; }
+  __host__ __device__ int64_t at(int x, int y, int z) const { return ((int64_t)(z + H) * py + (y + H)) * px + (x + H); }
+};
+
 // device atoms as handed to the context: AoS (N, 3) positions, (N,) charges
 struct AtomsIn {
   const void* pos;
@@ -54,17 +69,22 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, cudaStream_t s);
-int launch_spread_brick(int variant, bool sort, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
+int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
-                        const float* ta, float* rho, cudaStream_t s);
+                        const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad, cudaStream_t s);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s);
 int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64, const float4* rec,
                         const int* rcell, const int* perm, const int* counts, int cap, const float4* ovf_rec,
-                        const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const float* ta,
-                        const float* td, const float* fields, int64_t mesh, float cscale, void* force,
-                        cudaStream_t s);
+                        const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
+                        const CUtensorMap& field_map, const float* ta, const float* td, const float* fields_pad,
+                        float cscale, void* force, cudaStream_t s);
+// halo handling of the padded fp32 meshes (k_halo.cu)
+int launch_fold_halo(const Geom& g, const Pad& pd, float* rho_pad, cudaStream_t s);
+int launch_fill_halo(const Geom& g, const Pad& pd, float* fields_pad, int nfields, cudaStream_t s);
+int launch_unpad(const Geom& g, const Pad& pd, const float* src_pad, double* dst, cudaStream_t s);
+int launch_pad_in(const Geom& g, const Pad& pd, const double* src, float* dst_pad, cudaStream_t s);
 int launch_influence(bool f64, const GreenSpec& gs, void* g_half, double* g_full, cudaStream_t s);
 int launch_ik_vectors(const Geom& g, double* ik, cudaStream_t s);
 int launch_green(bool f64, int mode, bool fields, const void* rho_hat, const void* green, const Geom& g,
