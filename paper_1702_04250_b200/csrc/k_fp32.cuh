@@ -260,4 +260,69 @@ __device__ __forceinline__ int stage_sorted(const float4* __restrict__ rec, cons
   return cnt;
 }
 
+// ---------------------------------------------------------------------------
+// bank-bucketed staging: the brick's atoms into shared memory, grouped by the
+// shared-memory bank of their stencil corner in the tile ((z*D + y)*TXB + x
+// mod 32).  Round r of the brick = the r-th atom of every bucket, so in every
+// warp instruction of a round (uniform stencil offset across lanes) the lanes
+// touch 32 distinct banks: no conflicts for the tile loads (fieldforce) and no
+// conflicts / same-address serialisation for the tile atomics (make_rho).
+// Returns the number of rounds (largest bucket).
+
+struct BankSmem {
+  float4* r;
+  int* c;
+  int* p;
+  int* bsize;   // 32
+  int* bstart;  // 33 (bstart[32] = rounds)
+};
+
+template <bool PERM, int D, int TXB>
+__device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, const int* __restrict__ rcell,
+                                            const int* __restrict__ perm, int64_t base, int cnt, BankSmem sm) {
+  if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
+  __syncthreads();
+  float4 r[kPer];
+  int c[kPer], rk[kPer], p[kPer], bank[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int j = threadIdx.x + k * kThreads;
+    if (j < cnt) {
+      r[k] = rec[base + j];
+      c[k] = rcell[base + j];
+      if (PERM) p[k] = perm[base + j];
+      const int lx = c[k] & (kBrick - 1), ly = (c[k] >> 3) & (kBrick - 1), lz = c[k] >> 6;
+      bank[k] = ((lz * D + ly) * TXB + lx) & 31;
+      rk[k] = atomicAdd(sm.bsize + bank[k], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int v = sm.bsize[threadIdx.x];
+    int x = v, m = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (threadIdx.x >= o) x += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    sm.bstart[threadIdx.x] = x - v;
+    if (threadIdx.x == 0) sm.bstart[32] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int j = threadIdx.x + k * kThreads;
+    if (j < cnt) {
+      const int dst = sm.bstart[bank[k]] + rk[k];
+      sm.r[dst] = r[k];
+      sm.c[dst] = c[k];
+      if (PERM) sm.p[dst] = p[k];
+    }
+  }
+  __syncthreads();
+  return sm.bstart[32];
+}
+
 }  // namespace pppm

@@ -35,7 +35,6 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
     const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
-  constexpr int NC = kBrick * kBrick * kBrick;
   constexpr int F = MODE == 0 ? 3 : 1;
   constexpr uint32_t kBytes = (uint32_t)F * TN * sizeof(float);
   extern __shared__ __align__(128) float dyn_f[];
@@ -44,14 +43,14 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
   int* s_c = reinterpret_cast<int*>(s_r + cap);
   int* s_p = s_c + cap;
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ int hist[NC + 1];
-  __shared__ float red[2 * kThreads / 32];
+  __shared__ int bsize[32], bstart[33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   const int nb = bk.count();
   const float ihx = (float)g.ihx, ihy = (float)g.ihy, ihz = (float)g.ihz;
   const int64_t mesh = pd.count();
   auto box = [&](int b, int& x, int& y, int& z) {
     const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-    x = bx * kBrick - lo + pd.H;
+    x = bx * kBrick - lo + pd.hx;
     y = by * kBrick - lo + pd.H;
     z = bz * kBrick - lo + pd.H;
   };
@@ -81,12 +80,19 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
     int cnt = counts[(int64_t)b * kCountStride];
     cnt = cnt < cap ? cnt : cap;
     const int64_t base = (int64_t)b * cap;
-    StageSmem sm{s_r, s_c, s_p, hist, red};
-    float unused = 0.f, unused2 = 0.f;
-    if (sort && cnt > 0) stage_sorted<true, false>(rec, rcell, perm, base, cnt, sm, unused, unused2);
+    BankSmem sm{s_r, s_c, s_p, bsize, bstart};
+    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB>(rec, rcell, perm, base, cnt, sm) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * F * TN;
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
+    const int nloop = sort ? (rounds - warp + nwarp - 1) / nwarp : (cnt - (int)threadIdx.x + (int)blockDim.x - 1) / (int)blockDim.x;
+    for (int t = 0; t < nloop; ++t) {
+      int j = threadIdx.x + t * blockDim.x;
+      if (sort) {
+        const int rr = warp + t * nwarp;
+        if (rr >= bsize[lane]) continue;
+        j = bstart[lane] + rr;
+      }
       const float4 r = sort ? s_r[j] : rec[base + j];
       const int cc = sort ? s_c[j] : rcell[base + j];
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;

@@ -18,9 +18,9 @@ __global__ void k_fold_x(Geom g, Pad p, float* __restrict__ rho) {
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = k / per;
     const int h = (int)(k % per);
-    float* r = rho + row * p.px;
-    const int src = h < p.H ? h : g.nx + h;   // left halo [0, H) / right halo [nx + H, nx + 2H)
-    const int dst = h < p.H ? h + g.nx : h;   // periodic image in [H, nx + H)
+    float* r = rho + row * p.px + p.hx;       // r[x] = interior x
+    const int src = h < p.H ? h - p.H : g.nx + h - p.H;   // x in [-H, 0) / [nx, nx + H)
+    const int dst = h < p.H ? src + g.nx : src - g.nx;    // periodic image in [0, nx)
     r[dst] += r[src];
     r[src] = 0.f;
   }
@@ -31,7 +31,7 @@ __global__ void k_fold_y(Geom g, Pad p, float* __restrict__ rho) {
   const int per = 2 * p.H;
   const int64_t total = (int64_t)p.pz * per * g.nx;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(k % g.nx) + p.H;
+    const int x = (int)(k % g.nx) + p.hx;
     const int64_t r2 = k / g.nx;
     const int h = (int)(r2 % per);
     const int z = (int)(r2 / per);
@@ -49,7 +49,7 @@ __global__ void k_fold_z(Geom g, Pad p, float* __restrict__ rho) {
   const int64_t total = (int64_t)per * g.ny * g.nx;
   const int64_t plane = (int64_t)p.py * p.px;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(k % g.nx) + p.H;
+    const int x = (int)(k % g.nx) + p.hx;
     const int64_t r2 = k / g.nx;
     const int y = (int)(r2 % g.ny) + p.H;
     const int h = (int)(r2 / g.ny);
@@ -90,7 +90,8 @@ __global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
       y = (int)((q / per) % g.ny) + p.H;
       z = (int)(q / ((int64_t)per * g.ny)) + p.H;
     }
-    const int ix = wrap_index(x - p.H, g.nx) + p.H;
+    x += p.hx - p.H;  // enumerated x in [0, nx + 2H) -> padded [hx - H, hx + nx + H)
+    const int ix = wrap_index(x - p.hx, g.nx) + p.hx;
     const int iy = wrap_index(y - p.H, g.ny) + p.H;
     const int iz = wrap_index(z - p.H, g.nz) + p.H;
     const int64_t dst = ((int64_t)z * p.py + y) * p.px + x;

@@ -21,21 +21,26 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
     const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
-  __shared__ __align__(128) int tile[TN];
+  __shared__ __align__(128) int tiles[2][TN];  // double buffer: one may still be read by its TMA reduce
+  __shared__ int bsize[32], bstart[33];
+  extern __shared__ float4 dyn[];
+  BankSmem sm{dyn, reinterpret_cast<int*>(dyn + cap), nullptr, bsize, bstart};
   const int nb = bk.count();
   const float qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
   const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
-  float* ftile = reinterpret_cast<float*>(tile);
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  int issued = 0;
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     int cnt = counts[(int64_t)b * kCountStride];
     cnt = cnt < cap ? cnt : cap;
     if (cnt == 0) continue;
-    // the previous brick's reduce must have finished reading the tile
-    if (threadIdx.x == 0) bulk_wait_read<0>();
+    int* tile = tiles[issued & 1];
+    float* ftile = reinterpret_cast<float*>(tile);
+    // all reduces but the most recent (other buffer) have finished reading
+    if (threadIdx.x == 0) bulk_wait_read<1>();
     __syncthreads();
     for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
-    __syncthreads();
     float scale = inv_vcell, inv_scale = 1.f;
     if (FIX) {
       // int32 fixed point, power-of-two scale: every cell sum below 2^30
@@ -49,10 +54,12 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
       scale = ldexpf(1.f, sc);
       inv_scale = ldexpf(1.f, -sc) * inv_vcell;
     }
-    const int64_t base = (int64_t)b * cap;
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const float4 r = rec[base + j];
-      const int cc = rcell[base + j];
+    const int rounds = stage_banked<false, D, TXB>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
+    for (int rr = warp; rr < rounds; rr += nwarp) {
+      if (rr >= bsize[lane]) continue;
+      const int j = bstart[lane] + rr;
+      const float4 r = sm.r[j];
+      const int cc = sm.c[j];
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float wx[S], wy[S], wz[S], dd[S];
       rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
@@ -81,9 +88,10 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
     __syncthreads();
     if (threadIdx.x == 0) {
       const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-      tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.H, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
+      tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
       bulk_commit();
     }
+    ++issued;
   }
   if (threadIdx.x == 0) bulk_wait_read<0>();
   // overflow atoms (full buckets): straight into the padded interior
@@ -123,13 +131,15 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
         auto k = k_spread_tma<S, TAB, FIX>;
+        const size_t dyn = (size_t)cap * (sizeof(float4) + sizeof(int));
+        allow_smem(k, dyn);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
-        k<<<grid, kThreads, 0, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
+        k<<<grid, kThreads, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
         return 0;
       });
     });

@@ -499,7 +499,8 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
     c->pd = Pad{0, nx, ny, nz, 0};
   } else {
     const int lo = (order - 1) / 2, hi = order - 1 - lo, H = lo > hi ? lo : hi;
-    c->pd = Pad{H, (nx + 2 * H + 3) / 4 * 4, ny + 2 * H, nz + 2 * H, (kBrick + order - 1 + 3) / 4 * 4};
+    const int hx = (H + 3) / 4 * 4;
+    c->pd = Pad{H, (hx + nx + H + 3) / 4 * 4, ny + 2 * H, nz + 2 * H, hx};
   }
   c->nxh = nx / 2 + 1;
   c->half = (int64_t)c->nxh * ny * nz;

@@ -33,17 +33,18 @@ struct GreenSpec {
 };
 
 // Halo-padded mesh of the fp32 path: interior cell (x, y, z) lives at padded
-// ((z + H) * py + (y + H)) * px + (x + H).  H = max(ghost below, ghost above)
-// of the stencil; px is rounded to a multiple of 4 (16-byte rows for TMA).
+// ((z + H) * py + (y + H)) * px + (x + hx).  H = max(ghost below, ghost above)
+// of the stencil, hx = H rounded up to 4, px a multiple of 4 (16-byte rows for
+// TMA, 16-byte aligned interior for cuFFT).
 // Every brick tile (brick + halo) is then an in-bounds TMA box: no wrap in the
 // mapping kernels; halo contributions are folded back (make_rho) or filled
 // from their periodic images (fields) by k_halo.cu.
 struct Pad {
   int H, px, py, pz;
-  int txb;  // tile/box x extent: 8 + S - 1 rounded up to a multiple of 4
+  int hx;   // left x halo, H rounded up to 4: the interior starts 16-byte aligned (cuFFT)
   __host__ __device__ int64_t count() const { return (int64_t)px * py * pz; }
-  __host__ __device__ int64_t interior() const { return ((int64_t)H * py + H) * px + H; }
-  __host__ __device__ int64_t at(int x, int y, int z) const { return ((int64_t)(z + H) * py + (y + H)) * px + (x + H); }
+  __host__ __device__ int64_t interior() const { return ((int64_t)H * py + H) * px + hx; }
+  __host__ __device__ int64_t at(int x, int y, int z) const { return ((int64_t)(z + H) * py + (y + H)) * px + (x + hx); }
 };
 
 // device atoms as handed to the context: AoS (N, 3) positions, (N,) charges
