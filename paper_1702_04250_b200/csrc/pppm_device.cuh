@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <type_traits>
 
 #include "pppm_types.h"
@@ -227,13 +228,16 @@ inline int grid_for(int64_t n, int threads = kThreads) {
   return (int)g;
 }
 
-inline int launch_status() {
+inline int launch_status_at(const char* where) {
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
-    set_error(4, cudaGetErrorString(e));
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+    set_error(4, buf);
     return 4;
   }
   return 0;
 }
+#define launch_status() launch_status_at(__func__)
 
 }  // namespace pppm
