@@ -35,6 +35,7 @@ template <int S> struct TmaTile {
   static constexpr int D = kBrick + S - 1;         // brick + stencil halo (y, z)
   static constexpr int TXB = (D + 3) / 4 * 4;      // box x extent (16-byte rows)
   static constexpr int N = TXB * D * D;
+  static constexpr int NP = (N + 31) / 32 * 32;    // buffer stride: 128-byte aligned (TMA smem operand)
 };
 
 template <int S> struct Tile {

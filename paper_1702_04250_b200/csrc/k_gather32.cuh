@@ -38,8 +38,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
   constexpr int F = MODE == 0 ? 3 : 1;
   constexpr uint32_t kBytes = (uint32_t)F * TN * sizeof(float);
   extern __shared__ __align__(128) float dyn_f[];
-  float* tiles = dyn_f;                                     // [2][F][TN]
-  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * F * TN);
+  constexpr int BUF = (F * TN + 31) / 32 * 32;              // 128-byte aligned buffer stride
+  float* tiles = dyn_f;                                     // [2][BUF], buffer = F fields x TN
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);
   int* s_c = reinterpret_cast<int*>(s_r + cap);
   int* s_p = s_c + cap;
   __shared__ __align__(8) uint64_t bar[2];
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
       box(nxt, x, y, z);
       fence_proxy_async_smem();  // generic reads of this buffer (last brick) before the async-proxy write
       mbar_arrive_expect_tx(&bar[buf ^ 1], kBytes);
-      tma_load_4d(tiles + (buf ^ 1) * F * TN, &fmap, &bar[buf ^ 1], x, y, z, 0);
+      tma_load_4d(tiles + (buf ^ 1) * BUF, &fmap, &bar[buf ^ 1], x, y, z, 0);
     }
     int cnt = counts[(int64_t)b * kCountStride];
     cnt = cnt < cap ? cnt : cap;
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
     const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB>(rec, rcell, perm, base, cnt, sm) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
-    const float* tile = tiles + buf * F * TN;
+    const float* tile = tiles + buf * BUF;
     // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
     const int nloop = sort ? (rounds - warp + nwarp - 1) / nwarp : (cnt - (int)threadIdx.x + (int)blockDim.x - 1) / (int)blockDim.x;
     for (int t = 0; t < nloop; ++t) {
@@ -187,7 +188,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
-    const size_t dyn = 2 * (size_t)F * TmaTile<S>::N * sizeof(float) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
+    const size_t dyn = 2 * (size_t)((F * TmaTile<S>::N + 31) / 32 * 32) * sizeof(float) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
       auto k = k_gather_tma<S, TAB, MODE>;

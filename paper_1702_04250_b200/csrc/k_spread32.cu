@@ -21,10 +21,13 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
     const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
-  __shared__ __align__(128) int tiles[2][TN];  // double buffer: one may still be read by its TMA reduce
+  // dynamic smem: [tile 0 | tile 1 | staged atoms]; double-buffered tiles (one
+  // may still be read by its TMA reduce), 128-byte aligned for the bulk copy
+  extern __shared__ __align__(128) int dyn_i[];
+  int* tiles0 = dyn_i;
+  float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
   __shared__ int bsize[32], bstart[33];
-  extern __shared__ float4 dyn[];
-  BankSmem sm{dyn, reinterpret_cast<int*>(dyn + cap), nullptr, bsize, bstart};
+  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + cap), nullptr, bsize, bstart};
   const int nb = bk.count();
   const float qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
   const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
@@ -35,7 +38,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
     int cnt = counts[(int64_t)b * kCountStride];
     cnt = cnt < cap ? cnt : cap;
     if (cnt == 0) continue;
-    int* tile = tiles[issued & 1];
+    int* tile = tiles0 + (issued & 1) * T::NP;
     float* ftile = reinterpret_cast<float*>(tile);
     // all reduces but the most recent (other buffer) have finished reading
     if (threadIdx.x == 0) bulk_wait_read<1>();
@@ -131,7 +134,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
         auto k = k_spread_tma<S, TAB, FIX>;
-        const size_t dyn = (size_t)cap * (sizeof(float4) + sizeof(int));
+        const size_t dyn = 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
