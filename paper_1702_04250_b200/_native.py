@@ -16,7 +16,7 @@ import threading
 import numpy as np
 
 LIB_NAME = "libpppm_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("PPPM_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 OK, ERR_CONFIG, ERR_VALUE, ERR_RUNTIME, ERR_CUDA, ERR_CUFFT, ERR_STATE, ERR_NCCL = range(8)
 MODE_IK, MODE_AD = 0, 1

@@ -37,7 +37,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
   constexpr int F = MODE == 0 ? 3 : 1;
   constexpr uint32_t kBytes = (uint32_t)F * TN * sizeof(float);
-  extern __shared__ __align__(128) float dyn_f[];
+  // dynamic smem, explicitly 128-byte aligned (TMA destination): [2][BUF] tiles, staged atoms
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  float* dyn_f = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));
   constexpr int BUF = (F * TN + 31) / 32 * 32;              // 128-byte aligned buffer stride
   float* tiles = dyn_f;                                     // [2][BUF], buffer = F fields x TN
   float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);
@@ -188,7 +190,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
-    const size_t dyn = 2 * (size_t)((F * TmaTile<S>::N + 31) / 32 * 32) * sizeof(float) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
+    const size_t dyn = 128 + 2 * (size_t)((F * TmaTile<S>::N + 31) / 32 * 32) * sizeof(float) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
       auto k = k_gather_tma<S, TAB, MODE>;

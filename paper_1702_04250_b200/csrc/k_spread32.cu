@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
   // dynamic smem: [tile 0 | tile 1 | staged atoms]; double-buffered tiles (one
   // may still be read by its TMA reduce), 128-byte aligned for the bulk copy
-  extern __shared__ __align__(128) int dyn_i[];
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  int* dyn_i = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));
   int* tiles0 = dyn_i;
   float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
   __shared__ int bsize[32], bstart[33];
@@ -134,7 +135,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
         auto k = k_spread_tma<S, TAB, FIX>;
-        const size_t dyn = 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
+        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
