@@ -31,9 +31,16 @@ constexpr int kCapMax = 1024;      // bucket capacity limit (4 atoms per thread)
 constexpr int kPer = kCapMax / kThreads;
 constexpr int kOvfBlocks = 64;     // extra CTAs per launch for overflow atoms
 
+// Shared tile of a brick for the TMA path.  The padded mesh has a left x halo
+// HX = H rounded up to even (8-byte aligned interior for cuFFT); the TMA box x
+// start must be a multiple of 4 floats (16 bytes), so the box starts SH cells
+// left of the brick's lowest stencil node and is TXB = roundup4(D + SH) wide.
 template <int S> struct TmaTile {
+  static constexpr int lo = (S - 1) / 2, hi = S - 1 - lo, H = lo > hi ? lo : hi;
+  static constexpr int HX = (H + 1) / 2 * 2;
+  static constexpr int SH = ((HX - lo) % 4 + 4) % 4;
   static constexpr int D = kBrick + S - 1;         // brick + stencil halo (y, z)
-  static constexpr int TXB = (D + 3) / 4 * 4;      // box x extent (16-byte rows)
+  static constexpr int TXB = (D + SH + 3) / 4 * 4; // box x extent (16-byte rows)
   static constexpr int N = TXB * D * D;
   static constexpr int NP = (N + 31) / 32 * 32;    // buffer stride: 128-byte aligned (TMA smem operand)
 };
@@ -278,7 +285,7 @@ struct BankSmem {
   int* bstart;  // 33 (bstart[32] = rounds)
 };
 
-template <bool PERM, int D, int TXB>
+template <bool PERM, int D, int TXB, int SH>
 __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, const int* __restrict__ rcell,
                                             const int* __restrict__ perm, int64_t base, int cnt, BankSmem sm) {
   if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
@@ -293,7 +300,7 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
       c[k] = rcell[base + j];
       if (PERM) p[k] = perm[base + j];
       const int lx = c[k] & (kBrick - 1), ly = (c[k] >> 3) & (kBrick - 1), lz = c[k] >> 6;
-      bank[k] = ((lz * D + ly) * TXB + lx) & 31;
+      bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
       rk[k] = atomicAdd(sm.bsize + bank[k], 1);
     }
   }

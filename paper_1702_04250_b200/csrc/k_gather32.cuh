@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
   const int64_t mesh = pd.count();
   auto box = [&](int b, int& x, int& y, int& z) {
     const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-    x = bx * kBrick - lo + pd.hx;
+    x = bx * kBrick - lo + pd.hx - T::SH;
     y = by * kBrick - lo + pd.H;
     z = bz * kBrick - lo + pd.H;
   };
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
     cnt = cnt < cap ? cnt : cap;
     const int64_t base = (int64_t)b * cap;
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
-    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB>(rec, rcell, perm, base, cnt, sm) : 0;
+    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH>(rec, rcell, perm, base, cnt, sm) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_tma(
         float r0 = 0.f, r1 = 0.f, r2 = 0.f;
 #pragma unroll
         for (int bb = 0; bb < S; ++bb) {
-          const float* row = tile + ((lz + a) * D + (ly + bb)) * TXB + lx;
+          const float* row = tile + ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
           if (MODE == 0) {
             float e0 = 0.f, e1 = 0.f, e2 = 0.f;
 #pragma unroll

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
       scale = ldexpf(1.f, sc);
       inv_scale = ldexpf(1.f, -sc) * inv_vcell;
     }
-    const int rounds = stage_banked<false, D, TXB>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
+    const int rounds = stage_banked<false, D, TXB, T::SH>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     for (int rr = warp; rr < rounds; rr += nwarp) {
       if (rr >= bsize[lane]) continue;
       const int j = bstart[lane] + rr;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
 #pragma unroll
         for (int bb = 0; bb < S; ++bb) {
           const float qab = qa * wy[bb];
-          const int row = ((lz + a) * D + (ly + bb)) * TXB + lx;
+          const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
 #pragma unroll
           for (int c = 0; c < S; ++c) {
             if (FIX) atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
     __syncthreads();
     if (threadIdx.x == 0) {
       const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-      tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
+      tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
       bulk_commit();
     }
     ++issued;

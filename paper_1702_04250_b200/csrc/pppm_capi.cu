@@ -187,7 +187,9 @@ static int encode_maps(pppm_ctx* c) {
     fn = reinterpret_cast<Encode>(p);
   }
   const int D = kBrick + c->order - 1;
-  const int txb = (D + 3) / 4 * 4;
+  const int lo = (c->order - 1) / 2;
+  const int sh = ((c->pd.hx - lo) % 4 + 4) % 4;   // = TmaTile<S>::SH
+  const int txb = (D + sh + 3) / 4 * 4;             // = TmaTile<S>::TXB
   const cuuint64_t row = (cuuint64_t)c->pd.px * 4, plane = row * c->pd.py, vol = plane * c->pd.pz;
   {
     cuuint64_t dims[3] = {(cuuint64_t)c->pd.px, (cuuint64_t)c->pd.py, (cuuint64_t)c->pd.pz};
@@ -499,7 +501,7 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
     c->pd = Pad{0, nx, ny, nz, 0};
   } else {
     const int lo = (order - 1) / 2, hi = order - 1 - lo, H = lo > hi ? lo : hi;
-    const int hx = (H + 3) / 4 * 4;
+    const int hx = (H + 1) / 2 * 2;  // must match TmaTile<S>::HX
     c->pd = Pad{H, (hx + nx + H + 3) / 4 * 4, ny + 2 * H, nz + 2 * H, hx};
   }
   c->nxh = nx / 2 + 1;

@@ -34,14 +34,14 @@ struct GreenSpec {
 
 // Halo-padded mesh of the fp32 path: interior cell (x, y, z) lives at padded
 // ((z + H) * py + (y + H)) * px + (x + hx).  H = max(ghost below, ghost above)
-// of the stencil, hx = H rounded up to 4, px a multiple of 4 (16-byte rows for
-// TMA, 16-byte aligned interior for cuFFT).
+// of the stencil, hx = H rounded up to even, px a multiple of 4 (16-byte rows
+// for TMA, 8-byte aligned interior for cuFFT).
 // Every brick tile (brick + halo) is then an in-bounds TMA box: no wrap in the
 // mapping kernels; halo contributions are folded back (make_rho) or filled
 // from their periodic images (fields) by k_halo.cu.
 struct Pad {
   int H, px, py, pz;
-  int hx;   // left x halo, H rounded up to 4: the interior starts 16-byte aligned (cuFFT)
+  int hx;   // left x halo, H rounded up to even: 8-byte aligned interior (cuFFT)
   __host__ __device__ int64_t count() const { return (int64_t)px * py * pz; }
   __host__ __device__ int64_t interior() const { return ((int64_t)H * py + H) * px + hx; }
   __host__ __device__ int64_t at(int x, int y, int z) const { return ((int64_t)(z + H) * py + (y + H)) * px + (x + hx); }
