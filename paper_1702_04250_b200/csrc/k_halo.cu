@@ -2,49 +2,101 @@
 //
 // make_rho adds each brick tile (brick + stencil halo) into the padded charge
 // mesh with one TMA reduce-add; the periodic wrap is then a fold of the halo
-// shell into its periodic images (one warp per padded row).
+// shell into its periodic images, one axis at a time (x over every padded row,
+// then y, then z over the interior), so no cell receives two adds in one pass.
 // The field grids come out of the C2R transforms in the padded interior and
 // the halo is filled from periodic images before the fieldforce TMA loads.
 #include "pppm_device.cuh"
 
 namespace pppm {
 
-// One warp per padded row (z', y') of the used range [0, ny + 2H) x [0, nz + 2H).
-// fold: every halo element adds into its periodic image (atomic: an image row
-// can receive from several halo rows); fill: every halo element takes the value
-// of its periodic image (read from the interior only, so no ordering needed).
-template <bool FOLD>
-__global__ void __launch_bounds__(256) k_halo_rows(Geom g, Pad p, float* __restrict__ f, int nf) {
-  const int ey = g.ny + 2 * p.H, ez = g.nz + 2 * p.H;
-  const int lane = threadIdx.x & 31;
+// x: rows over the whole padded (y, z) range; 2H halo cells per row
+__global__ void k_fold_x(Geom g, Pad p, float* __restrict__ rho) {
+  const int64_t rows = (int64_t)p.py * p.pz;
+  const int per = 2 * p.H;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < rows * per;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = k / per;
+    const int h = (int)(k % per);
+    float* r = rho + row * p.px + p.hx;       // r[x] = interior x
+    const int src = h < p.H ? h - p.H : g.nx + h - p.H;   // x in [-H, 0) / [nx, nx + H)
+    const int dst = h < p.H ? src + g.nx : src - g.nx;    // periodic image in [0, nx)
+    r[dst] += r[src];
+    r[src] = 0.f;
+  }
+}
+
+// y: for every padded z, interior x
+__global__ void k_fold_y(Geom g, Pad p, float* __restrict__ rho) {
+  const int per = 2 * p.H;
+  const int64_t total = (int64_t)p.pz * per * g.nx;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(k % g.nx) + p.hx;
+    const int64_t r2 = k / g.nx;
+    const int h = (int)(r2 % per);
+    const int z = (int)(r2 / per);
+    const int ys = h < p.H ? h : g.ny + h;
+    const int yd = h < p.H ? h + g.ny : h;
+    float* base = rho + (int64_t)z * p.py * p.px + x;
+    base[(int64_t)yd * p.px] += base[(int64_t)ys * p.px];
+    base[(int64_t)ys * p.px] = 0.f;
+  }
+}
+
+// z: interior x, y
+__global__ void k_fold_z(Geom g, Pad p, float* __restrict__ rho) {
+  const int per = 2 * p.H;
+  const int64_t total = (int64_t)per * g.ny * g.nx;
+  const int64_t plane = (int64_t)p.py * p.px;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(k % g.nx) + p.hx;
+    const int64_t r2 = k / g.nx;
+    const int y = (int)(r2 % g.ny) + p.H;
+    const int h = (int)(r2 / g.ny);
+    const int zs = h < p.H ? h : g.nz + h;
+    const int zd = h < p.H ? h + g.nz : h;
+    float* base = rho + (int64_t)y * p.px + x;
+    base[zd * plane] += base[zs * plane];
+    base[zs * plane] = 0.f;
+  }
+}
+
+// halo fill: every cell of [0, nx+2H) x [0, ny+2H) x [0, nz+2H) outside the
+// interior takes the value of its periodic image, for `nf` fields
+__global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
+  const int ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H, per = 2 * p.H;
+  const int64_t ra = (int64_t)per * ey * ex;       // z halo planes
+  const int64_t rb = (int64_t)g.nz * per * ex;     // y halo rows, interior z
+  const int64_t rc = (int64_t)g.nz * g.ny * per;   // x halo cells, interior y, z
+  const int64_t total = ra + rb + rc;
   const int64_t mesh = p.count();
-  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < ey * ez;
-       row += (gridDim.x * blockDim.x) >> 5) {
-    const int yp = row % ey, zp = row / ey;                  // padded y, z
-    const int iy = wrap_index(yp - p.H, g.ny) + p.H, iz = wrap_index(zp - p.H, g.nz) + p.H;
-    const bool halo_row = (iy != yp) || (iz != zp);
-    const int64_t dst_row = ((int64_t)zp * p.py + yp) * p.px;
-    const int64_t img_row = ((int64_t)iz * p.py + iy) * p.px;
-    // halo rows: all of [hx - H, hx + nx + H); interior rows: the 2H x-halo cells
-    const int n = halo_row ? g.nx + 2 * p.H : 2 * p.H;
-    for (int k = lane; k < n; k += 32) {
-      int xp;
-      if (halo_row) xp = p.hx - p.H + k;
-      else xp = k < p.H ? p.hx - p.H + k : p.hx + g.nx + (k - p.H);
-      const int ix = wrap_index(xp - p.hx, g.nx) + p.hx;
-      if (!halo_row && ix == xp) continue;
-      for (int fi = 0; fi < nf; ++fi) {
-        float* fb = f + fi * mesh;
-        if (FOLD) {
-          if (halo_row || ix != xp) {
-            const float v = fb[dst_row + xp];
-            if (v != 0.f) atomicAdd(fb + img_row + ix, v);
-          }
-        } else {
-          fb[dst_row + xp] = fb[img_row + ix];
-        }
-      }
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    int x, y, z;
+    if (k < ra) {
+      x = (int)(k % ex);
+      y = (int)((k / ex) % ey);
+      const int h = (int)(k / ((int64_t)ex * ey));
+      z = h < p.H ? h : g.nz + h;
+    } else if (k < ra + rb) {
+      const int64_t q = k - ra;
+      x = (int)(q % ex);
+      const int h = (int)((q / ex) % per);
+      y = h < p.H ? h : g.ny + h;
+      z = (int)(q / ((int64_t)ex * per)) + p.H;
+    } else {
+      const int64_t q = k - ra - rb;
+      const int h = (int)(q % per);
+      x = h < p.H ? h : g.nx + h;
+      y = (int)((q / per) % g.ny) + p.H;
+      z = (int)(q / ((int64_t)per * g.ny)) + p.H;
     }
+    x += p.hx - p.H;  // enumerated x in [0, nx + 2H) -> padded [hx - H, hx + nx + H)
+    const int ix = wrap_index(x - p.hx, g.nx) + p.hx;
+    const int iy = wrap_index(y - p.H, g.ny) + p.H;
+    const int iz = wrap_index(z - p.H, g.nz) + p.H;
+    const int64_t dst = ((int64_t)z * p.py + y) * p.px + x;
+    const int64_t src = ((int64_t)iz * p.py + iy) * p.px + ix;
+    for (int fi = 0; fi < nf; ++fi) f[fi * mesh + dst] = f[fi * mesh + src];
   }
 }
 
@@ -70,15 +122,17 @@ __global__ void k_pad_in(Geom g, Pad p, const double* __restrict__ src, float* _
 
 int launch_fold_halo(const Geom& g, const Pad& p, float* rho, cudaStream_t s) {
   if (p.H == 0) return 0;
-  const int64_t rows = (int64_t)(g.ny + 2 * p.H) * (g.nz + 2 * p.H);
-  k_halo_rows<true><<<grid_for(rows * 32), 256, 0, s>>>(g, p, rho, 1);
+  k_fold_x<<<grid_for((int64_t)p.py * p.pz * 2 * p.H), kThreads, 0, s>>>(g, p, rho);
+  k_fold_y<<<grid_for((int64_t)p.pz * 2 * p.H * g.nx), kThreads, 0, s>>>(g, p, rho);
+  k_fold_z<<<grid_for((int64_t)2 * p.H * g.ny * g.nx), kThreads, 0, s>>>(g, p, rho);
   return launch_status();
 }
 
 int launch_fill_halo(const Geom& g, const Pad& p, float* f, int nf, cudaStream_t s) {
   if (p.H == 0) return 0;
-  const int64_t rows = (int64_t)(g.ny + 2 * p.H) * (g.nz + 2 * p.H);
-  k_halo_rows<false><<<grid_for(rows * 32), 256, 0, s>>>(g, p, f, nf);
+  const int64_t ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H;
+  const int64_t total = 2 * p.H * ey * ex + (int64_t)g.nz * 2 * p.H * ex + (int64_t)g.nz * g.ny * 2 * p.H;
+  k_fill<<<grid_for(total), kThreads, 0, s>>>(g, p, f, nf);
   return launch_status();
 }
 

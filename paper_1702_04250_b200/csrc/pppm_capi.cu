@@ -293,7 +293,7 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     TRY(launch_spread_brick(c->spread_variant & 1, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
                             c->bk, c->pd, c->rho_map, c->tab.as<float>(), c->rho.as<float>(), c->stream));
-    c->launches += 2;  // spread + halo fold
+    c->launches += 4;  // spread + 3 halo folds
   }
   c->have_rho = true;
   return PPPM_OK;
