@@ -51,6 +51,12 @@ enum pppm_precision { PPPM_PREC_FP64 = 0, PPPM_PREC_MIXED = 1 };  /* mixed: fp32
 enum pppm_dtype { PPPM_F64 = 0, PPPM_F32 = 1 };
 enum pppm_memory { PPPM_HOST = 0, PPPM_DEVICE = 1 };
 enum pppm_influence { PPPM_INFLUENCE_PME = 0, PPPM_INFLUENCE_OPTIMAL = 1 };
+enum pppm_slab_buffer_id {
+  PPPM_BUF_RHO_GHOST_LO = 0, PPPM_BUF_RHO_GHOST_HI = 1, PPPM_BUF_RECV_LO = 2, PPPM_BUF_RECV_HI = 3,
+  PPPM_BUF_A2A_SEND = 4, PPPM_BUF_A2A_RECV = 5, PPPM_BUF_A2A_SEND_F = 6, PPPM_BUF_A2A_RECV_F = 7,
+  PPPM_BUF_ENERGY = 8, PPPM_BUF_FIELD_BOTTOM = 9, PPPM_BUF_FIELD_TOP = 10, PPPM_BUF_FIELD_GHOST_LO = 11,
+  PPPM_BUF_FIELD_GHOST_HI = 12
+};
 enum pppm_phase { PPPM_PHASE_MAKE_RHO = 1, PPPM_PHASE_POISSON = 2, PPPM_PHASE_FIELDFORCE = 4, PPPM_PHASE_ALL = 7 };
 
 /* library ---------------------------------------------------------------- */
@@ -123,6 +129,29 @@ int pppm_ctx_time_steps(pppm_ctx* ctx, int steps, int warmup, int flush_l2, doub
  * (0: float CAS shared atomics, 1: int32 fixed-point shared atomics [default]),
  * kernel 1 = fp32 fieldforce (0: bucket order, 1: cell-sorted in shared memory [default]) */
 int pppm_ctx_set_variant(pppm_ctx* ctx, int kernel, int variant);
+/* z-slab decomposition over `nslabs` GPUs (no counterpart in the reference,
+ * which is single-process).  Slab `rank` owns global planes
+ * [rank*nz/P, (rank+1)*nz/P) and, in k-space, ky rows [rank*ny/P, ...).  The
+ * device halves of a step are below; between them the host exchanges the
+ * buffers named by pppm_slab_buffer over NCCL on the context stream:
+ *   make_rho -> RHO_GHOST_LO to slab-1 / RHO_GHOST_HI to slab+1 (received into
+ *   RECV_HI / RECV_LO) -> add_ghosts -> fft_fwd -> all-to-all A2A_SEND->A2A_RECV
+ *   -> green -> all-reduce ENERGY, all-to-all A2A_SEND_F->A2A_RECV_F -> fft_bwd
+ *   -> FIELD_BOTTOM to slab-1 (into its FIELD_GHOST_HI), FIELD_TOP to slab+1
+ *   (into its FIELD_GHOST_LO), per field -> fieldforce.  Mixed precision only. */
+int pppm_ctx_create_slab(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly,
+                         double lz, int order, int mode, int precision, double alpha,
+                         double coulomb_constant, double dielectric, int nslabs, int rank);
+int pppm_ctx_stream(pppm_ctx* ctx, void** stream);       /* the context's cudaStream_t */
+/* info[10]: nslabs, rank, z0, nzl, y0, nyl, H, px, py, pz */
+int pppm_slab_info(pppm_ctx* ctx, int* info);
+int pppm_slab_buffer(pppm_ctx* ctx, int id, int field, void** ptr, size_t* bytes);
+int pppm_slab_make_rho(pppm_ctx* ctx);
+int pppm_slab_add_ghosts(pppm_ctx* ctx);
+int pppm_slab_fft_fwd(pppm_ctx* ctx);
+int pppm_slab_green(pppm_ctx* ctx);
+int pppm_slab_fft_bwd(pppm_ctx* ctx);
+int pppm_slab_fieldforce(pppm_ctx* ctx);
 /* kernels launched by one step (for the bench's gpu_launches claim) */
 int pppm_ctx_launches_per_step(pppm_ctx* ctx, int* launches);
 

@@ -68,6 +68,17 @@ PROTOTYPES = {
     "pppm_ctx_time_steps": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
     "pppm_ctx_launches_per_step": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "pppm_ctx_set_variant": (_c_int, [_vp, _c_int, _c_int]),
+    "pppm_ctx_create_slab": (_c_int, [ctypes.POINTER(_vp), _c_int, _c_int, _c_int, _c_int, _c_dbl, _c_dbl,
+                                      _c_dbl, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl, _c_int, _c_int]),
+    "pppm_ctx_stream": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "pppm_slab_info": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
+    "pppm_slab_buffer": (_c_int, [_vp, _c_int, _c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)]),
+    "pppm_slab_make_rho": (_c_int, [_vp]),
+    "pppm_slab_add_ghosts": (_c_int, [_vp]),
+    "pppm_slab_fft_fwd": (_c_int, [_vp]),
+    "pppm_slab_green": (_c_int, [_vp]),
+    "pppm_slab_fft_bwd": (_c_int, [_vp]),
+    "pppm_slab_fieldforce": (_c_int, [_vp]),
 }
 
 

@@ -218,19 +218,24 @@ __device__ double influence_at(const GreenSpec& s, int ix, int iy, int iz) {
 }
 
 // half spectrum (nz, ny, nx/2+1) in the compute type, plus optional full grid in fp64
+// half spectrum of the ky chunk [y0, y0 + nyl) as (nz, nyl, nx/2+1) in the
+// compute type (the transposed layout of the slab FFT; y0 = 0, nyl = ny on one
+// GPU), or the full (nz, ny, nx) grid in fp64 (g_full)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_influence(GreenSpec s, T* __restrict__ g_half, double* __restrict__ g_full) {
+__global__ void __launch_bounds__(kThreads) k_influence(GreenSpec s, int y0, int nyl, T* __restrict__ g_half,
+                                                         double* __restrict__ g_full) {
   const int nxh = s.nx / 2 + 1;
-  const int64_t total = g_full ? (int64_t)s.nx * s.ny * s.nz : (int64_t)nxh * s.ny * s.nz;
   const int width = g_full ? s.nx : nxh;
+  const int rows = g_full ? s.ny : nyl;
+  const int64_t total = (int64_t)width * rows * s.nz;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int ix = (int)(i % width);
     const int64_t r = i / width;
-    const int iy = (int)(r % s.ny), iz = (int)(r / s.ny);
-    const double v = influence_at(s, ix, iy, iz);
+    const int iyl = (int)(r % rows), iz = (int)(r / rows);
+    const double v = influence_at(s, ix, g_full ? iyl : y0 + iyl, iz);
     if (g_full) g_full[i] = v;
-    if (g_half && ix < nxh) g_half[((int64_t)iz * s.ny + iy) * nxh + ix] = (T)v;
+    else g_half[i] = (T)v;
   }
 }
 
@@ -254,20 +259,22 @@ template <typename T> struct Cplx;
 template <> struct Cplx<float> { using C = cuFloatComplex; };
 template <> struct Cplx<double> { using C = cuDoubleComplex; };
 
+// Layout (kz, ky - y0, kx) with nyl ky rows: the whole half spectrum on one GPU
+// (y0 = 0, nyl = ny), the transposed ky chunk of a z-slab otherwise.
 template <typename T, int MODE, bool FIELDS>  // MODE 0 = ik, 1 = ad
 __global__ void __launch_bounds__(kThreads) k_green(
-    const typename Cplx<T>::C* __restrict__ rho_hat, const T* __restrict__ green, int nx, int ny, int nz,
+    const typename Cplx<T>::C* __restrict__ rho_hat, const T* __restrict__ green, int nx, int y0, int nyl, int nz,
     const T* __restrict__ ikx, const T* __restrict__ iky, const T* __restrict__ ikz, T inv_m,
     typename Cplx<T>::C* __restrict__ out, double* __restrict__ partial) {
   using C = typename Cplx<T>::C;
   const int nxh = nx / 2 + 1;
-  const int64_t half = (int64_t)nxh * ny * nz;
+  const int64_t half = (int64_t)nxh * nyl * nz;
   double e = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < half;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int kx = (int)(i % nxh);
     const int64_t r = i / nxh;
-    const int ky = (int)(r % ny), kz = (int)(r / ny);
+    const int ky = y0 + (int)(r % nyl), kz = (int)(r / nyl);
     const C c = rho_hat[i];
     const T gv = green[i];
     const double re = (double)c.x, im = (double)c.y;
@@ -507,11 +514,11 @@ int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const 
   return st ? st : launch_status();
 }
 
-int launch_influence(bool f64, const GreenSpec& gs, void* g_half, double* g_full, cudaStream_t s) {
-  const int64_t total = g_full ? (int64_t)gs.nx * gs.ny * gs.nz : (int64_t)(gs.nx / 2 + 1) * gs.ny * gs.nz;
+int launch_influence(bool f64, const GreenSpec& gs, int y0, int nyl, void* g_half, double* g_full, cudaStream_t s) {
+  const int64_t total = g_full ? (int64_t)gs.nx * gs.ny * gs.nz : (int64_t)(gs.nx / 2 + 1) * nyl * gs.nz;
   const int grid = grid_for(total);
-  if (f64) k_influence<double><<<grid, kThreads, 0, s>>>(gs, (double*)g_half, g_full);
-  else k_influence<float><<<grid, kThreads, 0, s>>>(gs, (float*)g_half, g_full);
+  if (f64) k_influence<double><<<grid, kThreads, 0, s>>>(gs, y0, nyl, (double*)g_half, g_full);
+  else k_influence<float><<<grid, kThreads, 0, s>>>(gs, y0, nyl, (float*)g_half, g_full);
   return launch_status();
 }
 
@@ -530,7 +537,7 @@ int launch_green(bool f64, int mode, bool fields, const void* rho_hat, const voi
     constexpr bool FL = decltype(FIELDS_)::value;
     using C = typename Cplx<T>::C;
     const T* k = (const T*)ik;
-    k_green<T, MODE, FL><<<kGreenBlocks, kThreads, 0, s>>>((const C*)rho_hat, (const T*)green, g.nx, g.ny, g.nz, k,
+    k_green<T, MODE, FL><<<kGreenBlocks, kThreads, 0, s>>>((const C*)rho_hat, (const T*)green, g.nx, g.y0, g.nyl, g.nz, k,
                                                            k + g.nx, k + g.nx + g.ny, (T)inv_m, (C*)out, partial);
   };
   auto by_mode = [&](auto T_) {

@@ -69,7 +69,9 @@ inline void allow_smem(K kernel, size_t bytes) {
 constexpr int kBinUnroll = 4;  // atoms per thread in flight (latency of the slot atomics)
 
 // One pass: particle_map (bit-exact nodes) -> brick, slot = atomicAdd(count),
-// record into the bucket (or the overflow list).  Also the global max |q|
+// record into the bucket (or the overflow list).  On a z-slab only the atoms
+// whose wrapped node_z lies in the slab are binned (the others belong to
+// another slab); overflow records carry slab-local nodes.  Also the global max |q|
 // (as float bits, counts[nb + 1]) for the make_rho fixed-point scale.
 template <int S, bool TAB, typename TIn>
 __global__ void __launch_bounds__(kThreads) k_bin_fixed(
@@ -106,6 +108,8 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
       n0 = n0 >= g.nx ? n0 - g.nx : n0;
       n1 = n1 >= g.ny ? n1 - g.ny : n1;
       n2 = n2 >= g.nz ? n2 - g.nz : n2;
+      n2 -= g.z0;                                    // slab-local plane
+      if (n2 < 0 || n2 >= g.nzl) continue;           // another slab's atom
       b[u] = ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
       lc[u] = (((n2 % kBrick) * kBrick) + (n1 % kBrick)) * kBrick + (n0 % kBrick);
       pk[u] = n0 | (n1 << 10) | (n2 << 20);

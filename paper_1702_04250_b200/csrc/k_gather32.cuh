@@ -156,11 +156,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather_tma(
     rows_f32<S, TAB, MODE == 1>(r.z, ta, td, az, dz);
     float s0 = 0.f, s1 = 0.f, s2 = 0.f;
     for (int a = 0; a < S; ++a) {
-      const int iz = wrap_index(n2 - lo + a, g.nz);
       for (int bb = 0; bb < S; ++bb) {
-        const int iy = wrap_index(n1 - lo + bb, g.ny);
         for (int c = 0; c < S; ++c) {
-          const int64_t gi = pd.at(wrap_index(n0 - lo + c, g.nx), iy, iz);
+          const int64_t gi = pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a);  // halos / ghosts filled
           if (MODE == 0) {
             const float w = az[a] * ay[bb] * ax[c];
             s0 += w * __ldg(fields + gi);

@@ -65,9 +65,10 @@ __global__ void k_fold_z(Geom g, Pad p, float* __restrict__ rho) {
 // interior takes the value of its periodic image, for `nf` fields
 __global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
   const int ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H, per = 2 * p.H;
-  const int64_t ra = (int64_t)per * ey * ex;       // z halo planes
-  const int64_t rb = (int64_t)g.nz * per * ex;     // y halo rows, interior z
-  const int64_t rc = (int64_t)g.nz * g.ny * per;   // x halo cells, interior y, z
+  const int nzl = p.pz - 2 * p.H;                  // interior planes of this slab
+  const int64_t ra = p.zper ? (int64_t)per * ey * ex : 0;  // z halo planes (one GPU only)
+  const int64_t rb = (int64_t)nzl * per * ex;      // y halo rows, interior z
+  const int64_t rc = (int64_t)nzl * g.ny * per;    // x halo cells, interior y, z
   const int64_t total = ra + rb + rc;
   const int64_t mesh = p.count();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
@@ -76,7 +77,7 @@ __global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
       x = (int)(k % ex);
       y = (int)((k / ex) % ey);
       const int h = (int)(k / ((int64_t)ex * ey));
-      z = h < p.H ? h : g.nz + h;
+      z = h < p.H ? h : nzl + h;
     } else if (k < ra + rb) {
       const int64_t q = k - ra;
       x = (int)(q % ex);
@@ -93,7 +94,7 @@ __global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
     x += p.hx - p.H;  // enumerated x in [0, nx + 2H) -> padded [hx - H, hx + nx + H)
     const int ix = wrap_index(x - p.hx, g.nx) + p.hx;
     const int iy = wrap_index(y - p.H, g.ny) + p.H;
-    const int iz = wrap_index(z - p.H, g.nz) + p.H;
+    const int iz = p.zper ? wrap_index(z - p.H, nzl) + p.H : z;
     const int64_t dst = ((int64_t)z * p.py + y) * p.px + x;
     const int64_t src = ((int64_t)iz * p.py + iy) * p.px + ix;
     for (int fi = 0; fi < nf; ++fi) f[fi * mesh + dst] = f[fi * mesh + src];
@@ -101,7 +102,7 @@ __global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
 }
 
 __global__ void k_unpad(Geom g, Pad p, const float* __restrict__ src, double* __restrict__ dst) {
-  const int64_t total = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t total = (int64_t)g.nx * g.ny * g.nzl;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
     const int x = (int)(k % g.nx);
     const int y = (int)((k / g.nx) % g.ny);
@@ -111,7 +112,7 @@ __global__ void k_unpad(Geom g, Pad p, const float* __restrict__ src, double* __
 }
 
 __global__ void k_pad_in(Geom g, Pad p, const double* __restrict__ src, float* __restrict__ dst) {
-  const int64_t total = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t total = (int64_t)g.nx * g.ny * g.nzl;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
     const int x = (int)(k % g.nx);
     const int y = (int)((k / g.nx) % g.ny);
@@ -124,25 +125,25 @@ int launch_fold_halo(const Geom& g, const Pad& p, float* rho, cudaStream_t s) {
   if (p.H == 0) return 0;
   k_fold_x<<<grid_for((int64_t)p.py * p.pz * 2 * p.H), kThreads, 0, s>>>(g, p, rho);
   k_fold_y<<<grid_for((int64_t)p.pz * 2 * p.H * g.nx), kThreads, 0, s>>>(g, p, rho);
-  k_fold_z<<<grid_for((int64_t)2 * p.H * g.ny * g.nx), kThreads, 0, s>>>(g, p, rho);
+  if (p.zper) k_fold_z<<<grid_for((int64_t)2 * p.H * g.ny * g.nx), kThreads, 0, s>>>(g, p, rho);
   return launch_status();
 }
 
 int launch_fill_halo(const Geom& g, const Pad& p, float* f, int nf, cudaStream_t s) {
   if (p.H == 0) return 0;
-  const int64_t ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H;
-  const int64_t total = 2 * p.H * ey * ex + (int64_t)g.nz * 2 * p.H * ex + (int64_t)g.nz * g.ny * 2 * p.H;
+  const int64_t ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H, nzl = p.pz - 2 * p.H;
+  const int64_t total = (p.zper ? 2 * p.H * ey * ex : 0) + nzl * 2 * p.H * ex + nzl * g.ny * 2 * p.H;
   k_fill<<<grid_for(total), kThreads, 0, s>>>(g, p, f, nf);
   return launch_status();
 }
 
 int launch_unpad(const Geom& g, const Pad& p, const float* src, double* dst, cudaStream_t s) {
-  k_unpad<<<grid_for((int64_t)g.nx * g.ny * g.nz), kThreads, 0, s>>>(g, p, src, dst);
+  k_unpad<<<grid_for((int64_t)g.nx * g.ny * g.nzl), kThreads, 0, s>>>(g, p, src, dst);
   return launch_status();
 }
 
 int launch_pad_in(const Geom& g, const Pad& p, const double* src, float* dst, cudaStream_t s) {
-  k_pad_in<<<grid_for((int64_t)g.nx * g.ny * g.nz), kThreads, 0, s>>>(g, p, src, dst);
+  k_pad_in<<<grid_for((int64_t)g.nx * g.ny * g.nzl), kThreads, 0, s>>>(g, p, src, dst);
   return launch_status();
 }
 

@@ -109,15 +109,16 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
     rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
     rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
     const float q = r.w * inv_vcell;
+    // unwrapped slab-local coordinates: stencil cells past the edges land in the
+    // halo / ghost planes and are folded or exchanged like the tiles' halos
 #pragma unroll
     for (int a = 0; a < S; ++a) {
-      const int iz = wrap_index(n2 - lo + a, g.nz);
 #pragma unroll
       for (int bb = 0; bb < S; ++bb) {
-        const int iy = wrap_index(n1 - lo + bb, g.ny);
         const float p = q * wz[a] * wy[bb];
+        float* row = rho + pd.at(n0 - lo, n1 - lo + bb, n2 - lo + a);
 #pragma unroll
-        for (int c = 0; c < S; ++c) atomicAdd(rho + pd.at(wrap_index(n0 - lo + c, g.nx), iy, iz), p * wx[c]);
+        for (int c = 0; c < S; ++c) atomicAdd(row + c, p * wx[c]);
       }
     }
   }

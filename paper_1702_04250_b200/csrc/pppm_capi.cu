@@ -110,7 +110,7 @@ struct pppm_ctx {
   int n_points = 0;  // 0 => exact rows
   int green_kind = -1;  // -1: none or uploaded from a foreign plan
   double green_floor = 1e-10;
-  int64_t M = 0, half = 0;
+  int64_t M = 0, half = 0, Ml = 0;  // global mesh, spectrum held here, local (slab) mesh
   Pad pd{};                          // fp32: halo-padded meshes; fp64: H = 0 (dense)
   CUtensorMap rho_map{}, field_map{};  // TMA descriptors of the padded fp32 meshes
   int nxh = 0;
@@ -126,6 +126,12 @@ struct pppm_ctx {
   int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SORTED;
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force;
+  // z-slab decomposition (P > 1): 2D spectra of the local planes, all-to-all
+  // buffers, received ghost planes of the charge mesh
+  int P = 1, rank = 0;
+  DevBuf spec2d, a2a_send, a2a_recv, ghost_lo, ghost_hi;
+  cufftHandle p2f = 0, pz = 0, p2b = 0;
+  bool slab_plans = false;
   int64_t n_res = 0;
   int res_dtype = PPPM_F64;
   int* h_err = nullptr;
@@ -373,11 +379,11 @@ static int flat_to_host(pppm_ctx* c, const void* dev, double* host, int64_t coun
 // one (padded) device mesh -> dense host fp64 (nz, ny, nx)
 static int mesh_to_host(pppm_ctx* c, const void* dev, double* host) {
   if (c->fp64()) {
-    CU(cudaMemcpyAsync(host, dev, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(host, dev, sizeof(double) * c->Ml, cudaMemcpyDeviceToHost, c->stream));
   } else {
-    TRY(c->out_stage.ensure(sizeof(double) * c->M));
+    TRY(c->out_stage.ensure(sizeof(double) * c->Ml));
     TRY(launch_unpad(c->g, c->pd, (const float*)dev, c->out_stage.as<double>(), c->stream));
-    CU(cudaMemcpyAsync(host, c->out_stage.p, sizeof(double) * c->M, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(host, c->out_stage.p, sizeof(double) * c->Ml, cudaMemcpyDeviceToHost, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   return PPPM_OK;
@@ -386,10 +392,10 @@ static int mesh_to_host(pppm_ctx* c, const void* dev, double* host) {
 // dense host fp64 mesh -> (padded) device mesh interior
 static int mesh_from_host(pppm_ctx* c, void* dev, const double* host) {
   if (c->fp64()) {
-    CU(cudaMemcpyAsync(dev, host, sizeof(double) * c->M, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(dev, host, sizeof(double) * c->Ml, cudaMemcpyHostToDevice, c->stream));
   } else {
-    TRY(c->out_stage.ensure(sizeof(double) * c->M));
-    CU(cudaMemcpyAsync(c->out_stage.p, host, sizeof(double) * c->M, cudaMemcpyHostToDevice, c->stream));
+    TRY(c->out_stage.ensure(sizeof(double) * c->Ml));
+    CU(cudaMemcpyAsync(c->out_stage.p, host, sizeof(double) * c->Ml, cudaMemcpyHostToDevice, c->stream));
     TRY(launch_pad_in(c->g, c->pd, c->out_stage.as<double>(), (float*)dev, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
@@ -469,9 +475,9 @@ int pppm_table_rows(int device, int order, int n_points, double* assign, double*
   return st;
 }
 
-int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
-                    int order, int mode, int precision, double alpha, double coulomb_constant,
-                    double dielectric) {
+static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
+                      int order, int mode, int precision, double alpha, double coulomb_constant,
+                      double dielectric, int P, int rank) {
   if (!out) return fail(PPPM_ERR_VALUE, "null output pointer");
   *out = nullptr;
   if (order < 3 || order > 7) return fail(PPPM_ERR_CONFIG, "stencil order must be one of (3, 4, 5, 6, 7)");
@@ -483,8 +489,17 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
     return fail(PPPM_ERR_CONFIG, "precision must be fp64 or mixed");
   if (!(alpha > 0.0)) return fail(PPPM_ERR_CONFIG, "alpha must be positive");
   if (!(dielectric > 0.0)) return fail(PPPM_ERR_CONFIG, "dielectric must be positive");
+  if (P < 1 || rank < 0 || rank >= P) return fail(PPPM_ERR_VALUE, "bad slab rank / count");
+  if (P > 1) {
+    if (precision != PPPM_PREC_MIXED) return fail(PPPM_ERR_CONFIG, "z-slab decomposition runs in mixed precision");
+    if (nz % P || ny % P) return fail(PPPM_ERR_CONFIG, "nz and ny must be divisible by the slab count");
+    const int lo = (order - 1) / 2, hi = order - 1 - lo;
+    if (nz / P < (lo > hi ? lo : hi)) return fail(PPPM_ERR_CONFIG, "slabs thinner than the stencil ghost depth");
+  }
   CU(cudaSetDevice(device));
   pppm_ctx* c = new pppm_ctx();
+  c->P = P;
+  c->rank = rank;
   c->device = device;
   c->g.nx = nx; c->g.ny = ny; c->g.nz = nz;
   c->g.lx = lx; c->g.ly = ly; c->g.lz = lz;
@@ -492,20 +507,25 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
   c->g.ihx = 1.0 / c->g.hx; c->g.ihy = 1.0 / c->g.hy; c->g.ihz = 1.0 / c->g.hz;
   c->bk.nbx = (nx + kBrick - 1) / kBrick;
   c->bk.nby = (ny + kBrick - 1) / kBrick;
-  c->bk.nbz = (nz + kBrick - 1) / kBrick;
+  c->g.nzl = nz / P;
+  c->g.z0 = rank * c->g.nzl;
+  c->g.nyl = ny / P;
+  c->g.y0 = rank * c->g.nyl;
+  c->bk.nbz = (c->g.nzl + kBrick - 1) / kBrick;
   c->order = order; c->mode = mode; c->prec = precision;
   c->alpha = alpha;
   c->cscale = coulomb_constant / dielectric;  // model.py:244-247
   c->M = (int64_t)nx * ny * nz;
+  c->Ml = (int64_t)nx * ny * (nz / P);
   if (precision == PPPM_PREC_FP64) {
-    c->pd = Pad{0, nx, ny, nz, 0};
+    c->pd = Pad{0, nx, ny, nz, 0, 1};
   } else {
     const int lo = (order - 1) / 2, hi = order - 1 - lo, H = lo > hi ? lo : hi;
     const int hx = (H + 1) / 2 * 2;  // must match TmaTile<S>::HX
-    c->pd = Pad{H, (hx + nx + H + 3) / 4 * 4, ny + 2 * H, nz + 2 * H, hx};
+    c->pd = Pad{H, (hx + nx + H + 3) / 4 * 4, ny + 2 * H, c->g.nzl + 2 * H, hx, P == 1};
   }
   c->nxh = nx / 2 + 1;
-  c->half = (int64_t)c->nxh * ny * nz;
+  c->half = (int64_t)c->nxh * c->g.nyl * nz;  // this context's spectrum (ky chunk on a slab)
   auto cleanup = [&](int st) {
     pppm_ctx_destroy(c);
     return st;
@@ -525,6 +545,15 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
     st = encode_maps(c);
   }
   if (st == PPPM_OK) st = c->green.ensure(rs * c->half);
+  if (st == PPPM_OK && P > 1) {
+    const int64_t nh = c->half * c->nfields();
+    const int64_t gb = (int64_t)c->pd.H * c->pd.py * c->pd.px;
+    st = c->spec2d.ensure(cs * nh);
+    if (st == PPPM_OK) st = c->a2a_send.ensure(cs * nh);
+    if (st == PPPM_OK) st = c->a2a_recv.ensure(cs * nh);
+    if (st == PPPM_OK) st = c->ghost_lo.ensure(rs * gb);
+    if (st == PPPM_OK) st = c->ghost_hi.ensure(rs * gb);
+  }
   if (st == PPPM_OK) st = c->ikc.ensure(rs * (nx + ny + nz));
   if (st == PPPM_OK) st = c->ik64.ensure(8 * (nx + ny + nz));
   if (st == PPPM_OK) st = c->partial.ensure(8 * kGreenBlocks);
@@ -556,6 +585,20 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
   return PPPM_OK;
 }
 
+int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
+                    int order, int mode, int precision, double alpha, double coulomb_constant,
+                    double dielectric) {
+  return ctx_create(out, device, nx, ny, nz, lx, ly, lz, order, mode, precision, alpha, coulomb_constant,
+                    dielectric, 1, 0);
+}
+
+int pppm_ctx_create_slab(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
+                         int order, int mode, int precision, double alpha, double coulomb_constant,
+                         double dielectric, int nslabs, int rank) {
+  return ctx_create(out, device, nx, ny, nz, lx, ly, lz, order, mode, precision, alpha, coulomb_constant,
+                    dielectric, nslabs, rank);
+}
+
 int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
@@ -572,7 +615,12 @@ int pppm_ctx_destroy(pppm_ctx* c) {
     cufftDestroy(c->fwd);
     cufftDestroy(c->bwd);
   }
-  DevBuf* bufs[] = {&c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
+  if (c->slab_plans) {
+    cufftDestroy(c->p2f);
+    cufftDestroy(c->pz);
+    cufftDestroy(c->p2b);
+  }
+  DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
                     &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force};
@@ -636,7 +684,7 @@ int pppm_ctx_build_influence(pppm_ctx* c, int kind, double deconv_floor) {
     return fail(PPPM_ERR_CONFIG, "unknown influence variant");
   GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, deconv_floor,
               kind == PPPM_INFLUENCE_OPTIMAL};
-  TRY(launch_influence(c->fp64(), s, c->green.p, nullptr, c->stream));
+  TRY(launch_influence(c->fp64(), s, c->g.y0, c->g.nyl, c->green.p, nullptr, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   c->have_green = true;
   c->green_kind = kind;
@@ -668,7 +716,7 @@ int pppm_ctx_get_influence(pppm_ctx* c, double* g_full) {
   GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, c->green_floor,
               c->green_kind == PPPM_INFLUENCE_OPTIMAL};
   TRY(c->out_stage.ensure(8 * c->M));
-  TRY(launch_influence(true, s, nullptr, c->out_stage.as<double>(), c->stream));
+  TRY(launch_influence(true, s, 0, c->g.ny, nullptr, c->out_stage.as<double>(), c->stream));
   CU(cudaMemcpyAsync(g_full, c->out_stage.p, 8 * c->M, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return PPPM_OK;
@@ -897,6 +945,147 @@ int pppm_ctx_time_steps(pppm_ctx* c, int steps, int warmup, int flush_l2, double
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   return check_err_flag(c);
+}
+
+// ---------------------------------------------------------------------------
+// z-slab decomposition: device halves of the distributed step; the host issues
+// the NCCL exchanges between them on the context stream (slab.py)
+
+static int ensure_slab_plans(pppm_ctx* c) {
+  if (c->slab_plans) return PPPM_OK;
+  const int ny = c->g.ny, nx = c->g.nx, nxh = c->nxh;
+  int n2[2] = {ny, nx};
+  int real_emb[2] = {c->pd.py, c->pd.px};
+  int cplx_emb[2] = {ny, nxh};
+  const int plane = c->pd.py * c->pd.px;
+  FFT(cufftPlanMany(&c->p2f, 2, n2, real_emb, 1, plane, cplx_emb, 1, ny * nxh, CUFFT_R2C, c->g.nzl));
+  FFT(cufftPlanMany(&c->p2b, 2, n2, cplx_emb, 1, ny * nxh, real_emb, 1, plane, CUFFT_C2R, c->g.nzl));
+  int nz1[1] = {c->g.nz};
+  const int cols = c->g.nyl * nxh;
+  FFT(cufftPlanMany(&c->pz, 1, nz1, nz1, cols, 1, nz1, cols, 1, CUFFT_C2C, cols));
+  FFT(cufftSetStream(c->p2f, c->stream));
+  FFT(cufftSetStream(c->p2b, c->stream));
+  FFT(cufftSetStream(c->pz, c->stream));
+  c->slab_plans = true;
+  return PPPM_OK;
+}
+
+int pppm_ctx_stream(pppm_ctx* c, void** stream) {
+  *stream = (void*)c->stream;
+  return PPPM_OK;
+}
+
+int pppm_slab_info(pppm_ctx* c, int* info) {
+  // nslabs, rank, z0, nzl, y0, nyl, H, px, py, pz
+  int v[10] = {c->P, c->rank, c->g.z0, c->g.nzl, c->g.y0, c->g.nyl, c->pd.H, c->pd.px, c->pd.py, c->pd.pz};
+  for (int i = 0; i < 10; ++i) info[i] = v[i];
+  return PPPM_OK;
+}
+
+int pppm_slab_buffer(pppm_ctx* c, int id, int field, void** ptr, size_t* bytes) {
+  const size_t plane = (size_t)c->pd.py * c->pd.px * sizeof(float);
+  const size_t gb = plane * c->pd.H;
+  const size_t mesh = (size_t)c->pd.count() * sizeof(float);
+  const size_t a2a = (size_t)c->half * 2 * sizeof(float);
+  char* rho = (char*)c->rho.p;
+  char* fl = (char*)c->fields.p + mesh * field;
+  if (field < 0 || field >= c->nfields()) return fail(PPPM_ERR_VALUE, "bad field index");
+  switch (id) {
+    case PPPM_BUF_RHO_GHOST_LO: *ptr = rho; *bytes = gb; break;
+    case PPPM_BUF_RHO_GHOST_HI: *ptr = rho + plane * (c->pd.H + c->g.nzl); *bytes = gb; break;
+    case PPPM_BUF_RECV_LO: *ptr = c->ghost_lo.p; *bytes = gb; break;
+    case PPPM_BUF_RECV_HI: *ptr = c->ghost_hi.p; *bytes = gb; break;
+    case PPPM_BUF_A2A_SEND: *ptr = c->a2a_send.p; *bytes = a2a; break;
+    case PPPM_BUF_A2A_RECV: *ptr = c->a2a_recv.p; *bytes = a2a; break;
+    case PPPM_BUF_A2A_SEND_F: *ptr = c->a2a_send.p; *bytes = a2a * c->nfields(); break;
+    case PPPM_BUF_A2A_RECV_F: *ptr = c->a2a_recv.p; *bytes = a2a * c->nfields(); break;
+    case PPPM_BUF_ENERGY: *ptr = c->scal.p; *bytes = sizeof(double); break;
+    case PPPM_BUF_FIELD_BOTTOM: *ptr = fl + plane * c->pd.H; *bytes = gb; break;
+    case PPPM_BUF_FIELD_TOP: *ptr = fl + plane * c->g.nzl; *bytes = gb; break;
+    case PPPM_BUF_FIELD_GHOST_LO: *ptr = fl; *bytes = gb; break;
+    case PPPM_BUF_FIELD_GHOST_HI: *ptr = fl + plane * (c->pd.H + c->g.nzl); *bytes = gb; break;
+    default: return fail(PPPM_ERR_VALUE, "unknown slab buffer id");
+  }
+  if (c->P == 1) return fail(PPPM_ERR_STATE, "not a slab context");
+  return PPPM_OK;
+}
+
+// bin + spread + x/y halo fold of the resident atoms of this slab; the z ghost
+// planes (RHO_GHOST_LO/HI) are then ready to be reverse-summed by the neighbours
+int pppm_slab_make_rho(pppm_ctx* c) {
+  TRY(activate(c));
+  if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  c->binned = false;
+  TRY(run_bin(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype));
+  return run_spread(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype);
+}
+
+// the neighbours' ghost planes (RECV_LO from the slab below, RECV_HI from above)
+// added into this slab's first / last H interior planes
+int pppm_slab_add_ghosts(pppm_ctx* c) {
+  TRY(activate(c));
+  const int64_t plane = (int64_t)c->pd.py * c->pd.px, n = plane * c->pd.H;
+  float* rho = c->rho.as<float>();
+  TRY(launch_add_planes(c->ghost_lo.as<float>(), rho + plane * c->pd.H, n, c->stream));
+  TRY(launch_add_planes(c->ghost_hi.as<float>(), rho + plane * c->g.nzl, n, c->stream));
+  c->launches += 2;
+  return PPPM_OK;
+}
+
+// 2D R2C of the local planes, packed per destination ky chunk (A2A_SEND)
+int pppm_slab_fft_fwd(pppm_ctx* c) {
+  TRY(activate(c));
+  TRY(ensure_slab_plans(c));
+  FFT(cufftExecR2C(c->p2f, c->rho.as<float>() + c->pd.interior(), c->spec2d.as<cufftComplex>()));
+  TRY(launch_pack_fwd(c->g, c->P, c->spec2d.p, c->a2a_send.p, c->stream));
+  c->launches += 1;
+  return PPPM_OK;
+}
+
+// after the forward all-to-all (A2A_RECV = (nz, nyl, nxh)): z FFT, Green / ik
+// multiply with the energy partial (ENERGY, to be all-reduced), inverse z FFT
+// of the field spectra, packed per destination slab (A2A_SEND_F)
+int pppm_slab_green(pppm_ctx* c) {
+  TRY(activate(c));
+  TRY(ensure_slab_plans(c));
+  if (!c->have_green) return fail(PPPM_ERR_STATE, "influence function not built");
+  cufftComplex* spec = c->a2a_recv.as<cufftComplex>();
+  FFT(cufftExecC2C(c->pz, spec, spec, CUFFT_FORWARD));
+  const double vol = c->g.lx * c->g.ly * c->g.lz;
+  const double vcell = vol / (double)c->M;
+  const double pref = c->cscale * vcell * vcell / (2.0 * vol);
+  TRY(launch_green(false, c->mode, true, spec, c->green.p, c->g, c->ikc.p, 1.0 / (double)c->M, c->ework.p,
+                   c->partial.as<double>(), pref, c->scal.as<double>(), c->stream));
+  cufftComplex* ew = c->ework.as<cufftComplex>();
+  for (int f = 0; f < c->nfields(); ++f) FFT(cufftExecC2C(c->pz, ew + f * c->half, ew + f * c->half, CUFFT_INVERSE));
+  TRY(launch_pack_bwd(c->g, c->P, c->nfields(), c->ework.p, c->a2a_send.p, c->stream));
+  c->launches += 3;
+  return PPPM_OK;
+}
+
+// after the backward all-to-all (A2A_RECV_F): unpack, 2D C2R of the local
+// planes into the padded fields, x/y halo fill; the interior boundary planes
+// (FIELD_BOTTOM/TOP) are then ready to be copied into the neighbours' ghosts
+int pppm_slab_fft_bwd(pppm_ctx* c) {
+  TRY(activate(c));
+  TRY(ensure_slab_plans(c));
+  const int nf = c->nfields();
+  TRY(launch_unpack_bwd(c->g, c->P, nf, c->a2a_recv.p, c->spec2d.p, c->stream));
+  const int64_t spec_f = (int64_t)c->g.nzl * c->g.ny * c->nxh;
+  for (int f = 0; f < nf; ++f)
+    FFT(cufftExecC2R(c->p2b, c->spec2d.as<cufftComplex>() + f * spec_f,
+                     c->fields.as<float>() + f * c->pd.count() + c->pd.interior()));
+  TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), nf, c->stream));
+  c->launches += 2;
+  c->have_fields = true;
+  return PPPM_OK;
+}
+
+// fieldforce of the resident atoms (ghost planes received into FIELD_GHOST_LO/HI)
+int pppm_slab_fieldforce(pppm_ctx* c) {
+  TRY(activate(c));
+  if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  return do_fieldforce(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype, !c->binned, c->res_force.p, false);
 }
 
 int pppm_ctx_launches_per_step(pppm_ctx* c, int* launches) {

@@ -19,6 +19,8 @@ struct Geom {
   double hx, hy, hz;
   double lx, ly, lz;
   double ihx, ihy, ihz;  // 1/h, host-computed (particle_map_fast)
+  int z0, nzl;           // z-slab owned by this context: global planes [z0, z0 + nzl); (0, nz) on one GPU
+  int y0, nyl;           // ky chunk of the transposed spectrum held by this context; (0, ny) on one GPU
 };
 
 struct Bricks {
@@ -42,6 +44,7 @@ struct GreenSpec {
 struct Pad {
   int H, px, py, pz;
   int hx;   // left x halo, H rounded up to even: 8-byte aligned interior (cuFFT)
+  int zper; // 1: z halo is periodic (one GPU); 0: z ghost planes come from the neighbour slabs
   __host__ __device__ int64_t count() const { return (int64_t)px * py * pz; }
   __host__ __device__ int64_t interior() const { return ((int64_t)H * py + H) * px + hx; }
   __host__ __device__ int64_t at(int x, int y, int z) const { return ((int64_t)(z + H) * py + (y + H)) * px + (x + hx); }
@@ -86,11 +89,16 @@ int launch_fold_halo(const Geom& g, const Pad& pd, float* rho_pad, cudaStream_t 
 int launch_fill_halo(const Geom& g, const Pad& pd, float* fields_pad, int nfields, cudaStream_t s);
 int launch_unpad(const Geom& g, const Pad& pd, const float* src_pad, double* dst, cudaStream_t s);
 int launch_pad_in(const Geom& g, const Pad& pd, const double* src, float* dst_pad, cudaStream_t s);
-int launch_influence(bool f64, const GreenSpec& gs, void* g_half, double* g_full, cudaStream_t s);
+int launch_influence(bool f64, const GreenSpec& gs, int y0, int nyl, void* g_half, double* g_full, cudaStream_t s);
 int launch_ik_vectors(const Geom& g, double* ik, cudaStream_t s);
 int launch_green(bool f64, int mode, bool fields, const void* rho_hat, const void* green, const Geom& g,
                  const void* ik, double inv_m, void* out, double* partial, double prefactor, double* energy,
                  cudaStream_t s);
 int launch_convert(bool to_f64, const void* src, void* dst, int64_t n, cudaStream_t s);
+// z-slab decomposition (k_slab.cu): transposes of the distributed FFT and ghost planes
+int launch_pack_fwd(const Geom& g, int P, const void* spec, void* send, cudaStream_t s);
+int launch_pack_bwd(const Geom& g, int P, int nf, const void* ework, void* send, cudaStream_t s);
+int launch_unpack_bwd(const Geom& g, int P, int nf, const void* recv, void* spec, cudaStream_t s);
+int launch_add_planes(const float* src, float* dst, int64_t n, cudaStream_t s);
 
 }  // namespace pppm
