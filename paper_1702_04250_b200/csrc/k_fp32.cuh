@@ -58,9 +58,10 @@ template <> struct WMax<5> { static constexpr float v = 0.5989584f; };
 template <> struct WMax<6> { static constexpr float v = 0.55f; };
 template <> struct WMax<7> { static constexpr float v = 0.5110244f; };
 
+// opt in to > 48 KB of dynamic shared memory (the 48 KB default counts static + dynamic)
 template <typename K>
 inline void allow_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (bytes > 32 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 // ---------------------------------------------------------------------------
