@@ -56,15 +56,20 @@ def parse():
     return ap.parse_args()
 
 
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, backend="gloo"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("gloo")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         pg = dist
     return rank, local, world, pg
 
@@ -74,12 +79,17 @@ def barrier(pg):
         pg.barrier()
 
 
+def _scalar(pg, value):
+    import torch
+
+    dev = "cuda" if pg.get_backend() == "nccl" else "cpu"
+    return torch.tensor([value], dtype=torch.float64, device=dev)
+
+
 def max_over_ranks(pg, value):
     if pg is None:
         return value
-    import torch
-
-    t = torch.tensor([value], dtype=torch.float64)
+    t = _scalar(pg, value)
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
@@ -87,9 +97,7 @@ def max_over_ranks(pg, value):
 def sum_over_ranks(pg, value):
     if pg is None:
         return value
-    import torch
-
-    t = torch.tensor([value], dtype=torch.float64)
+    t = _scalar(pg, value)
     pg.all_reduce(t, op=pg.ReduceOp.SUM)
     return float(t.item())
 
@@ -222,14 +230,115 @@ def run_reference(args, cfg, rank, pg):
     print(json.dumps(line), flush=True)
 
 
+def run_slabs(args, cfg, rank, local, world, pg):
+    """N > 1: one config, z-slab decomposed over the N GPUs (strong scaling):
+    NCCL ghost-plane exchanges and FFT all-to-all transposes (slab.py)."""
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_1702_04250_b200 as pb
+    from paper_1702_04250_b200 import _native as nat
+    from paper_1702_04250_b200.slab import SlabContext, SlabStep, TorchComm, owner_of_nodes
+
+    mode = args.mode or cfg.mode
+    pos, q, lengths = cfg.build()          # the same system on every rank, then partitioned
+    n_total = pos.shape[0]
+    p32 = pos.astype(np.float32)
+    probe = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
+                           device=local)
+    nodes = np.empty((3, n_total), dtype=np.int32)
+    probe.ctx("pppm_particle_map", nat.ptr(p32), n_total, nat.F32, nat.HOST, nat.ptr(nodes))
+    probe.close()
+    mine = np.nonzero(owner_of_nodes(nodes[2], cfg.dims[2], world) == rank)[0]
+    slab = SlabContext(cfg.dims, lengths, cfg.order, mode, cfg.alpha, world, rank, device=local)
+    slab.load_atoms(p32[mine], q[mine].astype(np.float32))
+    comm = TorchComm()
+    step = SlabStep(slab, comm)
+    stream = torch.cuda.ExternalStream(slab.stream_ptr, device=local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def run(k, timed):
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+        for i in range(k):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                ev[i][0].record(stream)
+            step.make_rho()
+            with torch.cuda.stream(stream):
+                ev[i][1].record(stream)
+            step.poisson()
+            with torch.cuda.stream(stream):
+                ev[i][2].record(stream)
+            step.fieldforce()
+            with torch.cuda.stream(stream):
+                ev[i][3].record(stream)
+        stream.synchronize()
+        return [(e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])) for e in ev]
+
+    run(max(3, args.warmup), False)
+    barrier(pg)
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_load = time.perf_counter()
+    while time.perf_counter() - t_load < 1.5:
+        run(5, False)
+    torch.cuda.synchronize()
+    barrier(pg)
+    t_wall = time.perf_counter()
+    times = run(args.steps, True)
+    torch.cuda.synchronize()
+    barrier(pg)
+    t_wall = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    k = args.steps
+    t_mr = sum(t[0] for t in times) / 1e3
+    t_po = sum(t[1] for t in times) / 1e3
+    t_ff = sum(t[2] for t in times) / 1e3
+    t_mf_max = max_over_ranks(pg, t_mr + t_ff)
+    t_step_max = max_over_ranks(pg, t_mr + t_po + t_ff)
+    n_local = float(len(mine))
+    value = n_total * k / t_mf_max
+    peak, peak_kind = peaks()
+    mesh_local = int(np.prod(cfg.dims)) // world
+    alg = n_local * 16 + mesh_local * 4 + n_local * 16 + 3 * mesh_local * 4 + 3 * n_local * 4
+    gbs = alg / ((t_mr + t_ff) / k) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
+        "ms_per_step": t_step_max / k * 1e3, "ms_make_rho_fieldforce": t_mf_max / k * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config{cfg.index}: {n_total} point charges, mesh {cfg.dims[0]}^3, order {cfg.order}, "
+                               f"{mode}, mixed, z-slab decomposed over {world} GPUs", "n_atoms": n_total,
+                   "mesh": list(cfg.dims), "order": cfg.order, "mode": mode, "precision": "mixed",
+                   "l2": "flushed before every step (256 MiB memset, outside the phase intervals)",
+                   "parallelism": f"zslab{world}: NCCL ghost send/recv + FFT all-to-all"},
+        "phases_ms_per_step_rank0": {"make_rho_incl_ghost_exchange": t_mr / k * 1e3, "poisson_incl_a2a": t_po / k * 1e3,
+                                     "fieldforce": t_ff / k * 1e3},
+        "whole_step_atom_steps_per_s": n_total * k / t_step_max,
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "traffic": None, "kernel": "make_rho+fieldforce per GPU (rank 0)", "peak_kind": peak_kind},
+        "clocks": clocks, "gpu_launches": None, "wall_s_timed_region": t_wall,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    slab.close()
+    pg.destroy_process_group()
+
+
 def main():
     args = parse()
     from paper_1702_04250_b200 import scenarios
 
     cfg = scenarios.CONFIGS[args.config]
-    rank, local, world, pg = dist_setup(args.gpus)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    ours_multi = args.impl == "ours" and world_env > 1
+    rank, local, world, pg = dist_setup(args.gpus, backend="nccl" if ours_multi else "gloo")
     if args.impl == "reference":
         run_reference(args, cfg, rank, pg)
+        return
+    if ours_multi:
+        run_slabs(args, cfg, rank, local, world, pg)
         return
     import __graft_entry__
 
