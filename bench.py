@@ -25,6 +25,7 @@ samples of the same workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -286,11 +287,15 @@ def run_slabs(args, cfg, rank, local, world, pg):
         run(5, False)
     torch.cuda.synchronize()
     barrier(pg)
+    cnt0 = ctypes.c_int64()
+    slab("pppm_ctx_launch_count", ctypes.byref(cnt0))
     t_wall = time.perf_counter()
     times = run(args.steps, True)
     torch.cuda.synchronize()
     barrier(pg)
     t_wall = time.perf_counter() - t_wall
+    cnt1 = ctypes.c_int64()
+    slab("pppm_ctx_launch_count", ctypes.byref(cnt1))
     clocks = sampler.stop()
     k = args.steps
     t_mr = sum(t[0] for t in times) / 1e3
@@ -318,7 +323,7 @@ def run_slabs(args, cfg, rank, local, world, pg):
         "whole_step_atom_steps_per_s": n_total * k / t_step_max,
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": None, "kernel": "make_rho+fieldforce per GPU (rank 0)", "peak_kind": peak_kind},
-        "clocks": clocks, "gpu_launches": None, "wall_s_timed_region": t_wall,
+        "clocks": clocks, "gpu_launches": int(cnt1.value - cnt0.value), "wall_s_timed_region": t_wall,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

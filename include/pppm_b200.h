@@ -143,6 +143,7 @@ int pppm_ctx_create_slab(pppm_ctx** out, int device, int nx, int ny, int nz, dou
                          double lz, int order, int mode, int precision, double alpha,
                          double coulomb_constant, double dielectric, int nslabs, int rank);
 int pppm_ctx_stream(pppm_ctx* ctx, void** stream);       /* the context's cudaStream_t */
+int pppm_ctx_launch_count(pppm_ctx* ctx, int64_t* count); /* kernels this context has launched so far */
 /* info[10]: nslabs, rank, z0, nzl, y0, nyl, H, px, py, pz */
 int pppm_slab_info(pppm_ctx* ctx, int* info);
 int pppm_slab_buffer(pppm_ctx* ctx, int id, int field, void** ptr, size_t* bytes);

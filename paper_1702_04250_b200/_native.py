@@ -71,6 +71,7 @@ PROTOTYPES = {
     "pppm_ctx_create_slab": (_c_int, [ctypes.POINTER(_vp), _c_int, _c_int, _c_int, _c_int, _c_dbl, _c_dbl,
                                       _c_dbl, _c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_dbl, _c_int, _c_int]),
     "pppm_ctx_stream": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "pppm_ctx_launch_count": (_c_int, [_vp, ctypes.POINTER(_c_i64)]),
     "pppm_slab_info": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "pppm_slab_buffer": (_c_int, [_vp, _c_int, _c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)]),
     "pppm_slab_make_rho": (_c_int, [_vp]),

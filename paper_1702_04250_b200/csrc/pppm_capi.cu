@@ -970,6 +970,11 @@ static int ensure_slab_plans(pppm_ctx* c) {
   return PPPM_OK;
 }
 
+int pppm_ctx_launch_count(pppm_ctx* c, int64_t* count) {
+  *count = c->launches;
+  return PPPM_OK;
+}
+
 int pppm_ctx_stream(pppm_ctx* c, void** stream) {
   *stream = (void*)c->stream;
   return PPPM_OK;
