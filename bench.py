@@ -165,7 +165,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-KERNEL_NAMES = {"spread": "k_spread_sorted", "gather": "k_gather_sorted", "bin": "k_bin_fixed"}
+KERNEL_NAMES = {"spread": "k_spread_tma", "gather": "k_gather_tma", "bin": "k_bin_fixed"}
 
 
 def load_traffic(config, mode, kernel):
@@ -378,7 +378,7 @@ def main():
 
     k = args.steps
     t_mf = (ms["bin"] + ms["spread"] + ms["gather"]) / 1e3        # make_rho + fieldforce, s
-    t_step = (ms["bin"] + ms["spread"] + ms["fft_fwd"] + ms["green"] + ms["fft_bwd"] + ms["gather"]) / 1e3
+    t_step = (ms["bin"] + ms["spread"] + ms["poisson"] + ms["gather"]) / 1e3
     t_mf_max = max_over_ranks(pg, t_mf)
     t_step_max = max_over_ranks(pg, t_step)
     atoms_total = sum_over_ranks(pg, float(n))

@@ -123,7 +123,9 @@ int pppm_ctx_get_forces(pppm_ctx* ctx, double* forces);  /* host (n,3) fp64 */
 int pppm_ctx_get_energy(pppm_ctx* ctx, double* energy);
 /* CUDA-event timing of `steps` full steps after `warmup`; flush_l2 writes a
  * 256 MiB buffer before each step (outside the phase intervals).
- * ms[0..6]: bin, spread, fft_fwd, green, fft_bwd, gather, total (summed over steps) */
+ * ms[0..4]: bin, spread (make_rho incl. halo fold), poisson (R2C, Green+energy,
+ * C2R, halo fill), gather (fieldforce), total (summed over steps).  After a
+ * first eager run each sub-phase is captured into a CUDA graph and replayed. */
 int pppm_ctx_time_steps(pppm_ctx* ctx, int steps, int warmup, int flush_l2, double* ms);
 /* kernel variants for A/B measurement: kernel 0 = fp32 make_rho
  * (0: float CAS shared atomics, 1: int32 fixed-point shared atomics [default]),

@@ -82,10 +82,10 @@ class PppmContext:
 
     def time_steps(self, steps, warmup, flush_l2=True):
         """CUDA-event phase times in ms summed over ``steps``:
-        dict(bin, spread, fft_fwd, green, fft_bwd, gather, total)."""
-        ms = np.zeros(7)
+        dict(bin, spread, poisson, gather, total)."""
+        ms = np.zeros(5)
         self.ctx("pppm_ctx_time_steps", int(steps), int(warmup), int(bool(flush_l2)), nat.ptr(ms))
-        keys = ("bin", "spread", "fft_fwd", "green", "fft_bwd", "gather", "total")
+        keys = ("bin", "spread", "poisson", "gather", "total")
         return dict(zip(keys, (float(v) for v in ms)))
 
     def launches_per_step(self):

@@ -6,8 +6,9 @@
 // [b*cap, b*cap + min(count_b, cap)); atoms beyond a full bucket go to an
 // overflow list handled by extra CTAs of the same launches).  A bucket slot
 // stores what the mapping kernels need, computed once by particle_map in the
-// binning pass: float4 {tx, ty, tz, q} (offsets, or table bins in table mode),
-// the brick-local cell (9 bits) and the input index.
+// binning pass, in one 32-byte slot: float4 {tx, ty, tz, q} (offsets, or table
+// bins in table mode) and int4 {brick-local cell (9 bits), input index, -, -}.
+// (`rec` points at the slots; `rcell` / `perm` are unused.)
 //
 // make_rho (gridmap.py:156-213): one CTA per brick.  The brick's atoms are
 // staged in shared memory and counting-sorted by cell (consecutive lanes get
@@ -133,10 +134,10 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
       if (b[u] < 0) continue;
       const int64_t i = i0 + u * stride;
       if (slot[u] < cap) {
+        // one 32-byte slot per atom (full-sector write): {tx, ty, tz, q}, {cell, input index}
         const int64_t k = (int64_t)b[u] * cap + slot[u];
-        rec[k] = r[u];
-        rcell[k] = lc[u];
-        perm[k] = (int)i;
+        rec[2 * k] = r[u];
+        reinterpret_cast<int4*>(rec)[2 * k + 1] = make_int4(lc[u], (int)i, 0, 0);
       } else {
         // overflow record: same payload, wrapped global node packed 10+10+10 bits (dims <= 1024)
         const int o = atomicAdd(ovf_count, 1);
@@ -205,9 +206,10 @@ __device__ __forceinline__ int stage_sorted(const float4* __restrict__ rec, cons
   for (int k = 0; k < kPer; ++k) {
     const int j = threadIdx.x + k * kThreads;
     if (j < cnt) {
-      r[k] = rec[base + j];
-      c[k] = rcell[base + j];
-      if (PERM) p[k] = perm[base + j];
+      r[k] = rec[2 * (base + j)];
+      const int4 m = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
+      c[k] = m.x;
+      if (PERM) p[k] = m.y;
       rk[k] = atomicAdd(sm.hist + c[k], 1);
       if (QSUM) {
         qa += fabsf(r[k].w);
@@ -301,9 +303,10 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
   for (int k = 0; k < kPer; ++k) {
     const int j = threadIdx.x + k * kThreads;
     if (j < cnt) {
-      r[k] = rec[base + j];
-      c[k] = rcell[base + j];
-      if (PERM) p[k] = perm[base + j];
+      r[k] = rec[2 * (base + j)];
+      const int4 m = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
+      c[k] = m.x;
+      if (PERM) p[k] = m.y;
       const int lx = c[k] & (kBrick - 1), ly = (c[k] >> 3) & (kBrick - 1), lz = c[k] >> 6;
       bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
       rk[k] = atomicAdd(sm.bsize + bank[k], 1);

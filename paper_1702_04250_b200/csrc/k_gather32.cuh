@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather_tma(
         if (rr >= bsize[lane]) continue;
         j = bstart[lane] + rr;
       }
-      const float4 r = sort ? s_r[j] : rec[base + j];
-      const int cc = sort ? s_c[j] : rcell[base + j];
+      const float4 r = sort ? s_r[j] : rec[2 * (base + j)];
+      const int cc = sort ? s_c[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].x;
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
       rows_f32<S, TAB, MODE == 1>(r.x, ta, td, ax, dx);
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather_tma(
         s2 = fmaf(MODE == 0 ? az[a] : dz[a], r2, s2);
       }
       const float sc = cscale * r.w;
-      const int64_t i = sort ? s_p[j] : perm[base + j];
+      const int64_t i = sort ? s_p[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].y;
       if (MODE == 0) store_force<S, MODE>(force, out_f64, i, sc * s0, sc * s1, sc * s2);
       else store_force<S, MODE>(force, out_f64, i, -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
     }

@@ -99,7 +99,7 @@ struct DevBuf {
 
 }  // namespace
 
-enum SubPhase { SP_BIN = 0, SP_SPREAD, SP_FFT_FWD, SP_GREEN, SP_FFT_BWD, SP_GATHER, SP_COUNT };
+enum SubPhase { SP_BIN = 0, SP_SPREAD, SP_POISSON, SP_GATHER, SP_COUNT };
 
 struct pppm_ctx {
   int device = 0;
@@ -137,6 +137,12 @@ struct pppm_ctx {
   int* h_err = nullptr;
   double* h_scal = nullptr;
   cudaEvent_t ev[SP_COUNT + 1] = {};
+  // CUDA graphs of the resident step's sub-phases (captured on the second run,
+  // once every buffer exists; dropped when atoms / table / variant change)
+  bool use_graphs = true;
+  cudaGraphExec_t gexec[SP_COUNT] = {};
+  bool warm[SP_COUNT] = {};
+  int sp_launches[SP_COUNT] = {};  // our kernels per sub-phase (counted on the eager run)
   int launches = 0;
 
   bool fp64() const { return prec == PPPM_PREC_FP64; }
@@ -146,6 +152,8 @@ struct pppm_ctx {
 
 // ---------------------------------------------------------------------------
 // internal helpers
+
+static void drop_graphs(pppm_ctx* c);
 
 static int activate(pppm_ctx* c) {
   CU(cudaSetDevice(c->device));
@@ -263,9 +271,7 @@ static int ensure_bins(pppm_ctx* c, int64_t n) {
   c->cap = bucket_cap(c, n);
   const int64_t slots = (int64_t)nb * c->cap;
   TRY(c->counts.ensure(sizeof(int) * (nb + 2) * kCountStride));
-  TRY(c->rec.ensure(sizeof(float4) * slots));
-  TRY(c->rcell.ensure(sizeof(int) * slots));
-  TRY(c->perm.ensure(sizeof(int) * slots));
+  TRY(c->rec.ensure(2 * sizeof(float4) * slots));  // 32-byte slots (k_fp32.cuh)
   TRY(c->ovf_rec.ensure(sizeof(float4) * n));
   TRY(c->ovf_cell.ensure(sizeof(int) * n));
   TRY(c->ovf_perm.ensure(sizeof(int) * n));
@@ -581,6 +587,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
     return cleanup(fail(PPPM_ERR_CUDA, "context setup kernels failed"));
   if (const char* v = getenv("PPPM_B200_SPREAD")) c->spread_variant = atoi(v);
   if (const char* v = getenv("PPPM_B200_GATHER")) c->gather_variant = atoi(v);
+  if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
   *out = c;
   return PPPM_OK;
 }
@@ -601,6 +608,7 @@ int pppm_ctx_create_slab(pppm_ctx** out, int device, int nx, int ny, int nz, dou
 
 int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
+  drop_graphs(c);
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
   else if (kernel == 1 && (variant == GATHER_PLAIN || variant == GATHER_SORTED)) c->gather_variant = variant;
   else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
@@ -611,6 +619,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   if (!c) return PPPM_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graphs(c);
   if (c->plans) {
     cufftDestroy(c->fwd);
     cufftDestroy(c->bwd);
@@ -636,6 +645,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
 
 int pppm_ctx_set_table(pppm_ctx* c, int n_points, const double* assign, const double* deriv) {
   TRY(activate(c));
+  drop_graphs(c);
   if (n_points == 0) {
     c->n_points = 0;
     return PPPM_OK;
@@ -659,6 +669,7 @@ int pppm_ctx_set_table(pppm_ctx* c, int n_points, const double* assign, const do
 
 int pppm_ctx_build_table(pppm_ctx* c, int n_points) {
   TRY(activate(c));
+  drop_graphs(c);
   if (n_points == 0) {
     c->n_points = 0;
     return PPPM_OK;
@@ -841,6 +852,7 @@ int pppm_compute(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dty
 
 int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
   TRY(activate(c));
+  drop_graphs(c);
   if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
   const size_t es = dtype == PPPM_F64 ? 8 : 4;
   TRY(c->res_pos.ensure(3 * n * es));
@@ -854,28 +866,82 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   return PPPM_OK;
 }
 
-static int step_phases(pppm_ctx* c, int phases, bool timing) {
+static void drop_graphs(pppm_ctx* c) {
+  for (int k = 0; k < SP_COUNT; ++k) {
+    if (c->gexec[k]) cudaGraphExecDestroy(c->gexec[k]);
+    c->gexec[k] = nullptr;
+    c->warm[k] = false;
+  }
+}
+
+static int run_subphase(pppm_ctx* c, int sp) {
   const int64_t n = c->n_res;
   const void* p = c->res_pos.p;
   const void* q = c->res_q.p;
+  switch (sp) {
+    case SP_BIN:
+      c->binned = false;
+      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype));
+      return PPPM_OK;
+    case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype);
+    case SP_POISSON:
+      TRY(run_fft_fwd(c));
+      TRY(run_green(c, true));
+      return run_fft_bwd(c);
+    case SP_GATHER:
+      return do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64());
+  }
+  return PPPM_OK;
+}
+
+// eager on the first run of a sub-phase, then captured into a CUDA graph and replayed
+static int launch_subphase(pppm_ctx* c, int sp) {
+  if (!c->use_graphs) return run_subphase(c, sp);
+  if (c->gexec[sp]) {
+    CU(cudaGraphLaunch(c->gexec[sp], c->stream));
+    c->launches += c->sp_launches[sp];
+    if (sp == SP_BIN) c->binned = true;
+    return PPPM_OK;
+  }
+  if (!c->warm[sp]) {
+    const int before = c->launches;
+    TRY(run_subphase(c, sp));
+    c->sp_launches[sp] = c->launches - before;
+    c->warm[sp] = true;
+    return PPPM_OK;
+  }
+  const int launches = c->launches;
+  cudaGraph_t graph = nullptr;
+  CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+  const int st = run_subphase(c, sp);
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (st != PPPM_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(PPPM_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  const cudaError_t ie = cudaGraphInstantiate(&c->gexec[sp], graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) return fail(PPPM_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+  c->launches = launches + c->sp_launches[sp];
+  CU(cudaGraphLaunch(c->gexec[sp], c->stream));
+  return PPPM_OK;
+}
+
+static int step_phases(pppm_ctx* c, int phases, bool timing) {
   if (phases & PPPM_PHASE_MAKE_RHO) {
-    c->binned = false;
     rec_event(c, SP_BIN, timing);
-    if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype));
+    TRY(launch_subphase(c, SP_BIN));
     rec_event(c, SP_SPREAD, timing);
-    TRY(run_spread(c, p, q, n, c->res_dtype));
+    TRY(launch_subphase(c, SP_SPREAD));
   }
   if (phases & PPPM_PHASE_POISSON) {
-    rec_event(c, SP_FFT_FWD, timing);
-    TRY(run_fft_fwd(c));
-    rec_event(c, SP_GREEN, timing);
-    TRY(run_green(c, true));
-    rec_event(c, SP_FFT_BWD, timing);
-    TRY(run_fft_bwd(c));
+    rec_event(c, SP_POISSON, timing);
+    TRY(launch_subphase(c, SP_POISSON));
   }
   if (phases & PPPM_PHASE_FIELDFORCE) {
     rec_event(c, SP_GATHER, timing);
-    TRY(do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64()));
+    TRY(launch_subphase(c, SP_GATHER));
   }
   rec_event(c, SP_COUNT, timing);
   return PPPM_OK;
