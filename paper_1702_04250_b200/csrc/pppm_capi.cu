@@ -153,7 +153,13 @@ struct pppm_ctx {
 // ---------------------------------------------------------------------------
 // internal helpers
 
-static void drop_graphs(pppm_ctx* c);
+static void drop_graphs(pppm_ctx* c) {
+  for (int k = 0; k < SP_COUNT; ++k) {
+    if (c->gexec[k]) cudaGraphExecDestroy(c->gexec[k]);
+    c->gexec[k] = nullptr;
+    c->warm[k] = false;
+  }
+}
 
 static int activate(pppm_ctx* c) {
   CU(cudaSetDevice(c->device));
@@ -866,13 +872,6 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   return PPPM_OK;
 }
 
-static void drop_graphs(pppm_ctx* c) {
-  for (int k = 0; k < SP_COUNT; ++k) {
-    if (c->gexec[k]) cudaGraphExecDestroy(c->gexec[k]);
-    c->gexec[k] = nullptr;
-    c->warm[k] = false;
-  }
-}
 
 static int run_subphase(pppm_ctx* c, int sp) {
   const int64_t n = c->n_res;
