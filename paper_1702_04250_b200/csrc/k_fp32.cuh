@@ -292,16 +292,17 @@ struct BankSmem {
   int* bstart;  // 33 (bstart[32] = rounds)
 };
 
-template <bool PERM, int D, int TXB, int SH>
+template <bool PERM, int D, int TXB, int SH, int NT = kThreads>
 __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, const int* __restrict__ rcell,
                                             const int* __restrict__ perm, int64_t base, int cnt, BankSmem sm) {
+  constexpr int PER = kCapMax / NT;
   if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
   __syncthreads();
-  float4 r[kPer];
-  int c[kPer], rk[kPer], p[kPer], bank[kPer];
+  float4 r[PER];
+  int c[PER], rk[PER], p[PER], bank[PER];
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int j = threadIdx.x + k * kThreads;
+  for (int k = 0; k < PER; ++k) {
+    const int j = threadIdx.x + k * NT;
     if (j < cnt) {
       r[k] = rec[2 * (base + j)];
       const int4 m = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
@@ -328,8 +329,8 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int j = threadIdx.x + k * kThreads;
+  for (int k = 0; k < PER; ++k) {
+    const int j = threadIdx.x + k * NT;
     if (j < cnt) {
       const int dst = sm.bstart[bank[k]] + rk[k];
       sm.r[dst] = r[k];

@@ -11,6 +11,11 @@
 
 namespace pppm {
 
+#ifndef PPPM_GATHER_THREADS
+#define PPPM_GATHER_THREADS 256
+#endif
+constexpr int kGatherThreads = PPPM_GATHER_THREADS;
+
 template <int S, int MODE>
 __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i, float f0, float f1, float f2) {
   if (out_f64) {
@@ -26,8 +31,8 @@ __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i
 // while brick i is computed from tile buffer i&1, the TMA engine loads brick
 // i+1's (TXB, D, D, F) box from the halo-padded fields into the other buffer
 // (mbarrier transaction barriers; the halo makes every box in bounds).
-template <int S, bool TAB, int MODE>
-__global__ void __launch_bounds__(kThreads, 4) k_gather_tma(
+template <int S, bool TAB, int MODE, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_gather_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ perm,
     const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
     const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather_tma(
     cnt = cnt < cap ? cnt : cap;
     const int64_t base = (int64_t)b * cap;
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
-    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH>(rec, rcell, perm, base, cnt, sm) : 0;
+    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
@@ -191,15 +196,16 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
     const size_t dyn = 128 + 2 * (size_t)((F * TmaTile<S>::N + 31) / 32 * 32) * sizeof(float) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
-      auto k = k_gather_tma<S, TAB, MODE>;
+      constexpr int NT = kGatherThreads;
+      auto k = k_gather_tma<S, TAB, MODE, NT>;
       allow_smem(k, dyn);
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
-      k<<<grid, kThreads, dyn, s>>>(rec, rcell, perm, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force,
+      k<<<grid, NT, dyn, s>>>(rec, rcell, perm, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force,
                                     out_f64, variant == GATHER_SORTED, ovf_rec, ovf_cell, ovf_perm);
       return 0;
     });

@@ -9,13 +9,18 @@
 
 namespace pppm {
 
+#ifndef PPPM_SPREAD_THREADS
+#define PPPM_SPREAD_THREADS 256
+#endif
+constexpr int kSpreadThreads = PPPM_SPREAD_THREADS;
+
 // make_rho, persistent CTAs: bricks b = blockIdx.x, += gridDim.x.  Per brick the
 // int32 fixed-point tile is accumulated with shared atomics, converted to fp32
 // in place and added to the padded mesh with ONE TMA reduce-add of the
 // (TXB, D, D) box at the brick origin - lo (always in bounds: the mesh carries
 // an H-cell halo, folded back periodically by k_halo.cu afterwards).
-template <int S, bool TAB, bool FIX>
-__global__ void __launch_bounds__(kThreads) k_spread_tma(
+template <int S, bool TAB, bool FIX, int NT>
+__global__ void __launch_bounds__(NT) k_spread_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
     const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
@@ -58,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) k_spread_tma(
       scale = ldexpf(1.f, sc);
       inv_scale = ldexpf(1.f, -sc) * inv_vcell;
     }
-    const int rounds = stage_banked<false, D, TXB, T::SH>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
+    const int rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     for (int rr = warp; rr < rounds; rr += nwarp) {
       if (rr >= bsize[lane]) continue;
       const int j = bstart[lane] + rr;
@@ -135,16 +140,17 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
       constexpr bool TAB = decltype(T_)::value;
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
-        auto k = k_spread_tma<S, TAB, FIX>;
+        constexpr int NT = kSpreadThreads;
+        auto k = k_spread_tma<S, TAB, FIX, NT>;
         const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
-        k<<<grid, kThreads, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
+        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
         return 0;
       });
     });
