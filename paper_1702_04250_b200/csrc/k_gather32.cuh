@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gather_tma(
     const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
     const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,
     float cscale, void* force, bool out_f64, bool sort, const float4* __restrict__ ovf_rec,
-    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm, const int* __restrict__ bankinfo) {
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
   constexpr int F = MODE == 0 ? 3 : 1;
@@ -89,26 +89,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gather_tma(
     cnt = cnt < cap ? cnt : cap;
     const int64_t base = (int64_t)b * cap;
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
-    // bank rounds: replayed from make_rho's bank-sorted slots (bankinfo), or staged here
-    int rounds = 0;
-    const bool pre = bankinfo != nullptr;
-    if (sort && cnt > 0) {
-      if (pre) {
-        if (threadIdx.x < 32) {
-          const int v = bankinfo[(int64_t)b * 64 + threadIdx.x];
-          bsize[threadIdx.x] = v;
-          bstart[threadIdx.x] = bankinfo[(int64_t)b * 64 + 32 + threadIdx.x];
-          int m = v;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-          if (threadIdx.x == 0) bstart[32] = m;
-        }
-        __syncthreads();
-        rounds = bstart[32];
-      } else {
-        rounds = stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm);
-      }
-    }
+    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
@@ -120,10 +101,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gather_tma(
         if (rr >= bsize[lane]) continue;
         j = bstart[lane] + rr;
       }
-      const bool from_smem = sort && !pre;
-      const float4 r = from_smem ? s_r[j] : rec[2 * (base + j)];
-      const int4 meta = from_smem ? make_int4(s_c[j], s_p[j], 0, 0) : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
-      const int cc = meta.x;
+      const float4 r = sort ? s_r[j] : rec[2 * (base + j)];
+      const int cc = sort ? s_c[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].x;
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
       rows_f32<S, TAB, MODE == 1>(r.x, ta, td, ax, dx);
@@ -164,7 +143,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_gather_tma(
         s2 = fmaf(MODE == 0 ? az[a] : dz[a], r2, s2);
       }
       const float sc = cscale * r.w;
-      const int64_t i = meta.y;
+      const int64_t i = sort ? s_p[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].y;
       if (MODE == 0) store_force<S, MODE>(force, out_f64, i, sc * s0, sc * s1, sc * s2);
       else store_force<S, MODE>(force, out_f64, i, -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
     }
@@ -210,7 +189,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
                        const int* perm, const int* counts, int cap, const float4* ovf_rec, const int* ovf_cell,
                        const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                        const CUtensorMap& fmap, const float* ta, const float* td, const float* fields, float cscale,
-                       void* force, const int* bankinfo, cudaStream_t s) {
+                       void* force, cudaStream_t s) {
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
@@ -227,7 +206,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
       k<<<grid, NT, dyn, s>>>(rec, rcell, perm, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force,
-                                    out_f64, variant == GATHER_SORTED, ovf_rec, ovf_cell, ovf_perm, bankinfo);
+                                    out_f64, variant == GATHER_SORTED, ovf_rec, ovf_cell, ovf_perm);
       return 0;
     });
   });

@@ -23,8 +23,7 @@ template <int S, bool TAB, bool FIX, int NT>
 __global__ void __launch_bounds__(NT) k_spread_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
-    const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell,
-    int* __restrict__ bankinfo) {
+    const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
   // dynamic smem: [tile 0 | tile 1 | staged atoms]; double-buffered tiles (one
@@ -34,7 +33,7 @@ __global__ void __launch_bounds__(NT) k_spread_tma(
   int* tiles0 = dyn_i;
   float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
   __shared__ int bsize[32], bstart[33];
-  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + cap), reinterpret_cast<int*>(s_r + cap) + cap, bsize, bstart};
+  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + cap), nullptr, bsize, bstart};
   const int nb = bk.count();
   const float qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
   const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
@@ -64,20 +63,7 @@ __global__ void __launch_bounds__(NT) k_spread_tma(
       scale = ldexpf(1.f, sc);
       inv_scale = ldexpf(1.f, -sc) * inv_vcell;
     }
-    const int rounds = stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
-    if (bankinfo) {
-      // write the bank-sorted order back (fieldforce replays the same rounds
-      // without re-staging): slots in bucket order + per-bank sizes / starts
-      float4* slots = const_cast<float4*>(rec) + 2 * (int64_t)b * cap;
-      for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-        slots[2 * j] = sm.r[j];
-        reinterpret_cast<int4*>(slots)[2 * j + 1] = make_int4(sm.c[j], sm.p[j], 0, 0);
-      }
-      if (threadIdx.x < 32) {
-        bankinfo[(int64_t)b * 64 + threadIdx.x] = bsize[threadIdx.x];
-        bankinfo[(int64_t)b * 64 + 32 + threadIdx.x] = bstart[threadIdx.x];
-      }
-    }
+    const int rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     for (int rr = warp; rr < rounds; rr += nwarp) {
       if (rr >= bsize[lane]) continue;
       const int j = bstart[lane] + rr;
@@ -145,8 +131,7 @@ __global__ void __launch_bounds__(NT) k_spread_tma(
 
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
-                        const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, int* bankinfo,
-                        cudaStream_t s) {
+                        const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, cudaStream_t s) {
   if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
   int st = with_order(order, [&](auto S_) -> int {
@@ -157,7 +142,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         constexpr bool FIX = decltype(F_)::value;
         constexpr int NT = kSpreadThreads;
         auto k = k_spread_tma<S, TAB, FIX, NT>;
-        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
+        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
@@ -165,8 +150,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
-        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
-                                bankinfo);
+        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
         return 0;
       });
     });

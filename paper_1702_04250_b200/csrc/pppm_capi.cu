@@ -121,8 +121,7 @@ struct pppm_ctx {
 
   DevBuf rho, rho_fix, rho_hat, ework, fields, green, ikc, ik64, tab;
   DevBuf pos_stage, q_stage, out_stage, node_stage;
-  DevBuf counts, rec, rcell, perm, ovf_rec, ovf_cell, ovf_perm, bankinfo;
-  bool presorted = false;  // slots left in bank-round order by make_rho (fieldforce skips its staging)
+  DevBuf counts, rec, rcell, perm, ovf_rec, ovf_cell, ovf_perm;
   int cap = 0;
   int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SORTED;
   DevBuf partial, scal, err, flush;
@@ -279,7 +278,6 @@ static int ensure_bins(pppm_ctx* c, int64_t n) {
   const int64_t slots = (int64_t)nb * c->cap;
   TRY(c->counts.ensure(sizeof(int) * (nb + 2) * kCountStride));
   TRY(c->rec.ensure(2 * sizeof(float4) * slots));  // 32-byte slots (k_fp32.cuh)
-  TRY(c->bankinfo.ensure(sizeof(int) * 64 * nb));
   TRY(c->ovf_rec.ensure(sizeof(float4) * n));
   TRY(c->ovf_cell.ensure(sizeof(int) * n));
   TRY(c->ovf_perm.ensure(sizeof(int) * n));
@@ -298,7 +296,6 @@ static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int d
                  c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->err.as<int>(), c->stream));
   c->launches += 1;
   c->binned = true;
-  c->presorted = false;
   return PPPM_OK;
 }
 
@@ -313,9 +310,7 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
     TRY(launch_spread_brick(c->spread_variant & 1, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
-                            c->bk, c->pd, c->rho_map, c->tab.as<float>(), c->rho.as<float>(), c->bankinfo.as<int>(),
-                            c->stream));
-    c->presorted = true;
+                            c->bk, c->pd, c->rho_map, c->tab.as<float>(), c->rho.as<float>(), c->stream));
     c->launches += 4;  // spread + 3 halo folds
   }
   c->have_rho = true;
@@ -374,8 +369,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     TRY(launch_gather_brick(c->gather_variant, c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
                             c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
-                            c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
-                            c->presorted ? c->bankinfo.as<int>() : nullptr, c->stream));
+                            c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out, c->stream));
   }
   c->launches += 1;
   return PPPM_OK;
@@ -643,7 +637,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   }
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
-                    &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->bankinfo, &c->partial,
+                    &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
                     &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)

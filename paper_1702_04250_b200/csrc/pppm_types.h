@@ -75,8 +75,7 @@ int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Brick
                int* err, cudaStream_t s);
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
-                        const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad, int* bankinfo,
-                        cudaStream_t s);
+                        const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad, cudaStream_t s);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s);
@@ -84,7 +83,7 @@ int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64
                         const int* rcell, const int* perm, const int* counts, int cap, const float4* ovf_rec,
                         const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                         const CUtensorMap& field_map, const float* ta, const float* td, const float* fields_pad,
-                        float cscale, void* force, const int* bankinfo, cudaStream_t s);
+                        float cscale, void* force, cudaStream_t s);
 // halo handling of the padded fp32 meshes (k_halo.cu)
 int launch_fold_halo(const Geom& g, const Pad& pd, float* rho_pad, cudaStream_t s);
 int launch_fill_halo(const Geom& g, const Pad& pd, float* fields_pad, int nfields, cudaStream_t s);
