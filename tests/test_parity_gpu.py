@@ -433,3 +433,73 @@ def test_config3_full_size_mixed(pb, mode):
         phi = orc.poisson_ad(rho_ref, g)
         f_ref = orc.fieldforce_ad(phi, pos[sub], q[sub], lengths, cfg.dims, cfg.order)
     assert rel_rms(forces[sub], f_ref) <= MIXED_TOL
+
+
+# --------------------------------------------------------------------------- fp32 path edge cases
+
+
+@pytest.mark.parametrize("mode", ["ik", "ad"])
+def test_mixed_overflow_buckets(pb, mode):
+    """A dense cluster overfills its brick buckets: the overflow records take
+    the global-atomic / direct-gather path (extra CTAs) and must agree too."""
+    from paper_1702_04250_b200.scenarios import round_to_f32
+
+    rng = np.random.default_rng(21)
+    lengths = np.array([32.0, 32.0, 32.0])
+    n = 6000
+    pos = np.concatenate([rng.uniform(0, 32, (n // 2, 3)), 5.0 + rng.uniform(0, 1.5, (n // 2, 3))])
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    p32 = round_to_f32(pos, lengths)
+    dims = (32, 32, 32)
+    ctx = pb.PppmContext(dims, lengths, order=5, mode=mode, precision="mixed", alpha=0.4)
+    ctx.load_atoms(p32, q.astype(np.float32))
+    ctx.step()
+    ctx.synchronize()
+    forces, energy, rho = ctx.forces(), ctx.energy(), ctx.rho()
+    ctx.close()
+    f_ref, e_ref, rho_ref = orc.pppm_step(p32.astype(np.float64), q, lengths, dims, 5, 0.4, mode)
+    assert rel_rms(rho, rho_ref) <= MIXED_TOL
+    assert rel_rms(forces, f_ref) <= MIXED_TOL
+    assert abs(energy - e_ref) <= MIXED_TOL * abs(e_ref)
+
+
+@pytest.mark.parametrize("order,dims", [(7, (7, 7, 7)), (3, (3, 4, 5)), (6, (9, 6, 11)), (4, (8, 8, 4))])
+def test_mixed_tiny_meshes(pb, order, dims):
+    """Meshes smaller than the brick tile (TMA boxes partly outside the padded mesh)."""
+    from paper_1702_04250_b200.scenarios import round_to_f32
+
+    rng = np.random.default_rng(order)
+    lengths = np.array(dims, dtype=np.float64) * 1.3
+    n = 200
+    pos = rng.uniform(0, 1, (n, 3)) * lengths
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    p32 = round_to_f32(pos, lengths)
+    for mode in ("ik", "ad"):
+        ctx = pb.PppmContext(dims, lengths, order=order, mode=mode, precision="mixed", alpha=0.8)
+        ctx.load_atoms(p32, q.astype(np.float32))
+        ctx.step()
+        ctx.synchronize()
+        forces, energy = ctx.forces(), ctx.energy()
+        ctx.close()
+        f_ref, e_ref, _ = orc.pppm_step(p32.astype(np.float64), q, lengths, dims, order, 0.8, mode)
+        assert rel_rms(forces, f_ref) <= MIXED_TOL
+        assert abs(energy - e_ref) <= MIXED_TOL * abs(e_ref)
+
+
+def test_resident_graph_replay_is_stable(pb):
+    """CUDA-graph replays of the resident step give the same forces as the first (eager) run."""
+    from paper_1702_04250_b200 import scenarios
+
+    pos, q, lengths = scenarios.random_gas(20000, 4, 45.0)
+    p32 = scenarios.round_to_f32(pos, lengths)
+    ctx = pb.PppmContext((32, 32, 32), lengths, order=5, mode="ik", precision="mixed", alpha=0.3)
+    ctx.load_atoms(p32, q.astype(np.float32))
+    ctx.step()
+    ctx.synchronize()
+    f0 = ctx.forces()
+    for _ in range(3):  # eager, capture, replay
+        ctx.step()
+    ctx.synchronize()
+    f3 = ctx.forces()
+    ctx.close()
+    assert rel_rms(f3, f0) <= 1e-6
