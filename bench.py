@@ -309,6 +309,18 @@ def run_slabs(args, cfg, rank, local, world, pg):
     mesh_local = int(np.prod(cfg.dims)) // world
     alg = n_local * 16 + mesh_local * 4 + n_local * 16 + 3 * mesh_local * 4 + 3 * n_local * 4
     gbs = alg / ((t_mr + t_ff) / k) / 1e9
+    # the binding on-chip roofline: shared-memory bandwidth (128 B/clk/SM), algorithmic
+    # shared bytes = one 4-byte tile access per stencil point per field
+    sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    smem_peak = 148 * 128 * sm_clk / 1e9
+    S3 = cfg.order ** 3
+    smem_alg = {"spread": n * S3 * 4, "gather": n * S3 * 4 * (nf if mode == "ik" else 1)}
+    onchip = {"bound": "smem", "unit": "GB/s", "peak": smem_peak,
+              "peak_basis": "148 SMs x 128 B/clk x measured SM clock"}
+    for key in ("spread", "gather"):
+        t = ms[key] / 1e3 / k
+        onchip[key] = {"alg_bytes": smem_alg[key], "achieved": smem_alg[key] / t / 1e9,
+                       "frac": smem_alg[key] / t / 1e9 / smem_peak}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
         "ms_per_step": t_step_max / k * 1e3, "ms_make_rho_fieldforce": t_mf_max / k * 1e3,
@@ -407,6 +419,18 @@ def main():
                 "make_rho_fieldforce_gbs": mf_bytes / (t_mf / k) / 1e9,
                 "make_rho_fieldforce_frac": mf_bytes / (t_mf / k) / 1e9 / peak}
 
+    # the binding on-chip roofline: shared-memory bandwidth (128 B/clk/SM), algorithmic
+    # shared bytes = one 4-byte tile access per stencil point per field
+    sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    smem_peak = 148 * 128 * sm_clk / 1e9
+    S3 = cfg.order ** 3
+    smem_alg = {"spread": n * S3 * 4, "gather": n * S3 * 4 * (nf if mode == "ik" else 1)}
+    onchip = {"bound": "smem", "unit": "GB/s", "peak": smem_peak,
+              "peak_basis": "148 SMs x 128 B/clk x measured SM clock"}
+    for key in ("spread", "gather"):
+        t = ms[key] / 1e3 / k
+        onchip[key] = {"alg_bytes": smem_alg[key], "achieved": smem_alg[key] / t / 1e9,
+                       "frac": smem_alg[key] / t / 1e9 / smem_peak}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
         "ms_per_step": t_step_max / k * 1e3, "ms_make_rho_fieldforce": t_mf_max / k * 1e3,
@@ -419,7 +443,8 @@ def main():
                    "parallelism": f"replicas{world}" if world > 1 else "single"},
         "phases_ms_per_step": {kk: v / k for kk, v in ms.items()},
         "whole_step_atom_steps_per_s": atoms_total * k / t_step_max,
-        "kernels": per_kernel, "roofline": roofline, "clocks": clocks, "gpu_launches": launches * k,
+        "kernels": per_kernel, "roofline": roofline, "onchip_roofline": onchip, "clocks": clocks,
+        "gpu_launches": launches * k,
         "wall_s_timed_region": t_wall,
     }
 

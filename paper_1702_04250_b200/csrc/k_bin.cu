@@ -5,7 +5,7 @@ namespace pppm {
 
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
-               int* err, cudaStream_t s) {
+               int* err, const int* orig, cudaStream_t s) {
   if (cudaMemsetAsync(counts, 0, sizeof(int) * (bk.count() + 2) * kCountStride, s) != cudaSuccess) return launch_status();
   const int grid = grid_for((a.n + kBinUnroll - 1) / kBinUnroll);
   int st = with_order(order, [&](auto S_) -> int {
@@ -15,15 +15,105 @@ int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Brick
       if (!a.f32)
         k_bin_fixed<S, TAB, double><<<grid, kThreads, 0, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, bk,
                                                               cap, n_points, counts, rec, rcell, perm, ovf_rec,
-                                                              ovf_cell, ovf_perm, err);
+                                                              ovf_cell, ovf_perm, err, orig);
       else
         k_bin_fixed<S, TAB, float><<<grid, kThreads, 0, s>>>((const float*)a.pos, (const float*)a.q, a.n, g, bk,
                                                              cap, n_points, counts, rec, rcell, perm, ovf_rec,
-                                                             ovf_cell, ovf_perm, err);
+                                                             ovf_cell, ovf_perm, err, orig);
       return 0;
     });
   });
   return st ? st : launch_status();
+}
+
+// ---------------------------------------------------------------------------
+// resident atoms kept in brick order (done once per load, like an MD engine's
+// periodic atom sort): exclusive scan of the clamped bucket counts, then a
+// gather of positions / charges into bucket order with the caller's index.
+
+__global__ void __launch_bounds__(1024) k_scan_buckets(const int* __restrict__ counts, int nb, int cap,
+                                                       int* __restrict__ start) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    int v = i < nb ? counts[(int64_t)i * kCountStride] : 0;
+    v = v < cap ? v : cap;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const int excl = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - v;
+    if (i < nb) start[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) start[nb] = carry;
+}
+
+template <typename T>
+__global__ void k_reorder_resident(const float4* __restrict__ rec, const int* __restrict__ counts,
+                                   const int* __restrict__ start, int nb, int cap,
+                                   const int* __restrict__ ovf_perm, const T* __restrict__ pos,
+                                   const T* __restrict__ q, T* __restrict__ pos_out, T* __restrict__ q_out,
+                                   int* __restrict__ orig_out) {
+  const int64_t slots = (int64_t)nb * cap;
+  const int novf = counts[(int64_t)nb * kCountStride];
+  const int bucketed = start[nb];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < slots + novf;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t dst, i;
+    if (k < slots) {
+      const int b = (int)(k / cap), s = (int)(k % cap);
+      int c = counts[(int64_t)b * kCountStride];
+      c = c < cap ? c : cap;
+      if (s >= c) continue;
+      dst = start[b] + s;
+      i = reinterpret_cast<const int4*>(rec)[2 * k + 1].y;
+    } else {
+      const int o = (int)(k - slots);
+      dst = bucketed + o;
+      i = ovf_perm[o];
+    }
+    pos_out[3 * dst] = pos[3 * i];
+    pos_out[3 * dst + 1] = pos[3 * i + 1];
+    pos_out[3 * dst + 2] = pos[3 * i + 2];
+    q_out[dst] = q[i];
+    orig_out[dst] = (int)i;
+  }
+}
+
+int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
+                            const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
+                            void* q_out, int* orig_out, cudaStream_t s) {
+  const int nb = bk.count();
+  k_scan_buckets<<<1, 1024, 0, s>>>(counts, nb, cap, start);
+  const int grid = grid_for((int64_t)nb * cap + n);
+  if (f32)
+    k_reorder_resident<float><<<grid, kThreads, 0, s>>>(rec, counts, start, nb, cap, ovf_perm, (const float*)pos,
+                                                       (const float*)q, (float*)pos_out, (float*)q_out, orig_out);
+  else
+    k_reorder_resident<double><<<grid, kThreads, 0, s>>>(rec, counts, start, nb, cap, ovf_perm, (const double*)pos,
+                                                        (const double*)q, (double*)pos_out, (double*)q_out, orig_out);
+  return launch_status();
 }
 
 }  // namespace pppm

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
     int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
-    int* __restrict__ err) {
+    int* __restrict__ err, const int* __restrict__ orig) {
   const int nb = bk.count();
   int* ovf_count = counts + (int64_t)nb * kCountStride;
   float qmax = 0.f;
@@ -126,24 +126,36 @@ __global__ void __launch_bounds__(kThreads) k_bin_fixed(
       }
       r[u].w = q;
     }
+    // warp-aggregated slot reservation: lanes with the same brick share one
+    // atomic (effective when the input is spatially sorted, e.g. resident atoms
+    // kept in brick order; no cost otherwise)
+    const unsigned am = __activemask();
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int u = 0; u < kBinUnroll; ++u)
-      if (b[u] >= 0) slot[u] = atomicAdd(counts + (int64_t)b[u] * kCountStride, 1);
+    for (int u = 0; u < kBinUnroll; ++u) {
+      const unsigned grp = __match_any_sync(am, b[u]);
+      const int leader = __ffs(grp) - 1;
+      int base = 0;
+      if (lane == leader && b[u] >= 0) base = atomicAdd(counts + (int64_t)b[u] * kCountStride, __popc(grp));
+      base = __shfl_sync(am, base, leader);
+      slot[u] = base + __popc(grp & ((1u << lane) - 1u));
+    }
 #pragma unroll
     for (int u = 0; u < kBinUnroll; ++u) {
       if (b[u] < 0) continue;
       const int64_t i = i0 + u * stride;
+      const int oi = orig ? orig[i] : (int)i;  // index in the caller's atom order
       if (slot[u] < cap) {
         // one 32-byte slot per atom (full-sector write): {tx, ty, tz, q}, {cell, input index}
         const int64_t k = (int64_t)b[u] * cap + slot[u];
         rec[2 * k] = r[u];
-        reinterpret_cast<int4*>(rec)[2 * k + 1] = make_int4(lc[u], (int)i, 0, 0);
+        reinterpret_cast<int4*>(rec)[2 * k + 1] = make_int4(lc[u], oi, 0, 0);
       } else {
         // overflow record: same payload, wrapped global node packed 10+10+10 bits (dims <= 1024)
         const int o = atomicAdd(ovf_count, 1);
         ovf_rec[o] = r[u];
         ovf_cell[o] = pk[u];
-        ovf_perm[o] = (int)i;
+        ovf_perm[o] = oi;
       }
     }
   }

@@ -125,7 +125,9 @@ struct pppm_ctx {
   int cap = 0;
   int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SORTED;
   DevBuf partial, scal, err, flush;
-  DevBuf res_pos, res_q, res_force;
+  DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
+  bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
+  bool sort_resident = true;
   // z-slab decomposition (P > 1): 2D spectra of the local planes, all-to-all
   // buffers, received ghost planes of the charge mesh
   int P = 1, rank = 0;
@@ -289,11 +291,12 @@ static void rec_event(pppm_ctx* c, int idx, bool timing) {
 }
 
 // make_rho on device atoms -----------------------------------------------------
-static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
+static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, const int* orig = nullptr) {
   TRY(ensure_bins(c, n));
   TRY(launch_bin(c->order, c->n_points > 0, atoms_in(pos, q, n, dtype), c->g, c->bk, c->cap, c->n_points,
                  c->counts.as<int>(), c->rec.as<float4>(), c->rcell.as<int>(), c->perm.as<int>(),
-                 c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->err.as<int>(), c->stream));
+                 c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->err.as<int>(), orig,
+                 c->stream));
   c->launches += 1;
   c->binned = true;
   return PPPM_OK;
@@ -594,6 +597,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_SPREAD")) c->spread_variant = atoi(v);
   if (const char* v = getenv("PPPM_B200_GATHER")) c->gather_variant = atoi(v);
   if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_SORT_RESIDENT")) c->sort_resident = atoi(v) != 0;
   *out = c;
   return PPPM_OK;
 }
@@ -638,7 +642,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
-                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force};
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -866,10 +870,26 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   TRY(c->res_force.ensure(3 * n * (c->fp64() ? 8 : 4)));
   CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * n * es, cudaMemcpyHostToDevice, c->stream));
   CU(cudaMemcpyAsync(c->res_q.p, q, n * es, cudaMemcpyHostToDevice, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
   c->n_res = n;
   c->res_dtype = dtype;
-  return PPPM_OK;
+  c->res_sorted = false;
+  if (!c->fp64() && c->sort_resident && c->g.nzl == c->g.nz) {  // single-mesh contexts only
+    // keep the resident atoms in brick order (as an MD engine sorts its atoms):
+    // bin once, then gather positions / charges into bucket order
+    TRY(run_bin(c, c->res_pos.p, c->res_q.p, n, dtype, nullptr));
+    TRY(c->res_orig.ensure(sizeof(int) * n));
+    TRY(c->res_tmp_pos.ensure(3 * n * es));
+    TRY(c->res_tmp_q.ensure(n * es));
+    TRY(c->bstart.ensure(sizeof(int) * (c->bk.count() + 1)));
+    TRY(launch_reorder_resident(dtype == PPPM_F32, c->bk, c->cap, c->rec.as<float4>(), c->counts.as<int>(),
+                                c->bstart.as<int>(), c->ovf_perm.as<int>(), n, c->res_pos.p, c->res_q.p,
+                                c->res_tmp_pos.p, c->res_tmp_q.p, c->res_orig.as<int>(), c->stream));
+    std::swap(c->res_pos, c->res_tmp_pos);
+    std::swap(c->res_q, c->res_tmp_q);
+    c->res_sorted = true;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return check_err_flag(c);
 }
 
 
@@ -880,7 +900,7 @@ static int run_subphase(pppm_ctx* c, int sp) {
   switch (sp) {
     case SP_BIN:
       c->binned = false;
-      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype));
+      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, c->res_sorted ? c->res_orig.as<int>() : nullptr));
       return PPPM_OK;
     case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype);
     case SP_POISSON:
@@ -1086,7 +1106,7 @@ int pppm_slab_make_rho(pppm_ctx* c) {
   TRY(activate(c));
   if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
   c->binned = false;
-  TRY(run_bin(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype));
+  TRY(run_bin(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype, c->res_sorted ? c->res_orig.as<int>() : nullptr));
   return run_spread(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype);
 }
 

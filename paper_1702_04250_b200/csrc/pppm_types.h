@@ -72,7 +72,10 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
                         double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s);
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
-               int* err, cudaStream_t s);
+               int* err, const int* orig, cudaStream_t s);
+int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
+                            const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
+                            void* q_out, int* orig_out, cudaStream_t s);
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad, cudaStream_t s);
