@@ -93,12 +93,18 @@ class PppmContext:
         self.ctx("pppm_ctx_launches_per_step", ctypes.byref(n))
         return n.value
 
-    def compute(self, positions, charges, mem=nat.HOST):
-        """One full evaluation through the C ABI with host buffers (H2D, step, D2H)."""
+    def compute(self, positions, charges, mem=nat.HOST, out=None):
+        """One full evaluation through the C ABI with host buffers (H2D, step, D2H).
+        ``out``: optional (n, 3) float64 destination (e.g. a pinned PinnedArray view)."""
         pos = np.ascontiguousarray(positions)
         q = np.ascontiguousarray(charges)
         dtype = nat.F32 if pos.dtype == np.float32 else nat.F64
-        forces = np.empty((pos.shape[0], 3))
+        if out is None:
+            forces = np.empty((pos.shape[0], 3))
+        else:
+            forces = out
+            if forces.shape != (pos.shape[0], 3) or forces.dtype != np.float64 or not forces.flags.c_contiguous:
+                raise ValueError("out must be a C-contiguous (n, 3) float64 array")
         e = np.zeros(1)
         self.ctx("pppm_compute", nat.ptr(pos), nat.ptr(q), pos.shape[0], dtype, mem, nat.ptr(forces),
                  e.ctypes.data_as(nat._dp))

@@ -60,9 +60,15 @@ template <> struct WMax<6> { static constexpr float v = 0.55f; };
 template <> struct WMax<7> { static constexpr float v = 0.5110244f; };
 
 // opt in to > 48 KB of dynamic shared memory (the 48 KB default counts static + dynamic)
+// and ask for the full shared-memory carveout (otherwise the driver may pick a
+// smaller L1/shared split and cap the resident CTAs per SM)
+#ifndef PPPM_CARVEOUT
+#define PPPM_CARVEOUT 100
+#endif
 template <typename K>
 inline void allow_smem(K kernel, size_t bytes) {
   if (bytes > 32 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (PPPM_CARVEOUT >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, PPPM_CARVEOUT);
 }
 
 // ---------------------------------------------------------------------------

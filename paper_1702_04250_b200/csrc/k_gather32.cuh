@@ -15,6 +15,9 @@ namespace pppm {
 #define PPPM_GATHER_THREADS 256
 #endif
 constexpr int kGatherThreads = PPPM_GATHER_THREADS;
+#ifndef PPPM_GATHER_MINB
+#define PPPM_GATHER_MINB (768 / PPPM_GATHER_THREADS)
+#endif
 
 template <int S, int MODE>
 __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i, float f0, float f1, float f2) {
@@ -32,7 +35,7 @@ __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i
 // i+1's (TXB, D, D, F) box from the halo-padded fields into the other buffer
 // (mbarrier transaction barriers; the halo makes every box in bounds).
 template <int S, bool TAB, int MODE, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_gather_tma(
+__global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ perm,
     const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
     const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,

@@ -61,35 +61,102 @@ __global__ void k_fold_z(Geom g, Pad p, float* __restrict__ rho) {
   }
 }
 
+// all axes in one pass: every interior cell of the boundary shell (within H
+// of a face along a folded axis) sums its periodic aliases in the halo.  Reads
+// touch only halo cells and writes only interior ones, so one launch suffices;
+// the halo is left as is (the mesh is cleared before the next make_rho and
+// the FFT reads the interior only).  On a z-slab (zper = 0) the ghost planes
+// are folded in x, y like the interior (they are reverse-summed into the
+// neighbours afterwards).  32-bit index math (meshes below 2^31 cells).
+// Requires nx, ny (and nz if zper) >= 2H.
+__global__ void k_fold_all(Geom g, Pad p, float* __restrict__ rho) {
+  const int H = p.H, nx = g.nx, ny = g.ny;
+  const int nzl = p.pz - 2 * H;
+  const int shell_planes = p.zper ? 2 * H : 0;     // whole planes (z near a face)
+  const int ring = 2 * H * nx + 2 * H * (ny - 2 * H);
+  const int ring_planes = p.zper ? nzl - 2 * H : nzl + 2 * H;
+  const int A = shell_planes * nx * ny;
+  const int total = A + ring_planes * ring;
+  const int plane = p.py * p.px;
+  float* r0 = rho + (int64_t)H * plane + (int64_t)H * p.px + p.hx;  // interior origin
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    int x, y, z;
+    if (k < A) {
+      const int idx = k / (nx * ny), r = k - idx * nx * ny;
+      z = idx < H ? idx : nzl - 2 * H + idx;
+      y = r / nx;
+      x = r - y * nx;
+    } else {
+      const int q = k - A;
+      const int pl = q / ring, r = q - pl * ring;
+      z = p.zper ? H + pl : pl - H;
+      if (r < 2 * H * nx) {
+        const int yy = r / nx;
+        x = r - yy * nx;
+        y = yy < H ? yy : ny - 2 * H + yy;
+      } else {
+        const int r2 = r - 2 * H * nx;
+        y = H + r2 / (2 * H);
+        const int xi = r2 % (2 * H);
+        x = xi < H ? xi : nx - 2 * H + xi;
+      }
+    }
+    const int ax = x < H ? nx : (x >= nx - H ? -nx : 0);
+    const int ay = y < H ? ny : (y >= ny - H ? -ny : 0);
+    const int az = p.zper ? (z < H ? nzl : (z >= nzl - H ? -nzl : 0)) : 0;
+    const int64_t o = ((int64_t)z * p.py + y) * p.px + x;
+    const int64_t ox = ax, oy = (int64_t)ay * p.px, oz = (int64_t)az * plane;
+    float s = r0[o];
+    if (ax) s += r0[o + ox];
+    if (ay) {
+      s += r0[o + oy];
+      if (ax) s += r0[o + oy + ox];
+    }
+    if (az) {
+      s += r0[o + oz];
+      if (ax) s += r0[o + oz + ox];
+      if (ay) {
+        s += r0[o + oz + oy];
+        if (ax) s += r0[o + oz + oy + ox];
+      }
+    }
+    r0[o] = s;
+  }
+}
+
 // halo fill: every cell of [0, nx+2H) x [0, ny+2H) x [0, nz+2H) outside the
 // interior takes the value of its periodic image, for `nf` fields
 __global__ void k_fill(Geom g, Pad p, float* __restrict__ f, int nf) {
+  // 32-bit index math (the halo shell is far below 2^31 cells)
   const int ex = g.nx + 2 * p.H, ey = g.ny + 2 * p.H, per = 2 * p.H;
-  const int nzl = p.pz - 2 * p.H;                  // interior planes of this slab
-  const int64_t ra = p.zper ? (int64_t)per * ey * ex : 0;  // z halo planes (one GPU only)
-  const int64_t rb = (int64_t)nzl * per * ex;      // y halo rows, interior z
-  const int64_t rc = (int64_t)nzl * g.ny * per;    // x halo cells, interior y, z
-  const int64_t total = ra + rb + rc;
+  const int nzl = p.pz - 2 * p.H;                 // interior planes of this slab
+  const int ra = p.zper ? per * ey * ex : 0;      // z halo planes (one GPU only)
+  const int rb = nzl * per * ex;                  // y halo rows, interior z
+  const int rc = nzl * g.ny * per;                // x halo cells, interior y, z
+  const int total = ra + rb + rc;
   const int64_t mesh = p.count();
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
     int x, y, z;
     if (k < ra) {
-      x = (int)(k % ex);
-      y = (int)((k / ex) % ey);
-      const int h = (int)(k / ((int64_t)ex * ey));
+      const int t = k / ex;
+      x = k - t * ex;
+      const int h = t / ey;
+      y = t - h * ey;
       z = h < p.H ? h : nzl + h;
     } else if (k < ra + rb) {
-      const int64_t q = k - ra;
-      x = (int)(q % ex);
-      const int h = (int)((q / ex) % per);
+      const int q = k - ra;
+      const int t = q / ex;
+      x = q - t * ex;
+      const int zz = t / per, h = t - zz * per;
       y = h < p.H ? h : g.ny + h;
-      z = (int)(q / ((int64_t)ex * per)) + p.H;
+      z = zz + p.H;
     } else {
-      const int64_t q = k - ra - rb;
-      const int h = (int)(q % per);
+      const int q = k - ra - rb;
+      const int t = q / per, h = q - t * per;
       x = h < p.H ? h : g.nx + h;
-      y = (int)((q / per) % g.ny) + p.H;
-      z = (int)(q / ((int64_t)per * g.ny)) + p.H;
+      const int zz = t / g.ny;
+      y = t - zz * g.ny + p.H;
+      z = zz + p.H;
     }
     x += p.hx - p.H;  // enumerated x in [0, nx + 2H) -> padded [hx - H, hx + nx + H)
     const int ix = wrap_index(x - p.hx, g.nx) + p.hx;
@@ -123,6 +190,14 @@ __global__ void k_pad_in(Geom g, Pad p, const double* __restrict__ src, float* _
 
 int launch_fold_halo(const Geom& g, const Pad& p, float* rho, cudaStream_t s) {
   if (p.H == 0) return 0;
+  const int nzl = p.pz - 2 * p.H;
+  if (g.nx >= 2 * p.H && g.ny >= 2 * p.H && (!p.zper || nzl >= 2 * p.H)) {
+    const int64_t ring = 2 * p.H * g.nx + 2 * p.H * (g.ny - 2 * p.H);
+    const int64_t total = (p.zper ? 2 * p.H * (int64_t)g.nx * g.ny : 0) +
+                          (p.zper ? nzl - 2 * p.H : nzl + 2 * p.H) * ring;
+    k_fold_all<<<grid_for(total), kThreads, 0, s>>>(g, p, rho);
+    return launch_status();
+  }
   k_fold_x<<<grid_for((int64_t)p.py * p.pz * 2 * p.H), kThreads, 0, s>>>(g, p, rho);
   k_fold_y<<<grid_for((int64_t)p.pz * 2 * p.H * g.nx), kThreads, 0, s>>>(g, p, rho);
   if (p.zper) k_fold_z<<<grid_for((int64_t)2 * p.H * g.ny * g.nx), kThreads, 0, s>>>(g, p, rho);
