@@ -24,6 +24,7 @@
 // same way, one thread per atom, forces scattered to the input order.
 #pragma once
 
+#include "bspline_poly.h"
 #include "pppm_device.cuh"
 
 namespace pppm {
@@ -193,7 +194,23 @@ __device__ __forceinline__ void rows_f32(float v, const float* __restrict__ ta, 
       for (int j = 0; j < S; ++j) d[j] = __ldg(rd + j);
     }
   } else {
-    bspline_rows<FastF32, S>(v, a, d);
+    // exact spline polynomials in t (tools/gen_bspline_poly.py), Horner
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      float x = bspline_a<S>(j, S - 1);
+#pragma unroll
+      for (int k = S - 2; k >= 0; --k) x = fmaf(x, v, bspline_a<S>(j, k));
+      a[j] = x;
+    }
+    if (DERIV) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        float x = bspline_d<S>(j, S - 2);
+#pragma unroll
+        for (int k = S - 3; k >= 0; --k) x = fmaf(x, v, bspline_d<S>(j, k));
+        d[j] = x;
+      }
+    }
   }
 }
 

@@ -30,6 +30,50 @@ __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i
   }
 }
 
+// overflow atoms (full buckets): gather straight from the padded fields
+template <int S, bool TAB, int MODE>
+__device__ __forceinline__ void gather_overflow(const int* __restrict__ counts, int nb, const Geom& g, const Pad& pd,
+                                                const float* __restrict__ ta, const float* __restrict__ td,
+                                                const float* __restrict__ fields, float cscale, void* force,
+                                                bool out_f64, const float4* __restrict__ ovf_rec,
+                                                const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
+  constexpr int lo = Stencil<S>::lo;
+  const float ihx = (float)g.ihx, ihy = (float)g.ihy, ihz = (float)g.ihz;
+  const int64_t mesh = pd.count();
+  const int novf = counts[(int64_t)nb * kCountStride];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
+    const float4 r = ovf_rec[k];
+    const int cc = ovf_cell[k];
+    const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
+    float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
+    rows_f32<S, TAB, MODE == 1>(r.x, ta, td, ax, dx);
+    rows_f32<S, TAB, MODE == 1>(r.y, ta, td, ay, dy);
+    rows_f32<S, TAB, MODE == 1>(r.z, ta, td, az, dz);
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    for (int a = 0; a < S; ++a) {
+      for (int bb = 0; bb < S; ++bb) {
+        for (int c = 0; c < S; ++c) {
+          const int64_t gi = pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a);  // halos / ghosts filled
+          if (MODE == 0) {
+            const float w = az[a] * ay[bb] * ax[c];
+            s0 += w * __ldg(fields + gi);
+            s1 += w * __ldg(fields + mesh + gi);
+            s2 += w * __ldg(fields + 2 * mesh + gi);
+          } else {
+            const float p = __ldg(fields + gi);
+            s0 += az[a] * ay[bb] * dx[c] * p;
+            s1 += az[a] * dy[bb] * ax[c] * p;
+            s2 += dz[a] * ay[bb] * ax[c] * p;
+          }
+        }
+      }
+    }
+    const float sc = cscale * r.w;
+    if (MODE == 0) store_force<S, MODE>(force, out_f64, ovf_perm[k], sc * s0, sc * s1, sc * s2);
+    else store_force<S, MODE>(force, out_f64, ovf_perm[k], -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
+  }
+}
+
 // fieldforce, persistent CTAs over bricks with double-buffered field tiles:
 // while brick i is computed from tile buffer i&1, the TMA engine loads brick
 // i+1's (TXB, D, D, F) box from the halo-padded fields into the other buffer
@@ -152,39 +196,124 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
     }
     __syncthreads();  // tile buffer `buf` and the staging arrays are free again
   }
-  // overflow atoms: gather straight from the padded fields
-  const int novf = counts[(int64_t)nb * kCountStride];
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
-    const float4 r = ovf_rec[k];
-    const int cc = ovf_cell[k];
-    const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
-    float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
-    rows_f32<S, TAB, MODE == 1>(r.x, ta, td, ax, dx);
-    rows_f32<S, TAB, MODE == 1>(r.y, ta, td, ay, dy);
-    rows_f32<S, TAB, MODE == 1>(r.z, ta, td, az, dz);
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    for (int a = 0; a < S; ++a) {
-      for (int bb = 0; bb < S; ++bb) {
-        for (int c = 0; c < S; ++c) {
-          const int64_t gi = pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a);  // halos / ghosts filled
-          if (MODE == 0) {
-            const float w = az[a] * ay[bb] * ax[c];
-            s0 += w * __ldg(fields + gi);
-            s1 += w * __ldg(fields + mesh + gi);
-            s2 += w * __ldg(fields + 2 * mesh + gi);
-          } else {
-            const float p = __ldg(fields + gi);
-            s0 += az[a] * ay[bb] * dx[c] * p;
-            s1 += az[a] * dy[bb] * ax[c] * p;
-            s2 += dz[a] * ay[bb] * ax[c] * p;
-          }
+  gather_overflow<S, TAB, MODE>(counts, nb, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+                                ovf_perm);
+}
+
+// fieldforce_ik with one task per (atom, field component).  The three field
+// tiles are loaded with their rows shifted by f (box y start - f, box height
+// D + 2), so component f of an atom sits f*TXB banks past its corner bank:
+// lane k serves the concatenation over f of the atom buckets k - f*TXB, whose
+// total is a sum of three bucket sizes - fuller conflict-free rounds than one
+// task per atom (SplitTile<S>::ok: TXB = 12 or 20 mod 32).
+template <int S> struct SplitTile {
+  static constexpr int TXB = TmaTile<S>::TXB, D = TmaTile<S>::D, DY = D + 2;
+  static constexpr int FTN = TXB * DY * D;          // floats per field box
+  static constexpr int FT = (FTN + 31) / 32 * 32;   // 128-byte aligned field stride
+  static constexpr bool ok = (TXB % 32 == 12 || TXB % 32 == 20);
+};
+
+template <int S, bool TAB, int NT>
+__global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
+    const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
+    const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
+    const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
+  using T = TmaTile<S>;
+  using ST = SplitTile<S>;
+  constexpr int TXB = T::TXB, DY = ST::DY, FT = ST::FT, lo = Stencil<S>::lo;
+  constexpr int BUF = 3 * FT;
+  constexpr uint32_t kBytes = 3u * ST::FTN * sizeof(float);
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  float* tiles = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);
+  int* s_c = reinterpret_cast<int*>(s_r + cap);
+  int* s_p = s_c + cap;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int bsize[32], bstart[33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  const int nb = bk.count();
+  auto issue = [&](int b, int buf) {
+    const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+    const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
+    mbar_arrive_expect_tx(&bar[buf], kBytes);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) tma_load_4d(tiles + buf * BUF + f * FT, &fmap, &bar[buf], x, y - f, z, f);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (int)blockIdx.x < nb) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int nxt = b + gridDim.x;
+    if (threadIdx.x == 0 && nxt < nb) {
+      fence_proxy_async_smem();  // generic reads of that buffer (previous brick) before the async-proxy write
+      issue(nxt, buf ^ 1);
+    }
+    int cnt = counts[(int64_t)b * kCountStride];
+    cnt = cnt < cap ? cnt : cap;
+    BankSmem sm{s_r, s_c, s_p, bsize, bstart};
+    if (cnt > 0) stage_banked<true, DY, TXB, T::SH, NT>(rec, nullptr, nullptr, (int64_t)b * cap, cnt, sm);
+    mbar_wait(&bar[buf], (it >> 1) & 1);
+    const float* tile = tiles + buf * BUF;
+    int seg0 = 0, seg1 = 0, seg2 = 0;
+    if (cnt > 0) {
+      seg0 = bsize[lane];
+      seg1 = bsize[(lane - TXB) & 31];
+      seg2 = bsize[(lane - 2 * TXB) & 31];
+    }
+    const int tot = seg0 + seg1 + seg2;
+    int trounds = tot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) trounds = max(trounds, __shfl_xor_sync(0xffffffffu, trounds, o));
+    for (int rr = warp; rr < trounds; rr += nwarp) {
+      if (rr >= tot) continue;
+      int f = 0, rk = rr;
+      if (rk >= seg0) {
+        rk -= seg0;
+        f = 1;
+        if (rk >= seg1) {
+          rk -= seg1;
+          f = 2;
         }
       }
+      const int j = bstart[(lane - f * TXB) & 31] + rk;
+      const float4 r = s_r[j];
+      const int cc = s_c[j];
+      const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+      float ax[S], ay[S], az[S], dd[S];
+      rows_f32<S, TAB, false>(r.x, ta, td, ax, dd);
+      rows_f32<S, TAB, false>(r.y, ta, td, ay, dd);
+      rows_f32<S, TAB, false>(r.z, ta, td, az, dd);
+      const float* tf = tile + f * FT + (lz * DY + ly + f) * TXB + lx + T::SH;
+      float s = 0.f;
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        float ra = 0.f;
+#pragma unroll
+        for (int bb = 0; bb < S; ++bb) {
+          const float* row = tf + (a * DY + bb) * TXB;
+          float e = 0.f;
+#pragma unroll
+          for (int c = 0; c < S; ++c) e = fmaf(ax[c], row[c], e);
+          ra = fmaf(ay[bb], e, ra);
+        }
+        s = fmaf(az[a], ra, s);
+      }
+      const float v = cscale * r.w * s;
+      const int64_t i = s_p[j];
+      if (out_f64) static_cast<double*>(force)[3 * i + f] = v;
+      else static_cast<float*>(force)[3 * i + f] = v;
     }
-    const float sc = cscale * r.w;
-    if (MODE == 0) store_force<S, MODE>(force, out_f64, ovf_perm[k], sc * s0, sc * s1, sc * s2);
-    else store_force<S, MODE>(force, out_f64, ovf_perm[k], -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
+    __syncthreads();  // tile buffer `buf` and the staging arrays are free again
   }
+  gather_overflow<S, TAB, 0>(counts, nb, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+                             ovf_perm);
 }
 
 template <int MODE>
@@ -196,6 +325,27 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if constexpr (MODE == 0 && SplitTile<S>::ok) {
+      if (variant == GATHER_SPLIT) {
+        const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
+                           (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
+        return with_bool(tab, [&](auto T_) -> int {
+          constexpr bool TAB = decltype(T_)::value;
+          constexpr int NT = kGatherThreads;
+          auto k = k_gather_split<S, TAB, NT>;
+          allow_smem(k, dyn);
+          int per_sm = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
+          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
+                                  ovf_rec, ovf_cell, ovf_perm);
+          return 0;
+        });
+      }
+    }
     const size_t dyn = 128 + 2 * (size_t)((F * TmaTile<S>::N + 31) / 32 * 32) * sizeof(float) + (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
@@ -204,12 +354,9 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
       allow_smem(k, dyn);
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
       k<<<grid, NT, dyn, s>>>(rec, rcell, perm, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force,
-                                    out_f64, variant == GATHER_SORTED, ovf_rec, ovf_cell, ovf_perm);
+                                    out_f64, variant != GATHER_PLAIN, ovf_rec, ovf_cell, ovf_perm);
       return 0;
     });
   });

@@ -123,7 +123,7 @@ struct pppm_ctx {
   DevBuf pos_stage, q_stage, out_stage, node_stage;
   DevBuf counts, rec, rcell, perm, ovf_rec, ovf_cell, ovf_perm;
   int cap = 0;
-  int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SORTED;
+  int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SPLIT;
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
@@ -195,6 +195,14 @@ static int ensure_plans(pppm_ctx* c) {
   return PPPM_OK;
 }
 
+// gather kernel actually used: the split (per-component) fieldforce needs ik
+// and a TXB of 12 or 20 mod 32, otherwise the bank-sorted one
+static int gather_eff(const pppm_ctx* c) {
+  if (c->gather_variant == GATHER_SPLIT && !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
+    return GATHER_SORTED;
+  return c->gather_variant;
+}
+
 // TMA descriptors of the padded fp32 meshes (driver entry point fetched at
 // run time, so the library does not link libcuda)
 static int encode_maps(pppm_ctx* c) {
@@ -227,7 +235,10 @@ static int encode_maps(pppm_ctx* c) {
     cuuint64_t dims[4] = {(cuuint64_t)c->pd.px, (cuuint64_t)c->pd.py, (cuuint64_t)c->pd.pz,
                           (cuuint64_t)c->nfields()};
     cuuint64_t strides[3] = {row, plane, vol};
-    cuuint32_t box[4] = {(cuuint32_t)txb, (cuuint32_t)D, (cuuint32_t)D, (cuuint32_t)c->nfields()};
+    // split gather: one component per box, two extra rows (row shift per component)
+    const bool split = gather_eff(c) == GATHER_SPLIT;
+    cuuint32_t box[4] = {(cuuint32_t)txb, (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
+                         (cuuint32_t)(split ? 1 : c->nfields())};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(&c->field_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->fields.p, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -369,7 +380,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
     const float* ta = c->tab.as<float>();
     const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
-    TRY(launch_gather_brick(c->gather_variant, c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
+    TRY(launch_gather_brick(gather_eff(c), c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
                             c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
                             c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out, c->stream));
@@ -598,6 +609,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_GATHER")) c->gather_variant = atoi(v);
   if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_SORT_RESIDENT")) c->sort_resident = atoi(v) != 0;
+  if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
   return PPPM_OK;
 }
@@ -620,8 +632,10 @@ int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
   drop_graphs(c);
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
-  else if (kernel == 1 && (variant == GATHER_PLAIN || variant == GATHER_SORTED)) c->gather_variant = variant;
+  else if (kernel == 1 && (variant == GATHER_PLAIN || variant == GATHER_SORTED || variant == GATHER_SPLIT))
+    c->gather_variant = variant;
   else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
+  if (!c->fp64() && c->fields.p) TRY(encode_maps(c));
   return PPPM_OK;
 }
 

@@ -60,7 +60,13 @@ struct AtomsIn {
 
 // kernel variants (selectable per context for A/B measurement)
 enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1 };  // + 2: same, cell-sorted in shared memory
-enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1 };
+enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2 };  // SPLIT: ik only (k_gather_split)
+// field tiles of the split gather: rows shifted per component (TXB = 12 or 20 mod 32)
+inline bool gather_split_ok(int order, int hx) {
+  const int D = 8 + order - 1, lo = (order - 1) / 2;
+  const int sh = ((hx - lo) % 4 + 4) % 4, txb = (D + sh + 3) / 4 * 4;
+  return txb % 32 == 12 || txb % 32 == 20;
+}
 
 // launchers: return 0, or a pppm_status code with the message set via set_error()
 void set_error(int code, const char* msg);
