@@ -168,6 +168,13 @@ class ClockSampler:
 KERNEL_NAMES = {"spread": "k_spread_tma", "gather": "k_gather_tma", "bin": "k_bin_fixed"}
 
 
+def kernel_name(kernel, mode):
+    """Name of the kernel behind a phase (fieldforce_ik: the warp-specialized split kernel)."""
+    if kernel == "gather" and mode == "ik":
+        return "k_gather_ws"
+    return KERNEL_NAMES[kernel]
+
+
 def load_traffic(config, mode, kernel):
     """ncu DRAM bytes (read + write) per launch of ``kernel``, from the committed
     profiles/traffic.json (tools/launch_summary.py --traffic), else None."""
@@ -175,7 +182,7 @@ def load_traffic(config, mode, kernel):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"config{config}_{mode}", {}).get(KERNEL_NAMES[kernel])
+        return d.get(f"config{config}_{mode}", {}).get(kernel_name(kernel, mode))
     except Exception:
         return None
 
@@ -414,7 +421,7 @@ def main():
     achieved = per_kernel[dom]["gbs"]
     mf_bytes = alg["spread"] + alg["gather"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(args.config, mode, dom), "kernel": KERNEL_NAMES[dom],
+                "traffic": load_traffic(args.config, mode, dom), "kernel": kernel_name(dom, mode),
                 "peak_kind": peak_kind,
                 "make_rho_fieldforce_gbs": mf_bytes / (t_mf / k) / 1e9,
                 "make_rho_fieldforce_frac": mf_bytes / (t_mf / k) / 1e9 / peak}

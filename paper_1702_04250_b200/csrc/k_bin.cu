@@ -101,6 +101,22 @@ __global__ void k_reorder_resident(const float4* __restrict__ rec, const int* __
   }
 }
 
+// forces of brick-ordered resident atoms back to the caller's order (fp64 out)
+__global__ void k_unpermute_forces(const float* __restrict__ f, const int* __restrict__ orig, int64_t n,
+                                   double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = orig[i];
+    out[3 * o] = f[3 * i];
+    out[3 * o + 1] = f[3 * i + 1];
+    out[3 * o + 2] = f[3 * i + 2];
+  }
+}
+
+int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s) {
+  k_unpermute_forces<<<grid_for(n), kThreads, 0, s>>>(f, orig, n, out);
+  return launch_status();
+}
+
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
                             void* q_out, int* orig_out, cudaStream_t s) {

@@ -316,6 +316,163 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
                              ovf_perm);
 }
 
+// fieldforce_ik, warp-specialized split variant: warp 0 stages brick i+1
+// (bank-bucketed counting sort of its records into shared memory, TMA loads of
+// its three row-shifted field tiles) while the consumer warps run brick i's
+// rounds; two stage slots handed over with mbarriers (full: staged + tile
+// bytes landed; empty: every consumer warp done), so no block-wide barrier and
+// no exposed record-load latency.  Same tasks / numerics as k_gather_split.
+constexpr int kWsConsumerWarps = 8;
+
+template <int S, bool TAB>
+__global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
+    const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
+    const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
+    const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
+  using T = TmaTile<S>;
+  using ST = SplitTile<S>;
+  constexpr int TXB = T::TXB, DY = ST::DY, FT = ST::FT, lo = Stencil<S>::lo;
+  constexpr int BUF = 3 * FT;
+  constexpr int NCW = kWsConsumerWarps;
+  constexpr uint32_t kBytes = 3u * ST::FTN * sizeof(float);
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  float* tiles = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][BUF]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);  // [2][cap]
+  int* s_c = reinterpret_cast<int*>(s_r + 2 * cap);          // [2][cap]
+  int* s_p = s_c + 2 * cap;                                  // [2][cap]
+  __shared__ __align__(8) uint64_t full[2], tmaf[2], empty[2];
+  __shared__ int bsize[2][32], bstart[2][32], cursor[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = bk.count();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&tmaf[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer
+    int k = 0;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
+      const int s = k & 1, use = k >> 1;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      if (lane == 0) {
+        const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+        const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&tmaf[s], kBytes);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+      }
+      int cnt = counts[(int64_t)b * kCountStride];
+      cnt = cnt < cap ? cnt : cap;
+      const int64_t base = (int64_t)b * cap;
+      const int4* meta = reinterpret_cast<const int4*>(rec);
+      bsize[s][lane] = 0;
+      __syncwarp();
+      // pass 1: bank histogram
+      for (int j = lane; j < cnt; j += 32) {
+        const int cc = meta[2 * (base + j) + 1].x;
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        atomicAdd(&bsize[s][((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
+      }
+      __syncwarp();
+      {
+        const int v = bsize[s][lane];
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        bstart[s][lane] = x - v;
+        cursor[lane] = x - v;
+      }
+      __syncwarp();
+      // pass 2: scatter into bank order
+      float4* sr = s_r + s * cap;
+      int* sc = s_c + s * cap;
+      int* sp = s_p + s * cap;
+      for (int j = lane; j < cnt; j += 32) {
+        const float4 r = rec[2 * (base + j)];
+        const int4 m = meta[2 * (base + j) + 1];
+        const int lx = m.x & (kBrick - 1), ly = (m.x >> 3) & (kBrick - 1), lz = m.x >> 6;
+        const int dst = atomicAdd(&cursor[((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
+        sr[dst] = r;
+        sc[dst] = m.x;
+        sp[dst] = m.y;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else {
+    // ---------------- consumers
+    const int cw = warp - 1;
+    int k = 0;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
+      const int s = k & 1, ph = (k >> 1) & 1;
+      mbar_wait(&full[s], ph);
+      mbar_wait(&tmaf[s], ph);
+      const float* tile = tiles + s * BUF;
+      const float4* sr = s_r + s * cap;
+      const int* sc = s_c + s * cap;
+      const int* sp = s_p + s * cap;
+      const int seg0 = bsize[s][lane], seg1 = bsize[s][(lane - TXB) & 31], seg2 = bsize[s][(lane - 2 * TXB) & 31];
+      const int tot = seg0 + seg1 + seg2;
+      int trounds = tot;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) trounds = max(trounds, __shfl_xor_sync(0xffffffffu, trounds, o));
+      for (int rr = cw; rr < trounds; rr += NCW) {
+        if (rr >= tot) continue;
+        int f = 0, rk = rr;
+        if (rk >= seg0) {
+          rk -= seg0;
+          f = 1;
+          if (rk >= seg1) {
+            rk -= seg1;
+            f = 2;
+          }
+        }
+        const int j = bstart[s][(lane - f * TXB) & 31] + rk;
+        const float4 r = sr[j];
+        const int cc = sc[j];
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        float ax[S], ay[S], az[S], dd[S];
+        rows_f32<S, TAB, false>(r.x, ta, td, ax, dd);
+        rows_f32<S, TAB, false>(r.y, ta, td, ay, dd);
+        rows_f32<S, TAB, false>(r.z, ta, td, az, dd);
+        const float* tf = tile + f * FT + (lz * DY + ly + f) * TXB + lx + T::SH;
+        float acc = 0.f;
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          float ra = 0.f;
+#pragma unroll
+          for (int bb = 0; bb < S; ++bb) {
+            const float* row = tf + (a * DY + bb) * TXB;
+            float e = 0.f;
+#pragma unroll
+            for (int c = 0; c < S; ++c) e = fmaf(ax[c], row[c], e);
+            ra = fmaf(ay[bb], e, ra);
+          }
+          acc = fmaf(az[a], ra, acc);
+        }
+        const float v = cscale * r.w * acc;
+        const int64_t i = sp[j];
+        if (out_f64) static_cast<double*>(force)[3 * i + f] = v;
+        else static_cast<float*>(force)[3 * i + f] = v;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  gather_overflow<S, TAB, 0>(counts, nb, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+                             ovf_perm);
+}
+
 template <int MODE>
 int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const float4* rec, const int* rcell,
                        const int* perm, const int* counts, int cap, const float4* ovf_rec, const int* ovf_cell,
@@ -329,6 +486,22 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if constexpr (MODE == 0 && SplitTile<S>::ok) {
+      if (variant == GATHER_WS) {
+        const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
+                           2 * (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
+        return with_bool(tab, [&](auto T_) -> int {
+          constexpr bool TAB = decltype(T_)::value;
+          auto k = k_gather_ws<S, TAB>;
+          allow_smem(k, dyn);
+          constexpr int NT = 32 * (kWsConsumerWarps + 1);
+          int per_sm = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
+          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
+                                  ovf_rec, ovf_cell, ovf_perm);
+          return 0;
+        });
+      }
       if (variant == GATHER_SPLIT) {
         const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
                            (size_t)cap * (sizeof(float4) + 2 * sizeof(int));

@@ -123,7 +123,7 @@ struct pppm_ctx {
   DevBuf pos_stage, q_stage, out_stage, node_stage;
   DevBuf counts, rec, rcell, perm, ovf_rec, ovf_cell, ovf_perm;
   int cap = 0;
-  int spread_variant = SPREAD_FIX32, gather_variant = GATHER_SPLIT;
+  int spread_variant = SPREAD_FIX32, gather_variant = GATHER_WS;
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
@@ -198,7 +198,8 @@ static int ensure_plans(pppm_ctx* c) {
 // gather kernel actually used: the split (per-component) fieldforce needs ik
 // and a TXB of 12 or 20 mod 32, otherwise the bank-sorted one
 static int gather_eff(const pppm_ctx* c) {
-  if (c->gather_variant == GATHER_SPLIT && !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
+  if ((c->gather_variant == GATHER_SPLIT || c->gather_variant == GATHER_WS) &&
+      !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
     return GATHER_SORTED;
   return c->gather_variant;
 }
@@ -236,7 +237,7 @@ static int encode_maps(pppm_ctx* c) {
                           (cuuint64_t)c->nfields()};
     cuuint64_t strides[3] = {row, plane, vol};
     // split gather: one component per box, two extra rows (row shift per component)
-    const bool split = gather_eff(c) == GATHER_SPLIT;
+    const bool split = gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS;
     cuuint32_t box[4] = {(cuuint32_t)txb, (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
                          (cuuint32_t)(split ? 1 : c->nfields())};
     cuuint32_t es[4] = {1, 1, 1, 1};
@@ -276,10 +277,11 @@ static AtomsIn atoms_in(const void* pos, const void* q, int64_t n, int dtype) {
   return AtomsIn{pos, q, n, dtype == PPPM_F32 ? 1 : 0};
 }
 
-// bucket capacity: twice the mean brick occupancy plus slack, in [128, 1024]
+// bucket capacity: 1.75x the mean brick occupancy plus slack, in [128, 1024]
+// (fuller buckets spill to the overflow list)
 static int bucket_cap(pppm_ctx* c, int64_t n) {
   const int64_t nb = c->bk.count();
-  int64_t cap = 2 * ((n + nb - 1) / nb) + 64;
+  int64_t cap = 7 * ((n + nb - 1) / nb) / 4 + 64;
   cap = (cap + 31) / 32 * 32;
   cap = std::max<int64_t>(128, std::min<int64_t>(cap, 1024));
   return (int)cap;
@@ -632,7 +634,7 @@ int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
   drop_graphs(c);
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
-  else if (kernel == 1 && (variant == GATHER_PLAIN || variant == GATHER_SORTED || variant == GATHER_SPLIT))
+  else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_WS)
     c->gather_variant = variant;
   else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
   if (!c->fp64() && c->fields.p) TRY(encode_maps(c));
@@ -914,7 +916,9 @@ static int run_subphase(pppm_ctx* c, int sp) {
   switch (sp) {
     case SP_BIN:
       c->binned = false;
-      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, c->res_sorted ? c->res_orig.as<int>() : nullptr));
+      // sorted resident atoms: slots carry the resident index (forces land in
+      // brick order, contiguous per brick) and get_forces un-permutes
+      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, nullptr));
       return PPPM_OK;
     case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype);
     case SP_POISSON:
@@ -996,6 +1000,14 @@ int pppm_ctx_get_forces(pppm_ctx* c, double* forces) {
   const int64_t cnt = 3 * c->n_res;
   if (c->fp64()) {
     CU(cudaMemcpyAsync(forces, c->res_force.p, 8 * cnt, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return PPPM_OK;
+  }
+  if (c->res_sorted) {
+    TRY(c->out_stage.ensure(sizeof(double) * cnt));
+    TRY(launch_unpermute_forces(c->res_force.as<float>(), c->res_orig.as<int>(), c->n_res, c->out_stage.as<double>(),
+                                c->stream));
+    CU(cudaMemcpyAsync(forces, c->out_stage.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return PPPM_OK;
   }

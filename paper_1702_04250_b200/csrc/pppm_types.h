@@ -60,7 +60,7 @@ struct AtomsIn {
 
 // kernel variants (selectable per context for A/B measurement)
 enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1 };  // + 2: same, cell-sorted in shared memory
-enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2 };  // SPLIT: ik only (k_gather_split)
+enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3 };  // SPLIT, WS: ik only
 // field tiles of the split gather: rows shifted per component (TXB = 12 or 20 mod 32)
 inline bool gather_split_ok(int order, int hx) {
   const int D = 8 + order - 1, lo = (order - 1) / 2;
@@ -79,6 +79,7 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, const int* orig, cudaStream_t s);
+int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
                             void* q_out, int* orig_out, cudaStream_t s);
