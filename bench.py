@@ -12,10 +12,11 @@ context stream; L2 (126 MB) is flushed with a 256 MiB memset before every
 step.  ``e2e`` is the same workload through the C ABI with pinned host
 buffers (H2D of positions/charges, full step, D2H of forces and energy).
 
-Multi-GPU (torchrun, one rank per GPU): every rank runs its own config-3
-system (weak scaling, independent replicas; the z-slab decomposition is
-not in this round), barrier + device sync around the timed region, max
-time over ranks.
+Multi-GPU (torchrun, one rank per GPU, NCCL): the config is z-slab
+decomposed over the N GPUs (strong scaling, paper_1702_04250_b200/slab.py):
+ghost-plane reverse sums / forward copies and the FFT all-to-all transposes
+over NCCL; barrier + device sync around the timed region, max time over
+ranks.
 
 ``--impl reference`` times the CPU oracle port of the reference algorithm
 (oracle/pppm_oracle.py, numpy, all host threads for make_rho) on bounded
@@ -204,7 +205,7 @@ def cpu_sample_rate(pos, q, lengths, dims, order, mode, sample, workers, reps=1)
         else:
             orc.fieldforce_ad(fields[0], p, qq, lengths, dims, order)
         times.append(time.perf_counter() - t0)
-    return sample / min(times), times
+    return sample * reps / sum(times), times
 
 
 def run_reference(args, cfg, rank, pg):
@@ -483,11 +484,13 @@ def main():
         cores = len(os.sched_getaffinity(0))
         p64 = pos.astype(np.float64)
         cal, _ = cpu_sample_rate(p64, q, lengths, cfg.dims, cfg.order, mode, 16384, cores)
-        sample = int(min(n, max(16384, cal * 15.0)))   # ~15 s of CPU work
-        rate, times = cpu_sample_rate(p64, q, lengths, cfg.dims, cfg.order, mode, sample, cores)
+        sample = int(min(n, max(16384, cal * 12.0)))   # ~12 s of CPU work per pass ...
+        reps = max(1, int(np.ceil(12.0 / max(sample / cal, 1e-3))))  # ... repeated to >= ~12 s
+        rate, times = cpu_sample_rate(p64, q, lengths, cfg.dims, cfg.order, mode, sample, cores, reps=reps)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"make_rho(workers={cores}) + fieldforce_{mode} on the first {sample} atoms "
-                                          f"of config {cfg.index} (numpy oracle port, fp64), {times[0]:.1f} s"}
+                                          f"of config {cfg.index}, {reps} pass(es) (numpy oracle port, fp64), "
+                                          f"{sum(times):.1f} s total"}
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
