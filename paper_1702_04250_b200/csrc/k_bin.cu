@@ -1,3 +1,4 @@
+#include <algorithm>
 // Binning of atoms into brick buckets (fp32 path), see k_fp32.cuh.
 #include "k_fp32.cuh"
 
@@ -7,11 +8,22 @@ int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Brick
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, const int* orig, cudaStream_t s) {
   if (cudaMemsetAsync(counts, 0, sizeof(int) * (bk.count() + 2) * kCountStride, s) != cudaSuccess) return launch_status();
-  const int grid = grid_for((a.n + kBinUnroll - 1) / kBinUnroll);
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
+      int grid = grid_for((a.n + kBinUnroll - 1) / kBinUnroll);
+#ifdef PPPM_BIN_PERSIST
+      {
+        // one resident wave (grid-stride), no tail wave
+        int per_sm = 0, dev = 0, sms = 148;
+        if (a.f32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bin_fixed<S, TAB, float>, kThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bin_fixed<S, TAB, double>, kThreads, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = std::min(grid, std::max(1, per_sm) * sms);
+      }
+#endif
       if (!a.f32)
         k_bin_fixed<S, TAB, double><<<grid, kThreads, 0, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, bk,
                                                               cap, n_points, counts, rec, rcell, perm, ovf_rec,

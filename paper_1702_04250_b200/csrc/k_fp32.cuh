@@ -75,7 +75,18 @@ inline void allow_smem(K kernel, size_t bytes) {
 // ---------------------------------------------------------------------------
 // binning
 
-constexpr int kBinUnroll = 4;  // atoms per thread in flight (latency of the slot atomics)
+// measured on config 3 (tools/ab_lib.sh): 2 atoms per thread, 6 CTAs / SM, one
+// persistent wave (latency-bound on the position loads and slot atomics)
+#ifndef PPPM_BIN_UNROLL
+#define PPPM_BIN_UNROLL 2
+#endif
+#ifndef PPPM_BIN_MINB
+#define PPPM_BIN_MINB 6
+#endif
+#ifndef PPPM_BIN_NO_PERSIST
+#define PPPM_BIN_PERSIST
+#endif
+constexpr int kBinUnroll = PPPM_BIN_UNROLL;  // atoms per thread in flight (latency of the slot atomics)
 
 // One pass: particle_map (bit-exact nodes) -> brick, slot = atomicAdd(count),
 // record into the bucket (or the overflow list).  On a z-slab only the atoms
@@ -83,7 +94,7 @@ constexpr int kBinUnroll = 4;  // atoms per thread in flight (latency of the slo
 // another slab); overflow records carry slab-local nodes.  Also the global max |q|
 // (as float bits, counts[nb + 1]) for the make_rho fixed-point scale.
 template <int S, bool TAB, typename TIn>
-__global__ void __launch_bounds__(kThreads) k_bin_fixed(
+__global__ void __launch_bounds__(kThreads, PPPM_BIN_MINB) k_bin_fixed(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
     int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
