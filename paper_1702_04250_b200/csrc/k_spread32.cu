@@ -13,6 +13,9 @@ namespace pppm {
 #define PPPM_SPREAD_THREADS 256
 #endif
 constexpr int kSpreadThreads = PPPM_SPREAD_THREADS;
+#ifndef PPPM_SPREAD_MINB
+#define PPPM_SPREAD_MINB 4
+#endif
 
 // make_rho, persistent CTAs: bricks b = blockIdx.x, += gridDim.x.  Per brick the
 // int32 fixed-point tile is accumulated with shared atomics, converted to fp32
@@ -20,7 +23,7 @@ constexpr int kSpreadThreads = PPPM_SPREAD_THREADS;
 // (TXB, D, D) box at the brick origin - lo (always in bounds: the mesh carries
 // an H-cell halo, folded back periodically by k_halo.cu afterwards).
 template <int S, bool TAB, bool FIX, int NT>
-__global__ void __launch_bounds__(NT) k_spread_tma(
+__global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
     const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
