@@ -4,7 +4,7 @@ import csv, subprocess, sys
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-h, v = rows[0], rows[2]
+h, u, v = rows[0], rows[1], rows[2]
 want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
@@ -15,7 +15,7 @@ want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "l1tex__data_pipe_l
         "dram__bytes_read.sum", "dram__bytes_write.sum"]
 idx = {n: i for i, n in enumerate(h)}
 for w in want:
-    if w in idx: print(f"{w:70s} {v[idx[w]]}")
+    if w in idx: print(f"{w:70s} {v[idx[w]]} {u[idx[w]]}")
 st = []
 for i, n in enumerate(h):
     if "pcsamp_warps_issue_stalled" in n and not n.endswith("not_issued"):
