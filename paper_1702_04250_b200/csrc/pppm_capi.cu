@@ -11,6 +11,8 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -117,6 +119,11 @@ struct pppm_ctx {
   cudaStream_t stream = nullptr;
   cufftHandle fwd = 0, bwd = 0;
   bool plans = false;
+  // fused Poisson (fp32, one GPU, power-of-two nz): cuFFT 2D plane transforms
+  // around k_zfft_green (z FFTs + Green + energy in one kernel)
+  bool use_zfft = true, zfft = false;
+  cufftHandle fwd2 = 0, bwd2 = 0;
+  DevBuf ztw, zdone;
   bool have_green = false, have_rho = false, have_fields = false, binned = false;
 
   DevBuf rho, rho_fix, rho_hat, ework, fields, green, ikc, ik64, tab;
@@ -191,6 +198,36 @@ static int ensure_plans(pppm_ctx* c) {
                     d ? CUFFT_Z2D : CUFFT_C2R, c->nfields()));
   FFT(cufftSetStream(c->fwd, c->stream));
   FFT(cufftSetStream(c->bwd, c->stream));
+  c->zfft = c->use_zfft && !d && c->P == 1 && zfft_supported(c->g.nz);
+  if (c->zfft) {
+    // (y, x) plane transforms batched over z; k_zfft_green does z
+    int n2[2] = {c->g.ny, c->g.nx};
+    int remb[2] = {c->pd.py, c->pd.px}, cemb[2] = {c->g.ny, c->nxh};
+    const int plane = c->pd.py * c->pd.px, cplane = c->g.ny * c->nxh;
+    FFT(cufftPlanMany(&c->fwd2, 2, n2, remb, 1, plane, cemb, 1, cplane, CUFFT_R2C, c->g.nz));
+    // inverse: one call over all F fields' padded planes (uniform plane stride
+    // across fields); the 2H halo planes per field transform zeros and are
+    // overwritten by the halo fill
+    FFT(cufftPlanMany(&c->bwd2, 2, n2, cemb, 1, cplane, remb, 1, plane, CUFFT_C2R, c->nfields() * c->pd.pz));
+    FFT(cufftSetStream(c->fwd2, c->stream));
+    FFT(cufftSetStream(c->bwd2, c->stream));
+    // twiddles exp(-2 pi i m / nz), m < nz, in fp64 then rounded
+    const int nz = c->g.nz;
+    std::vector<float> tw(2 * nz);
+    for (int m = 0; m < nz; ++m) {
+      const double a = -2.0 * M_PI * m / nz;
+      tw[2 * m] = (float)cos(a);
+      tw[2 * m + 1] = (float)sin(a);
+    }
+    const size_t ez = sizeof(float2) * (size_t)c->nfields() * c->pd.pz * cplane;
+    TRY(c->ework.ensure(ez));
+    CU(cudaMemset(c->ework.p, 0, ez));
+    TRY(c->ztw.ensure(sizeof(float) * 2 * nz));
+    TRY(c->zdone.ensure(sizeof(unsigned)));
+    TRY(c->partial.ensure(8 * std::max<int64_t>(kGreenBlocks, zfft_blocks(nz, c->g.ny * c->nxh))));
+    CU(cudaMemcpy(c->ztw.p, tw.data(), sizeof(float) * 2 * nz, cudaMemcpyHostToDevice));
+    CU(cudaMemset(c->zdone.p, 0, sizeof(unsigned)));
+  }
   c->plans = true;
   return PPPM_OK;
 }
@@ -353,6 +390,37 @@ static int run_green(pppm_ctx* c, bool fields) {
                    c->ework.p, c->partial.as<double>(), pref, sc, c->stream));
   c->launches += 2;
   return PPPM_OK;
+}
+
+static int run_fft_bwd(pppm_ctx* c);
+
+// fused fp32 Poisson with fields: 2D R2C planes -> k_zfft_green -> 2D C2R planes
+static int run_poisson_fused(pppm_ctx* c) {
+  if (!c->have_green) return fail(PPPM_ERR_STATE, "influence function not built");
+  const double vol = c->g.lx * c->g.ly * c->g.lz;
+  const double vcell = vol / (double)c->M;
+  const double pref = c->cscale * vcell * vcell / (2.0 * vol);
+  FFT(cufftExecR2C(c->fwd2, c->rho.as<float>() + c->pd.interior(), c->rho_hat.as<cufftComplex>()));
+  // spectra out as [f][pz][ny][nx/2+1] (interior planes at H..H+nz-1)
+  TRY(launch_zfft_green(c->mode, c->g.nz, c->g.ny, c->g.nx, c->rho_hat.as<float2>(), c->green.as<float>(),
+                        c->ikc.as<float>(), (float)(1.0 / (double)c->M), c->ztw.as<float2>(),
+                        c->ework.as<float2>() + (int64_t)c->pd.H * c->g.ny * c->nxh,
+                        (int64_t)c->pd.pz * c->g.ny * c->nxh, c->partial.as<double>(), c->zdone.as<unsigned>(), pref,
+                        c->scal.as<double>(), c->stream));
+  FFT(cufftExecC2R(c->bwd2, c->ework.as<cufftComplex>(), c->fields.as<float>() + (int64_t)c->pd.H * c->pd.px + c->pd.hx));
+  TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), c->nfields(), c->stream));
+  c->launches += 2;
+  c->have_fields = true;
+  return PPPM_OK;
+}
+
+// Poisson with fields (kspace.poisson_ik / poisson_ad + kspace_energy)
+static int run_poisson(pppm_ctx* c) {
+  TRY(ensure_plans(c));
+  if (c->zfft) return run_poisson_fused(c);
+  TRY(run_fft_fwd(c));
+  TRY(run_green(c, true));
+  return run_fft_bwd(c);
 }
 
 static int run_fft_bwd(pppm_ctx* c) {
@@ -611,6 +679,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_GATHER")) c->gather_variant = atoi(v);
   if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_SORT_RESIDENT")) c->sort_resident = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_ZFFT")) c->use_zfft = atoi(v) != 0;
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
   return PPPM_OK;
@@ -649,6 +718,10 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   if (c->plans) {
     cufftDestroy(c->fwd);
     cufftDestroy(c->bwd);
+    if (c->zfft) {
+      cufftDestroy(c->fwd2);
+      cufftDestroy(c->bwd2);
+    }
   }
   if (c->slab_plans) {
     cufftDestroy(c->p2f);
@@ -658,7 +731,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
-                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart};
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -807,9 +880,12 @@ int pppm_get_rho(pppm_ctx* c, double* rho) {
 int pppm_poisson(pppm_ctx* c, int want_fields, double* energy) {
   TRY(activate(c));
   if (!c->have_rho) return fail(PPPM_ERR_STATE, "no charge grid on the device");
-  TRY(run_fft_fwd(c));
-  TRY(run_green(c, want_fields != 0));
-  if (want_fields) TRY(run_fft_bwd(c));
+  if (want_fields) {
+    TRY(run_poisson(c));
+  } else {
+    TRY(run_fft_fwd(c));
+    TRY(run_green(c, false));
+  }
   if (energy) {
     CU(cudaMemcpyAsync(c->h_scal, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -864,9 +940,7 @@ int pppm_compute(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dty
   const void *dpos, *dq;
   TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
   TRY(do_make_rho(c, dpos, dq, n, dtype));
-  TRY(run_fft_fwd(c));
-  TRY(run_green(c, true));
-  TRY(run_fft_bwd(c));
+  TRY(run_poisson(c));
   TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
   TRY(do_fieldforce(c, dpos, dq, n, dtype, false, c->out_stage.p, true));
   CU(cudaMemcpyAsync(forces, c->out_stage.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
@@ -922,9 +996,7 @@ static int run_subphase(pppm_ctx* c, int sp) {
       return PPPM_OK;
     case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype);
     case SP_POISSON:
-      TRY(run_fft_fwd(c));
-      TRY(run_green(c, true));
-      return run_fft_bwd(c);
+      return run_poisson(c);
     case SP_GATHER:
       return do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64());
   }

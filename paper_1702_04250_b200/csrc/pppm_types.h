@@ -79,6 +79,11 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, const int* orig, cudaStream_t s);
+bool zfft_supported(int nz);
+int zfft_blocks(int nz, int ncols);
+int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,
+                      float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial, unsigned* done,
+                      double prefactor, double* energy, cudaStream_t s);
 int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
