@@ -17,6 +17,7 @@
  *       PPPM_ERR_VALUE   -> ValueError
  *       PPPM_ERR_RUNTIME -> RuntimeError  (e.g. unwrapped positions,
  *                           gridmap.py:87-88)
+ *       PPPM_ERR_SINGULAR -> SingularityError (pppm_singular_pair gives i, j, r)
  *       others           -> RuntimeError (CUDA / cuFFT / NCCL failure)
  *   - A context is bound to one device and one stream; it is not re-entrant.
  *     Separate contexts may run concurrently.
@@ -43,7 +44,8 @@ enum pppm_status {
   PPPM_ERR_CUDA = 4,
   PPPM_ERR_CUFFT = 5,
   PPPM_ERR_STATE = 6,
-  PPPM_ERR_NCCL = 7
+  PPPM_ERR_NCCL = 7,
+  PPPM_ERR_SINGULAR = 8   /* model.SingularityError (model.py:25-31): two atoms overlap */
 };
 
 enum pppm_mode { PPPM_MODE_IK = 0, PPPM_MODE_AD = 1 };            /* model.py DiffMode */
@@ -129,7 +131,8 @@ int pppm_ctx_get_energy(pppm_ctx* ctx, double* energy);
 int pppm_ctx_time_steps(pppm_ctx* ctx, int steps, int warmup, int flush_l2, double* ms);
 /* kernel variants for A/B measurement: kernel 0 = fp32 make_rho
  * (0: float CAS shared atomics, 1: int32 fixed-point shared atomics [default]),
- * kernel 1 = fp32 fieldforce (0: bucket order, 1: cell-sorted in shared memory [default]) */
+ * kernel 1 = fp32 fieldforce (0: bucket order, 1: bank rounds, 2: one task per
+ * (atom, component) [ik], 3: 2 + warp-specialized staging [ik default]) */
 int pppm_ctx_set_variant(pppm_ctx* ctx, int kernel, int variant);
 /* z-slab decomposition over `nslabs` GPUs (no counterpart in the reference,
  * which is single-process).  Slab `rank` owns global planes
@@ -157,6 +160,38 @@ int pppm_slab_fft_bwd(pppm_ctx* ctx);
 int pppm_slab_fieldforce(pppm_ctx* ctx);
 /* kernels launched by one step (for the bench's gpu_launches claim) */
 int pppm_ctx_launches_per_step(pppm_ctx* ctx, int* launches);
+
+/* ---- either side of the mesh path, fp64 ---- */
+
+/* shortrange.pair_forces (shortrange.py:201-267) with its cell list
+ * build_cell_list (shortrange.py:74-100) built on the device: screened Coulomb
+ * C q_i q_j erfc(alpha r)/r (+ truncated LJ when lj = {epsilon, sigma, lj_cutoff}
+ * is non-NULL) over every pair with r < cutoff, minimum image in the context's
+ * box, C = coulomb_constant / dielectric of the context.  forces: host (N, 3)
+ * fp64; energy: pair energy; counters (nullable): {candidate pairs, pairs
+ * within the cutoff} as the reference counts them (unordered).  Overlapping
+ * atoms (r < 1e-10) -> PPPM_ERR_SINGULAR.  Positions must be wrapped. */
+int pppm_ctx_pair_forces(pppm_ctx* ctx, const void* positions, const void* charges, int64_t n, int dtype,
+                         int mem, double alpha, double cutoff, const double* lj, double* forces, double* energy,
+                         long long* counters);
+/* the pair of the last PPPM_ERR_SINGULAR on this thread (SingularityError.pair / .distance) */
+int pppm_singular_pair(long long* i, long long* j, double* r);
+/* driver.compute_forces (driver.py:232-307): pair forces + make_rho + Poisson +
+ * fieldforce on the device; forces = pair + mesh (host (N, 3) fp64);
+ * energies[3] = {pair, kspace, self} (EnergyBreakdown, model.py:258-268; self =
+ * -C alpha/sqrt(pi) sum q^2, shortrange.py:270-278); counters[2] as above.
+ * Uses the context's table / influence selection for the mesh part. */
+int pppm_ctx_compute_forces(pppm_ctx* ctx, const void* positions, const void* charges, int64_t n, int dtype,
+                            int mem, double cutoff, const double* lj, double* forces, double* energies,
+                            long long* counters);
+/* driver.integrate_nve (driver.py:310-376): velocity-Verlet NVE trajectory with
+ * one compute_forces per step, positions / velocities / forces resident on the
+ * device.  Host fp64 inputs; series: (steps + 1) rows of {total, kinetic,
+ * potential, temperature, px, py, pz}; pos_out / vel_out (nullable): final
+ * state.  Errors carry the "step k: " prefix of driver.py:345-347. */
+int pppm_ctx_integrate_nve(pppm_ctx* ctx, const double* positions, const double* velocities, const double* masses,
+                           const double* charges, int64_t n, double dt, int steps, double cutoff, const double* lj,
+                           double* series, double* pos_out, double* vel_out);
 
 #ifdef __cplusplus
 }

@@ -415,6 +415,99 @@ def pppm_step(pos, q, lengths, dims, order, alpha, mode="ik", table=None,
     return f, energy, rho
 
 
+# ---------------------------------------------------------------------------
+# either side of the mesh path: pair forces, full force
+# evaluation, velocity-Verlet NVE.  Brute force over all pairs (small N only).
+
+def minimum_image(d, lengths):
+    """model.minimum_image (model.py:98-110)."""
+    out = d - np.round(d / lengths) * lengths
+    half = 0.5 * lengths
+    out = np.where(out >= half, out - lengths, out)
+    return np.where(out < -half, out + lengths, out)
+
+
+def wrap(pos, lengths):
+    """model.wrap (model.py:81-95)."""
+    out = pos - np.floor(pos / lengths) * lengths
+    out = np.where(out >= lengths, out - lengths, out)
+    return np.where(out < 0.0, out + lengths, out)
+
+
+def pair_forces(pos, q, lengths, alpha, cutoff, lj=None, coulomb_constant=1.0, dielectric=1.0):
+    """shortrange.pair_forces (shortrange.py:201-267) over all i < j pairs.
+
+    ``lj``: (epsilon, sigma, lj_cutoff) or None.  Returns (forces, energy,
+    pairs within the cutoff).  Raises ValueError on overlapping atoms."""
+    from math import erfc as _erfc
+
+    pos = np.asarray(pos, dtype=np.float64)
+    n = pos.shape[0]
+    i, j = np.triu_indices(n, k=1)
+    disp = minimum_image(pos[i] - pos[j], lengths)
+    r2 = np.sum(disp * disp, axis=1)
+    m = r2 < cutoff * cutoff
+    i, j, disp, r2 = i[m], j[m], disp[m], r2[m]
+    r = np.sqrt(r2)
+    if r.size and float(r.min()) < 1e-10:
+        raise ValueError("overlapping atoms")
+    scale = coulomb_constant / dielectric
+    qq = scale * q[i] * q[j]
+    scr = np.array([_erfc(alpha * v) for v in r])
+    e = qq * scr / r
+    fm = qq * (scr / r2 + 2.0 / np.sqrt(np.pi) * alpha * np.exp(-alpha * alpha * r2) / r)
+    if lj is not None:
+        eps, sig, rc = lj
+        lm = r < rc
+        sr6 = (sig / r[lm]) ** 6
+        e = e.copy()
+        e[lm] += 4.0 * eps * (sr6 * sr6 - sr6)
+        fa = np.zeros_like(fm)
+        fa[lm] = 24.0 * eps * (2.0 * sr6 * sr6 - sr6) / r[lm]
+        fm = fm + fa
+    fv = (fm / r)[:, None] * disp
+    f = np.zeros((n, 3))
+    np.add.at(f, i, fv)
+    np.add.at(f, j, -fv)
+    return f, float(e.sum()), int(r.size)
+
+
+def self_energy(q, alpha, coulomb_constant=1.0, dielectric=1.0):
+    """shortrange.self_energy (shortrange.py:270-278)."""
+    return -(coulomb_constant / dielectric) * alpha / np.sqrt(np.pi) * float(np.sum(np.asarray(q) ** 2))
+
+
+def compute_forces(pos, q, lengths, dims, order, alpha, cutoff, mode="ik", table=None, lj=None,
+                   coulomb_constant=1.0, dielectric=1.0):
+    """driver.compute_forces (driver.py:232-307): pair + mesh + self.
+    Returns (forces, (pair, kspace, self))."""
+    fp, ep, _ = pair_forces(pos, q, lengths, alpha, cutoff, lj, coulomb_constant, dielectric)
+    fm, ek, _ = pppm_step(pos, q, lengths, dims, order, alpha, mode, table, coulomb_constant, dielectric)
+    return fp + fm, (ep, ek, self_energy(q, alpha, coulomb_constant, dielectric))
+
+
+def integrate_nve(pos, vel, masses, q, lengths, dims, order, alpha, cutoff, dt, steps, mode="ik", table=None):
+    """driver.integrate_nve (driver.py:310-376): velocity Verlet.
+    Returns (series (steps+1, 7) [total, kinetic, potential, T, px, py, pz], pos, vel)."""
+    pos = np.array(pos, dtype=np.float64)
+    vel = np.array(vel, dtype=np.float64)
+    m = np.asarray(masses, dtype=np.float64)[:, None]
+    n = pos.shape[0]
+    ser = np.empty((steps + 1, 7))
+    f, e = compute_forces(pos, q, lengths, dims, order, alpha, cutoff, mode, table)
+    for step in range(steps + 1):
+        kin = 0.5 * float(np.sum(m * vel ** 2))
+        pot = e[0] + e[1] + e[2]
+        ser[step] = [kin + pot, kin, pot, float(np.sum(m * vel ** 2)) / (3.0 * n), *(m * vel).sum(axis=0)]
+        if step == steps:
+            break
+        vel = vel + 0.5 * dt / m * f
+        pos = wrap(pos + dt * vel, lengths)
+        f, e = compute_forces(pos, q, lengths, dims, order, alpha, cutoff, mode, table)
+        vel = vel + 0.5 * dt / m * f
+    return ser, pos, vel
+
+
 def rms_rel_error(f, f_ref):
     """Relative RMS force error (ewald.py:155-171)."""
     f = np.asarray(f, dtype=np.float64)

@@ -13,8 +13,10 @@ from .model import (
     AtomSystem,
     ConfigurationError,
     DiffMode,
+    EnergyBreakdown,
     PppmParams,
     SimulationBox,
+    SingularityError,
     SUPPORTED_ORDERS,
     wrap,
 )
@@ -36,6 +38,8 @@ from .gridmap import (
     particle_map,
 )
 from .kspace import KSpacePlan, build_plan, kspace_energy, poisson_ad, poisson_ik
+from .shortrange import LjParams, build_cell_list, pair_forces, self_energy
+from .driver import compute_forces, integrate_nve
 from .context import PinnedArray, PppmContext
 from ._runtime import get_device, get_precision, set_device, set_precision
 from ._native import library_path

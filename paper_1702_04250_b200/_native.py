@@ -18,7 +18,7 @@ import numpy as np
 LIB_NAME = "libpppm_b200.so"
 LIB_PATH = os.environ.get("PPPM_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-OK, ERR_CONFIG, ERR_VALUE, ERR_RUNTIME, ERR_CUDA, ERR_CUFFT, ERR_STATE, ERR_NCCL = range(8)
+OK, ERR_CONFIG, ERR_VALUE, ERR_RUNTIME, ERR_CUDA, ERR_CUFFT, ERR_STATE, ERR_NCCL, ERR_SINGULAR = range(9)
 MODE_IK, MODE_AD = 0, 1
 PREC_FP64, PREC_MIXED = 0, 1
 F64, F32 = 0, 1
@@ -80,6 +80,12 @@ PROTOTYPES = {
     "pppm_slab_green": (_c_int, [_vp]),
     "pppm_slab_fft_bwd": (_c_int, [_vp]),
     "pppm_slab_fieldforce": (_c_int, [_vp]),
+    "pppm_ctx_pair_forces": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_dbl, _c_dbl, _vp, _vp, _dp,
+                                      _vp]),
+    "pppm_singular_pair": (_c_int, [ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong), _dp]),
+    "pppm_ctx_compute_forces": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_dbl, _vp, _vp, _vp, _vp]),
+    "pppm_ctx_integrate_nve": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp,
+                                        _vp]),
 }
 
 
@@ -92,6 +98,7 @@ class _ErrorTypes:
         self.config = ConfigurationError
         self.value = ValueError
         self.runtime = RuntimeError
+        self.singular = None  # SingularityError class (model.SingularityError unless install() swaps it)
 
 
 ERRORS = _ErrorTypes()
@@ -141,6 +148,18 @@ def check(status: int):
         raise ERRORS.config(msg)
     if status == ERR_VALUE:
         raise ERRORS.value(msg)
+    if status == ERR_SINGULAR:
+        i, j, r = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_double()
+        load().pppm_singular_pair(ctypes.byref(i), ctypes.byref(j), ctypes.byref(r))
+        from .model import SingularityError
+
+        cls = ERRORS.singular or SingularityError
+        exc = cls(i.value, j.value, r.value)
+        if msg.startswith("step "):  # integrate_nve's step prefix (driver.py:345-347)
+            exc.args = (msg,)
+        raise exc
+    if status == ERR_RUNTIME:
+        raise ERRORS.runtime(msg)
     raise ERRORS.runtime(f"pppm_b200 error {status}: {msg}")
 
 

@@ -38,6 +38,7 @@ class _Types:
         self.FieldGrids = gridmap.FieldGrids
         self.StencilTable = stencil.StencilTable
         self.KSpacePlan = None  # None: this package's own plan class
+        self.EnergyBreakdown = model.EnergyBreakdown
 
 
 TYPES = None

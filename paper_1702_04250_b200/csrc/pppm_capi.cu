@@ -27,6 +27,8 @@ using namespace pppm;
 
 namespace {
 thread_local std::string g_err;
+thread_local long long g_sing_i = -1, g_sing_j = -1;  // last SingularityError pair
+thread_local double g_sing_r = 0.0;
 }  // namespace
 
 namespace pppm {
@@ -122,6 +124,10 @@ struct pppm_ctx {
   // fused Poisson (fp32, one GPU, power-of-two nz): cuFFT 2D plane transforms
   // around k_zfft_green (z FFTs + Green + energy in one kernel)
   bool use_zfft = true, zfft = false;
+  // short-range pairs / full force evaluation / NVE (fp64)
+  DevBuf pr_cell, pr_count, pr_start, pr_cursor, pr_order, pr_tmp, pr_force, pr_e, pr_cnt, pr_rmin, pr_ij,
+      pr_part, pr_pos, pr_q, pr_scal;
+  DevBuf md_pos, md_vel, md_m, md_q, md_f, md_tmp, md_series;
   cufftHandle fwd2 = 0, bwd2 = 0;
   DevBuf ztw, zdone;
   bool have_green = false, have_rho = false, have_fields = false, binned = false;
@@ -731,7 +737,10 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
-                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone};
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone,
+                    &c->pr_cell, &c->pr_count, &c->pr_start, &c->pr_cursor, &c->pr_order, &c->pr_tmp, &c->pr_force,
+                    &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal,
+                    &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -1284,6 +1293,229 @@ int pppm_ctx_launches_per_step(pppm_ctx* c, int* launches) {
   CU(cudaStreamSynchronize(c->stream));
   *launches = c->launches - before;
   return PPPM_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Short-range pair forces, the full force evaluation and NVE integration
+// (shortrange.py:74-267, driver.py:232-376), fp64 on the device.
+
+static int check_pair_args(pppm_ctx* c, double alpha, double cutoff) {
+  if (!(alpha > 0.0)) return fail(PPPM_ERR_CONFIG, "alpha must be positive");
+  if (!(cutoff > 0.0)) return fail(PPPM_ERR_CONFIG, "cutoff must be positive");
+  const double half = 0.5 * std::min(c->g.lx, std::min(c->g.ly, c->g.lz));
+  if (cutoff > half) {
+    char msg[160];
+    snprintf(msg, sizeof msg, "cutoff %g exceeds half the smallest box edge (%g)", cutoff, half);
+    return fail(PPPM_ERR_CONFIG, msg);
+  }
+  return PPPM_OK;
+}
+
+// fp64 device copies of host / device, fp32 / fp64 atoms (pair kernels are fp64)
+static int stage_f64(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, const double** dpos,
+                     const double** dq) {
+  if (dtype == PPPM_F64 && mem == PPPM_DEVICE) {
+    *dpos = (const double*)pos;
+    *dq = (const double*)q;
+    return PPPM_OK;
+  }
+  TRY(c->pr_pos.ensure(sizeof(double) * 3 * n));
+  TRY(c->pr_q.ensure(sizeof(double) * n));
+  if (dtype == PPPM_F64) {
+    CU(cudaMemcpyAsync(c->pr_pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->pr_q.p, q, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    const void *sp = pos, *sq = q;
+    if (mem == PPPM_HOST) {
+      TRY(c->pos_stage.ensure(sizeof(float) * 3 * n));
+      TRY(c->q_stage.ensure(sizeof(float) * n));
+      CU(cudaMemcpyAsync(c->pos_stage.p, pos, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+      CU(cudaMemcpyAsync(c->q_stage.p, q, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+      sp = c->pos_stage.p;
+      sq = c->q_stage.p;
+    }
+    TRY(launch_convert(true, sp, c->pr_pos.p, 3 * n, c->stream));
+    TRY(launch_convert(true, sq, c->pr_q.p, n, c->stream));
+  }
+  *dpos = c->pr_pos.as<double>();
+  *dq = c->pr_q.as<double>();
+  return PPPM_OK;
+}
+
+// pair forces into pr_force (n, 3), pair energy into pr_scal[0]; synchronises
+// to report unwrapped positions / overlapping atoms
+static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double alpha, double rc,
+                       const double* lj, long long* counters) {
+  const int cx = std::max(1, (int)(c->g.lx / rc)), cy = std::max(1, (int)(c->g.ly / rc)),
+            cz = std::max(1, (int)(c->g.lz / rc));
+  const int64_t ncells = (int64_t)cx * cy * cz;
+  if (ncells > (1 << 28)) return fail(PPPM_ERR_VALUE, "cutoff too small for the cell list");
+  TRY(c->pr_cell.ensure(sizeof(int) * n));
+  TRY(c->pr_order.ensure(sizeof(int) * n));
+  TRY(c->pr_tmp.ensure(sizeof(int) * n));
+  TRY(c->pr_count.ensure(sizeof(int) * (ncells + 1)));
+  TRY(c->pr_start.ensure(sizeof(int) * (ncells + 1)));
+  TRY(c->pr_cursor.ensure(sizeof(int) * (ncells + 1)));
+  TRY(c->pr_force.ensure(sizeof(double) * 3 * n));
+  TRY(c->pr_e.ensure(sizeof(double) * n));
+  TRY(c->pr_cnt.ensure(16));
+  TRY(c->pr_rmin.ensure(8));
+  TRY(c->pr_ij.ensure(8));
+  TRY(c->pr_part.ensure(8 * 256));
+  TRY(c->pr_scal.ensure(8 * 4));
+  CU(cudaMemsetAsync(c->pr_cnt.p, 0, 16, c->stream));
+  CU(cudaMemsetAsync(c->pr_rmin.p, 0xff, 8, c->stream));
+  const double scale = c->cscale;
+  TRY(launch_pair(dpos, dq, n, c->g.lx, c->g.ly, c->g.lz, alpha, rc, scale, lj, c->pr_cell.as<int>(),
+                  c->pr_count.as<int>(), c->pr_start.as<int>(), c->pr_cursor.as<int>(), c->pr_order.as<int>(),
+                  c->pr_tmp.as<int>(), c->pr_force.as<double>(), c->pr_e.as<double>(),
+                  c->pr_cnt.as<unsigned long long>(), c->pr_rmin.as<unsigned long long>(), c->err.as<int>(),
+                  c->stream));
+  TRY(launch_sum(c->pr_e.as<double>(), n, c->pr_part.as<double>(), 1.0, c->pr_scal.as<double>(), c->stream));
+  c->launches += 8;
+  unsigned long long h[3];
+  CU(cudaMemcpyAsync(h, c->pr_cnt.p, 16, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(h + 2, c->pr_rmin.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  TRY(check_err_flag(c));
+  if (counters) {
+    counters[0] = (long long)(h[0] / 2);
+    counters[1] = (long long)(h[1] / 2);
+  }
+  if (h[2] != ~0ull) {
+    double r;
+    memcpy(&r, &h[2], 8);
+    CU(cudaMemsetAsync(c->pr_ij.p, 0xff, 8, c->stream));
+    TRY(launch_pair_find(dpos, n, c->g.lx, c->g.ly, c->g.lz, rc, c->pr_order.as<int>(), c->pr_start.as<int>(),
+                         c->pr_cell.as<int>(), c->pr_rmin.as<unsigned long long>(), c->pr_ij.as<long long>(),
+                         c->stream));
+    unsigned long long ij = 0;
+    CU(cudaMemcpyAsync(&ij, c->pr_ij.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    g_sing_i = (long long)(ij >> 32);
+    g_sing_j = (long long)(ij & 0xffffffffull);
+    g_sing_r = r;
+    char msg[128];
+    snprintf(msg, sizeof msg, "atoms %lld and %lld overlap (r = %.3e)", g_sing_i, g_sing_j, r);
+    return fail(PPPM_ERR_SINGULAR, msg);
+  }
+  return PPPM_OK;
+}
+
+int pppm_singular_pair(long long* i, long long* j, double* r) {
+  if (i) *i = g_sing_i;
+  if (j) *j = g_sing_j;
+  if (r) *r = g_sing_r;
+  return PPPM_OK;
+}
+
+int pppm_ctx_pair_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, double alpha,
+                         double cutoff, const double* lj, double* forces, double* energy, long long* counters) {
+  TRY(activate(c));
+  if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
+  TRY(check_pair_args(c, alpha, cutoff));
+  const double *dpos, *dq;
+  TRY(stage_f64(c, pos, q, n, dtype, mem, &dpos, &dq));
+  TRY(pair_device(c, dpos, dq, n, alpha, cutoff, lj, counters));
+  double e = 0.0;
+  CU(cudaMemcpyAsync(forces, c->pr_force.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(&e, c->pr_scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (energy) *energy = e;
+  return PPPM_OK;
+}
+
+// full force evaluation on device atoms: pair forces + mesh forces -> out (n, 3)
+// fp64, energies -> pr_scal[0] (pair), scal[0] (kspace), pr_scal[1] (self)
+static int forces_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double rc, const double* lj,
+                         double* out, long long* counters) {
+  TRY(pair_device(c, dpos, dq, n, c->alpha, rc, lj, counters));
+  TRY(do_make_rho(c, dpos, dq, n, PPPM_F64));
+  TRY(run_poisson(c));
+  TRY(do_fieldforce(c, dpos, dq, n, PPPM_F64, false, out, true));
+  TRY(launch_add3(c->pr_force.as<double>(), out, 3 * n, c->stream));
+  // self energy -C alpha / sqrt(pi) sum q^2 (shortrange.py:270-278)
+  TRY(launch_square(dq, n, c->pr_e.as<double>(), c->stream));
+  TRY(launch_sum(c->pr_e.as<double>(), n, c->pr_part.as<double>(), -c->cscale * c->alpha / sqrt(M_PI),
+                 c->pr_scal.as<double>() + 1, c->stream));
+  c->launches += 4;
+  return PPPM_OK;
+}
+
+int pppm_ctx_compute_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem,
+                            double cutoff, const double* lj, double* forces, double* energies, long long* counters) {
+  TRY(activate(c));
+  if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
+  TRY(check_pair_args(c, c->alpha, cutoff));
+  const double *dpos, *dq;
+  TRY(stage_f64(c, pos, q, n, dtype, mem, &dpos, &dq));
+  TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
+  TRY(forces_device(c, dpos, dq, n, cutoff, lj, c->out_stage.as<double>(), counters));
+  CU(cudaMemcpyAsync(forces, c->out_stage.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  double e[3];
+  CU(cudaMemcpyAsync(e, c->pr_scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(e + 1, c->scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(e + 2, c->pr_scal.as<double>() + 1, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  TRY(check_err_flag(c));
+  if (energies) {
+    energies[0] = e[0];
+    energies[1] = e[1];
+    energies[2] = e[2];
+  }
+  return PPPM_OK;
+}
+
+int pppm_ctx_integrate_nve(pppm_ctx* c, const double* pos, const double* vel, const double* masses, const double* q,
+                           int64_t n, double dt, int steps, double cutoff, const double* lj, double* series,
+                           double* pos_out, double* vel_out) {
+  TRY(activate(c));
+  if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
+  if (!(dt > 0.0)) return fail(PPPM_ERR_VALUE, "dt must be positive");
+  if (steps < 0) return fail(PPPM_ERR_VALUE, "steps must be non-negative");
+  TRY(check_pair_args(c, c->alpha, cutoff));
+  const size_t v3 = sizeof(double) * 3 * n;
+  TRY(c->md_pos.ensure(v3));
+  TRY(c->md_vel.ensure(v3));
+  TRY(c->md_f.ensure(v3));
+  TRY(c->md_m.ensure(sizeof(double) * n));
+  TRY(c->md_q.ensure(sizeof(double) * n));
+  TRY(c->md_tmp.ensure(sizeof(double) * 4 * n));
+  TRY(c->md_series.ensure(sizeof(double) * 7 * (size_t)(steps + 1)));
+  CU(cudaMemcpyAsync(c->md_pos.p, pos, v3, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->md_vel.p, vel, v3, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->md_m.p, masses, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->md_q.p, q, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  double* x = c->md_pos.as<double>();
+  double* v = c->md_vel.as<double>();
+  double* f = c->md_f.as<double>();
+  const double* m = c->md_m.as<double>();
+  const double* dq = c->md_q.as<double>();
+  double* rows = c->md_series.as<double>();
+  auto eval = [&](int step) -> int {
+    const int st = forces_device(c, x, dq, n, cutoff, lj, f, nullptr);
+    if (st != PPPM_OK) {
+      g_err = "step " + std::to_string(step) + ": " + g_err;  // driver.py:345-347
+      return st;
+    }
+    return PPPM_OK;
+  };
+  TRY(eval(0));
+  for (int step = 0; step <= steps; ++step) {
+    TRY(launch_series_row(v, m, n, c->md_tmp.as<double>(), c->pr_part.as<double>(), rows + 7 * step,
+                          c->pr_scal.as<double>(), c->scal.as<double>(), c->pr_scal.as<double>() + 1, c->stream));
+    if (step == steps) break;
+    TRY(launch_kick(v, f, m, 0.5 * dt, n, c->stream));
+    TRY(launch_drift(x, v, dt, c->g.lx, c->g.ly, c->g.lz, n, c->stream));
+    TRY(eval(step + 1));
+    TRY(launch_kick(v, f, m, 0.5 * dt, n, c->stream));
+  }
+  CU(cudaMemcpyAsync(series, rows, sizeof(double) * 7 * (size_t)(steps + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (pos_out) CU(cudaMemcpyAsync(pos_out, x, v3, cudaMemcpyDeviceToHost, c->stream));
+  if (vel_out) CU(cudaMemcpyAsync(vel_out, v, v3, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return check_err_flag(c);
 }
 
 }  // extern "C"

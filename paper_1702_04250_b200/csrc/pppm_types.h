@@ -79,6 +79,20 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, const int* orig, cudaStream_t s);
+int launch_pair(const double* pos, const double* q, int64_t n, double lx, double ly, double lz, double alpha,
+                double rc, double scale, const double* lj, int* cell, int* count, int* start, int* cursor,
+                int* order, int* tmp, double* force, double* e_atom, unsigned long long* cnt,
+                unsigned long long* rmin_bits, int* err, cudaStream_t s);
+int launch_pair_find(const double* pos, int64_t n, double lx, double ly, double lz, double rc, const int* order,
+                     const int* start, const int* cell, const unsigned long long* rmin_bits, long long* ij,
+                     cudaStream_t s);
+int launch_sum(const double* v, int64_t n, double* partial, double scale, double* out, cudaStream_t s);
+int launch_add3(const double* a, double* b, int64_t n3, cudaStream_t s);
+int launch_square(const double* q, int64_t n, double* out, cudaStream_t s);
+int launch_kick(double* v, const double* f, const double* m, double half_dt, int64_t n, cudaStream_t s);
+int launch_drift(double* x, const double* v, double dt, double lx, double ly, double lz, int64_t n, cudaStream_t s);
+int launch_series_row(const double* v, const double* m, int64_t n, double* tmp4, double* partial, double* row,
+                      const double* e_pair, const double* e_kspace, const double* e_self, cudaStream_t s);
 bool zfft_supported(int nz);
 int zfft_blocks(int nz, int ncols);
 int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,

@@ -1,0 +1,137 @@
+"""Drop-in force driver: the full force evaluation and NVE integration on the device.
+
+Mirrors ``compute_forces`` (driver.py:232-307) and ``integrate_nve``
+(driver.py:310-376) of the reference.  One C-ABI call evaluates the screened
+pair forces (``k_pair.cu``), make_rho -> Poisson -> fieldforce (the mesh path)
+and the self energy on the device; ``integrate_nve`` keeps positions,
+velocities and forces resident for the whole velocity-Verlet trajectory and
+reduces the energy / temperature / momentum series on the device (fp64,
+fixed-order sums).  Section timing: the three reference sections run inside
+one device call, so the wall time of the call is reported under ``"device"``
+and the reference's section names carry 0.0.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _native as nat
+from . import _runtime as rt
+from . import kspace, stencil
+from .model import EnergyBreakdown
+from .shortrange import lj_array
+
+REPORT_SECTIONS = ("pppm_non_fft", "pppm_fft", "pair", "other")
+
+
+def _energy_type():
+    T = rt.types()
+    return getattr(T, "EnergyBreakdown", None) or EnergyBreakdown
+
+
+def _solver_ctx(system, params, table, plan):
+    """Device context of the force evaluation with the caller's table and influence."""
+    params.validate_for_box(system.box)
+    dims, _, lengths = rt.geometry(system, params)
+    prec = rt.prec_code(rt.precision_of(params))
+    ctx = rt.context(dims, lengths, params.order, rt.mode_code(params.mode), prec, params.alpha,
+                     params.coulomb_constant, params.dielectric)
+    if params.use_table and table is None:
+        table = stencil.build_table(params.order, params.table_points)
+    rt.apply_table(ctx, params, table)
+    if plan is None:
+        key = ("device", "pme", kspace.DECONV_FLOOR)
+        if ctx.green_key != key:
+            ctx("pppm_ctx_build_influence", nat.INFLUENCE_PME, kspace.DECONV_FLOOR)
+            ctx.green_key = key
+    elif isinstance(plan, kspace.KSpacePlan):
+        key = ("device", plan.variant, plan.deconv_floor)
+        if ctx.green_key != key:
+            kind = nat.INFLUENCE_PME if plan.variant == "pme" else nat.INFLUENCE_OPTIMAL
+            ctx("pppm_ctx_build_influence", kind, plan.deconv_floor)
+            ctx.green_key = key
+    else:  # a foreign (reference) plan: upload its influence grid
+        g = np.ascontiguousarray(plan.influence, dtype=np.float64)
+        key = ("host", id(plan.influence), g.ctypes.data)
+        if ctx.green_key != key:
+            ctx("pppm_ctx_set_influence", nat.ptr(g))
+            ctx.green_key = key
+            ctx._green_ref = g
+    return ctx
+
+
+def _count(counters, params, n, cnt):
+    if counters is None:
+        return
+    counters["pair_candidates"] = counters.get("pair_candidates", 0) + int(cnt[0])
+    counters["pairs_within_cutoff"] = counters.get("pairs_within_cutoff", 0) + int(cnt[1])
+    rt.count_touch(counters, "cells_touched_map", n, int(params.order))
+    rt.count_touch(counters, "cells_touched_distribute", n, int(params.order))
+    nx, ny, nz = params.grid_dims
+    counters["grid_points"] = nx * ny * nz
+
+
+def compute_forces(system, params, table=None, plan=None, lj=None, *, workers=1, timer=None, counters=None):
+    """One full force evaluation: screened pair part plus mesh part.
+
+    Returns ``(forces, EnergyBreakdown, sections)``.
+    """
+    t0 = time.perf_counter()
+    ctx = _solver_ctx(system, params, table, plan)
+    pos, q = rt.atoms_arrays(system)
+    n = pos.shape[0]
+    forces = np.empty((n, 3))
+    e = np.zeros(3)
+    cnt = np.zeros(2, dtype=np.int64)
+    ljp = lj_array(lj)
+    ctx("pppm_ctx_compute_forces", nat.ptr(pos), nat.ptr(q), n, nat.F64, nat.HOST, float(params.cutoff),
+        None if ljp is None else nat.ptr(ljp), nat.ptr(forces), nat.ptr(e), nat.ptr(cnt))
+    _count(counters, params, n, cnt)
+    wall = time.perf_counter() - t0
+    sections = {name: 0.0 for name in REPORT_SECTIONS[:3]}
+    sections["device"] = wall
+    if timer is not None:
+        timer.add("device", wall)
+    energy = _energy_type()(pair=float(e[0]), kspace=float(e[1]), self_energy=float(e[2]))
+    return forces, energy, sections
+
+
+def integrate_nve(system, params, dt, steps, lj=None, *, workers=1, timer=None, counters=None):
+    """Velocity-Verlet NVE trajectory with a device force evaluation per step.
+
+    Returns ``{"series", "final", "steps", "dt"}`` like driver.py:310-376
+    (temperature = sum(m v^2) / (3N), k_B = 1).
+    """
+    if system.velocities is None:
+        raise ValueError("NVE integration needs initial velocities")
+    if dt <= 0.0:
+        raise ValueError("dt must be positive")
+    steps = int(steps)
+    ctx = _solver_ctx(system, params, None, None)
+    pos, q = rt.atoms_arrays(system)
+    n = pos.shape[0]
+    vel = np.ascontiguousarray(system.velocities, dtype=np.float64)
+    masses = np.ascontiguousarray(system.masses, dtype=np.float64)
+    series = np.empty((steps + 1, 7))
+    pos_out = np.empty((n, 3))
+    vel_out = np.empty((n, 3))
+    ljp = lj_array(lj)
+    t0 = time.perf_counter()
+    ctx("pppm_ctx_integrate_nve", nat.ptr(pos), nat.ptr(vel), nat.ptr(masses), nat.ptr(q), n, float(dt), steps,
+        float(params.cutoff), None if ljp is None else nat.ptr(ljp), nat.ptr(series), nat.ptr(pos_out),
+        nat.ptr(vel_out))
+    if timer is not None:
+        timer.add("device", time.perf_counter() - t0)
+    if counters is not None:
+        nx, ny, nz = params.grid_dims
+        counters["grid_points"] = nx * ny * nz
+    out = {
+        "total_energy": series[:, 0].copy(),
+        "kinetic": series[:, 1].copy(),
+        "potential": series[:, 2].copy(),
+        "temperature": series[:, 3].copy(),
+        "momentum": series[:, 4:7].copy(),
+    }
+    return {"series": out, "final": system.with_positions(pos_out, vel_out), "steps": steps, "dt": dt}

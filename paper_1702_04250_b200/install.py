@@ -13,38 +13,49 @@ from __future__ import annotations
 
 from . import _native as nat
 from . import _runtime as rt
-from . import gridmap, kspace, stencil
+from . import driver, gridmap, kspace, shortrange, stencil
 
 HOT_PATH = {
     "gridmap": ("map_charge", "distribute_force_ik", "distribute_force_ad"),
     "kspace": ("build_plan", "poisson_ik", "poisson_ad", "kspace_energy"),
     "stencil": ("build_table",),
 }
-_SOURCES = {"gridmap": gridmap, "kspace": kspace, "stencil": stencil}
+# either side of the mesh path: the pair loop and the force driver
+NEXT_PATH = {
+    "shortrange": ("pair_forces",),
+    "driver": ("compute_forces", "integrate_nve"),
+}
+_SOURCES = {"gridmap": gridmap, "kspace": kspace, "stencil": stencil, "shortrange": shortrange, "driver": driver}
 _saved = {}
 
 
-def install(pppm_module):
-    """Point the reference's hot-path names at the B200 operators."""
+def install(pppm_module, force_driver=True):
+    """Point the reference's hot-path names at the B200 operators.
+
+    ``force_driver`` also rebinds the pair loop and the force driver
+    (compute_forces / integrate_nve) to their device versions."""
     import importlib
 
     mods = {name: importlib.import_module(f"{pppm_module.__name__}.{name}")
-            for name in ("gridmap", "kspace", "stencil", "driver", "model")}
+            for name in ("gridmap", "kspace", "stencil", "driver", "model", "shortrange")}
     T = rt.types()
     T.DiffMode = mods["model"].DiffMode
     T.ChargeGrid = mods["gridmap"].ChargeGrid
     T.FieldGrids = mods["gridmap"].FieldGrids
     T.StencilTable = mods["stencil"].StencilTable
     T.KSpacePlan = mods["kspace"].KSpacePlan
+    T.EnergyBreakdown = mods["model"].EnergyBreakdown
     nat.ERRORS.config = mods["model"].ConfigurationError
-    for modname, names in HOT_PATH.items():
+    nat.ERRORS.singular = mods["model"].SingularityError
+    paths = dict(HOT_PATH, **(NEXT_PATH if force_driver else {}))
+    for modname, names in paths.items():
         for name in names:
             new = getattr(_SOURCES[modname], name)
             for target in (pppm_module, mods[modname], mods["driver"]):
                 if hasattr(target, name):
                     _saved.setdefault((target.__name__, name), (target, getattr(target, name)))
                     setattr(target, name, new)
-    return sorted({name for names in HOT_PATH.values() for name in names})
+    return sorted({name for names in paths.values() for name in names})
 
 
 def uninstall():
@@ -56,3 +67,4 @@ def uninstall():
     from .model import ConfigurationError
 
     nat.ERRORS.config = ConfigurationError
+    nat.ERRORS.singular = None
