@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--mode", default=None, choices=(None, "ik", "ad"))
+    ap.add_argument("--order", type=int, default=None, help="override the config's stencil order (config 4 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -356,6 +357,10 @@ def main():
     from paper_1702_04250_b200 import scenarios
 
     cfg = scenarios.CONFIGS[args.config]
+    if args.order is not None:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, order=args.order)
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     ours_multi = args.impl == "ours" and world_env > 1
     rank, local, world, pg = dist_setup(args.gpus, backend="nccl" if ours_multi else "gloo")
