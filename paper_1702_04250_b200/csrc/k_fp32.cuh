@@ -94,7 +94,7 @@ constexpr int kBinUnroll = PPPM_BIN_UNROLL;  // atoms per thread in flight (late
 // another slab); overflow records carry slab-local nodes.  Also the global max |q|
 // (as float bits, counts[nb + 1]) for the make_rho fixed-point scale.
 template <int S, bool TAB, typename TIn>
-__global__ void __launch_bounds__(kThreads, PPPM_BIN_MINB) k_bin_fixed(
+__global__ void __launch_bounds__(kThreads, (S >= 6 ? 4 : PPPM_BIN_MINB)) k_bin_fixed(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
     int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,

@@ -14,6 +14,8 @@
 // ends, as the reference applies it equal and opposite).  Energy: half of the
 // per-atom sums, reduced in a fixed order.  Counters: unordered candidate /
 // in-cutoff pairs (the ordered counts halved).
+#include <algorithm>
+
 #include "pppm_device.cuh"
 
 namespace pppm {
@@ -122,75 +124,181 @@ __device__ __forceinline__ void axis_offsets(int n, int& lo, int& cnt) {
   else { lo = 0; cnt = 1; }
 }
 
-template <bool LJ>
-__global__ void k_pair_forces(const double* __restrict__ pos, const double* __restrict__ q, int64_t n,
-                              const int* __restrict__ order, const int* __restrict__ start,
-                              const int* __restrict__ cell, PairGeom pg, PairParams pp, double* __restrict__ force,
-                              double* __restrict__ e_atom, unsigned long long* __restrict__ cnt,
-                              unsigned long long* __restrict__ rmin_bits) {
-  constexpr double kTwoOverSqrtPi = 1.1283791670955126;
-  unsigned long long cand = 0, within = 0;
+// positions / charges in cell-sorted order (coalesced candidate loads)
+__global__ void k_pair_sorted(const double* __restrict__ pos, const double* __restrict__ q,
+                              const int* __restrict__ order, int64_t n, double4* __restrict__ sp,
+                              float4* __restrict__ spf) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-    const int i = order[s];  // cell-sorted: neighbouring threads share cells
-    const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2], qi = q[i];
-    const int c = cell[i];
-    const int cx = c % pg.nx, cy = (c / pg.nx) % pg.ny, cz = c / (pg.nx * pg.ny);
-    int olx, onx, oly, ony, olz, onz;
-    axis_offsets(pg.nx, olx, onx);
-    axis_offsets(pg.ny, oly, ony);
-    axis_offsets(pg.nz, olz, onz);
+    const int i = order[s];
+    sp[s] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], q[i]);
+    spf[s] = make_float4((float)pos[3 * i], (float)pos[3 * i + 1], (float)pos[3 * i + 2], 0.f);
+  }
+}
+
+__device__ __forceinline__ float min_image_f(float d, float l, float il) {
+  float o = d - rintf(d * il) * l;
+  const float h = 0.5f * l;
+  if (o >= h) o -= l;
+  if (o < -h) o += l;
+  return o;
+}
+
+__device__ __forceinline__ double min_image_inv(double d, double l, double il) {
+  // as min_image, with d / L as d * (1 / L): a different rint only within an
+  // ulp of a half box, and the fold below lands both in [-L/2, L/2)
+  double o = d - rint(d * il) * l;
+  const double h = 0.5 * l;
+  if (o >= h) o -= l;
+  if (o < -h) o += l;
+  return o;
+}
+
+// one warp per atom (cell-sorted order): the lanes stride over the
+// concatenated atom lists of the atom's distinct stencil cells, then a fixed
+// shuffle tree sums the partial forces (deterministic); thread-per-atom would
+// leave the SMs nearly empty for the 10^4-10^5 atoms of a typical system.
+constexpr int kPairWarps = 8;
+
+template <bool LJ>
+__global__ void __launch_bounds__(32 * kPairWarps) k_pair_forces(
+    const double4* __restrict__ sp, const float4* __restrict__ spf, const int* __restrict__ order, int64_t n,
+    const int* __restrict__ start, PairGeom pg, PairParams pp, double* __restrict__ force, double* __restrict__ e_atom,
+    unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ rmin_bits) {
+  constexpr double kTwoOverSqrtPi = 1.1283791670955126;
+  __shared__ int c_start[kPairWarps][27], c_cnt[kPairWarps][28], c_queue[kPairWarps][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double ilx = 1.0 / pg.lx, ily = 1.0 / pg.ly, ilz = 1.0 / pg.lz;
+  const float flx = (float)pg.lx, fly = (float)pg.ly, flz = (float)pg.lz;
+  const float filx = 1.f / flx, fily = 1.f / fly, filz = 1.f / flz;
+  // fp32 pre-filter: a candidate is dropped only if its fp32 distance^2 exceeds
+  // rc^2 by far more than the fp32 rounding of box-sized coordinates; the
+  // survivors are evaluated (and cut) in fp64, so the pair set is exact
+  const float rc2f = (float)pp.rc2 * 1.0001f + 1e-3f;
+  unsigned long long cand = 0, within = 0;
+  int olx, onx, oly, ony, olz, onz;
+  axis_offsets(pg.nx, olx, onx);
+  axis_offsets(pg.ny, oly, ony);
+  axis_offsets(pg.nz, olz, onz);
+  const int noff = onx * ony * onz;
+  const int64_t warps = (int64_t)gridDim.x * kPairWarps;
+  for (int64_t s = blockIdx.x * (int64_t)kPairWarps + w; s < n; s += warps) {
+    const double4 a = sp[s];
+    // the atom's cell from its sorted position (same arithmetic as k_cell_of)
+    const int cx = min((int)floor(a.x / pg.sx), pg.nx - 1);
+    const int cy = min((int)floor(a.y / pg.sy), pg.ny - 1);
+    const int cz = min((int)floor(a.z / pg.sz), pg.nz - 1);
+    const float4 af = spf[s];
+    if (lane < noff) {
+      const int dx = lane % onx, dy = (lane / onx) % ony, dz = lane / (onx * ony);
+      const int nc = ((((cz + olz + dz + pg.nz) % pg.nz) * pg.ny + (cy + oly + dy + pg.ny) % pg.ny) * pg.nx) +
+                     (cx + olx + dx + pg.nx) % pg.nx;
+      c_start[w][lane] = start[nc];
+      c_cnt[w][lane] = start[nc + 1] - start[nc];
+    }
+    __syncwarp();
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
-    for (int dz = 0; dz < onz; ++dz) {
-      const int nzc = (cz + olz + dz + pg.nz) % pg.nz;
-      for (int dy = 0; dy < ony; ++dy) {
-        const int nyc = (cy + oly + dy + pg.ny) % pg.ny;
-        for (int dx = 0; dx < onx; ++dx) {
-          const int nxc = (cx + olx + dx + pg.nx) % pg.nx;
-          const int nc = (nzc * pg.ny + nyc) * pg.nx + nxc;
-          const int e0 = start[nc + 1];
-          for (int t = start[nc]; t < e0; ++t) {
-            const int j = order[t];
-            if (j == i) continue;
-            ++cand;
-            const double ddx = min_image(xi - pos[3 * j], pg.lx);
-            const double ddy = min_image(yi - pos[3 * j + 1], pg.ly);
-            const double ddz = min_image(zi - pos[3 * j + 2], pg.lz);
-            const double r2 = ddx * ddx + ddy * ddy + ddz * ddz;
-            if (!(r2 < pp.rc2)) continue;
-            ++within;
-            const double r = sqrt(r2);
-            if (r < 1e-10) atomicMin(rmin_bits, (unsigned long long)__double_as_longlong(r));
-            const double qq = pp.scale * qi * q[j];
-            const double scr = erfc(pp.alpha * r);
-            double et = qq * scr / r;
-            double fm = qq * (scr / r2 + kTwoOverSqrtPi * pp.alpha * exp(-pp.alpha * pp.alpha * r2) / r);
-            if (LJ && r < pp.lj_rc) {
-              const double sr = pp.lj_sigma / r;
-              const double sr2 = sr * sr, sr6 = sr2 * sr2 * sr2;
-              et += 4.0 * pp.lj_eps * (sr6 * sr6 - sr6);
-              fm += 24.0 * pp.lj_eps * (2.0 * sr6 * sr6 - sr6) / r;
-            }
-            const double fr = fm / r;
-            fx += fr * ddx;
-            fy += fr * ddy;
-            fz += fr * ddz;
-            e += et;
-          }
+    // pair evaluation (fp64) of one queued candidate
+    auto eval = [&](int js) {
+      const double4 b = sp[js];
+      const double ddx = min_image_inv(a.x - b.x, pg.lx, ilx);
+      const double ddy = min_image_inv(a.y - b.y, pg.ly, ily);
+      const double ddz = min_image_inv(a.z - b.z, pg.lz, ilz);
+      const double r2 = ddx * ddx + ddy * ddy + ddz * ddz;
+      if (!(r2 < pp.rc2)) return;
+      ++within;
+      // 1/r from one rsqrt, erfc = erfcx * exp(-x^2) sharing the exponential
+      // of the force term (a few ulps from the reference's erfc / divisions)
+      if (sqrt(r2) < 1e-10) {  // overlapping atoms: reported, not evaluated (SingularityError)
+        atomicMin(rmin_bits, (unsigned long long)__double_as_longlong(sqrt(r2)));
+        return;
+      }
+      const double ir = rsqrt(r2);
+      const double r = r2 * ir;
+      const double qq = pp.scale * a.w * b.w;
+      const double x = pp.alpha * r;
+      const double ex = exp(-x * x);
+      const double scr = erfcx(x) * ex;
+      double et = qq * scr * ir;
+      double fm = qq * (scr * ir * ir + kTwoOverSqrtPi * pp.alpha * ex * ir);
+      if (LJ && r < pp.lj_rc) {
+        const double sr = pp.lj_sigma * ir;
+        const double sr2 = sr * sr, sr6 = sr2 * sr2 * sr2;
+        et += 4.0 * pp.lj_eps * (sr6 * sr6 - sr6);
+        fm += 24.0 * pp.lj_eps * (2.0 * sr6 * sr6 - sr6) * ir;
+      }
+      const double fr = fm * ir;
+      fx += fr * ddx;
+      fy += fr * ddy;
+      fz += fr * ddz;
+      e += et;
+    };
+    // candidates: the warp walks the concatenated cell lists 32 at a time; the
+    // fp32 survivors are compacted into a per-warp queue (ballot) and
+    // evaluated 32 at a time with every lane busy (no divergence on the fp64
+    // path, which only ~15 % of the candidates reach)
+    int total = 0;
+    for (int kk = 0; kk < noff; ++kk) total += c_cnt[w][kk];
+    int k = 0, t = lane, qn = 0;
+    int* queue = c_queue[w];
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = 0; base < total; base += 32) {
+      bool pass = false;
+      int js = 0;
+      if (base + lane < total) {
+        while (t >= c_cnt[w][k]) {
+          t -= c_cnt[w][k];
+          ++k;
+        }
+        js = c_start[w][k] + t;
+        t += 32;
+        if (js != s) {
+          ++cand;
+          const float4 bf = spf[js];
+          const float fx_ = min_image_f(af.x - bf.x, flx, filx);
+          const float fy_ = min_image_f(af.y - bf.y, fly, fily);
+          const float fz_ = min_image_f(af.z - bf.z, flz, filz);
+          pass = fx_ * fx_ + fy_ * fy_ + fz_ * fz_ <= rc2f;
         }
       }
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) queue[qn + __popc(m & lt)] = js;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) {
+        eval(queue[lane]);
+        __syncwarp();
+        const int rest = qn - 32;
+        const int mv = lane < rest ? queue[32 + lane] : 0;
+        __syncwarp();
+        if (lane < rest) queue[lane] = mv;
+        qn = rest;
+        __syncwarp();
+      }
     }
-    force[3 * i] = fx;
-    force[3 * i + 1] = fy;
-    force[3 * i + 2] = fz;
-    e_atom[i] = 0.5 * e;
+    if (lane < qn) eval(queue[lane]);
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      fx += __shfl_xor_sync(0xffffffffu, fx, o);
+      fy += __shfl_xor_sync(0xffffffffu, fy, o);
+      fz += __shfl_xor_sync(0xffffffffu, fz, o);
+      e += __shfl_xor_sync(0xffffffffu, e, o);
+    }
+    if (lane == 0) {
+      const int i = order[s];
+      force[3 * i] = fx;
+      force[3 * i + 1] = fy;
+      force[3 * i + 2] = fz;
+      e_atom[i] = 0.5 * e;
+    }
+    __syncwarp();
   }
-  // ordered pair counts (each unordered pair twice)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cand += __shfl_xor_sync(0xffffffffu, cand, o);
     within += __shfl_xor_sync(0xffffffffu, within, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     atomicAdd(cnt, cand);
     atomicAdd(cnt + 1, within);
   }
@@ -373,8 +481,9 @@ PairGeom make_pair_geom(double lx, double ly, double lz, double rc) {
 // count/start (ncells + 1) ints; cnt 2 u64, rmin 1 u64 (pre-set by the caller)
 int launch_pair(const double* pos, const double* q, int64_t n, double lx, double ly, double lz, double alpha,
                 double rc, double scale, const double* lj, int* cell, int* count, int* start, int* cursor,
-                int* order, int* tmp, double* force, double* e_atom, unsigned long long* cnt,
+                int* order, int* tmp, double4* sp, double* force, double* e_atom, unsigned long long* cnt,
                 unsigned long long* rmin_bits, int* err, cudaStream_t s) {
+  float4* spf = reinterpret_cast<float4*>(sp + n);  // fp32 copy after the fp64 one
   const PairGeom pg = make_pair_geom(lx, ly, lz, rc);
   const int ncells = pg.nx * pg.ny * pg.nz;
   if (cudaMemsetAsync(count, 0, sizeof(int) * (ncells + 1), s) != cudaSuccess) return launch_status();
@@ -390,12 +499,16 @@ int launch_pair(const double* pos, const double* q, int64_t n, double lx, double
     pp.lj_sigma = lj[1];
     pp.lj_rc = lj[2];
   }
+  k_pair_sorted<<<grid_for(n), kThreads, 0, s>>>(pos, q, order, n, sp, spf);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + kPairWarps - 1) / kPairWarps;
+  const int grid = (int)std::min<int64_t>(want, (int64_t)sms * 8);
   if (lj)
-    k_pair_forces<true><<<grid_for(n, 128), 128, 0, s>>>(pos, q, n, order, start, cell, pg, pp, force, e_atom, cnt,
-                                                        rmin_bits);
+    k_pair_forces<true><<<grid, 32 * kPairWarps, 0, s>>>(sp, spf, order, n, start, pg, pp, force, e_atom, cnt, rmin_bits);
   else
-    k_pair_forces<false><<<grid_for(n, 128), 128, 0, s>>>(pos, q, n, order, start, cell, pg, pp, force, e_atom, cnt,
-                                                         rmin_bits);
+    k_pair_forces<false><<<grid, 32 * kPairWarps, 0, s>>>(sp, spf, order, n, start, pg, pp, force, e_atom, cnt, rmin_bits);
   return launch_status();
 }
 

@@ -126,7 +126,7 @@ struct pppm_ctx {
   bool use_zfft = true, zfft = false;
   // short-range pairs / full force evaluation / NVE (fp64)
   DevBuf pr_cell, pr_count, pr_start, pr_cursor, pr_order, pr_tmp, pr_force, pr_e, pr_cnt, pr_rmin, pr_ij,
-      pr_part, pr_pos, pr_q, pr_scal;
+      pr_part, pr_pos, pr_q, pr_scal, pr_sp;
   DevBuf md_pos, md_vel, md_m, md_q, md_f, md_tmp, md_series;
   cufftHandle fwd2 = 0, bwd2 = 0;
   DevBuf ztw, zdone;
@@ -739,7 +739,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
                     &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone,
                     &c->pr_cell, &c->pr_count, &c->pr_start, &c->pr_cursor, &c->pr_order, &c->pr_tmp, &c->pr_force,
-                    &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal,
+                    &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal, &c->pr_sp,
                     &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)
@@ -1359,6 +1359,7 @@ static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_
   TRY(c->pr_cursor.ensure(sizeof(int) * (ncells + 1)));
   TRY(c->pr_force.ensure(sizeof(double) * 3 * n));
   TRY(c->pr_e.ensure(sizeof(double) * n));
+  TRY(c->pr_sp.ensure(sizeof(double) * 4 * n + sizeof(float) * 4 * n));
   TRY(c->pr_cnt.ensure(16));
   TRY(c->pr_rmin.ensure(8));
   TRY(c->pr_ij.ensure(8));
@@ -1369,7 +1370,7 @@ static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_
   const double scale = c->cscale;
   TRY(launch_pair(dpos, dq, n, c->g.lx, c->g.ly, c->g.lz, alpha, rc, scale, lj, c->pr_cell.as<int>(),
                   c->pr_count.as<int>(), c->pr_start.as<int>(), c->pr_cursor.as<int>(), c->pr_order.as<int>(),
-                  c->pr_tmp.as<int>(), c->pr_force.as<double>(), c->pr_e.as<double>(),
+                  c->pr_tmp.as<int>(), c->pr_sp.as<double4>(), c->pr_force.as<double>(), c->pr_e.as<double>(),
                   c->pr_cnt.as<unsigned long long>(), c->pr_rmin.as<unsigned long long>(), c->err.as<int>(),
                   c->stream));
   TRY(launch_sum(c->pr_e.as<double>(), n, c->pr_part.as<double>(), 1.0, c->pr_scal.as<double>(), c->stream));

@@ -81,7 +81,7 @@ int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Brick
                int* err, const int* orig, cudaStream_t s);
 int launch_pair(const double* pos, const double* q, int64_t n, double lx, double ly, double lz, double alpha,
                 double rc, double scale, const double* lj, int* cell, int* count, int* start, int* cursor,
-                int* order, int* tmp, double* force, double* e_atom, unsigned long long* cnt,
+                int* order, int* tmp, double4* sp, double* force, double* e_atom, unsigned long long* cnt,
                 unsigned long long* rmin_bits, int* err, cudaStream_t s);
 int launch_pair_find(const double* pos, int64_t n, double lx, double ly, double lz, double rc, const int* order,
                      const int* start, const int* cell, const unsigned long long* rmin_bits, long long* ij,
