@@ -136,7 +136,8 @@ __global__ void k_pair_sorted(const double* __restrict__ pos, const double* __re
 }
 
 __device__ __forceinline__ float min_image_f(float d, float l, float il) {
-  float o = d - rintf(d * il) * l;
+  (void)il;
+  float o = d;
   const float h = 0.5f * l;
   if (o >= h) o -= l;
   if (o < -h) o += l;
@@ -144,9 +145,11 @@ __device__ __forceinline__ float min_image_f(float d, float l, float il) {
 }
 
 __device__ __forceinline__ double min_image_inv(double d, double l, double il) {
-  // as min_image, with d / L as d * (1 / L): a different rint only within an
-  // ulp of a half box, and the fold below lands both in [-L/2, L/2)
-  double o = d - rint(d * il) * l;
+  // minimum image of a difference of two wrapped coordinates (|d| < L):
+  // round(d / L) is -1, 0 or 1, so model.minimum_image reduces to the fold
+  // alone (same result, no division / rounding instruction)
+  (void)il;
+  double o = d;
   const double h = 0.5 * l;
   if (o >= h) o -= l;
   if (o < -h) o += l;
