@@ -188,6 +188,14 @@ __global__ void k_pad_in(Geom g, Pad p, const double* __restrict__ src, float* _
   }
 }
 
+// kernels launch_fold_halo launches (for the launch-count bookkeeping)
+int fold_launches(const Geom& g, const Pad& p) {
+  if (p.H == 0) return 0;
+  const int nzl = p.pz - 2 * p.H;
+  if (g.nx >= 2 * p.H && g.ny >= 2 * p.H && (!p.zper || nzl >= 2 * p.H)) return 1;
+  return p.zper ? 3 : 2;
+}
+
 int launch_fold_halo(const Geom& g, const Pad& p, float* rho, cudaStream_t s) {
   if (p.H == 0) return 0;
   const int nzl = p.pz - 2 * p.H;

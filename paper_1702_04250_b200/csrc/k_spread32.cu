@@ -17,6 +17,38 @@ constexpr int kSpreadThreads = PPPM_SPREAD_THREADS;
 #define PPPM_SPREAD_MINB 4
 #endif
 
+// overflow atoms (full buckets): straight into the padded interior
+template <int S, bool TAB>
+__device__ __forceinline__ void spread_overflow(const int* __restrict__ counts, int nb, const Geom& g, const Pad& pd,
+                                                const float* __restrict__ ta, float inv_vcell,
+                                                float* __restrict__ rho, const float4* __restrict__ ovf_rec,
+                                                const int* __restrict__ ovf_cell) {
+  constexpr int lo = Stencil<S>::lo;
+  const int novf = counts[(int64_t)nb * kCountStride];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
+    const float4 r = ovf_rec[k];
+    const int cc = ovf_cell[k];
+    const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
+    float wx[S], wy[S], wz[S], dd[S];
+    rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+    rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+    rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+    const float q = r.w * inv_vcell;
+    // unwrapped slab-local coordinates: stencil cells past the edges land in the
+    // halo / ghost planes and are folded or exchanged like the tiles' halos
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+#pragma unroll
+      for (int bb = 0; bb < S; ++bb) {
+        const float p = q * wz[a] * wy[bb];
+        float* row = rho + pd.at(n0 - lo, n1 - lo + bb, n2 - lo + a);
+#pragma unroll
+        for (int c = 0; c < S; ++c) atomicAdd(row + c, p * wx[c]);
+      }
+    }
+  }
+}
+
 // make_rho, persistent CTAs: bricks b = blockIdx.x, += gridDim.x.  Per brick the
 // int32 fixed-point tile is accumulated with shared atomics, converted to fp32
 // in place and added to the padded mesh with ONE TMA reduce-add of the
@@ -106,30 +138,173 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     ++issued;
   }
   if (threadIdx.x == 0) bulk_wait_read<0>();
-  // overflow atoms (full buckets): straight into the padded interior
-  const int novf = counts[(int64_t)nb * kCountStride];
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
-    const float4 r = ovf_rec[k];
-    const int cc = ovf_cell[k];
-    const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
-    float wx[S], wy[S], wz[S], dd[S];
-    rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
-    rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
-    rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
-    const float q = r.w * inv_vcell;
-    // unwrapped slab-local coordinates: stencil cells past the edges land in the
-    // halo / ghost planes and are folded or exchanged like the tiles' halos
+  spread_overflow<S, TAB>(counts, nb, g, pd, ta, inv_vcell, rho, ovf_rec, ovf_cell);
+}
+
+
+// make_rho, warp-specialized: warp 0 stages brick i+1 (two-pass bank-bucketed
+// counting sort of its slots into one of two stage slots) and finishes brick
+// i-1 (int32 tile -> fp32, TMA reduce-add into the padded rho, re-zero once
+// the bulk read is done) while the consumer warps run brick i's bank rounds
+// into its tile; slots handed over with mbarriers (full: staged; done: every
+// consumer warp finished the brick).  Same fixed-point arithmetic as
+// k_spread_tma (bitwise identical mesh).
+constexpr int kSpreadWsWarps = 8;
+
+template <int S, bool TAB>
+__global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
+    const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
+    const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho, const __grid_constant__ CUtensorMap rmap,
+    const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
+  using T = TmaTile<S>;
+  constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
+  constexpr int NCW = kSpreadWsWarps;
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  int* tiles = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][NP]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * T::NP);                                    // [2][cap]
+  int* s_c = reinterpret_cast<int*>(s_r + 2 * cap);                                               // [2][cap]
+  __shared__ __align__(8) uint64_t full[2], done[2];
+  __shared__ int bsize[2][32], bstart[2][32], cursor[32];
+  __shared__ float sscale[2], sinv[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = bk.count();
+  const float qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
+  const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  // the CTA's non-empty bricks in order: b = blockIdx.x + j * gridDim.x with counts > 0
+  auto next_brick = [&](int b) {
+    for (b += gridDim.x; b < nb; b += gridDim.x)
+      if (counts[(int64_t)b * kCountStride] > 0) return b;
+    return nb;
+  };
+  int first = blockIdx.x;
+  if (first < nb && counts[(int64_t)first * kCountStride] == 0) first = next_brick(first);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  for (int k = threadIdx.x; k < 2 * T::NP; k += blockDim.x) tiles[k] = 0;
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer: stage the next brick into the free slot
+    int k = 0;
+    for (int b = first; b < nb; b = next_brick(b), ++k) {
+      const int s = k & 1, use = k >> 1;
+      if (use > 0) mbar_wait(&done[s], (use - 1) & 1);  // consumers released slot s (brick k-2)
+      int cnt = counts[(int64_t)b * kCountStride];
+      cnt = cnt < cap ? cnt : cap;
+      const int64_t base = (int64_t)b * cap;
+      const int4* meta = reinterpret_cast<const int4*>(rec);
+      if (lane == 0) {
+        int e_sum = 0, e_one = 0;
+        frexpf(qmax > 0.f ? (float)cnt * qmax * w3 : 1.f, &e_sum);
+        frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);
+        const int sc = min(30 - e_sum, 22 - e_one);
+        sscale[s] = ldexpf(1.f, sc);
+        sinv[s] = ldexpf(1.f, -sc) * inv_vcell;
+      }
+      bsize[s][lane] = 0;
+      __syncwarp();
+      for (int j = lane; j < cnt; j += 32) {
+        const int cc = meta[2 * (base + j) + 1].x;
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        atomicAdd(&bsize[s][((lz * D + ly) * TXB + lx + T::SH) & 31], 1);
+      }
+      __syncwarp();
+      {
+        const int v = bsize[s][lane];
+        int x = v;
 #pragma unroll
-    for (int a = 0; a < S; ++a) {
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        bstart[s][lane] = x - v;
+        cursor[lane] = x - v;
+      }
+      __syncwarp();
+      float4* sr = s_r + s * cap;
+      int* sc = s_c + s * cap;
+      for (int j = lane; j < cnt; j += 32) {
+        const float4 r = rec[2 * (base + j)];
+        const int cc = meta[2 * (base + j) + 1].x;
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        const int dst = atomicAdd(&cursor[((lz * D + ly) * TXB + lx + T::SH) & 31], 1);
+        sr[dst] = r;
+        sc[dst] = cc;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else {
+    // ---------------- consumers: bank rounds, then convert + TMA reduce-add
+    // (consumer-only named barrier 1; the producer runs ahead)
+    const int cw = warp - 1, ct = threadIdx.x - 32;
+    auto cbar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory"); };
+    const bool issuer = ct == 0;
+    int k = 0;
+    for (int b = first; b < nb; b = next_brick(b), ++k) {
+      const int s = k & 1, ph = (k >> 1) & 1;
+      mbar_wait(&full[s], ph);
+      int* tile = tiles + s * T::NP;
+      float* ftile = reinterpret_cast<float*>(tile);
+      const float scale = sscale[s], inv = sinv[s];
+      if (k >= 2) {
+        // tile s was reduced at brick k-2: wait for that bulk read, re-zero
+        if (issuer) bulk_wait_read<1>();
+        cbar();
+        for (int t = ct; t < TN; t += NCW * 32) tile[t] = 0;
+        cbar();
+      }
+      const float4* sr = s_r + s * cap;
+      const int* sc = s_c + s * cap;
+      int rounds = bsize[s][lane];
 #pragma unroll
-      for (int bb = 0; bb < S; ++bb) {
-        const float p = q * wz[a] * wy[bb];
-        float* row = rho + pd.at(n0 - lo, n1 - lo + bb, n2 - lo + a);
+      for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+      const int mine = bsize[s][lane], st = bstart[s][lane];
+      for (int rr = cw; rr < rounds; rr += NCW) {
+        if (rr >= mine) continue;
+        const int j = st + rr;
+        const float4 r = sr[j];
+        const int cc = sc[j];
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        float wx[S], wy[S], wz[S], dd[S];
+        rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+        rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+        rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+        const float qs = r.w * scale;
 #pragma unroll
-        for (int c = 0; c < S; ++c) atomicAdd(row + c, p * wx[c]);
+        for (int a = 0; a < S; ++a) {
+          const float qa = qs * wz[a];
+#pragma unroll
+          for (int bb = 0; bb < S; ++bb) {
+            const float qab = qa * wy[bb];
+            const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+#pragma unroll
+            for (int c = 0; c < S; ++c)
+              atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);  // staging slot s is free (tile s is not yet)
+      cbar();
+      for (int t = ct; t < TN; t += NCW * 32) ftile[t] = (float)tile[t] * inv;
+      fence_proxy_async_smem();
+      cbar();
+      if (issuer) {
+        const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+        tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H,
+                          bz * kBrick - lo + pd.H);
+        bulk_commit();
       }
     }
+    if (issuer) bulk_wait_read<0>();
   }
+  spread_overflow<S, TAB>(counts, nb, g, pd, ta, inv_vcell, rho, ovf_rec, ovf_cell);
 }
 
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
@@ -141,6 +316,20 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
+      if (variant == SPREAD_WS) {
+        auto k = k_spread_ws<S, TAB>;
+        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + 2 * (size_t)cap * (sizeof(float4) + sizeof(int));
+        allow_smem(k, dyn);
+        constexpr int NT = 32 * (kSpreadWsWarps + 1);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+        k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
+        return 0;
+      }
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
         constexpr int NT = kSpreadThreads;

@@ -367,10 +367,10 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     c->launches += 4;
   } else {
     if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
-    TRY(launch_spread_brick(c->spread_variant & 1, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
+    TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
                             c->bk, c->pd, c->rho_map, c->tab.as<float>(), c->rho.as<float>(), c->stream));
-    c->launches += 4;  // spread + 3 halo folds
+    c->launches += 1 + fold_launches(c->g, c->pd);  // spread + halo fold
   }
   c->have_rho = true;
   return PPPM_OK;

@@ -59,7 +59,7 @@ struct AtomsIn {
 };
 
 // kernel variants (selectable per context for A/B measurement)
-enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1 };  // + 2: same, cell-sorted in shared memory
+enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1, SPREAD_WS = 3 };  // WS: FIX32, warp-specialized
 enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3 };  // SPLIT, WS: ik only
 // field tiles of the split gather: rows shifted per component (TXB = 12 or 20 mod 32)
 inline bool gather_split_ok(int order, int hx) {
@@ -94,6 +94,7 @@ int launch_drift(double* x, const double* v, double dt, double lx, double ly, do
 int launch_series_row(const double* v, const double* m, int64_t n, double* tmp4, double* partial, double* row,
                       const double* e_pair, const double* e_kspace, const double* e_self, cudaStream_t s);
 bool zfft_supported(int nz);
+int fold_launches(const Geom& g, const Pad& p);
 int zfft_blocks(int nz, int ncols);
 int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,
                       float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial, unsigned* done,

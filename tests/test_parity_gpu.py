@@ -503,3 +503,31 @@ def test_resident_graph_replay_is_stable(pb):
     f3 = ctx.forces()
     ctx.close()
     assert rel_rms(f3, f0) <= 1e-6
+
+
+@pytest.mark.parametrize("mode", ["ik", "ad"])
+def test_kernel_variants_agree(pb, mode):
+    """Every make_rho / fieldforce variant of the fp32 path (A/B switches of
+    pppm_ctx_set_variant) gives the same charge mesh (fixed-point variants:
+    bitwise) and the same forces (1e-6)."""
+    from paper_1702_04250_b200 import _native as nat
+    from paper_1702_04250_b200 import scenarios
+
+    pos, q, lengths = scenarios.random_gas(30000, 8, 50.0)
+    p32 = scenarios.round_to_f32(pos, lengths)
+    ctx = pb.PppmContext((32, 32, 32), lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
+    ctx.load_atoms(p32, q.astype(np.float32))
+    ctx.step()
+    ctx.synchronize()
+    rho0, f0 = ctx.rho(), ctx.forces()
+    for kernel, variant in ((0, 3), (1, 1), (1, 2), (1, 0), (0, 0)):
+        ctx.ctx("pppm_ctx_set_variant", kernel, variant)
+        ctx.step()
+        ctx.synchronize()
+        rho, f = ctx.rho(), ctx.forces()
+        if kernel == 0 and variant == 3:
+            assert np.array_equal(rho, rho0)   # same fixed-point arithmetic
+        else:
+            assert rel_rms(rho, rho0) <= 1e-6
+        assert rel_rms(f, f0) <= 1e-6
+    ctx.close()
