@@ -179,11 +179,13 @@ int pppm_singular_pair(long long* i, long long* j, double* r);
 /* driver.compute_forces (driver.py:232-307): pair forces + make_rho + Poisson +
  * fieldforce on the device; forces = pair + mesh (host (N, 3) fp64);
  * energies[3] = {pair, kspace, self} (EnergyBreakdown, model.py:258-268; self =
- * -C alpha/sqrt(pi) sum q^2, shortrange.py:270-278); counters[2] as above.
+ * -C alpha/sqrt(pi) sum q^2, shortrange.py:270-278); counters[2] as above;
+ * sections[3] (nullable): device seconds of the reference's report sections
+ * {pppm_non_fft, pppm_fft, pair} (driver.py:36, CUDA events).
  * Uses the context's table / influence selection for the mesh part. */
 int pppm_ctx_compute_forces(pppm_ctx* ctx, const void* positions, const void* charges, int64_t n, int dtype,
                             int mem, double cutoff, const double* lj, double* forces, double* energies,
-                            long long* counters);
+                            long long* counters, double* sections);
 /* driver.integrate_nve (driver.py:310-376): velocity-Verlet NVE trajectory with
  * one compute_forces per step, positions / velocities / forces resident on the
  * device.  Host fp64 inputs; series: (steps + 1) rows of {total, kinetic,

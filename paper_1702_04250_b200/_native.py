@@ -83,7 +83,8 @@ PROTOTYPES = {
     "pppm_ctx_pair_forces": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_dbl, _c_dbl, _vp, _vp, _dp,
                                       _vp]),
     "pppm_singular_pair": (_c_int, [ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong), _dp]),
-    "pppm_ctx_compute_forces": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_dbl, _vp, _vp, _vp, _vp]),
+    "pppm_ctx_compute_forces": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_dbl, _vp, _vp, _vp, _vp,
+                                         _vp]),
     "pppm_ctx_integrate_nve": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp,
                                         _vp]),
 }

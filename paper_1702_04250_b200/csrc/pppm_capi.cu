@@ -1428,13 +1428,19 @@ int pppm_ctx_pair_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n,
 }
 
 // full force evaluation on device atoms: pair forces + mesh forces -> out (n, 3)
-// fp64, energies -> pr_scal[0] (pair), scal[0] (kspace), pr_scal[1] (self)
+// fp64, energies -> pr_scal[0] (pair), scal[0] (kspace), pr_scal[1] (self).
+// ev (nullable): 5 events bracketing pair | make_rho | Poisson | fieldforce
 static int forces_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double rc, const double* lj,
-                         double* out, long long* counters) {
+                         double* out, long long* counters, cudaEvent_t* ev = nullptr) {
+  if (ev) cudaEventRecord(ev[0], c->stream);
   TRY(pair_device(c, dpos, dq, n, c->alpha, rc, lj, counters));
+  if (ev) cudaEventRecord(ev[1], c->stream);
   TRY(do_make_rho(c, dpos, dq, n, PPPM_F64));
+  if (ev) cudaEventRecord(ev[2], c->stream);
   TRY(run_poisson(c));
+  if (ev) cudaEventRecord(ev[3], c->stream);
   TRY(do_fieldforce(c, dpos, dq, n, PPPM_F64, false, out, true));
+  if (ev) cudaEventRecord(ev[4], c->stream);
   TRY(launch_add3(c->pr_force.as<double>(), out, 3 * n, c->stream));
   // self energy -C alpha / sqrt(pi) sum q^2 (shortrange.py:270-278)
   TRY(launch_square(dq, n, c->pr_e.as<double>(), c->stream));
@@ -1445,20 +1451,42 @@ static int forces_device(pppm_ctx* c, const double* dpos, const double* dq, int6
 }
 
 int pppm_ctx_compute_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem,
-                            double cutoff, const double* lj, double* forces, double* energies, long long* counters) {
+                            double cutoff, const double* lj, double* forces, double* energies, long long* counters,
+                            double* sections) {
   TRY(activate(c));
   if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
   TRY(check_pair_args(c, c->alpha, cutoff));
+  cudaEvent_t ev[5] = {};
+  if (sections)
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+  auto destroy = [&]() {
+    if (sections)
+      for (auto& e : ev) cudaEventDestroy(e);
+  };
   const double *dpos, *dq;
-  TRY(stage_f64(c, pos, q, n, dtype, mem, &dpos, &dq));
-  TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
-  TRY(forces_device(c, dpos, dq, n, cutoff, lj, c->out_stage.as<double>(), counters));
+  int st = stage_f64(c, pos, q, n, dtype, mem, &dpos, &dq);
+  if (st == PPPM_OK) st = c->out_stage.ensure(sizeof(double) * 3 * n);
+  if (st == PPPM_OK) st = forces_device(c, dpos, dq, n, cutoff, lj, c->out_stage.as<double>(), counters,
+                                        sections ? ev : nullptr);
+  if (st != PPPM_OK) {
+    destroy();
+    return st;
+  }
   CU(cudaMemcpyAsync(forces, c->out_stage.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
   double e[3];
   CU(cudaMemcpyAsync(e, c->pr_scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaMemcpyAsync(e + 1, c->scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaMemcpyAsync(e + 2, c->pr_scal.as<double>() + 1, 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  if (sections) {
+    // driver.REPORT_SECTIONS: pppm_non_fft (make_rho + fieldforce), pppm_fft, pair; seconds
+    float t[4] = {};
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    sections[0] = 1e-3 * ((double)t[1] + (double)t[3]);
+    sections[1] = 1e-3 * (double)t[2];
+    sections[2] = 1e-3 * (double)t[0];
+  }
+  destroy();
   TRY(check_err_flag(c));
   if (energies) {
     energies[0] = e[0];

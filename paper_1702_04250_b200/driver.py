@@ -6,13 +6,15 @@ pair forces (``k_pair.cu``), make_rho -> Poisson -> fieldforce (the mesh path)
 and the self energy on the device; ``integrate_nve`` keeps positions,
 velocities and forces resident for the whole velocity-Verlet trajectory and
 reduces the energy / temperature / momentum series on the device (fp64,
-fixed-order sums).  Section timing: the three reference sections run inside
-one device call, so the wall time of the call is reported under ``"device"``
-and the reference's section names carry 0.0.
+fixed-order sums).  Section timing: the reference's three measured sections
+(``pair``, ``pppm_fft``, ``pppm_non_fft``, driver.py:1-9) are CUDA-event times
+of the device call, so ``make_report`` records (driver.py:383-423) keep their
+schema with GPU timings.
 """
 
 from __future__ import annotations
 
+import json
 import time
 
 import numpy as np
@@ -85,17 +87,64 @@ def compute_forces(system, params, table=None, plan=None, lj=None, *, workers=1,
     forces = np.empty((n, 3))
     e = np.zeros(3)
     cnt = np.zeros(2, dtype=np.int64)
+    sec = np.zeros(3)
     ljp = lj_array(lj)
     ctx("pppm_ctx_compute_forces", nat.ptr(pos), nat.ptr(q), n, nat.F64, nat.HOST, float(params.cutoff),
-        None if ljp is None else nat.ptr(ljp), nat.ptr(forces), nat.ptr(e), nat.ptr(cnt))
+        None if ljp is None else nat.ptr(ljp), nat.ptr(forces), nat.ptr(e), nat.ptr(cnt), nat.ptr(sec))
     _count(counters, params, n, cnt)
-    wall = time.perf_counter() - t0
-    sections = {name: 0.0 for name in REPORT_SECTIONS[:3]}
-    sections["device"] = wall
+    sections = {"pppm_non_fft": float(sec[0]), "pppm_fft": float(sec[1]), "pair": float(sec[2])}
     if timer is not None:
-        timer.add("device", wall)
+        for name, dt in sections.items():
+            timer.add(name, dt)
+        timer.add("other", max(0.0, time.perf_counter() - t0 - sum(sections.values())))
     energy = _energy_type()(pair=float(e[0]), kspace=float(e[1]), self_energy=float(e[2]))
     return forces, energy, sections
+
+
+def make_report(*, sections, wall_total, n_atoms, params, steps, workers, counters=None, extra=None):
+    """A timing record with the reference's schema (driver.py:383-423)."""
+    from . import __version__
+
+    measured = {k: float(sections.get(k, 0.0)) for k in REPORT_SECTIONS if k != "other"}
+    record = {
+        "sections": {**measured, "other": max(0.0, wall_total - sum(measured.values()))},
+        "n_atoms": int(n_atoms),
+        "steps": int(steps),
+        "workers": int(workers),
+        "params": {
+            "cutoff": params.cutoff, "accuracy": params.accuracy, "order": params.order,
+            "mode": getattr(params.mode, "value", params.mode), "alpha": params.alpha,
+            "grid_dims": list(params.grid_dims), "table_points": params.table_points,
+            "use_table": params.use_table,
+        },
+        "counters": dict(counters or {}),
+        "build_id": f"paper_1702_04250_b200-{__version__}",
+    }
+    if extra:
+        record.update(extra)
+    return record
+
+
+def validate_report(record) -> None:
+    """Raise ValueError unless ``record`` matches the report schema (driver.py:426-441)."""
+    if not isinstance(record, dict):
+        raise ValueError("report record must be a dict")
+    sections = record.get("sections")
+    if not isinstance(sections, dict) or set(sections) != set(REPORT_SECTIONS):
+        raise ValueError(f"report sections must be exactly {REPORT_SECTIONS}")
+    for key, value in sections.items():
+        if not isinstance(value, (int, float)) or value < 0:
+            raise ValueError(f"section {key} must be a non-negative number")
+    for key in ("n_atoms", "steps", "workers", "params", "build_id"):
+        if key not in record:
+            raise ValueError(f"report record missing {key!r}")
+    if not isinstance(record["params"], dict):
+        raise ValueError("params echo must be a dict")
+
+
+def report_line(record) -> str:
+    """One JSON line, keys sorted (driver.write_records, fmt json)."""
+    return json.dumps(record, sort_keys=True)
 
 
 def integrate_nve(system, params, dt, steps, lj=None, *, workers=1, timer=None, counters=None):

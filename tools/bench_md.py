@@ -68,7 +68,7 @@ def main():
                            alpha=cfg.alpha, grid_dims=cfg.dims, precision=args.precision)
     counters = {}
     f, e, _ = pb.compute_forces(s, params, counters=counters)
-    f, e, _ = pb.compute_forces(s, params)
+    f, e, sections = pb.compute_forces(s, params)
     times = []
     for _ in range(args.calls):
         t0 = time.perf_counter()
@@ -83,7 +83,13 @@ def main():
     out = pb.integrate_nve(sv, params, 1e-4, args.nve_steps)
     tn = time.perf_counter() - t0
     drift = float(np.max(np.abs(out["series"]["total_energy"] - out["series"]["total_energy"][0])))
+    from paper_1702_04250_b200 import driver
+
+    report = driver.make_report(sections=sections, wall_total=tf, n_atoms=n, params=params, steps=1, workers=1,
+                                counters=counters)
+    driver.validate_report(report)
     line.update({"impl": f"b200 ({args.precision})", "compute_forces_s": tf, "atoms_per_s": n / tf,
+                 "report": report,
                  "pairs_within_cutoff": counters.get("pairs_within_cutoff", 0),
                  "energy_total": e.total, "nve_steps": args.nve_steps, "nve_s_per_step": tn / args.nve_steps,
                  "nve_atom_steps_per_s": n * args.nve_steps / tn, "nve_energy_drift": drift})
