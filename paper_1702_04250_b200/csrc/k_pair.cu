@@ -163,7 +163,7 @@ __device__ __forceinline__ double min_image_inv(double d, double l, double il) {
 constexpr int kPairWarps = 8;
 
 template <bool LJ>
-__global__ void __launch_bounds__(32 * kPairWarps) k_pair_forces(
+__global__ void __launch_bounds__(32 * kPairWarps, 4) k_pair_forces(
     const double4* __restrict__ sp, const float4* __restrict__ spf, const int* __restrict__ order, int64_t n,
     const int* __restrict__ start, PairGeom pg, PairParams pp, double* __restrict__ force, double* __restrict__ e_atom,
     unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ rmin_bits) {
@@ -244,27 +244,35 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pair_forces(
     int k = 0, t = lane, qn = 0;
     int* queue = c_queue[w];
     const unsigned lt = (1u << lane) - 1u;
+    // the lane's next candidate slot in the concatenated lists (t: offset into cell k)
+    auto advance = [&]() {
+      while (t >= c_cnt[w][k]) {
+        t -= c_cnt[w][k];
+        ++k;
+      }
+      const int js = c_start[w][k] + t;
+      t += 32;
+      return js;
+    };
+    // software pipeline: the next candidate's fp32 position is in flight while
+    // the current one is filtered / queued
+    bool v_cur = lane < total;
+    int js_cur = v_cur ? advance() : 0;
+    float4 bf_cur = v_cur ? spf[js_cur] : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int base = 0; base < total; base += 32) {
+      const bool v_nxt = base + 32 + lane < total;
+      const int js_nxt = v_nxt ? advance() : 0;
+      const float4 bf_nxt = v_nxt ? spf[js_nxt] : make_float4(0.f, 0.f, 0.f, 0.f);
       bool pass = false;
-      int js = 0;
-      if (base + lane < total) {
-        while (t >= c_cnt[w][k]) {
-          t -= c_cnt[w][k];
-          ++k;
-        }
-        js = c_start[w][k] + t;
-        t += 32;
-        if (js != s) {
-          ++cand;
-          const float4 bf = spf[js];
-          const float fx_ = min_image_f(af.x - bf.x, flx, filx);
-          const float fy_ = min_image_f(af.y - bf.y, fly, fily);
-          const float fz_ = min_image_f(af.z - bf.z, flz, filz);
-          pass = fx_ * fx_ + fy_ * fy_ + fz_ * fz_ <= rc2f;
-        }
+      if (v_cur && js_cur != s) {
+        ++cand;
+        const float fx_ = min_image_f(af.x - bf_cur.x, flx, filx);
+        const float fy_ = min_image_f(af.y - bf_cur.y, fly, fily);
+        const float fz_ = min_image_f(af.z - bf_cur.z, flz, filz);
+        pass = fx_ * fx_ + fy_ * fy_ + fz_ * fz_ <= rc2f;
       }
       const unsigned m = __ballot_sync(0xffffffffu, pass);
-      if (pass) queue[qn + __popc(m & lt)] = js;
+      if (pass) queue[qn + __popc(m & lt)] = js_cur;
       qn += __popc(m);
       __syncwarp();
       if (qn >= 32) {
@@ -277,6 +285,9 @@ __global__ void __launch_bounds__(32 * kPairWarps) k_pair_forces(
         qn = rest;
         __syncwarp();
       }
+      v_cur = v_nxt;
+      js_cur = js_nxt;
+      bf_cur = bf_nxt;
     }
     if (lane < qn) eval(queue[lane]);
     __syncwarp();
