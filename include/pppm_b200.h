@@ -121,7 +121,13 @@ int pppm_compute(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int d
 int pppm_ctx_load_atoms(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int dtype);
 int pppm_ctx_step(pppm_ctx* ctx, int phases);            /* async on the context stream */
 int pppm_ctx_synchronize(pppm_ctx* ctx);
-int pppm_ctx_get_forces(pppm_ctx* ctx, double* forces);  /* host (n,3) fp64 */
+int pppm_ctx_get_forces(pppm_ctx* ctx, double* forces);
+/* new positions of the resident atoms (caller's order, same count), kept in the
+ * context's brick order: a time-stepping caller (driver.integrate_nve's
+ * position update, driver.py:369) moves atoms without re-sorting; make_rho /
+ * fieldforce send atoms that left their brick down a direct path until the
+ * next pppm_ctx_load_atoms re-sorts them. */
+int pppm_ctx_update_positions(pppm_ctx* ctx, const void* positions, int dtype, int mem);  /* host (n,3) fp64 */
 int pppm_ctx_get_energy(pppm_ctx* ctx, double* energy);
 /* CUDA-event timing of `steps` full steps after `warmup`; flush_l2 writes a
  * 256 MiB buffer before each step (outside the phase intervals).

@@ -64,6 +64,7 @@ PROTOTYPES = {
     "pppm_ctx_step": (_c_int, [_vp, _c_int]),
     "pppm_ctx_synchronize": (_c_int, [_vp]),
     "pppm_ctx_get_forces": (_c_int, [_vp, _vp]),
+    "pppm_ctx_update_positions": (_c_int, [_vp, _vp, _c_int, _c_int]),
     "pppm_ctx_get_energy": (_c_int, [_vp, _dp]),
     "pppm_ctx_time_steps": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
     "pppm_ctx_launches_per_step": (_c_int, [_vp, ctypes.POINTER(_c_int)]),

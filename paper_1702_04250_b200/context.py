@@ -52,6 +52,14 @@ class PppmContext:
         self.ctx("pppm_ctx_load_atoms", nat.ptr(pos), nat.ptr(q), pos.shape[0], dtype)
         self.n_atoms = pos.shape[0]
 
+    def update_positions(self, positions):
+        """Move the resident atoms (caller's order) without re-sorting them."""
+        pos = np.ascontiguousarray(positions)
+        if pos.dtype != np.float32:
+            pos = pos.astype(np.float64, copy=False)
+        dtype = nat.F32 if pos.dtype == np.float32 else nat.F64
+        self.ctx("pppm_ctx_update_positions", nat.ptr(pos), dtype, nat.HOST)
+
     def step(self, phases=nat.PHASE_ALL):
         self.ctx("pppm_ctx_step", int(phases))
 

@@ -113,6 +113,27 @@ __global__ void k_reorder_resident(const float4* __restrict__ rec, const int* __
   }
 }
 
+// new positions (caller's order) into the brick-ordered resident array (fp32)
+template <typename TIn>
+__global__ void k_update_resident(const TIn* __restrict__ pos, const int* __restrict__ orig, int64_t n, Geom g,
+                                  float* __restrict__ res_pos, int* __restrict__ err) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = orig[k];
+    const float x = (float)pos[3 * i], y = (float)pos[3 * i + 1], z = (float)pos[3 * i + 2];
+    if (outside((double)x, g.lx) || outside((double)y, g.ly) || outside((double)z, g.lz)) atomicOr(err, 1);
+    res_pos[3 * k] = x;
+    res_pos[3 * k + 1] = y;
+    res_pos[3 * k + 2] = z;
+  }
+}
+
+int launch_update_resident(bool f32, const void* pos, const int* orig, int64_t n, const Geom& g, float* res_pos,
+                           int* err, cudaStream_t s) {
+  if (f32) k_update_resident<float><<<grid_for(n), kThreads, 0, s>>>((const float*)pos, orig, n, g, res_pos, err);
+  else k_update_resident<double><<<grid_for(n), kThreads, 0, s>>>((const double*)pos, orig, n, g, res_pos, err);
+  return launch_status();
+}
+
 // forces of brick-ordered resident atoms back to the caller's order (fp64 out)
 __global__ void k_unpermute_forces(const float* __restrict__ f, const int* __restrict__ orig, int64_t n,
                                    double* __restrict__ out) {

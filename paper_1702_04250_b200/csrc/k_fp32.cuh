@@ -226,6 +226,45 @@ __device__ __forceinline__ void rows_f32(float v, const float* __restrict__ ta, 
 }
 
 // ---------------------------------------------------------------------------
+// Resident brick-ordered atoms (pppm_ctx_load_atoms keeps them sorted by
+// brick): make_rho maps the positions itself each step instead of a separate
+// binning pass.  Brick b owns resident atoms [start[b], start[b+1]);
+// [start[nb], n) overflowed their bucket at load.  make_rho writes every
+// atom's 32-byte slot record at its resident index (cell -1 if the atom has
+// left the brick it was sorted into) for fieldforce, handles atoms that moved
+// out of their brick ("movers") straight from global memory and appends them
+// to the overflow list (count *novf) that fieldforce processes directly.
+
+// the slot record of resident atom i, exactly as k_bin_fixed computes it;
+// returns the atom's brick (pk: wrapped node packed 10+10+10 bits)
+template <int S, bool TAB>
+__device__ __forceinline__ int atom_record(const Resident& res, int64_t i, const Geom& g, const Bricks& bk,
+                                           int n_points, float4& r, int& lc, int& pk) {
+  const double x = (double)res.pos[3 * i], y = (double)res.pos[3 * i + 1], z = (double)res.pos[3 * i + 2];
+  int n0, n1, n2;
+  double tx, ty, tz;
+  particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
+  particle_map_fast<S>(y, g.hy, g.ihy, n1, ty);
+  particle_map_fast<S>(z, g.hz, g.ihz, n2, tz);
+  n0 = n0 >= g.nx ? n0 - g.nx : n0;
+  n1 = n1 >= g.ny ? n1 - g.ny : n1;
+  n2 = n2 >= g.nz ? n2 - g.nz : n2;
+  lc = (((n2 % kBrick) * kBrick) + (n1 % kBrick)) * kBrick + (n0 % kBrick);
+  pk = n0 | (n1 << 10) | (n2 << 20);
+  if (TAB) {
+    r.x = __int_as_float(table_bin(tx, n_points));
+    r.y = __int_as_float(table_bin(ty, n_points));
+    r.z = __int_as_float(table_bin(tz, n_points));
+  } else {
+    r.x = (float)tx;
+    r.y = (float)ty;
+    r.z = (float)tz;
+  }
+  r.w = res.q[i];
+  return ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
+}
+
+// ---------------------------------------------------------------------------
 // in-CTA staging: the brick's atoms into shared memory, counting-sorted by
 // brick-local cell.  Returns the atom count; fills s_r / s_c (/ s_p) in
 // sorted order and (optionally) the block sum of |q|.
@@ -340,7 +379,8 @@ struct BankSmem {
 
 template <bool PERM, int D, int TXB, int SH, int NT = kThreads>
 __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, const int* __restrict__ rcell,
-                                            const int* __restrict__ perm, int64_t base, int cnt, BankSmem sm) {
+                                            const int* __restrict__ perm, int64_t base, int cnt, BankSmem sm,
+                                            bool skip_movers = false) {
   constexpr int PER = kCapMax / NT;
   if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
   __syncthreads();
@@ -354,9 +394,13 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
       const int4 m = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
       c[k] = m.x;
       if (PERM) p[k] = m.y;
-      const int lx = c[k] & (kBrick - 1), ly = (c[k] >> 3) & (kBrick - 1), lz = c[k] >> 6;
-      bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
-      rk[k] = atomicAdd(sm.bsize + bank[k], 1);
+      if (skip_movers && c[k] < 0) {
+        bank[k] = -1;  // moved out of the brick: handled from the overflow list
+      } else {
+        const int lx = c[k] & (kBrick - 1), ly = (c[k] >> 3) & (kBrick - 1), lz = c[k] >> 6;
+        bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
+        rk[k] = atomicAdd(sm.bsize + bank[k], 1);
+      }
     }
   }
   __syncthreads();
@@ -377,7 +421,7 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int j = threadIdx.x + k * NT;
-    if (j < cnt) {
+    if (j < cnt && bank[k] >= 0) {
       const int dst = sm.bstart[bank[k]] + rk[k];
       sm.r[dst] = r[k];
       sm.c[dst] = c[k];

@@ -32,7 +32,7 @@ __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i
 
 // overflow atoms (full buckets): gather straight from the padded fields
 template <int S, bool TAB, int MODE>
-__device__ __forceinline__ void gather_overflow(const int* __restrict__ counts, int nb, const Geom& g, const Pad& pd,
+__device__ __forceinline__ void gather_overflow(const int* __restrict__ novf_ptr, const Geom& g, const Pad& pd,
                                                 const float* __restrict__ ta, const float* __restrict__ td,
                                                 const float* __restrict__ fields, float cscale, void* force,
                                                 bool out_f64, const float4* __restrict__ ovf_rec,
@@ -40,7 +40,7 @@ __device__ __forceinline__ void gather_overflow(const int* __restrict__ counts, 
   constexpr int lo = Stencil<S>::lo;
   const float ihx = (float)g.ihx, ihy = (float)g.ihy, ihz = (float)g.ihz;
   const int64_t mesh = pd.count();
-  const int novf = counts[(int64_t)nb * kCountStride];
+  const int novf = *novf_ptr;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
     const float4 r = ovf_rec[k];
     const int cc = ovf_cell[k];
@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
     const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
     const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,
     float cscale, void* force, bool out_f64, bool sort, const float4* __restrict__ ovf_rec,
-    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm, const int* __restrict__ rstart,
+    const int* __restrict__ novf_res) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
   constexpr int F = MODE == 0 ? 3 : 1;
@@ -132,11 +133,19 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
       mbar_arrive_expect_tx(&bar[buf ^ 1], kBytes);
       tma_load_4d(tiles + (buf ^ 1) * BUF, &fmap, &bar[buf ^ 1], x, y, z, 0);
     }
-    int cnt = counts[(int64_t)b * kCountStride];
-    cnt = cnt < cap ? cnt : cap;
-    const int64_t base = (int64_t)b * cap;
+    int cnt;
+    int64_t base;
+    if (rstart) {  // resident brick-ordered atoms: records at the resident index
+      base = rstart[b];
+      cnt = rstart[b + 1] - rstart[b];
+    } else {
+      cnt = counts[(int64_t)b * kCountStride];
+      cnt = cnt < cap ? cnt : cap;
+      base = (int64_t)b * cap;
+    }
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
-    const int rounds = (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm) : 0;
+    const int rounds =
+        (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm, rstart != nullptr) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
@@ -150,6 +159,7 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
       }
       const float4 r = sort ? s_r[j] : rec[2 * (base + j)];
       const int cc = sort ? s_c[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].x;
+      if (cc < 0) continue;  // resident atom that left the brick: overflow list
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
       rows_f32<S, TAB, MODE == 1>(r.x, ta, td, ax, dx);
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
     }
     __syncthreads();  // tile buffer `buf` and the staging arrays are free again
   }
-  gather_overflow<S, TAB, MODE>(counts, nb, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+  gather_overflow<S, TAB, MODE>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
                                 ovf_perm);
 }
 
@@ -218,7 +228,8 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
     const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
     const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
-    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm, const int* __restrict__ rstart,
+    const int* __restrict__ novf_res) {
   using T = TmaTile<S>;
   using ST = SplitTile<S>;
   constexpr int TXB = T::TXB, DY = ST::DY, FT = ST::FT, lo = Stencil<S>::lo;
@@ -255,10 +266,18 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
       fence_proxy_async_smem();  // generic reads of that buffer (previous brick) before the async-proxy write
       issue(nxt, buf ^ 1);
     }
-    int cnt = counts[(int64_t)b * kCountStride];
-    cnt = cnt < cap ? cnt : cap;
+    int cnt;
+    int64_t base;
+    if (rstart) {
+      base = rstart[b];
+      cnt = rstart[b + 1] - rstart[b];
+    } else {
+      cnt = counts[(int64_t)b * kCountStride];
+      cnt = cnt < cap ? cnt : cap;
+      base = (int64_t)b * cap;
+    }
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
-    if (cnt > 0) stage_banked<true, DY, TXB, T::SH, NT>(rec, nullptr, nullptr, (int64_t)b * cap, cnt, sm);
+    if (cnt > 0) stage_banked<true, DY, TXB, T::SH, NT>(rec, nullptr, nullptr, base, cnt, sm, rstart != nullptr);
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     int seg0 = 0, seg1 = 0, seg2 = 0;
@@ -312,7 +331,7 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
     }
     __syncthreads();  // tile buffer `buf` and the staging arrays are free again
   }
-  gather_overflow<S, TAB, 0>(counts, nb, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+  gather_overflow<S, TAB, 0>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
                              ovf_perm);
 }
 
@@ -329,7 +348,8 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
     const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
     const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
-    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm, const int* __restrict__ rstart,
+    const int* __restrict__ novf_res) {
   using T = TmaTile<S>;
   using ST = SplitTile<S>;
   constexpr int TXB = T::TXB, DY = ST::DY, FT = ST::FT, lo = Stencil<S>::lo;
@@ -368,15 +388,23 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
 #pragma unroll
         for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
       }
-      int cnt = counts[(int64_t)b * kCountStride];
-      cnt = cnt < cap ? cnt : cap;
-      const int64_t base = (int64_t)b * cap;
+      int cnt;
+      int64_t base;
+      if (rstart) {
+        base = rstart[b];
+        cnt = rstart[b + 1] - rstart[b];
+      } else {
+        cnt = counts[(int64_t)b * kCountStride];
+        cnt = cnt < cap ? cnt : cap;
+        base = (int64_t)b * cap;
+      }
       const int4* meta = reinterpret_cast<const int4*>(rec);
       bsize[s][lane] = 0;
       __syncwarp();
       // pass 1: bank histogram
       for (int j = lane; j < cnt; j += 32) {
         const int cc = meta[2 * (base + j) + 1].x;
+        if (cc < 0) continue;  // left the brick (resident mode): overflow list
         const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
         atomicAdd(&bsize[s][((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
       }
@@ -398,8 +426,9 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
       int* sc = s_c + s * cap;
       int* sp = s_p + s * cap;
       for (int j = lane; j < cnt; j += 32) {
-        const float4 r = rec[2 * (base + j)];
         const int4 m = meta[2 * (base + j) + 1];
+        if (m.x < 0) continue;
+        const float4 r = rec[2 * (base + j)];
         const int lx = m.x & (kBrick - 1), ly = (m.x >> 3) & (kBrick - 1), lz = m.x >> 6;
         const int dst = atomicAdd(&cursor[((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
         sr[dst] = r;
@@ -469,7 +498,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
-  gather_overflow<S, TAB, 0>(counts, nb, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+  gather_overflow<S, TAB, 0>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
                              ovf_perm);
 }
 
@@ -478,7 +507,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
                        const int* perm, const int* counts, int cap, const float4* ovf_rec, const int* ovf_cell,
                        const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                        const CUtensorMap& fmap, const float* ta, const float* td, const float* fields, float cscale,
-                       void* force, cudaStream_t s) {
+                       void* force, const int* rstart, const int* novf_res, cudaStream_t s) {
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
@@ -498,7 +527,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
           const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
           k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
-                                  ovf_rec, ovf_cell, ovf_perm);
+                                  ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
           return 0;
         });
       }
@@ -514,7 +543,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
           const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
           k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
-                                  ovf_rec, ovf_cell, ovf_perm);
+                                  ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
           return 0;
         });
       }
@@ -529,7 +558,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
       const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
       k<<<grid, NT, dyn, s>>>(rec, rcell, perm, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force,
-                                    out_f64, variant != GATHER_PLAIN, ovf_rec, ovf_cell, ovf_perm);
+                                    out_f64, variant != GATHER_PLAIN, ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
       return 0;
     });
   });

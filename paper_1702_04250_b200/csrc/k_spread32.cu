@@ -49,18 +49,114 @@ __device__ __forceinline__ void spread_overflow(const int* __restrict__ counts, 
   }
 }
 
+// one atom straight into the padded mesh (global fp32 atomics): overflow atoms
+// and resident atoms that left their brick
+template <int S, bool TAB>
+__device__ __forceinline__ void spread_direct(const float4& r, int cc, const Pad& pd, const float* __restrict__ ta,
+                                              float inv_vcell, float* __restrict__ rho) {
+  constexpr int lo = Stencil<S>::lo;
+  const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
+  float wx[S], wy[S], wz[S], dd[S];
+  rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+  rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+  rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+  const float q = r.w * inv_vcell;
+#pragma unroll
+  for (int a = 0; a < S; ++a) {
+#pragma unroll
+    for (int bb = 0; bb < S; ++bb) {
+      const float p = q * wz[a] * wy[bb];
+      float* row = rho + pd.at(n0 - lo, n1 - lo + bb, n2 - lo + a);
+#pragma unroll
+      for (int c = 0; c < S; ++c) atomicAdd(row + c, p * wx[c]);
+    }
+  }
+}
+
+// resident mode: stage brick b's atoms from their positions (the binning
+// pass folded into make_rho), write their slot records at the resident index
+// for fieldforce, send movers down the direct path; returns the rounds
+template <int S, bool TAB, int D, int TXB, int SH, int NT>
+__device__ __forceinline__ int stage_resident(const Resident& res, int b, int cnt, const Geom& g, const Bricks& bk,
+                                              const Pad& pd, int n_points, const float* __restrict__ ta,
+                                              float inv_vcell, float* __restrict__ rho, float4* __restrict__ rec,
+                                              float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
+                                              int* __restrict__ ovf_perm, BankSmem sm) {
+  constexpr int PER = kCapMax / NT;
+  if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
+  __syncthreads();
+  // pass 1: map positions, write the slot records (fieldforce reads them at
+  // the resident index), bank histogram; only bank / rank stay in registers
+  int rk[PER], bank[PER];
+  const int64_t base = res.start[b];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int j = threadIdx.x + k * NT;
+    bank[k] = -1;
+    if (j < cnt) {
+      const int64_t i = base + j;
+      float4 r;
+      int lc, pk;
+      const int ab = atom_record<S, TAB>(res, i, g, bk, n_points, r, lc, pk);
+      rec[2 * i] = r;
+      if (ab == b) {
+        reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(lc, (int)i, 0, 0);
+        const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
+        bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
+        rk[k] = atomicAdd(sm.bsize + bank[k], 1);
+      } else {
+        reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(-1, (int)i, 0, 0);
+        spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
+        const int o = atomicAdd(res.novf, 1);
+        ovf_rec[o] = r;
+        ovf_cell[o] = pk;
+        ovf_perm[o] = (int)i;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int v = sm.bsize[threadIdx.x];
+    int x = v, m = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (threadIdx.x >= o) x += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    sm.bstart[threadIdx.x] = x - v;
+    if (threadIdx.x == 0) sm.bstart[32] = m;
+  }
+  __syncthreads();
+  // pass 2: the thread's own records back (just written: cache hits) into bank order
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    if (bank[k] >= 0) {
+      const int64_t i = base + threadIdx.x + k * NT;
+      const int dst = sm.bstart[bank[k]] + rk[k];
+      sm.r[dst] = rec[2 * i];
+      sm.c[dst] = reinterpret_cast<const int4*>(rec)[2 * i + 1].x;
+    }
+  }
+  __syncthreads();
+  return sm.bstart[32];
+}
+
 // make_rho, persistent CTAs: bricks b = blockIdx.x, += gridDim.x.  Per brick the
 // int32 fixed-point tile is accumulated with shared atomics, converted to fp32
 // in place and added to the padded mesh with ONE TMA reduce-add of the
 // (TXB, D, D) box at the brick origin - lo (always in bounds: the mesh carries
 // an H-cell halo, folded back periodically by k_halo.cu afterwards).
-template <int S, bool TAB, bool FIX, int NT>
+template <int S, bool TAB, bool FIX, int NT, bool RES>
 __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
-    const __grid_constant__ CUtensorMap rmap, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell) {
+    const __grid_constant__ CUtensorMap rmap, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
+    int* __restrict__ ovf_perm, Resident res, int n_points, float4* __restrict__ rec_out) {
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
+  constexpr bool resident = RES;  // resident brick-ordered atoms (Resident), else binned slots
   // dynamic smem: [tile 0 | tile 1 | staged atoms]; double-buffered tiles (one
   // may still be read by its TMA reduce), 128-byte aligned for the bulk copy
   extern __shared__ __align__(16) unsigned char dyn_raw[];
@@ -70,14 +166,19 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   __shared__ int bsize[32], bstart[33];
   BankSmem sm{s_r, reinterpret_cast<int*>(s_r + cap), nullptr, bsize, bstart};
   const int nb = bk.count();
-  const float qmax = __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
+  const float qmax = resident ? res.qmax : __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
   const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
-    int cnt = counts[(int64_t)b * kCountStride];
-    cnt = cnt < cap ? cnt : cap;
+    int cnt;
+    if (resident) {
+      cnt = res.start[b + 1] - res.start[b];
+    } else {
+      cnt = counts[(int64_t)b * kCountStride];
+      cnt = cnt < cap ? cnt : cap;
+    }
     if (cnt == 0) continue;
     int* tile = tiles0 + (issued & 1) * T::NP;
     float* ftile = reinterpret_cast<float*>(tile);
@@ -98,7 +199,12 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
       scale = ldexpf(1.f, sc);
       inv_scale = ldexpf(1.f, -sc) * inv_vcell;
     }
-    const int rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
+    int rounds;
+    if constexpr (RES)
+      rounds = stage_resident<S, TAB, D, TXB, T::SH, NT>(res, b, cnt, g, bk, pd, n_points, ta, inv_vcell, rho,
+                                                            rec_out, ovf_rec, ovf_cell, ovf_perm, sm);
+    else
+      rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     for (int rr = warp; rr < rounds; rr += nwarp) {
       if (rr >= bsize[lane]) continue;
       const int j = bstart[lane] + rr;
@@ -138,7 +244,22 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     ++issued;
   }
   if (threadIdx.x == 0) bulk_wait_read<0>();
-  spread_overflow<S, TAB>(counts, nb, g, pd, ta, inv_vcell, rho, ovf_rec, ovf_cell);
+  if constexpr (RES) {
+    // atoms that overflowed their bucket at load: direct path, and on the list for fieldforce
+    for (int64_t i = res.start[nb] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < res.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float4 r;
+      int lc, pk;
+      atom_record<S, TAB>(res, i, g, bk, n_points, r, lc, pk);
+      spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
+      const int o = atomicAdd(res.novf, 1);
+      ovf_rec[o] = r;
+      ovf_cell[o] = pk;
+      ovf_perm[o] = (int)i;
+    }
+  } else {
+    spread_overflow<S, TAB>(counts, nb, g, pd, ta, inv_vcell, rho, ovf_rec, ovf_cell);
+  }
 }
 
 
@@ -308,15 +429,16 @@ __global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
 }
 
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
-                        int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
-                        const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, cudaStream_t s) {
+                        int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
+                        const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, const Resident& res,
+                        int n_points, float4* rec_out, cudaStream_t s) {
   if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
-      if (variant == SPREAD_WS) {
+      if (variant == SPREAD_WS && !res.pos) {
         auto k = k_spread_ws<S, TAB>;
         const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + 2 * (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
@@ -333,7 +455,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
         constexpr int NT = kSpreadThreads;
-        auto k = k_spread_tma<S, TAB, FIX, NT>;
+        auto k = res.pos ? k_spread_tma<S, TAB, FIX, NT, true> : k_spread_tma<S, TAB, FIX, NT, false>;
         const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
         int per_sm = 0;
@@ -342,7 +464,8 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
-        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
+        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
+                                ovf_perm, res, n_points, rec_out);
         return 0;
       });
     });

@@ -140,6 +140,11 @@ struct pppm_ctx {
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
+  // resident step without a binning pass: make_rho maps the brick-ordered fp32
+  // positions itself (Resident in pppm_types.h); bstart = per-brick ranges
+  bool res_direct = true;
+  float res_qmax = 0.f;
+  DevBuf res_novf;
   bool sort_resident = true;
   // z-slab decomposition (P > 1): 2D spectra of the local planes, all-to-all
   // buffers, received ghost planes of the charge mesh
@@ -358,7 +363,18 @@ static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int d
   return PPPM_OK;
 }
 
-static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
+static Resident resident_of(pppm_ctx* c) {
+  Resident r;
+  r.pos = c->res_pos.as<float>();
+  r.q = c->res_q.as<float>();
+  r.start = c->bstart.as<int>();
+  r.n = c->n_res;
+  r.qmax = c->res_qmax;
+  r.novf = c->res_novf.as<int>();
+  return r;
+}
+
+static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, bool resident = false) {
   const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
     TRY(launch_spread_fix64(c->order, c->n_points > 0, a, c->g, c->tab.as<double>(), c->n_points,
@@ -366,10 +382,12 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
                             c->err.as<int>(), c->stream));
     c->launches += 4;
   } else {
-    if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
+    if (!c->binned && !resident) return fail(PPPM_ERR_STATE, "atoms not binned");
     TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
-                            c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->g,
-                            c->bk, c->pd, c->rho_map, c->tab.as<float>(), c->rho.as<float>(), c->stream));
+                            c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(),
+                            c->ovf_perm.as<int>(), c->g, c->bk, c->pd, c->rho_map, c->tab.as<float>(),
+                            c->rho.as<float>(), resident ? resident_of(c) : Resident{}, c->n_points,
+                            c->rec.as<float4>(), c->stream));
     c->launches += 1 + fold_launches(c->g, c->pd);  // spread + halo fold
   }
   c->have_rho = true;
@@ -444,7 +462,7 @@ static int run_fft_bwd(pppm_ctx* c) {
 // fieldforce ---------------------------------------------------------------------
 // out: device buffer of (n, 3) fp64 (out_f64) or fp32
 static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, void* out,
-                      bool out_f64) {
+                      bool out_f64, bool resident = false) {
   if (!c->have_fields) return fail(PPPM_ERR_STATE, "no field grids on the device");
   const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
@@ -453,13 +471,15 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     TRY(launch_gather_direct(c->order, c->n_points > 0, c->mode, a, c->g, ta, td, c->n_points,
                              c->fields.as<double>(), c->M, c->cscale, (double*)out, c->err.as<int>(), c->stream));
   } else {
-    if (!c->binned) return fail(PPPM_ERR_STATE, "atoms not binned");
+    if (!c->binned && !resident) return fail(PPPM_ERR_STATE, "atoms not binned");
     const float* ta = c->tab.as<float>();
     const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
     TRY(launch_gather_brick(gather_eff(c), c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
                             c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
-                            c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out, c->stream));
+                            c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
+                            resident ? c->bstart.as<int>() : nullptr, resident ? c->res_novf.as<int>() : nullptr,
+                            c->stream));
   }
   c->launches += 1;
   return PPPM_OK;
@@ -511,9 +531,9 @@ static int do_make_rho(pppm_ctx* c, const void* dpos, const void* dq, int64_t n,
 }
 
 static int do_fieldforce(pppm_ctx* c, const void* dpos, const void* dq, int64_t n, int dtype,
-                         bool rebin, void* out, bool out_f64) {
-  if (!c->fp64() && rebin) TRY(run_bin(c, dpos, dq, n, dtype));
-  return run_gather(c, dpos, dq, n, dtype, out, out_f64);
+                         bool rebin, void* out, bool out_f64, bool resident = false) {
+  if (!c->fp64() && rebin && !resident) TRY(run_bin(c, dpos, dq, n, dtype));
+  return run_gather(c, dpos, dq, n, dtype, out, out_f64, resident);
 }
 
 // ---------------------------------------------------------------------------
@@ -686,6 +706,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_SORT_RESIDENT")) c->sort_resident = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_ZFFT")) c->use_zfft = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
   return PPPM_OK;
@@ -737,7 +758,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
-                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone,
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone, &c->res_novf,
                     &c->pr_cell, &c->pr_count, &c->pr_start, &c->pr_cursor, &c->pr_order, &c->pr_tmp, &c->pr_force,
                     &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal, &c->pr_sp,
                     &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series};
@@ -986,11 +1007,32 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
     std::swap(c->res_pos, c->res_tmp_pos);
     std::swap(c->res_q, c->res_tmp_q);
     c->res_sorted = true;
+    if (dtype == PPPM_F64) {
+      // mixed precision maps fp32-rounded positions anyway: keep fp32 residents
+      TRY(c->res_tmp_pos.ensure(3 * n * sizeof(float)));
+      TRY(c->res_tmp_q.ensure(n * sizeof(float)));
+      TRY(launch_convert(false, c->res_pos.p, c->res_tmp_pos.p, 3 * n, c->stream));
+      TRY(launch_convert(false, c->res_q.p, c->res_tmp_q.p, n, c->stream));
+      std::swap(c->res_pos, c->res_tmp_pos);
+      std::swap(c->res_q, c->res_tmp_q);
+      c->res_dtype = PPPM_F32;
+    }
+    // max |q| of the load-time binning pass (fixed-point scale of make_rho)
+    int qbits = 0;
+    CU(cudaMemcpyAsync(&qbits, c->counts.as<int>() + ((int64_t)c->bk.count() + 1) * kCountStride, sizeof(int),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    memcpy(&c->res_qmax, &qbits, sizeof(float));
+    TRY(c->res_novf.ensure(sizeof(int)));
   }
   CU(cudaStreamSynchronize(c->stream));
   return check_err_flag(c);
 }
 
+
+static bool resident_step(const pppm_ctx* c) {
+  return !c->fp64() && c->res_sorted && c->res_direct && c->res_dtype == PPPM_F32;
+}
 
 static int run_subphase(pppm_ctx* c, int sp) {
   const int64_t n = c->n_res;
@@ -999,15 +1041,21 @@ static int run_subphase(pppm_ctx* c, int sp) {
   switch (sp) {
     case SP_BIN:
       c->binned = false;
+      if (resident_step(c)) {
+        // brick-ordered residents: make_rho maps the positions itself; only the
+        // per-step list of atoms that left their brick is reset
+        CU(cudaMemsetAsync(c->res_novf.p, 0, sizeof(int), c->stream));
+        return PPPM_OK;
+      }
       // sorted resident atoms: slots carry the resident index (forces land in
       // brick order, contiguous per brick) and get_forces un-permutes
       if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, nullptr));
       return PPPM_OK;
-    case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype);
+    case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype, resident_step(c));
     case SP_POISSON:
       return run_poisson(c);
     case SP_GATHER:
-      return do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64());
+      return do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64(), resident_step(c));
   }
   return PPPM_OK;
 }
@@ -1073,6 +1121,32 @@ int pppm_ctx_step(pppm_ctx* c, int phases) {
 
 int pppm_ctx_synchronize(pppm_ctx* c) {
   TRY(activate(c));
+  return check_err_flag(c);
+}
+
+int pppm_ctx_update_positions(pppm_ctx* c, const void* pos, int dtype, int mem) {
+  TRY(activate(c));
+  if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  if (!c->res_sorted || c->res_dtype != PPPM_F32) {
+    // unsorted residents: plain copy in the caller's order
+    const size_t es = c->res_dtype == PPPM_F64 ? 8 : 4;
+    if (dtype != c->res_dtype) return fail(PPPM_ERR_VALUE, "positions dtype differs from the resident atoms");
+    CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * c->n_res * es, mem == PPPM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                                 : cudaMemcpyHostToDevice,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return PPPM_OK;
+  }
+  const void* dp = pos;
+  if (mem == PPPM_HOST) {
+    const size_t es = dtype == PPPM_F64 ? 8 : 4;
+    TRY(c->pos_stage.ensure(3 * c->n_res * es));
+    CU(cudaMemcpyAsync(c->pos_stage.p, pos, 3 * c->n_res * es, cudaMemcpyHostToDevice, c->stream));
+    dp = c->pos_stage.p;
+  }
+  TRY(launch_update_resident(dtype == PPPM_F32, dp, c->res_orig.as<int>(), c->n_res, c->g, c->res_pos.as<float>(),
+                             c->err.as<int>(), c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   return check_err_flag(c);
 }
 

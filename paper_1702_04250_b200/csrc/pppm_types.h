@@ -58,6 +58,15 @@ struct AtomsIn {
   int f32;  // 0: fp64 elements, 1: fp32 elements
 };
 
+struct Resident {
+  const float* pos = nullptr;  // (n, 3) fp32, brick order; nullptr: binned mode
+  const float* q = nullptr;
+  const int* start = nullptr;  // nb + 1
+  int64_t n = 0;
+  float qmax = 0.f;            // max |q| (the fixed-point scale of make_rho)
+  int* novf = nullptr;         // movers this step
+};
+
 // kernel variants (selectable per context for A/B measurement)
 enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1, SPREAD_WS = 3 };  // WS: FIX32, warp-specialized
 enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3 };  // SPLIT, WS: ik only
@@ -99,13 +108,16 @@ int zfft_blocks(int nz, int ncols);
 int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,
                       float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial, unsigned* done,
                       double prefactor, double* energy, cudaStream_t s);
+int launch_update_resident(bool f32, const void* pos, const int* orig, int64_t n, const Geom& g, float* res_pos,
+                           int* err, cudaStream_t s);
 int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
                             void* q_out, int* orig_out, cudaStream_t s);
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
-                        int cap, const float4* ovf_rec, const int* ovf_cell, const Geom& g, const Bricks& bk,
-                        const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad, cudaStream_t s);
+                        int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
+                        const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad,
+                        const Resident& res, int n_points, float4* rec_out, cudaStream_t s);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s);
@@ -113,7 +125,7 @@ int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64
                         const int* rcell, const int* perm, const int* counts, int cap, const float4* ovf_rec,
                         const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                         const CUtensorMap& field_map, const float* ta, const float* td, const float* fields_pad,
-                        float cscale, void* force, cudaStream_t s);
+                        float cscale, void* force, const int* rstart, const int* novf_res, cudaStream_t s);
 // halo handling of the padded fp32 meshes (k_halo.cu)
 int launch_fold_halo(const Geom& g, const Pad& pd, float* rho_pad, cudaStream_t s);
 int launch_fill_halo(const Geom& g, const Pad& pd, float* fields_pad, int nfields, cudaStream_t s);

@@ -529,3 +529,36 @@ def test_kernel_variants_agree(pb, mode):
         assert rel_rms(rho, rho0) <= 1e-5
         assert rel_rms(f, f0) <= 1e-5
     ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["ik", "ad"])
+def test_resident_direct_movers_and_overflow(pb, mode):
+    """Brick-ordered residents (make_rho maps positions itself, no binning
+    pass): same forces / energy as the one-shot binned path, after moving
+    atoms across bricks with update_positions (direct path for movers) and
+    with a dense cluster that overflows its bucket at load."""
+    from paper_1702_04250_b200 import scenarios
+
+    rng = np.random.default_rng(21)
+    n, edge = 40000, 50.0
+    pos, q, lengths = scenarios.random_gas(n, 9, edge)
+    pos[:3000] = 20.0 + rng.uniform(0, 2.0, (3000, 3))      # one overfull brick
+    p32 = scenarios.round_to_f32(pos, lengths)
+    q32 = q.astype(np.float32)
+    ctx = pb.PppmContext((32, 32, 32), lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
+    ref = pb.PppmContext((32, 32, 32), lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
+    ctx.load_atoms(p32, q32)
+    for trial in range(3):
+        for _ in range(2):  # eager, then graph replay
+            ctx.step()
+        ctx.synchronize()
+        f, e = ctx.forces(), ctx.energy()
+        fr, er = ref.compute(p32, q32)
+        assert rel_rms(f, fr) <= 1e-6
+        assert abs(e - er) <= 1e-6 * abs(er)
+        # move every atom by up to ~1.5 mesh cells: many leave their brick
+        p32 = scenarios.round_to_f32(np.mod(p32.astype(np.float64) + rng.uniform(-2.3, 2.3, p32.shape), edge),
+                                     lengths)
+        ctx.update_positions(p32)
+    ctx.close()
+    ref.close()
