@@ -1041,17 +1041,18 @@ static int run_subphase(pppm_ctx* c, int sp) {
   switch (sp) {
     case SP_BIN:
       c->binned = false;
-      if (resident_step(c)) {
-        // brick-ordered residents: make_rho maps the positions itself; only the
-        // per-step list of atoms that left their brick is reset
-        CU(cudaMemsetAsync(c->res_novf.p, 0, sizeof(int), c->stream));
-        return PPPM_OK;
-      }
+      if (resident_step(c)) return PPPM_OK;  // make_rho maps the positions itself
       // sorted resident atoms: slots carry the resident index (forces land in
       // brick order, contiguous per brick) and get_forces un-permutes
       if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, nullptr));
       return PPPM_OK;
-    case SP_SPREAD: return run_spread(c, p, q, n, c->res_dtype, resident_step(c));
+    case SP_SPREAD:
+      if (resident_step(c)) {
+        // reset the per-step list of atoms that left their brick, then make_rho
+        CU(cudaMemsetAsync(c->res_novf.p, 0, sizeof(int), c->stream));
+        return run_spread(c, p, q, n, c->res_dtype, true);
+      }
+      return run_spread(c, p, q, n, c->res_dtype);
     case SP_POISSON:
       return run_poisson(c);
     case SP_GATHER:
@@ -1063,6 +1064,7 @@ static int run_subphase(pppm_ctx* c, int sp) {
 // eager on the first run of a sub-phase, then captured into a CUDA graph and replayed
 static int launch_subphase(pppm_ctx* c, int sp) {
   if (!c->use_graphs) return run_subphase(c, sp);
+  if (sp == SP_BIN && resident_step(c)) return PPPM_OK;  // nothing to launch
   if (c->gexec[sp]) {
     CU(cudaGraphLaunch(c->gexec[sp], c->stream));
     c->launches += c->sp_launches[sp];
