@@ -81,7 +81,8 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
                                               const Pad& pd, int n_points, const float* __restrict__ ta,
                                               float inv_vcell, float* __restrict__ rho, float4* __restrict__ rec,
                                               float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
-                                              int* __restrict__ ovf_perm, BankSmem sm) {
+                                              int* __restrict__ ovf_perm, BankSmem sm, float4* __restrict__ t_r,
+                                              int* __restrict__ t_c) {
   constexpr int PER = kCapMax / NT;
   if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
   __syncthreads();
@@ -101,6 +102,8 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
       rec[2 * i] = r;
       if (ab == b) {
         reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(lc, (int)i, 0, 0);
+        t_r[j] = r;  // unsorted copy in shared memory for pass 2
+        t_c[j] = lc;
         const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
         bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
@@ -129,14 +132,14 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
     if (threadIdx.x == 0) sm.bstart[32] = m;
   }
   __syncthreads();
-  // pass 2: the thread's own records back (just written: cache hits) into bank order
+  // pass 2: the thread's own records (shared-memory copy) into bank order
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     if (bank[k] >= 0) {
-      const int64_t i = base + threadIdx.x + k * NT;
+      const int j = threadIdx.x + k * NT;
       const int dst = sm.bstart[bank[k]] + rk[k];
-      sm.r[dst] = rec[2 * i];
-      sm.c[dst] = reinterpret_cast<const int4*>(rec)[2 * i + 1].x;
+      sm.r[dst] = t_r[j];
+      sm.c[dst] = t_c[j];
     }
   }
   __syncthreads();
@@ -164,7 +167,8 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   int* tiles0 = dyn_i;
   float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
   __shared__ int bsize[32], bstart[33];
-  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + cap), nullptr, bsize, bstart};
+  // staged atoms: s_r[cap] | (resident: t_r[cap]) | s_c[cap] | (resident: t_c[cap])
+  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + (RES ? 2 * cap : cap)), nullptr, bsize, bstart};
   const int nb = bk.count();
   const float qmax = resident ? res.qmax : __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
   const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
@@ -202,7 +206,8 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     int rounds;
     if constexpr (RES)
       rounds = stage_resident<S, TAB, D, TXB, T::SH, NT>(res, b, cnt, g, bk, pd, n_points, ta, inv_vcell, rho,
-                                                            rec_out, ovf_rec, ovf_cell, ovf_perm, sm);
+                                                            rec_out, ovf_rec, ovf_cell, ovf_perm, sm,
+                                                            s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap);
     else
       rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     for (int rr = warp; rr < rounds; rr += nwarp) {
@@ -456,7 +461,8 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         constexpr bool FIX = decltype(F_)::value;
         constexpr int NT = kSpreadThreads;
         auto k = res.pos ? k_spread_tma<S, TAB, FIX, NT, true> : k_spread_tma<S, TAB, FIX, NT, false>;
-        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)cap * (sizeof(float4) + sizeof(int));
+        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) +
+                           (res.pos ? 2 : 1) * (size_t)cap * (sizeof(float4) + sizeof(int));
         allow_smem(k, dyn);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
