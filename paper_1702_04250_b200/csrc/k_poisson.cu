@@ -21,95 +21,15 @@
 // a table built in fp64.
 #include <cuComplex.h>
 
+#include "fft_smem.cuh"
 #include "pppm_device.cuh"
 
 namespace pppm {
 
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-// multiply by -i (forward) or +i (inverse)
-template <bool INV>
-__device__ __forceinline__ float2 rot90(float2 a) {
-  return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
-}
-
-// in-register DFT of R = 2, 4, 8 points (forward: exp(-2 pi i jk / R))
-template <int R, bool INV>
-__device__ __forceinline__ void dft(float2 (&v)[R]) {
-  if constexpr (R == 2) {
-    const float2 a = v[0], b = v[1];
-    v[0] = cadd(a, b);
-    v[1] = csub(a, b);
-  } else if constexpr (R == 4) {
-    const float2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-    const float2 t2 = cadd(v[1], v[3]), t3 = rot90<INV>(csub(v[1], v[3]));
-    v[0] = cadd(t0, t2);
-    v[2] = csub(t0, t2);
-    v[1] = cadd(t1, t3);
-    v[3] = csub(t1, t3);
-  } else {
-    float2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
-    dft<4, INV>(e);
-    dft<4, INV>(o);
-    constexpr float h = 0.70710678118654752f;
-    // w8^k o[k], w8 = exp(-+ 2 pi i / 8)
-    const float2 o1 = INV ? make_float2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
-                          : make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-    const float2 o2 = rot90<INV>(o[2]);
-    const float2 o3 = INV ? make_float2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
-                          : make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-    v[0] = cadd(e[0], o[0]);
-    v[4] = csub(e[0], o[0]);
-    v[1] = cadd(e[1], o1);
-    v[5] = csub(e[1], o1);
-    v[2] = cadd(e[2], o2);
-    v[6] = csub(e[2], o2);
-    v[3] = cadd(e[3], o3);
-    v[7] = csub(e[3], o3);
-  }
-}
-
-// One mixed-radix Stockham autosort pass (natural order in and out) over the
-// T columns of x -> y, then the remaining passes; radix 8 while it divides,
-// then 4 or 2.  W: exp(-2 pi i m / NZ), m < NZ.
-template <int NZ, int T, bool INV, int NS>
-__device__ __forceinline__ float2* fft_pass(float2* x, float2* y, const float2* __restrict__ W) {
-  if constexpr (NS >= NZ) {
-    return x;
-  } else {
-    constexpr int R = (NZ / NS >= 8) ? 8 : NZ / NS;
-    constexpr int L = NZ / R;  // butterflies per column
-    for (int i = threadIdx.x; i < L * T; i += blockDim.x) {
-      const int t = i % T, j = i / T;
-      const int k = j & (NS - 1);
-      float2 v[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = x[(j + r * L) * T + t];
-      if (NS > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          float2 w = W[k * r * (NZ / (NS * R))];
-          if (INV) w.y = -w.y;
-          v[r] = cmul(v[r], w);
-        }
-      }
-      dft<R, INV>(v);
-      const int d = (j - k) * R + k;  // (j / NS) * NS * R + k
-#pragma unroll
-      for (int r = 0; r < R; ++r) y[(d + r * NS) * T + t] = v[r];
-    }
-    __syncthreads();
-    return fft_pass<NZ, T, INV, NS * R>(y, x, W);
-  }
-}
-
+// T columns of NZ points side by side: element (z, t) at [z * T + t]
 template <int NZ, int T, bool INV>
 __device__ __forceinline__ float2* fft_cols(float2* x, float2* y, const float2* __restrict__ W) {
-  return fft_pass<NZ, T, INV, 1>(x, y, W);
+  return fft_batch<NZ, T, 1, T, INV>(x, y, W);
 }
 
 constexpr int kZfftThreads = 256;

@@ -124,6 +124,8 @@ struct pppm_ctx {
   // fused Poisson (fp32, one GPU, power-of-two nz): cuFFT 2D plane transforms
   // around k_zfft_green (z FFTs + Green + energy in one kernel)
   bool use_zfft = true, zfft = false;
+  bool use_plane = true, plane = false;  // own (y, x) plane FFT kernels (k_plane.cu) instead of cuFFT 2D
+  DevBuf ptw;
   // short-range pairs / full force evaluation / NVE (fp64)
   DevBuf pr_cell, pr_count, pr_start, pr_cursor, pr_order, pr_tmp, pr_force, pr_e, pr_cnt, pr_rmin, pr_ij,
       pr_part, pr_pos, pr_q, pr_scal, pr_sp;
@@ -233,6 +235,14 @@ static int ensure_plans(pppm_ctx* c) {
     const size_t ez = sizeof(float2) * (size_t)c->nfields() * c->pd.pz * cplane;
     TRY(c->ework.ensure(ez));
     CU(cudaMemset(c->ework.p, 0, ez));
+    c->plane = c->use_plane && plane_supported(c->g.nx, c->g.ny);
+    if (c->plane) {
+      const int ntw = c->g.nx / 2 + c->g.ny + c->g.nx / 2 + 1;
+      std::vector<float> ptw(2 * ntw);
+      plane_twiddles(c->g.nx, c->g.ny, ptw.data());
+      TRY(c->ptw.ensure(sizeof(float) * 2 * ntw));
+      CU(cudaMemcpy(c->ptw.p, ptw.data(), sizeof(float) * 2 * ntw, cudaMemcpyHostToDevice));
+    }
     TRY(c->ztw.ensure(sizeof(float) * 2 * nz));
     TRY(c->zdone.ensure(sizeof(unsigned)));
     TRY(c->partial.ensure(8 * std::max<int64_t>(kGreenBlocks, zfft_blocks(nz, c->g.ny * c->nxh))));
@@ -424,16 +434,28 @@ static int run_poisson_fused(pppm_ctx* c) {
   const double vol = c->g.lx * c->g.ly * c->g.lz;
   const double vcell = vol / (double)c->M;
   const double pref = c->cscale * vcell * vcell / (2.0 * vol);
-  FFT(cufftExecR2C(c->fwd2, c->rho.as<float>() + c->pd.interior(), c->rho_hat.as<cufftComplex>()));
+  if (c->plane)
+    TRY(launch_plane_r2c(c->g.nx, c->g.ny, c->g.nz, c->rho.as<float>(), c->pd, c->rho_hat.as<float2>(),
+                         c->ptw.as<float2>(), c->stream));
+  else
+    FFT(cufftExecR2C(c->fwd2, c->rho.as<float>() + c->pd.interior(), c->rho_hat.as<cufftComplex>()));
   // spectra out as [f][pz][ny][nx/2+1] (interior planes at H..H+nz-1)
   TRY(launch_zfft_green(c->mode, c->g.nz, c->g.ny, c->g.nx, c->rho_hat.as<float2>(), c->green.as<float>(),
                         c->ikc.as<float>(), (float)(1.0 / (double)c->M), c->ztw.as<float2>(),
                         c->ework.as<float2>() + (int64_t)c->pd.H * c->g.ny * c->nxh,
                         (int64_t)c->pd.pz * c->g.ny * c->nxh, c->partial.as<double>(), c->zdone.as<unsigned>(), pref,
                         c->scal.as<double>(), c->stream));
-  FFT(cufftExecC2R(c->bwd2, c->ework.as<cufftComplex>(), c->fields.as<float>() + (int64_t)c->pd.H * c->pd.px + c->pd.hx));
-  TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), c->nfields(), c->stream));
-  c->launches += 2;
+  if (c->plane) {
+    // plane C2R kernels write the x / y / z halos themselves
+    TRY(launch_plane_c2r(c->g.nx, c->g.ny, c->g.nz, c->nfields(), c->ework.as<float2>(), c->pd,
+                         c->fields.as<float>(), c->ptw.as<float2>(), c->stream));
+    c->launches += 3;
+  } else {
+    FFT(cufftExecC2R(c->bwd2, c->ework.as<cufftComplex>(),
+                     c->fields.as<float>() + (int64_t)c->pd.H * c->pd.px + c->pd.hx));
+    TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), c->nfields(), c->stream));
+    c->launches += 2;
+  }
   c->have_fields = true;
   return PPPM_OK;
 }
@@ -706,6 +728,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_SORT_RESIDENT")) c->sort_resident = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_ZFFT")) c->use_zfft = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_PLANE")) c->use_plane = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
@@ -758,7 +781,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
-                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone, &c->res_novf,
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone, &c->res_novf, &c->ptw,
                     &c->pr_cell, &c->pr_count, &c->pr_start, &c->pr_cursor, &c->pr_order, &c->pr_tmp, &c->pr_force,
                     &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal, &c->pr_sp,
                     &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series};

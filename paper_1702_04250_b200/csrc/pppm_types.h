@@ -103,6 +103,12 @@ int launch_drift(double* x, const double* v, double dt, double lx, double ly, do
 int launch_series_row(const double* v, const double* m, int64_t n, double* tmp4, double* partial, double* row,
                       const double* e_pair, const double* e_kspace, const double* e_self, cudaStream_t s);
 bool zfft_supported(int nz);
+bool plane_supported(int nx, int ny);
+void plane_twiddles(int nx, int ny, float* out);
+int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, float2* spec, const float2* tw,
+                     cudaStream_t s);
+int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, const Pad& pd, float* fields,
+                     const float2* tw, cudaStream_t s);
 int fold_launches(const Geom& g, const Pad& p);
 int zfft_blocks(int nz, int ncols);
 int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,
