@@ -562,3 +562,29 @@ def test_resident_direct_movers_and_overflow(pb, mode):
         ctx.update_positions(p32)
     ctx.close()
     ref.close()
+
+
+@pytest.mark.parametrize("dims,order", [((64, 32, 16), 5), ((16, 128, 32), 3), ((128, 16, 64), 7),
+                                        ((32, 32, 256), 4), ((48, 64, 32), 5)])
+def test_mixed_fused_poisson_shapes(pb, dims, order):
+    """The fused Poisson path on non-cubic power-of-two meshes (own plane FFT
+    kernels for nx != ny, the z kernel at several nz, the cuFFT 2D fallback for
+    nx = 48) against the oracle: rho, fields-driven forces and energy."""
+    from paper_1702_04250_b200.scenarios import round_to_f32
+
+    rng = np.random.default_rng(sum(dims))
+    lengths = np.array(dims, dtype=np.float64) * 0.7
+    n = 3000
+    pos = rng.uniform(0, 1, (n, 3)) * lengths
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    p32 = round_to_f32(pos, lengths)
+    for mode in ("ik", "ad"):
+        ctx = pb.PppmContext(dims, lengths, order=order, mode=mode, precision="mixed", alpha=0.5)
+        ctx.load_atoms(p32, q.astype(np.float32))
+        ctx.step()
+        ctx.synchronize()
+        forces, energy = ctx.forces(), ctx.energy()
+        ctx.close()
+        f_ref, e_ref, _ = orc.pppm_step(p32.astype(np.float64), q, lengths, dims, order, 0.5, mode)
+        assert rel_rms(forces, f_ref) <= MIXED_TOL, (dims, order, mode)
+        assert abs(energy - e_ref) <= MIXED_TOL * abs(e_ref), (dims, order, mode)
