@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--order", type=int, default=None, help="override the config's stencil order (config 4 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-slab", action="store_true",
+                    help="run the z-slab (NCCL) path even at one rank (torchrun --nproc-per-node 1): a smoke test")
     return ap.parse_args()
 
 
@@ -64,7 +66,7 @@ def dist_setup(n_gpus, backend="gloo"):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
-    if world > 1:
+    if world > 1 or (backend == "nccl" and "WORLD_SIZE" in os.environ):
         import torch
         import torch.distributed as dist
 
@@ -323,11 +325,13 @@ def run_slabs(args, cfg, rank, local, world, pg):
     sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
     smem_peak = 148 * 128 * sm_clk / 1e9
     S3 = cfg.order ** 3
-    smem_alg = {"spread": n * S3 * 4, "gather": n * S3 * 4 * (nf if mode == "ik" else 1)}
+    nf = 3 if mode == "ik" else 1
+    # rank 0's slab: its atoms and its make_rho (incl. ghost exchange) / fieldforce times
+    smem_alg = {"spread": n_local * S3 * 4, "gather": n_local * S3 * 4 * nf}
     onchip = {"bound": "smem", "unit": "GB/s", "peak": smem_peak,
-              "peak_basis": "148 SMs x 128 B/clk x measured SM clock"}
-    for key in ("spread", "gather"):
-        t = ms[key] / 1e3 / k
+              "peak_basis": "148 SMs x 128 B/clk x measured SM clock (rank 0)"}
+    for key, tt in (("spread", t_mr), ("gather", t_ff)):
+        t = tt / k
         onchip[key] = {"alg_bytes": smem_alg[key], "achieved": smem_alg[key] / t / 1e9,
                        "frac": smem_alg[key] / t / 1e9 / smem_peak}
     line = {
@@ -344,7 +348,7 @@ def run_slabs(args, cfg, rank, local, world, pg):
         "whole_step_atom_steps_per_s": n_total * k / t_step_max,
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": None, "kernel": "make_rho+fieldforce per GPU (rank 0)", "peak_kind": peak_kind},
-        "clocks": clocks, "gpu_launches": int(cnt1.value - cnt0.value), "wall_s_timed_region": t_wall,
+        "onchip_roofline": onchip, "clocks": clocks, "gpu_launches": int(cnt1.value - cnt0.value), "wall_s_timed_region": t_wall,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -362,7 +366,7 @@ def main():
 
         cfg = dataclasses.replace(cfg, order=args.order)
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
-    ours_multi = args.impl == "ours" and world_env > 1
+    ours_multi = args.impl == "ours" and (world_env > 1 or (args.force_slab and "WORLD_SIZE" in os.environ))
     rank, local, world, pg = dist_setup(args.gpus, backend="nccl" if ours_multi else "gloo")
     if args.impl == "reference":
         run_reference(args, cfg, rank, pg)

@@ -148,9 +148,10 @@ struct pppm_ctx {
   float res_qmax = 0.f;
   DevBuf res_novf;
   bool sort_resident = true;
-  // z-slab decomposition (P > 1): 2D spectra of the local planes, all-to-all
+  // z-slab decomposition (slab contexts): 2D spectra of the local planes, all-to-all
   // buffers, received ghost planes of the charge mesh
   int P = 1, rank = 0;
+  bool slab = false;  // created by pppm_ctx_create_slab (ghost planes, exchange buffers), even for P = 1
   DevBuf spec2d, a2a_send, a2a_recv, ghost_lo, ghost_hi;
   cufftHandle p2f = 0, pz = 0, p2b = 0;
   bool slab_plans = false;
@@ -211,7 +212,7 @@ static int ensure_plans(pppm_ctx* c) {
                     d ? CUFFT_Z2D : CUFFT_C2R, c->nfields()));
   FFT(cufftSetStream(c->fwd, c->stream));
   FFT(cufftSetStream(c->bwd, c->stream));
-  c->zfft = c->use_zfft && !d && c->P == 1 && zfft_supported(c->g.nz);
+  c->zfft = c->use_zfft && !d && !c->slab && zfft_supported(c->g.nz);
   if (c->zfft) {
     // (y, x) plane transforms batched over z; k_zfft_green does z
     int n2[2] = {c->g.ny, c->g.nx};
@@ -621,7 +622,7 @@ int pppm_table_rows(int device, int order, int n_points, double* assign, double*
 
 static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
                       int order, int mode, int precision, double alpha, double coulomb_constant,
-                      double dielectric, int P, int rank) {
+                      double dielectric, int P, int rank, bool slab) {
   if (!out) return fail(PPPM_ERR_VALUE, "null output pointer");
   *out = nullptr;
   if (order < 3 || order > 7) return fail(PPPM_ERR_CONFIG, "stencil order must be one of (3, 4, 5, 6, 7)");
@@ -634,7 +635,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (!(alpha > 0.0)) return fail(PPPM_ERR_CONFIG, "alpha must be positive");
   if (!(dielectric > 0.0)) return fail(PPPM_ERR_CONFIG, "dielectric must be positive");
   if (P < 1 || rank < 0 || rank >= P) return fail(PPPM_ERR_VALUE, "bad slab rank / count");
-  if (P > 1) {
+  if (slab) {
     if (precision != PPPM_PREC_MIXED) return fail(PPPM_ERR_CONFIG, "z-slab decomposition runs in mixed precision");
     if (nz % P || ny % P) return fail(PPPM_ERR_CONFIG, "nz and ny must be divisible by the slab count");
     const int lo = (order - 1) / 2, hi = order - 1 - lo;
@@ -644,6 +645,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   pppm_ctx* c = new pppm_ctx();
   c->P = P;
   c->rank = rank;
+  c->slab = slab;
   c->device = device;
   c->g.nx = nx; c->g.ny = ny; c->g.nz = nz;
   c->g.lx = lx; c->g.ly = ly; c->g.lz = lz;
@@ -666,7 +668,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   } else {
     const int lo = (order - 1) / 2, hi = order - 1 - lo, H = lo > hi ? lo : hi;
     const int hx = (H + 1) / 2 * 2;  // must match TmaTile<S>::HX
-    c->pd = Pad{H, (hx + nx + H + 3) / 4 * 4, ny + 2 * H, c->g.nzl + 2 * H, hx, P == 1};
+    c->pd = Pad{H, (hx + nx + H + 3) / 4 * 4, ny + 2 * H, c->g.nzl + 2 * H, hx, !slab};
   }
   c->nxh = nx / 2 + 1;
   c->half = (int64_t)c->nxh * c->g.nyl * nz;  // this context's spectrum (ky chunk on a slab)
@@ -689,7 +691,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
     st = encode_maps(c);
   }
   if (st == PPPM_OK) st = c->green.ensure(rs * c->half);
-  if (st == PPPM_OK && P > 1) {
+  if (st == PPPM_OK && slab) {
     const int64_t nh = c->half * c->nfields();
     const int64_t gb = (int64_t)c->pd.H * c->pd.py * c->pd.px;
     st = c->spec2d.ensure(cs * nh);
@@ -739,14 +741,14 @@ int pppm_ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double l
                     int order, int mode, int precision, double alpha, double coulomb_constant,
                     double dielectric) {
   return ctx_create(out, device, nx, ny, nz, lx, ly, lz, order, mode, precision, alpha, coulomb_constant,
-                    dielectric, 1, 0);
+                    dielectric, 1, 0, false);
 }
 
 int pppm_ctx_create_slab(pppm_ctx** out, int device, int nx, int ny, int nz, double lx, double ly, double lz,
                          int order, int mode, int precision, double alpha, double coulomb_constant,
                          double dielectric, int nslabs, int rank) {
   return ctx_create(out, device, nx, ny, nz, lx, ly, lz, order, mode, precision, alpha, coulomb_constant,
-                    dielectric, nslabs, rank);
+                    dielectric, nslabs, rank, true);
 }
 
 int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
@@ -1016,7 +1018,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   c->n_res = n;
   c->res_dtype = dtype;
   c->res_sorted = false;
-  if (!c->fp64() && c->sort_resident && c->g.nzl == c->g.nz) {  // single-mesh contexts only
+  if (!c->fp64() && c->sort_resident && !c->slab) {  // single-mesh contexts only
     // keep the resident atoms in brick order (as an MD engine sorts its atoms):
     // bin once, then gather positions / charges into bucket order
     TRY(run_bin(c, c->res_pos.p, c->res_q.p, n, dtype, nullptr));
@@ -1309,7 +1311,7 @@ int pppm_slab_buffer(pppm_ctx* c, int id, int field, void** ptr, size_t* bytes) 
     case PPPM_BUF_FIELD_GHOST_HI: *ptr = fl + plane * (c->pd.H + c->g.nzl); *bytes = gb; break;
     default: return fail(PPPM_ERR_VALUE, "unknown slab buffer id");
   }
-  if (c->P == 1) return fail(PPPM_ERR_STATE, "not a slab context");
+  if (!c->slab) return fail(PPPM_ERR_STATE, "not a slab context");
   return PPPM_OK;
 }
 

@@ -21,7 +21,7 @@ def pb():
     return pb
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [1, 2, 4])
 @pytest.mark.parametrize("mode", ["ik", "ad"])
 @pytest.mark.parametrize("order", [5, 4, 7])
 def test_loopback_slabs_vs_oracle(pb, P, mode, order):
