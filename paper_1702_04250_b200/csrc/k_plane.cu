@@ -81,11 +81,12 @@ __global__ void __launch_bounds__(kPlaneThreads) k_plane_r2c(const float* __rest
   for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) out[i] = R[i];
 }
 
-// field f's spectrum plane z: (f * pz + H + z) * NY * RS in `spec`; writes the
-// padded field plane with its x / y halo, and the periodic z-halo copy
+// field f's spectrum plane z: (f * spec_fplanes + spec_z0 + z) * NY * RS in
+// `spec`; writes the padded field plane with its x / y halo and, when the z
+// halo is periodic (one GPU), the periodic z-halo copy
 template <int NX, int NY>
-__global__ void __launch_bounds__(kPlaneThreads) k_plane_c2r(const float2* __restrict__ spec, Pad pd, int nz,
-                                                            float* __restrict__ fields,
+__global__ void __launch_bounds__(kPlaneThreads) k_plane_c2r(const float2* __restrict__ spec, int64_t spec_fplanes,
+                                                            int spec_z0, Pad pd, int nz, float* __restrict__ fields,
                                                             const float2* __restrict__ tw) {
   using P = PlaneDims<NX, NY>;
   constexpr int M = P::M, RS = P::RS;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kPlaneThreads) k_plane_c2r(const float2* __res
   load_twiddles<NX, NY>(tw, Wr);
   const int z = blockIdx.x % nz, f = blockIdx.x / nz;
   const int H = pd.H;
-  const float2* in = spec + ((int64_t)f * pd.pz + H + z) * NY * RS;
+  const float2* in = spec + ((int64_t)f * spec_fplanes + spec_z0 + z) * NY * RS;
   for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) A[i] = in[i];
   __syncthreads();
   float2* X = fft_batch<NY, RS, 1, RS, true>(A, B, Wc);
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kPlaneThreads) k_plane_c2r(const float2* __res
   const int ex = NX + 2 * H, ey = NY + 2 * H;
   // interior plane and, near a z face, its periodic image in the z halo
   const int zi = H + z;
-  const int zh = z < H ? H + z + nz : (z >= nz - H ? H + z - nz : -1);
+  const int zh = !pd.zper ? -1 : (z < H ? H + z + nz : (z >= nz - H ? H + z - nz : -1));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   for (int yy = warp; yy < ey; yy += nwarp) {
     int sy = yy - H;
@@ -195,14 +196,14 @@ int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, fl
   return st ? st : launch_status();
 }
 
-int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, const Pad& pd, float* fields,
-                     const float2* tw, cudaStream_t s) {
+int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, int64_t spec_fplanes, int spec_z0,
+                     const Pad& pd, float* fields, const float2* tw, cudaStream_t s) {
   int st = with_plane(nx, ny, [&](auto NX_, auto NY_) -> int {
     constexpr int NX = decltype(NX_)::value, NY = decltype(NY_)::value;
     auto k = k_plane_c2r<NX, NY>;
     constexpr size_t dyn = PlaneDims<NX, NY>::smem;
     if (dyn > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k<<<nz * nfields, kPlaneThreads, dyn, s>>>(spec, pd, nz, fields, tw);
+    k<<<nz * nfields, kPlaneThreads, dyn, s>>>(spec, spec_fplanes, spec_z0, pd, nz, fields, tw);
     return 0;
   });
   return st ? st : launch_status();

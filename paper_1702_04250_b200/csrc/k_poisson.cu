@@ -146,11 +146,13 @@ int zfft_blocks(int nz, int ncols) {
   return (ncols + t - 1) / t;
 }
 
-int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,
-                      float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial, unsigned* done,
-                      double prefactor, double* energy, cudaStream_t s) {
-  const int nxh = nx / 2 + 1, ncols = ny * nxh;
-  const float *ikx = ik, *iky = ik + nx, *ikz = ik + nx + ny;
+// ny_full, y0, nyl: the spectrum holds ky rows [y0, y0 + nyl) (the transposed
+// chunk of a z-slab; y0 = 0, nyl = ny_full on one GPU); ik = (nx, ny_full, nz) vectors
+int launch_zfft_green(int mode, int nz, int ny_full, int y0, int nyl, int nx, const float2* spec, const float* green,
+                      const float* ik, float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial,
+                      unsigned* done, double prefactor, double* energy, cudaStream_t s) {
+  const int nxh = nx / 2 + 1, ncols = nyl * nxh;
+  const float *ikx = ik, *iky = ik + nx + y0, *ikz = ik + nx + ny_full;
   auto go = [&](auto NZ_, auto MODE_) -> int {
     constexpr int NZ = decltype(NZ_)::value;
     constexpr int MODE = decltype(MODE_)::value;

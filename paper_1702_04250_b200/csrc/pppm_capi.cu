@@ -441,14 +441,14 @@ static int run_poisson_fused(pppm_ctx* c) {
   else
     FFT(cufftExecR2C(c->fwd2, c->rho.as<float>() + c->pd.interior(), c->rho_hat.as<cufftComplex>()));
   // spectra out as [f][pz][ny][nx/2+1] (interior planes at H..H+nz-1)
-  TRY(launch_zfft_green(c->mode, c->g.nz, c->g.ny, c->g.nx, c->rho_hat.as<float2>(), c->green.as<float>(),
-                        c->ikc.as<float>(), (float)(1.0 / (double)c->M), c->ztw.as<float2>(),
+  TRY(launch_zfft_green(c->mode, c->g.nz, c->g.ny, 0, c->g.ny, c->g.nx, c->rho_hat.as<float2>(),
+                        c->green.as<float>(), c->ikc.as<float>(), (float)(1.0 / (double)c->M), c->ztw.as<float2>(),
                         c->ework.as<float2>() + (int64_t)c->pd.H * c->g.ny * c->nxh,
                         (int64_t)c->pd.pz * c->g.ny * c->nxh, c->partial.as<double>(), c->zdone.as<unsigned>(), pref,
                         c->scal.as<double>(), c->stream));
   if (c->plane) {
     // plane C2R kernels write the x / y / z halos themselves
-    TRY(launch_plane_c2r(c->g.nx, c->g.ny, c->g.nz, c->nfields(), c->ework.as<float2>(), c->pd,
+    TRY(launch_plane_c2r(c->g.nx, c->g.ny, c->g.nz, c->nfields(), c->ework.as<float2>(), c->pd.pz, c->pd.H, c->pd,
                          c->fields.as<float>(), c->ptw.as<float2>(), c->stream));
     c->launches += 3;
   } else {
@@ -1266,6 +1266,31 @@ static int ensure_slab_plans(pppm_ctx* c) {
   FFT(cufftSetStream(c->p2f, c->stream));
   FFT(cufftSetStream(c->p2b, c->stream));
   FFT(cufftSetStream(c->pz, c->stream));
+  // own kernels where the mesh allows: plane FFTs of the local planes, the
+  // fused z FFT / Green kernel on the transposed ky chunk
+  c->plane = c->use_plane && plane_supported(nx, ny);
+  c->zfft = c->use_zfft && zfft_supported(c->g.nz);
+  if (c->plane) {
+    const int ntw = nx / 2 + ny + nx / 2 + 1;
+    std::vector<float> ptw(2 * ntw);
+    plane_twiddles(nx, ny, ptw.data());
+    TRY(c->ptw.ensure(sizeof(float) * 2 * ntw));
+    CU(cudaMemcpy(c->ptw.p, ptw.data(), sizeof(float) * 2 * ntw, cudaMemcpyHostToDevice));
+  }
+  if (c->zfft) {
+    const int nz = c->g.nz;
+    std::vector<float> tw(2 * nz);
+    for (int m = 0; m < nz; ++m) {
+      const double a = -2.0 * M_PI * m / nz;
+      tw[2 * m] = (float)cos(a);
+      tw[2 * m + 1] = (float)sin(a);
+    }
+    TRY(c->ztw.ensure(sizeof(float) * 2 * nz));
+    TRY(c->zdone.ensure(sizeof(unsigned)));
+    TRY(c->partial.ensure(8 * std::max<int64_t>(kGreenBlocks, zfft_blocks(nz, c->g.nyl * nxh))));
+    CU(cudaMemcpy(c->ztw.p, tw.data(), sizeof(float) * 2 * nz, cudaMemcpyHostToDevice));
+    CU(cudaMemset(c->zdone.p, 0, sizeof(unsigned)));
+  }
   c->slab_plans = true;
   return PPPM_OK;
 }
@@ -1341,7 +1366,11 @@ int pppm_slab_add_ghosts(pppm_ctx* c) {
 int pppm_slab_fft_fwd(pppm_ctx* c) {
   TRY(activate(c));
   TRY(ensure_slab_plans(c));
-  FFT(cufftExecR2C(c->p2f, c->rho.as<float>() + c->pd.interior(), c->spec2d.as<cufftComplex>()));
+  if (c->plane)
+    TRY(launch_plane_r2c(c->g.nx, c->g.ny, c->g.nzl, c->rho.as<float>(), c->pd, c->spec2d.as<float2>(),
+                         c->ptw.as<float2>(), c->stream));
+  else
+    FFT(cufftExecR2C(c->p2f, c->rho.as<float>() + c->pd.interior(), c->spec2d.as<cufftComplex>()));
   TRY(launch_pack_fwd(c->g, c->P, c->spec2d.p, c->a2a_send.p, c->stream));
   c->launches += 1;
   return PPPM_OK;
@@ -1355,14 +1384,23 @@ int pppm_slab_green(pppm_ctx* c) {
   TRY(ensure_slab_plans(c));
   if (!c->have_green) return fail(PPPM_ERR_STATE, "influence function not built");
   cufftComplex* spec = c->a2a_recv.as<cufftComplex>();
-  FFT(cufftExecC2C(c->pz, spec, spec, CUFFT_FORWARD));
   const double vol = c->g.lx * c->g.ly * c->g.lz;
   const double vcell = vol / (double)c->M;
   const double pref = c->cscale * vcell * vcell / (2.0 * vol);
-  TRY(launch_green(false, c->mode, true, spec, c->green.p, c->g, c->ikc.p, 1.0 / (double)c->M, c->ework.p,
-                   c->partial.as<double>(), pref, c->scal.as<double>(), c->stream));
-  cufftComplex* ew = c->ework.as<cufftComplex>();
-  for (int f = 0; f < c->nfields(); ++f) FFT(cufftExecC2C(c->pz, ew + f * c->half, ew + f * c->half, CUFFT_INVERSE));
+  if (c->zfft) {
+    // z FFTs + Green / ik + energy partial + inverse z FFTs in one kernel
+    TRY(launch_zfft_green(c->mode, c->g.nz, c->g.ny, c->g.y0, c->g.nyl, c->g.nx, c->a2a_recv.as<float2>(),
+                          c->green.as<float>(), c->ikc.as<float>(), (float)(1.0 / (double)c->M), c->ztw.as<float2>(),
+                          c->ework.as<float2>(), c->half, c->partial.as<double>(), c->zdone.as<unsigned>(), pref,
+                          c->scal.as<double>(), c->stream));
+  } else {
+    FFT(cufftExecC2C(c->pz, spec, spec, CUFFT_FORWARD));
+    TRY(launch_green(false, c->mode, true, spec, c->green.p, c->g, c->ikc.p, 1.0 / (double)c->M, c->ework.p,
+                     c->partial.as<double>(), pref, c->scal.as<double>(), c->stream));
+    cufftComplex* ew = c->ework.as<cufftComplex>();
+    for (int f = 0; f < c->nfields(); ++f)
+      FFT(cufftExecC2C(c->pz, ew + f * c->half, ew + f * c->half, CUFFT_INVERSE));
+  }
   TRY(launch_pack_bwd(c->g, c->P, c->nfields(), c->ework.p, c->a2a_send.p, c->stream));
   c->launches += 3;
   return PPPM_OK;
@@ -1377,10 +1415,16 @@ int pppm_slab_fft_bwd(pppm_ctx* c) {
   const int nf = c->nfields();
   TRY(launch_unpack_bwd(c->g, c->P, nf, c->a2a_recv.p, c->spec2d.p, c->stream));
   const int64_t spec_f = (int64_t)c->g.nzl * c->g.ny * c->nxh;
-  for (int f = 0; f < nf; ++f)
-    FFT(cufftExecC2R(c->p2b, c->spec2d.as<cufftComplex>() + f * spec_f,
-                     c->fields.as<float>() + f * c->pd.count() + c->pd.interior()));
-  TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), nf, c->stream));
+  if (c->plane) {
+    // plane C2R writes the x / y halo (the z ghosts come from the neighbours)
+    TRY(launch_plane_c2r(c->g.nx, c->g.ny, c->g.nzl, nf, c->spec2d.as<float2>(), c->g.nzl, 0, c->pd,
+                         c->fields.as<float>(), c->ptw.as<float2>(), c->stream));
+  } else {
+    for (int f = 0; f < nf; ++f)
+      FFT(cufftExecC2R(c->p2b, c->spec2d.as<cufftComplex>() + f * spec_f,
+                       c->fields.as<float>() + f * c->pd.count() + c->pd.interior()));
+    TRY(launch_fill_halo(c->g, c->pd, c->fields.as<float>(), nf, c->stream));
+  }
   c->launches += 2;
   c->have_fields = true;
   return PPPM_OK;

@@ -107,13 +107,13 @@ bool plane_supported(int nx, int ny);
 void plane_twiddles(int nx, int ny, float* out);
 int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, float2* spec, const float2* tw,
                      cudaStream_t s);
-int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, const Pad& pd, float* fields,
-                     const float2* tw, cudaStream_t s);
+int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, int64_t spec_fplanes, int spec_z0,
+                     const Pad& pd, float* fields, const float2* tw, cudaStream_t s);
 int fold_launches(const Geom& g, const Pad& p);
 int zfft_blocks(int nz, int ncols);
-int launch_zfft_green(int mode, int nz, int ny, int nx, const float2* spec, const float* green, const float* ik,
-                      float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial, unsigned* done,
-                      double prefactor, double* energy, cudaStream_t s);
+int launch_zfft_green(int mode, int nz, int ny_full, int y0, int nyl, int nx, const float2* spec, const float* green,
+                      const float* ik, float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial,
+                      unsigned* done, double prefactor, double* energy, cudaStream_t s);
 int launch_update_resident(bool f32, const void* pos, const int* orig, int64_t n, const Geom& g, float* res_pos,
                            int* err, cudaStream_t s);
 int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
