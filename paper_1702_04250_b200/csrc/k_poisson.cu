@@ -47,24 +47,40 @@ __global__ void __launch_bounds__(kZfftThreads) k_zfft_green(
   float2* W = P + (MODE == 0 ? NZ * T : 0);  // [NZ]
   const int c0 = blockIdx.x * T;
   for (int i = threadIdx.x; i < NZ; i += blockDim.x) W[i] = tw[i];
-  for (int i = threadIdx.x; i < NZ * T; i += blockDim.x) {
-    const int z = i / T, c = c0 + i % T;
-    A[i] = c < ncols ? spec[(int64_t)z * ncols + c] : make_float2(0.f, 0.f);
+  // the thread's elements i = threadIdx.x + u * kZfftThreads: spectrum into
+  // shared memory, influence values into registers (their load latency then
+  // overlaps the forward FFT instead of stalling the multiply)
+  constexpr int PER = (NZ * T + kZfftThreads - 1) / kZfftThreads;
+  float gv[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = threadIdx.x + u * kZfftThreads;
+    gv[u] = 0.f;
+    if (i < NZ * T) {
+      const int z = i / T, c = c0 + i % T;
+      const bool ok = c < ncols;
+      A[i] = ok ? spec[(int64_t)z * ncols + c] : make_float2(0.f, 0.f);
+      if (ok) gv[u] = green[(int64_t)z * ncols + c];
+    }
   }
   __syncthreads();
   float2* X = fft_cols<NZ, T, false>(A, B, W);
   float2* Y = X == A ? B : A;
   // Green multiply + energy (rho_hat in X, phi -> X and P)
   double e = 0.0;
-  for (int i = threadIdx.x; i < NZ * T; i += blockDim.x) {
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = threadIdx.x + u * kZfftThreads;
+    if (i >= NZ * T) continue;
     const int z = i / T, c = c0 + i % T;
     if (c >= ncols) {
       X[i] = make_float2(0.f, 0.f);
       if (MODE == 0) P[i] = X[i];
       continue;
     }
+    (void)z;
     const int kx = c % nxh;
-    const float g = green[(int64_t)z * ncols + c];
+    const float g = gv[u];
     const float2 r = X[i];
     const double wgt = (kx == 0 || (nx % 2 == 0 && kx == nx / 2)) ? 1.0 : 2.0;
     e += wgt * (double)g * ((double)r.x * r.x + (double)r.y * r.y);
