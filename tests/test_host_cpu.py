@@ -66,6 +66,11 @@ def test_status_mapping(lib):
         _native.check(_native.ERR_VALUE)
     with pytest.raises(RuntimeError):
         _native.check(_native.ERR_CUDA)
+    from paper_1702_04250_b200.model import SingularityError
+
+    with pytest.raises(SingularityError) as ei:
+        _native.check(_native.ERR_SINGULAR)
+    assert isinstance(ei.value.pair, tuple)
     _native.check(_native.OK)
 
 
@@ -147,7 +152,21 @@ def test_install_rebinds_reference_names():
         assert pppm.driver.map_charge is pb.map_charge
         assert pppm.gridmap.distribute_force_ad is pb.distribute_force_ad
         assert pppm.kspace.kspace_energy is pb.kspace_energy
+        # the force driver either side of the path
+        assert "compute_forces" in names and "pair_forces" in names
+        assert pppm.compute_forces is pb.compute_forces
+        assert pppm.driver.integrate_nve is pb.integrate_nve
+        assert pppm.shortrange.pair_forces is pb.pair_forces
+        from paper_1702_04250_b200 import _native, _runtime
+
+        assert _native.ERRORS.singular is pppm.model.SingularityError
+        assert _runtime.types().EnergyBreakdown is pppm.model.EnergyBreakdown
         pb.uninstall()
         assert pppm.driver.map_charge is orig
+        assert pppm.driver.compute_forces is not pb.compute_forces
+        assert _native.ERRORS.singular is None
+        mesh_only = pb.install(pppm, force_driver=False)
+        assert "compute_forces" not in mesh_only and pppm.driver.compute_forces is not pb.compute_forces
+        pb.uninstall()
     finally:
         sys.path.remove("/root/reference/pkg/src")
