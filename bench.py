@@ -219,9 +219,13 @@ def run_reference(args, cfg, rank, pg):
     mode = args.mode or cfg.mode
     pos, q, lengths = cfg.build()
     cores = len(os.sched_getaffinity(0))
-    sample = 16384
     for _ in range(max(args.warmup, 0)):
         cpu_sample_rate(pos, q, lengths, cfg.dims, cfg.order, mode, 4096, cores)
+    # each timed step: as many atoms of the workload as ~2 min / steps allows
+    # (the whole config when it fits), so per-call overheads do not dominate
+    cal, _ = cpu_sample_rate(pos, q, lengths, cfg.dims, cfg.order, mode, 65536, cores)
+    budget = 120.0 / max(args.steps, 1)
+    sample = int(min(pos.shape[0], max(16384, cal * budget)))
     times = []
     for s in range(args.steps):
         _, t = cpu_sample_rate(pos, q, lengths, cfg.dims, cfg.order, mode, sample, cores)
