@@ -98,8 +98,9 @@ __global__ void k_reorder_resident(const float4* __restrict__ rec, const int* __
       int c = counts[(int64_t)b * kCountStride];
       c = c < cap ? c : cap;
       if (s >= c) continue;
-      dst = start[b] + s;
-      i = reinterpret_cast<const int4*>(rec)[2 * k + 1].y;
+      const int4 m = reinterpret_cast<const int4*>(rec)[2 * k + 1];
+      dst = start[b] + m.z;  // cell-order rank within the bucket (k_rank_cells)
+      i = m.y;
     } else {
       const int o = (int)(k - slots);
       dst = bucketed + o;
@@ -110,6 +111,30 @@ __global__ void k_reorder_resident(const float4* __restrict__ rec, const int* __
     pos_out[3 * dst + 2] = pos[3 * i + 2];
     q_out[dst] = q[i];
     orig_out[dst] = (int)i;
+  }
+}
+
+// Within each bucket, the stable rank of every slot by brick-local cell
+// (z-major, then y, then x; ties in slot order) -> int4 .z of the slot record.
+// The resident order then runs in cell order inside each brick, so 32
+// consecutive atoms cover ~one z layer (the tensor-core fieldforce epilogue
+// reads only the z rows a warp needs).  Deterministic (no atomics).
+__global__ void k_rank_cells(float4* __restrict__ rec, const int* __restrict__ counts, int cap) {
+  __shared__ int key[kCapMax];
+  const int b = blockIdx.x;
+  int cnt = counts[(int64_t)b * kCountStride];
+  cnt = cnt < cap ? cnt : cap;
+  int4* meta = reinterpret_cast<int4*>(rec) + 2 * (int64_t)b * cap + 1;
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) key[j] = meta[2 * j].x;
+  __syncthreads();
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    const int kj = key[j];
+    int r = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const int ki = key[i];
+      r += (ki < kj) || (ki == kj && i < j);
+    }
+    meta[2 * j].z = r;
   }
 }
 
@@ -155,6 +180,7 @@ int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* r
                             void* q_out, int* orig_out, cudaStream_t s) {
   const int nb = bk.count();
   k_scan_buckets<<<1, 1024, 0, s>>>(counts, nb, cap, start);
+  k_rank_cells<<<nb, kThreads, 0, s>>>(const_cast<float4*>(rec), counts, cap);
   const int grid = grid_for((int64_t)nb * cap + n);
   if (f32)
     k_reorder_resident<float><<<grid, kThreads, 0, s>>>(rec, counts, start, nb, cap, ovf_perm, (const float*)pos,

@@ -257,6 +257,10 @@ static int ensure_plans(pppm_ctx* c) {
 // gather kernel actually used: the split (per-component) fieldforce needs ik
 // and a TXB of 12 or 20 mod 32, otherwise the bank-sorted one
 static int gather_eff(const pppm_ctx* c) {
+  if (c->gather_variant == GATHER_MMA) {
+    if (c->mode == 0 && gather_mma_ok(c->order)) return GATHER_MMA;
+    return gather_split_ok(c->order, c->pd.hx) && c->mode == 0 ? GATHER_WS : GATHER_SORTED;
+  }
   if ((c->gather_variant == GATHER_SPLIT || c->gather_variant == GATHER_WS) &&
       !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
     return GATHER_SORTED;
@@ -297,7 +301,9 @@ static int encode_maps(pppm_ctx* c) {
     cuuint64_t strides[3] = {row, plane, vol};
     // split gather: one component per box, two extra rows (row shift per component)
     const bool split = gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS;
-    cuuint32_t box[4] = {(cuuint32_t)txb, (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
+    // tensor-core gather: all fields, 16-float rows starting at the brick's lowest stencil node
+    const bool mma = gather_eff(c) == GATHER_MMA;
+    cuuint32_t box[4] = {(cuuint32_t)(mma ? 16 : txb), (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
                          (cuuint32_t)(split ? 1 : c->nfields())};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(&c->field_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->fields.p, dims, strides, box, es,
@@ -497,6 +503,13 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     if (!c->binned && !resident) return fail(PPPM_ERR_STATE, "atoms not binned");
     const float* ta = c->tab.as<float>();
     const float* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
+    if (gather_eff(c) == GATHER_MMA)
+      TRY(launch_gather_mma(c->order, c->n_points > 0, out_f64, c->rec.as<float4>(), c->counts.as<int>(), c->cap,
+                            c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
+                            c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
+                            resident ? c->bstart.as<int>() : nullptr, resident ? c->res_novf.as<int>() : nullptr,
+                            c->stream));
+    else
     TRY(launch_gather_brick(gather_eff(c), c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
                             c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
@@ -755,7 +768,7 @@ int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
   drop_graphs(c);
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
-  else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_WS)
+  else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_MMA)
     c->gather_variant = variant;
   else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
   if (!c->fp64() && c->fields.p) TRY(encode_maps(c));

@@ -69,7 +69,7 @@ struct Resident {
 
 // kernel variants (selectable per context for A/B measurement)
 enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1, SPREAD_WS = 3 };  // WS: FIX32, warp-specialized
-enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3 };  // SPLIT, WS: ik only
+enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3, GATHER_MMA = 4 };  // SPLIT, WS, MMA: ik only
 // field tiles of the split gather: rows shifted per component (TXB = 12 or 20 mod 32)
 inline bool gather_split_ok(int order, int hx) {
   const int D = 8 + order - 1, lo = (order - 1) / 2;
@@ -132,6 +132,13 @@ int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64
                         const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                         const CUtensorMap& field_map, const float* ta, const float* td, const float* fields_pad,
                         float cscale, void* force, const int* rstart, const int* novf_res, cudaStream_t s);
+// fieldforce_ik on the tensor cores (k_gather_mma.cu): orders whose 3 field tiles fit TMEM
+bool gather_mma_ok(int order);
+int launch_gather_mma(int order, bool tab, bool out_f64, const float4* rec, const int* counts, int cap,
+                      const float4* ovf_rec, const int* ovf_cell, const int* ovf_perm, const Geom& g,
+                      const Bricks& bk, const Pad& pd, const CUtensorMap& fmap, const float* ta, const float* td,
+                      const float* fields, float cscale, void* force, const int* rstart, const int* novf_res,
+                      cudaStream_t s);
 // halo handling of the padded fp32 meshes (k_halo.cu)
 int launch_fold_halo(const Geom& g, const Pad& pd, float* rho_pad, cudaStream_t s);
 int launch_fill_halo(const Geom& g, const Pad& pd, float* fields_pad, int nfields, cudaStream_t s);
