@@ -341,10 +341,29 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
 // rounds; two stage slots handed over with mbarriers (full: staged + tile
 // bytes landed; empty: every consumer warp done), so no block-wide barrier and
 // no exposed record-load latency.  Same tasks / numerics as k_gather_split.
-constexpr int kWsConsumerWarps = 8;
+#ifndef PPPM_WS_CW
+#define PPPM_WS_CW 8
+#endif
+#ifndef PPPM_WS_PW
+#define PPPM_WS_PW 1
+#endif
+constexpr int kWsConsumerWarps = PPPM_WS_CW, kWsProducerWarps = PPPM_WS_PW;
+// A/B probe only (wrong forces): x loads per stencil row in k_gather_ws
+#ifndef PPPM_WS_XL
+#define PPPM_WS_XL 99
+#endif
+template <int S> constexpr int kWsXl = PPPM_WS_XL < S ? PPPM_WS_XL : S;
+// producer staging: records loaded per batch (memory round trips per brick)
+#ifndef PPPM_WS_U1
+#define PPPM_WS_U1 8
+#endif
+#ifndef PPPM_WS_U2
+#define PPPM_WS_U2 4
+#endif
+constexpr int kWsU1 = PPPM_WS_U1, kWsU2 = PPPM_WS_U2;
 
 template <int S, bool TAB>
-__global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
+__global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3) k_gather_ws(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
     const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
     const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
@@ -367,20 +386,26 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
   const int nb = bk.count();
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kWsProducerWarps);
       mbar_init(&tmaf[s], 1);
       mbar_init(&empty[s], NCW);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0) {
+  constexpr int NPW = kWsProducerWarps;
+  const int pt = threadIdx.x;  // producer thread (warps 0 .. NPW-1)
+  auto pbar = [&]() {
+    if (NPW > 1) asm volatile("bar.sync 1, %0;" ::"n"(NPW * 32) : "memory");
+    else __syncwarp();
+  };
+  if (warp < NPW) {
     // ---------------- producer
     int k = 0;
     for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
       const int s = k & 1, use = k >> 1;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
-      if (lane == 0) {
+      if (pt == 0) {
         const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
         const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
         fence_proxy_async_smem();
@@ -399,17 +424,25 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
         base = (int64_t)b * cap;
       }
       const int4* meta = reinterpret_cast<const int4*>(rec);
-      bsize[s][lane] = 0;
-      __syncwarp();
-      // pass 1: bank histogram
-      for (int j = lane; j < cnt; j += 32) {
-        const int cc = meta[2 * (base + j) + 1].x;
-        if (cc < 0) continue;  // left the brick (resident mode): overflow list
-        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
-        atomicAdd(&bsize[s][((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
+      if (warp == 0) bsize[s][lane] = 0;
+      pbar();
+      // pass 1: bank histogram (loads batched: one memory round trip per kWsU1 x 32 records)
+      for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsU1) {
+        int cc[kWsU1];
+#pragma unroll
+        for (int u = 0; u < kWsU1; ++u) {
+          const int j = j0 + u * 32 * NPW + pt;
+          cc[u] = j < cnt ? __ldg(&meta[2 * (base + j) + 1].x) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kWsU1; ++u) {
+          if (cc[u] < 0) continue;  // left the brick (resident mode): overflow list
+          const int lx = cc[u] & (kBrick - 1), ly = (cc[u] >> 3) & (kBrick - 1), lz = cc[u] >> 6;
+          atomicAdd(&bsize[s][((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
+        }
       }
-      __syncwarp();
-      {
+      pbar();
+      if (warp == 0) {
         const int v = bsize[s][lane];
         int x = v;
 #pragma unroll
@@ -420,27 +453,39 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
         bstart[s][lane] = x - v;
         cursor[lane] = x - v;
       }
-      __syncwarp();
+      pbar();
       // pass 2: scatter into bank order
       float4* sr = s_r + s * cap;
       int* sc = s_c + s * cap;
       int* sp = s_p + s * cap;
-      for (int j = lane; j < cnt; j += 32) {
-        const int4 m = meta[2 * (base + j) + 1];
-        if (m.x < 0) continue;
-        const float4 r = rec[2 * (base + j)];
-        const int lx = m.x & (kBrick - 1), ly = (m.x >> 3) & (kBrick - 1), lz = m.x >> 6;
-        const int dst = atomicAdd(&cursor[((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
-        sr[dst] = r;
-        sc[dst] = m.x;
-        sp[dst] = m.y;
+      for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsU2) {
+        int4 m[kWsU2];
+        float4 r[kWsU2];
+#pragma unroll
+        for (int u = 0; u < kWsU2; ++u) {
+          const int j = j0 + u * 32 * NPW + pt;
+          m[u].x = -1;
+          if (j < cnt) {
+            m[u] = __ldg(&meta[2 * (base + j) + 1]);
+            r[u] = __ldg(&rec[2 * (base + j)]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kWsU2; ++u) {
+          if (m[u].x < 0) continue;
+          const int lx = m[u].x & (kBrick - 1), ly = (m[u].x >> 3) & (kBrick - 1), lz = m[u].x >> 6;
+          const int dst = atomicAdd(&cursor[((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
+          sr[dst] = r[u];
+          sc[dst] = m[u].x;
+          sp[dst] = m[u].y;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
     }
   } else {
     // ---------------- consumers
-    const int cw = warp - 1;
+    const int cw = warp - NPW;
     int k = 0;
     for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
       const int s = k & 1, ph = (k >> 1) & 1;
@@ -484,7 +529,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
             const float* row = tf + (a * DY + bb) * TXB;
             float e = 0.f;
 #pragma unroll
-            for (int c = 0; c < S; ++c) e = fmaf(ax[c], row[c], e);
+            for (int c = 0; c < kWsXl<S>; ++c) e = fmaf(ax[c], row[c], e);
             ra = fmaf(ay[bb], e, ra);
           }
           acc = fmaf(az[a], ra, acc);
@@ -502,9 +547,299 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + 1), 3) k_gather_ws(
                              ovf_perm);
 }
 
+// fieldforce_ik, warp-specialized split variant with x-adjacent atom pairs:
+// two atoms in the same (y, z) cell row whose cells are 0 or 1 apart in x
+// (consecutive in the cell-ordered resident records) share one task per
+// component: each stencil row is loaded once as 6 values (instead of 5 + 5)
+// and feeds both atoms' x sums - ~29% fewer shared-memory loads per atom at
+// 0.5 atoms / cell.  Singles and pairs are bank-bucketed separately and run as
+// two round sets.  Same per-atom arithmetic (and bitwise the same forces) as
+// k_gather_ws.
+template <int S, bool TAB>
+__global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3) k_gather_wsp(
+    const float4* __restrict__ rec, const int* __restrict__ counts, int cap, int scap, Geom g, Bricks bk, Pad pd,
+    const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
+    const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
+    const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm, const int* __restrict__ rstart,
+    const int* __restrict__ novf_res) {
+  using T = TmaTile<S>;
+  using ST = SplitTile<S>;
+  constexpr int TXB = T::TXB, DY = ST::DY, FT = ST::FT, lo = Stencil<S>::lo;
+  constexpr int BUF = 3 * FT;
+  constexpr int NCW = kWsConsumerWarps, NPW = kWsProducerWarps;
+  constexpr uint32_t kBytes = 3u * ST::FTN * sizeof(float);
+  const int hcap = (scap + 1) / 2;
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  float* tiles = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][BUF]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);  // [2][scap]   task atom (A)
+  float4* s_r2 = s_r + 2 * scap;                             // [2][hcap]   pair partner (B)
+  int* s_c = reinterpret_cast<int*>(s_r2 + 2 * hcap);        // [2][scap]   cell | dx << 9
+  int* s_p = s_c + 2 * scap;                                 // [2][scap]
+  int* s_p2 = s_p + 2 * scap;                                // [2][hcap]
+  __shared__ __align__(8) uint64_t full[2], tmaf[2], empty[2];
+  __shared__ int bsize[2][2][32], bstart[2][2][32], cursor[2][32], nsingle[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = bk.count();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], NPW);
+      mbar_init(&tmaf[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int pt = threadIdx.x;
+  auto pbar = [&]() {
+    if (NPW > 1) asm volatile("bar.sync 1, %0;" ::"n"(NPW * 32) : "memory");
+    else __syncwarp();
+  };
+  auto bank_of = [&](int cc) {
+    const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+    return ((lz * DY + ly) * TXB + lx + T::SH) & 31;
+  };
+  // pairing of the warp's 32 consecutive records: 1 = single, 2 = pair head, 0 = tail / none
+  auto classify = [&](int cc) {
+    const int nx = __shfl_down_sync(0xffffffffu, cc, 1);
+    const int ddx = (nx & 7) - (cc & 7);
+    const bool link = lane < 31 && cc >= 0 && nx >= 0 && (nx >> 3) == (cc >> 3) && ddx >= 0 && ddx <= 1;
+    const unsigned L = __ballot_sync(0xffffffffu, link);
+    const unsigned below = L & ((1u << lane) - 1u);
+    const unsigned zeros = ~below & ((1u << lane) - 1u);
+    const int off = zeros ? lane - 1 - (31 - __clz(zeros)) : lane;  // links in a row right below this lane
+    const bool head = link && !(off & 1);
+    const unsigned H = __ballot_sync(0xffffffffu, head);
+    const bool tail = lane > 0 && ((H >> (lane - 1)) & 1u);
+    return head ? 2 : ((cc >= 0 && !tail) ? 1 : 0);
+  };
+  if (warp < NPW) {
+    // ---------------- producers
+    int k = 0;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
+      const int s = k & 1, use = k >> 1;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      if (pt == 0) {
+        const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+        const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&tmaf[s], kBytes);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+      }
+      int cnt;
+      int64_t base;
+      if (rstart) {
+        base = rstart[b];
+        cnt = rstart[b + 1] - rstart[b];
+      } else {
+        cnt = counts[(int64_t)b * kCountStride];
+        cnt = cnt < cap ? cnt : cap;
+        base = (int64_t)b * cap;
+      }
+      const int4* meta = reinterpret_cast<const int4*>(rec);
+      if (warp == 0) {
+        bsize[s][0][lane] = 0;
+        bsize[s][1][lane] = 0;
+      }
+      pbar();
+      // pass 1: bank histograms of single and pair tasks
+      for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsU1) {
+        int cc[kWsU1];
+#pragma unroll
+        for (int u = 0; u < kWsU1; ++u) {
+          const int j = j0 + u * 32 * NPW + pt;
+          cc[u] = j < cnt ? __ldg(&meta[2 * (base + j) + 1].x) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kWsU1; ++u) {
+          const int kind = classify(cc[u]);
+          if (kind) atomicAdd(&bsize[s][kind - 1][bank_of(cc[u])], 1);
+        }
+      }
+      pbar();
+      if (warp == 0) {
+        const int v0 = bsize[s][0][lane], v1 = bsize[s][1][lane];
+        int x0 = v0, x1 = v1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+          if (lane >= o) {
+            x0 += y0;
+            x1 += y1;
+          }
+        }
+        const int ns = __shfl_sync(0xffffffffu, x0, 31);
+        bstart[s][0][lane] = x0 - v0;
+        bstart[s][1][lane] = ns + x1 - v1;
+        cursor[0][lane] = x0 - v0;
+        cursor[1][lane] = ns + x1 - v1;
+        if (lane == 0) nsingle[s] = ns;
+      }
+      pbar();
+      // pass 2: scatter the tasks into bank order (pair partner from the next lane)
+      float4* sr = s_r + s * scap;
+      float4* sr2 = s_r2 + s * hcap;
+      int* sc = s_c + s * scap;
+      int* sp = s_p + s * scap;
+      int* sp2 = s_p2 + s * hcap;
+      const int ns = nsingle[s];
+      for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsU2) {
+        int4 m[kWsU2];
+        float4 r[kWsU2];
+#pragma unroll
+        for (int u = 0; u < kWsU2; ++u) {
+          const int j = j0 + u * 32 * NPW + pt;
+          m[u] = make_int4(-1, 0, 0, 0);
+          r[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j < cnt) {
+            m[u] = __ldg(&meta[2 * (base + j) + 1]);
+            r[u] = __ldg(&rec[2 * (base + j)]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kWsU2; ++u) {
+          const int kind = classify(m[u].x);
+          float4 rb;
+          rb.x = __shfl_down_sync(0xffffffffu, r[u].x, 1);
+          rb.y = __shfl_down_sync(0xffffffffu, r[u].y, 1);
+          rb.z = __shfl_down_sync(0xffffffffu, r[u].z, 1);
+          rb.w = __shfl_down_sync(0xffffffffu, r[u].w, 1);
+          const int cb = __shfl_down_sync(0xffffffffu, m[u].x, 1);
+          const int pb = __shfl_down_sync(0xffffffffu, m[u].y, 1);
+          if (!kind) continue;
+          const int dst = atomicAdd(&cursor[kind - 1][bank_of(m[u].x)], 1);
+          sr[dst] = r[u];
+          sp[dst] = m[u].y;
+          if (kind == 2) {
+            sc[dst] = m[u].x | (((cb & 7) - (m[u].x & 7)) << 9);
+            sr2[dst - ns] = rb;
+            sp2[dst - ns] = pb;
+          } else {
+            sc[dst] = m[u].x;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else {
+    // ---------------- consumers
+    const int cw = warp - NPW;
+    int k = 0;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
+      const int s = k & 1, ph = (k >> 1) & 1;
+      mbar_wait(&full[s], ph);
+      mbar_wait(&tmaf[s], ph);
+      const float* tile = tiles + s * BUF;
+      const float4* sr = s_r + s * scap;
+      const float4* sr2 = s_r2 + s * hcap;
+      const int* sc = s_c + s * scap;
+      const int* sp = s_p + s * scap;
+      const int* sp2 = s_p2 + s * hcap;
+      const int ns = nsingle[s];
+#pragma unroll 1
+      for (int kind = 0; kind < 2; ++kind) {
+        const int seg0 = bsize[s][kind][lane], seg1 = bsize[s][kind][(lane - TXB) & 31],
+                  seg2 = bsize[s][kind][(lane - 2 * TXB) & 31];
+        const int tot = seg0 + seg1 + seg2;
+        int trounds = tot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) trounds = max(trounds, __shfl_xor_sync(0xffffffffu, trounds, o));
+        for (int rr = cw; rr < trounds; rr += NCW) {
+          if (rr >= tot) continue;
+          int f = 0, rk = rr;
+          if (rk >= seg0) {
+            rk -= seg0;
+            f = 1;
+            if (rk >= seg1) {
+              rk -= seg1;
+              f = 2;
+            }
+          }
+          const int j = bstart[s][kind][(lane - f * TXB) & 31] + rk;
+          const float4 r = sr[j];
+          const int cc = sc[j];
+          const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = (cc >> 6) & (kBrick - 1);
+          float ax[S], ay[S], az[S], dd[S];
+          rows_f32<S, TAB, false>(r.x, ta, td, ax, dd);
+          rows_f32<S, TAB, false>(r.y, ta, td, ay, dd);
+          rows_f32<S, TAB, false>(r.z, ta, td, az, dd);
+          const float* tf = tile + f * FT + (lz * DY + ly + f) * TXB + lx + T::SH;
+          if (kind == 0) {
+            float acc = 0.f;
+#pragma unroll
+            for (int a = 0; a < S; ++a) {
+              float ra = 0.f;
+#pragma unroll
+              for (int bb = 0; bb < S; ++bb) {
+                const float* row = tf + (a * DY + bb) * TXB;
+                float e = 0.f;
+#pragma unroll
+                for (int c = 0; c < S; ++c) e = fmaf(ax[c], row[c], e);
+                ra = fmaf(ay[bb], e, ra);
+              }
+              acc = fmaf(az[a], ra, acc);
+            }
+            const float v = cscale * r.w * acc;
+            const int64_t i = sp[j];
+            if (out_f64) static_cast<double*>(force)[3 * i + f] = v;
+            else static_cast<float*>(force)[3 * i + f] = v;
+          } else {
+            const int dx = cc >> 9;  // 0 or 1: partner's cell offset in x
+            const float4 r2 = sr2[j - ns];
+            float bx[S], by[S], bz[S];
+            rows_f32<S, TAB, false>(r2.x, ta, td, bx, dd);
+            rows_f32<S, TAB, false>(r2.y, ta, td, by, dd);
+            rows_f32<S, TAB, false>(r2.z, ta, td, bz, dd);
+            // partner's x weights over the 6 loaded values (its stencil starts dx cells right)
+            float b6[S + 1];
+#pragma unroll
+            for (int c = 0; c <= S; ++c) b6[c] = dx ? (c > 0 ? bx[c - 1] : 0.f) : (c < S ? bx[c] : 0.f);
+            float acc = 0.f, acc2 = 0.f;
+#pragma unroll
+            for (int a = 0; a < S; ++a) {
+              float ra = 0.f, ra2 = 0.f;
+#pragma unroll
+              for (int bb = 0; bb < S; ++bb) {
+                const float* row = tf + (a * DY + bb) * TXB;
+                float v[S + 1];
+#pragma unroll
+                for (int c = 0; c < S; ++c) v[c] = row[c];
+                v[S] = row[S - 1 + dx];  // in the row for dx = 1; a harmless re-read (weight 0) for dx = 0
+                float e = 0.f, e2 = 0.f;
+#pragma unroll
+                for (int c = 0; c < S; ++c) e = fmaf(ax[c], v[c], e);
+#pragma unroll
+                for (int c = 0; c <= S; ++c) e2 = fmaf(b6[c], v[c], e2);
+                ra = fmaf(ay[bb], e, ra);
+                ra2 = fmaf(by[bb], e2, ra2);
+              }
+              acc = fmaf(az[a], ra, acc);
+              acc2 = fmaf(bz[a], ra2, acc2);
+            }
+            const float v = cscale * r.w * acc, v2 = cscale * r2.w * acc2;
+            const int64_t i = sp[j], i2 = sp2[j - ns];
+            if (out_f64) {
+              static_cast<double*>(force)[3 * i + f] = v;
+              static_cast<double*>(force)[3 * i2 + f] = v2;
+            } else {
+              static_cast<float*>(force)[3 * i + f] = v;
+              static_cast<float*>(force)[3 * i2 + f] = v2;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  gather_overflow<S, TAB, 0>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale,
+                             force, out_f64, ovf_rec, ovf_cell, ovf_perm);
+}
+
 template <int MODE>
 int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const float4* rec, const int* rcell,
-                       const int* perm, const int* counts, int cap, const float4* ovf_rec, const int* ovf_cell,
+                       const int* perm, const int* counts, int cap, int scap, const float4* ovf_rec, const int* ovf_cell,
                        const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                        const CUtensorMap& fmap, const float* ta, const float* td, const float* fields, float cscale,
                        void* force, const int* rstart, const int* novf_res, cudaStream_t s) {
@@ -515,6 +850,24 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if constexpr (MODE == 0 && SplitTile<S>::ok) {
+      if (variant == GATHER_WSP) {
+        const int hc = (scap + 1) / 2;
+        const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
+                           2 * (size_t)scap * (sizeof(float4) + 2 * sizeof(int)) +
+                           2 * (size_t)hc * (sizeof(float4) + sizeof(int));
+        return with_bool(tab, [&](auto T_) -> int {
+          constexpr bool TAB = decltype(T_)::value;
+          auto k = k_gather_wsp<S, TAB>;
+          allow_smem(k, dyn);
+          constexpr int NT = 32 * (kWsConsumerWarps + kWsProducerWarps);
+          int per_sm = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
+          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          k<<<grid, NT, dyn, s>>>(rec, counts, cap, scap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
+                                  ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+          return 0;
+        });
+      }
       if (variant == GATHER_WS) {
         const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
                            2 * (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
@@ -522,7 +875,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
           constexpr bool TAB = decltype(T_)::value;
           auto k = k_gather_ws<S, TAB>;
           allow_smem(k, dyn);
-          constexpr int NT = 32 * (kWsConsumerWarps + 1);
+          constexpr int NT = 32 * (kWsConsumerWarps + kWsProducerWarps);
           int per_sm = 0;
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
           const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));

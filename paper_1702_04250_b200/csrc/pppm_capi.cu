@@ -142,6 +142,7 @@ struct pppm_ctx {
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
+  int res_maxcnt = 0;       // largest resident brick (staging capacity of the resident fieldforce)
   // resident step without a binning pass: make_rho maps the brick-ordered fp32
   // positions itself (Resident in pppm_types.h); bstart = per-brick ranges
   bool res_direct = true;
@@ -261,7 +262,7 @@ static int gather_eff(const pppm_ctx* c) {
     if (c->mode == 0 && gather_mma_ok(c->order)) return GATHER_MMA;
     return gather_split_ok(c->order, c->pd.hx) && c->mode == 0 ? GATHER_WS : GATHER_SORTED;
   }
-  if ((c->gather_variant == GATHER_SPLIT || c->gather_variant == GATHER_WS) &&
+  if ((c->gather_variant == GATHER_SPLIT || c->gather_variant == GATHER_WS || c->gather_variant == GATHER_WSP) &&
       !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
     return GATHER_SORTED;
   return c->gather_variant;
@@ -300,7 +301,7 @@ static int encode_maps(pppm_ctx* c) {
                           (cuuint64_t)c->nfields()};
     cuuint64_t strides[3] = {row, plane, vol};
     // split gather: one component per box, two extra rows (row shift per component)
-    const bool split = gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS;
+    const bool split = gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS || gather_eff(c) == GATHER_WSP;
     // tensor-core gather: all fields, 16-float rows starting at the brick's lowest stencil node
     const bool mma = gather_eff(c) == GATHER_MMA;
     cuuint32_t box[4] = {(cuuint32_t)(mma ? 16 : txb), (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
@@ -512,6 +513,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     else
     TRY(launch_gather_brick(gather_eff(c), c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
+                            resident && c->res_maxcnt > 0 ? std::min(c->res_maxcnt, c->cap) : c->cap,
                             c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
                             c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
                             resident ? c->bstart.as<int>() : nullptr, resident ? c->res_novf.as<int>() : nullptr,
@@ -768,7 +770,7 @@ int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
   drop_graphs(c);
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
-  else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_MMA)
+  else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_WSP)
     c->gather_variant = variant;
   else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
   if (!c->fp64() && c->fields.p) TRY(encode_maps(c));
@@ -1031,6 +1033,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   c->n_res = n;
   c->res_dtype = dtype;
   c->res_sorted = false;
+  c->res_maxcnt = 0;
   if (!c->fp64() && c->sort_resident && !c->slab) {  // single-mesh contexts only
     // keep the resident atoms in brick order (as an MD engine sorts its atoms):
     // bin once, then gather positions / charges into bucket order
@@ -1062,6 +1065,11 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
     CU(cudaStreamSynchronize(c->stream));
     memcpy(&c->res_qmax, &qbits, sizeof(float));
     TRY(c->res_novf.ensure(sizeof(int)));
+    // largest resident brick: shared-memory staging capacity of the resident fieldforce
+    std::vector<int> st(c->bk.count() + 1);
+    CU(cudaMemcpy(st.data(), c->bstart.as<int>(), sizeof(int) * st.size(), cudaMemcpyDeviceToHost));
+    c->res_maxcnt = 1;
+    for (int b = 0; b < c->bk.count(); ++b) c->res_maxcnt = std::max(c->res_maxcnt, st[b + 1] - st[b]);
   }
   CU(cudaStreamSynchronize(c->stream));
   return check_err_flag(c);

@@ -69,7 +69,7 @@ struct Resident {
 
 // kernel variants (selectable per context for A/B measurement)
 enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1, SPREAD_WS = 3 };  // WS: FIX32, warp-specialized
-enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3, GATHER_MMA = 4 };  // SPLIT, WS, MMA: ik only
+enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3, GATHER_MMA = 4, GATHER_WSP = 5 };  // SPLIT, WS, MMA, WSP: ik only
 // field tiles of the split gather: rows shifted per component (TXB = 12 or 20 mod 32)
 inline bool gather_split_ok(int order, int hx) {
   const int D = 8 + order - 1, lo = (order - 1) / 2;
@@ -128,7 +128,7 @@ int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const 
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s);
 int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64, const float4* rec,
-                        const int* rcell, const int* perm, const int* counts, int cap, const float4* ovf_rec,
+                        const int* rcell, const int* perm, const int* counts, int cap, int scap, const float4* ovf_rec,
                         const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                         const CUtensorMap& field_map, const float* ta, const float* td, const float* fields_pad,
                         float cscale, void* force, const int* rstart, const int* novf_res, cudaStream_t s);

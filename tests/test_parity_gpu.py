@@ -521,7 +521,7 @@ def test_kernel_variants_agree(pb, mode):
     ctx.step()
     ctx.synchronize()
     rho0, f0 = ctx.rho(), ctx.forces()
-    for kernel, variant in ((0, 3), (1, 4), (1, 1), (1, 2), (1, 0), (0, 0)):
+    for kernel, variant in ((0, 3), (1, 4), (1, 5), (1, 1), (1, 2), (1, 0), (0, 0)):
         ctx.ctx("pppm_ctx_set_variant", kernel, variant)
         ctx.step()
         ctx.synchronize()
