@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   int* s_c = reinterpret_cast<int*>(s_r + 2 * cap);          // [2][cap]
   int* s_p = s_c + 2 * cap;                                  // [2][cap]
   __shared__ __align__(8) uint64_t full[2], tmaf[2], empty[2];
-  __shared__ int bsize[2][32], bstart[2][32], cursor[32];
+  __shared__ int bsize[2][32], bstart[2][32], cursor[32], sbrick[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = bk.count();
   if (threadIdx.x == 0) {
@@ -402,9 +402,28 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   if (warp < NPW) {
     // ---------------- producer
     int k = 0;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
+    for (int b = blockIdx.x;; b += gridDim.x, ++k) {
       const int s = k & 1, use = k >> 1;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      if (bk.sched) {  // dynamic: the next unclaimed brick
+        int nbk = 0;
+        if (pt == 0) nbk = atomicAdd(bk.sched, 1);
+        if (NPW > 1) {
+          if (pt == 0) sbrick[s] = nbk;
+          pbar();
+          b = sbrick[s];
+          pbar();
+        } else {
+          b = __shfl_sync(0xffffffffu, nbk, 0);
+        }
+      }
+      if (b >= nb) {  // end marker for the consumers
+        if (pt == 0) sbrick[s] = -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        break;
+      }
+      if (pt == 0) sbrick[s] = b;
       if (pt == 0) {
         const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
         const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
@@ -486,10 +505,10 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   } else {
     // ---------------- consumers
     const int cw = warp - NPW;
-    int k = 0;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x, ++k) {
+    for (int k = 0;; ++k) {
       const int s = k & 1, ph = (k >> 1) & 1;
       mbar_wait(&full[s], ph);
+      if (sbrick[s] < 0) break;
       mbar_wait(&tmaf[s], ph);
       const float* tile = tiles + s * BUF;
       const float4* sr = s_r + s * cap;

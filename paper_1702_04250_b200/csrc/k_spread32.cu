@@ -175,7 +175,14 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
-  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+  __shared__ int s_brick;
+  for (int b = blockIdx.x;; b += gridDim.x) {
+    if (bk.sched) {  // dynamic: the next unclaimed brick
+      if (threadIdx.x == 0) s_brick = atomicAdd(bk.sched + 32, 1);
+      __syncthreads();
+      b = s_brick;
+    }
+    if (b >= nb) break;
     int cnt;
     if (resident) {
       cnt = res.start[b + 1] - res.start[b];

@@ -143,6 +143,8 @@ struct pppm_ctx {
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
   int res_maxcnt = 0;       // largest resident brick (staging capacity of the resident fieldforce)
+  DevBuf sched;             // brick-scheduling counters of the persistent fieldforce / make_rho
+  bool dyn_sched = true;
   // resident step without a binning pass: make_rho maps the brick-ordered fp32
   // positions itself (Resident in pppm_types.h); bstart = per-brick ranges
   bool res_direct = true;
@@ -401,9 +403,16 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     c->launches += 4;
   } else {
     if (!c->binned && !resident) return fail(PPPM_ERR_STATE, "atoms not binned");
+    // the persistent make_rho takes bricks from a counter (ints 32.., zeroed here, inside the graph)
+    Bricks bks = c->bk;
+    if (c->dyn_sched && c->spread_variant != SPREAD_WS) {
+      TRY(c->sched.ensure(256));
+      CU(cudaMemsetAsync(c->sched.as<char>() + 128, 0, 128, c->stream));
+      bks.sched = c->sched.as<int>();
+    }
     TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(),
-                            c->ovf_perm.as<int>(), c->g, c->bk, c->pd, c->rho_map, c->tab.as<float>(),
+                            c->ovf_perm.as<int>(), c->g, bks, c->pd, c->rho_map, c->tab.as<float>(),
                             c->rho.as<float>(), resident ? resident_of(c) : Resident{}, c->n_points,
                             c->rec.as<float4>(), c->stream));
     c->launches += 1 + fold_launches(c->g, c->pd);  // spread + halo fold
@@ -510,14 +519,22 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
                             c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
                             resident ? c->bstart.as<int>() : nullptr, resident ? c->res_novf.as<int>() : nullptr,
                             c->stream));
-    else
+    else {
+    // the warp-specialized fieldforce takes bricks from a counter (zeroed here, inside the graph)
+    Bricks bkg = c->bk;
+    if (c->dyn_sched && gather_eff(c) == GATHER_WS) {
+      TRY(c->sched.ensure(256));
+      CU(cudaMemsetAsync(c->sched.p, 0, 128, c->stream));
+      bkg.sched = c->sched.as<int>();
+    }
     TRY(launch_gather_brick(gather_eff(c), c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
                             c->rcell.as<int>(), c->perm.as<int>(), c->counts.as<int>(), c->cap,
                             resident && c->res_maxcnt > 0 ? std::min(c->res_maxcnt, c->cap) : c->cap,
-                            c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, c->bk, c->pd,
+                            c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, bkg, c->pd,
                             c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
                             resident ? c->bstart.as<int>() : nullptr, resident ? c->res_novf.as<int>() : nullptr,
                             c->stream));
+    }
   }
   c->launches += 1;
   return PPPM_OK;
@@ -747,6 +764,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_ZFFT")) c->use_zfft = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_PLANE")) c->use_plane = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
   return PPPM_OK;

@@ -25,6 +25,8 @@ struct Geom {
 
 struct Bricks {
   int nbx, nby, nbz;
+  int* sched = nullptr;  // optional brick-scheduling counter (zeroed before the launch): persistent CTAs
+                         // take bricks dynamically instead of striding by gridDim.x
   __host__ __device__ __forceinline__ int count() const { return nbx * nby * nbz; }
 };
 
