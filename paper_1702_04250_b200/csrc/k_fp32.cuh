@@ -205,21 +205,44 @@ __device__ __forceinline__ void rows_f32(float v, const float* __restrict__ ta, 
       for (int j = 0; j < S; ++j) d[j] = __ldg(rd + j);
     }
   } else {
-    // exact spline polynomials in t (tools/gen_bspline_poly.py), Horner
+    // exact spline polynomials in t (tools/gen_bspline_poly.py).  Mirror
+    // symmetry (stencil.py:38-77): w_{S-1-j}(t) = w_j(-t), d_{S-1-j}(t) = -d_j(-t),
+    // so each node pair shares its even / odd parts in u = t^2 (Horner in u):
+    // w_j = E + t O, w_{S-1-j} = E - t O  (13 instead of 20 FMA at S = 5)
+    const float u = v * v;
 #pragma unroll
-    for (int j = 0; j < S; ++j) {
-      float x = bspline_a<S>(j, S - 1);
+    for (int j = 0; j < (S + 1) / 2; ++j) {
+      float e = bspline_a<S>(j, (S - 1) & ~1);
 #pragma unroll
-      for (int k = S - 2; k >= 0; --k) x = fmaf(x, v, bspline_a<S>(j, k));
-      a[j] = x;
+      for (int k = ((S - 1) & ~1) - 2; k >= 0; k -= 2) e = fmaf(e, u, bspline_a<S>(j, k));
+      if (2 * j + 1 == S) {
+        a[j] = e;  // middle node (odd S): even in t
+      } else {
+        constexpr int ko = (S - 1) & 1 ? S - 1 : S - 2;  // highest odd power
+        float o = bspline_a<S>(j, ko);
+#pragma unroll
+        for (int k = ko - 2; k >= 1; k -= 2) o = fmaf(o, u, bspline_a<S>(j, k));
+        a[j] = fmaf(v, o, e);
+        a[S - 1 - j] = fmaf(-v, o, e);
+      }
     }
     if (DERIV) {
 #pragma unroll
-      for (int j = 0; j < S; ++j) {
-        float x = bspline_d<S>(j, S - 2);
+      for (int j = 0; j < (S + 1) / 2; ++j) {
+        constexpr int ke = (S - 2) & ~1;                 // highest even power (degree S-2)
+        constexpr int ko = (S - 2) & 1 ? S - 2 : S - 3;  // highest odd power
+        float e = bspline_d<S>(j, ke);
 #pragma unroll
-        for (int k = S - 3; k >= 0; --k) x = fmaf(x, v, bspline_d<S>(j, k));
-        d[j] = x;
+        for (int k = ke - 2; k >= 0; k -= 2) e = fmaf(e, u, bspline_d<S>(j, k));
+        float o = bspline_d<S>(j, ko);
+#pragma unroll
+        for (int k = ko - 2; k >= 1; k -= 2) o = fmaf(o, u, bspline_d<S>(j, k));
+        if (2 * j + 1 == S) {
+          d[j] = v * o;  // middle node: odd in t
+        } else {
+          d[j] = fmaf(v, o, e);
+          d[S - 1 - j] = fmaf(v, o, -e);
+        }
       }
     }
   }

@@ -402,12 +402,17 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   if (warp < NPW) {
     // ---------------- producer
     int k = 0;
+    // dynamic scheduling: the brick after the current one is claimed one iteration ahead
+    int claim = (bk.sched && pt == 0) ? atomicAdd(bk.sched, 1) : 0;
     for (int b = blockIdx.x;; b += gridDim.x, ++k) {
       const int s = k & 1, use = k >> 1;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
       if (bk.sched) {  // dynamic: the next unclaimed brick
         int nbk = 0;
-        if (pt == 0) nbk = atomicAdd(bk.sched, 1);
+        if (pt == 0) {
+          nbk = claim;
+          if (claim < nb) claim = atomicAdd(bk.sched, 1);
+        }
         if (NPW > 1) {
           if (pt == 0) sbrick[s] = nbk;
           pbar();

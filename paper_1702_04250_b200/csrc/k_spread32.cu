@@ -176,9 +176,14 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
   __shared__ int s_brick;
+  // dynamic scheduling: the brick after the current one is claimed one iteration ahead
+  int claim = (bk.sched && threadIdx.x == 0) ? atomicAdd(bk.sched + 32, 1) : 0;
   for (int b = blockIdx.x;; b += gridDim.x) {
     if (bk.sched) {  // dynamic: the next unclaimed brick
-      if (threadIdx.x == 0) s_brick = atomicAdd(bk.sched + 32, 1);
+      if (threadIdx.x == 0) {
+        s_brick = claim;
+        if (claim < nb) claim = atomicAdd(bk.sched + 32, 1);
+      }
       __syncthreads();
       b = s_brick;
     }
