@@ -362,7 +362,7 @@ template <int S> constexpr int kWsXl = PPPM_WS_XL < S ? PPPM_WS_XL : S;
 #endif
 constexpr int kWsU1 = PPPM_WS_U1, kWsU2 = PPPM_WS_U2;
 
-template <int S, bool TAB>
+template <int S, bool TAB, int MODE = 0>
 __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3) k_gather_ws(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
     const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
@@ -371,10 +371,12 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
     const int* __restrict__ novf_res) {
   using T = TmaTile<S>;
   using ST = SplitTile<S>;
-  constexpr int TXB = T::TXB, DY = ST::DY, FT = ST::FT, lo = Stencil<S>::lo;
-  constexpr int BUF = 3 * FT;
+  // ik (MODE 0): three component tiles, rows shifted by the component (DY = D + 2);
+  // ad (MODE 1): one potential tile (DY = D), one task per atom, three derivative sums
+  constexpr int TXB = T::TXB, DY = MODE == 0 ? ST::DY : T::D, FT = MODE == 0 ? ST::FT : T::NP, lo = Stencil<S>::lo;
+  constexpr int BUF = MODE == 0 ? 3 * FT : FT;
   constexpr int NCW = kWsConsumerWarps;
-  constexpr uint32_t kBytes = 3u * ST::FTN * sizeof(float);
+  constexpr uint32_t kBytes = MODE == 0 ? 3u * ST::FTN * sizeof(float) : (uint32_t)T::N * sizeof(float);
   extern __shared__ __align__(16) unsigned char dyn_raw[];
   float* tiles = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][BUF]
   float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);  // [2][cap]
@@ -434,8 +436,12 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
         const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&tmaf[s], kBytes);
+        if constexpr (MODE == 0) {
 #pragma unroll
-        for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+          for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+        } else {
+          tma_load_4d(tiles + s * BUF, &fmap, &tmaf[s], x, y, z, 0);
+        }
       }
       int cnt;
       int64_t base;
@@ -519,7 +525,8 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
       const float4* sr = s_r + s * cap;
       const int* sc = s_c + s * cap;
       const int* sp = s_p + s * cap;
-      const int seg0 = bsize[s][lane], seg1 = bsize[s][(lane - TXB) & 31], seg2 = bsize[s][(lane - 2 * TXB) & 31];
+      const int seg0 = bsize[s][lane];
+      const int seg1 = MODE == 0 ? bsize[s][(lane - TXB) & 31] : 0, seg2 = MODE == 0 ? bsize[s][(lane - 2 * TXB) & 31] : 0;
       const int tot = seg0 + seg1 + seg2;
       int trounds = tot;
 #pragma unroll
@@ -539,6 +546,40 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
         const float4 r = sr[j];
         const int cc = sc[j];
         const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        if constexpr (MODE == 1) {
+          // fieldforce_ad (gridmap.py:299-310): split-atom derivative sums over one potential tile
+          float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
+          rows_f32<S, TAB, true>(r.x, ta, td, ax, dx);
+          rows_f32<S, TAB, true>(r.y, ta, td, ay, dy);
+          rows_f32<S, TAB, true>(r.z, ta, td, az, dz);
+          const float* tf = tile + (lz * DY + ly) * TXB + lx + T::SH;
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int a = 0; a < S; ++a) {
+            float r0 = 0.f, r1 = 0.f, r2 = 0.f;
+#pragma unroll
+            for (int bb = 0; bb < S; ++bb) {
+              const float* row = tf + (a * DY + bb) * TXB;
+              float pdv = 0.f, pa = 0.f;
+#pragma unroll
+              for (int c = 0; c < S; ++c) {
+                pdv = fmaf(dx[c], row[c], pdv);
+                pa = fmaf(ax[c], row[c], pa);
+              }
+              r0 = fmaf(ay[bb], pdv, r0);
+              r1 = fmaf(dy[bb], pa, r1);
+              r2 = fmaf(ay[bb], pa, r2);
+            }
+            s0 = fmaf(az[a], r0, s0);
+            s1 = fmaf(az[a], r1, s1);
+            s2 = fmaf(dz[a], r2, s2);
+          }
+          const float sc = cscale * r.w;
+          const int64_t i = sp[j];
+          store_force<S, 1>(force, out_f64, i, -sc * s0 * (float)g.ihx, -sc * s1 * (float)g.ihy,
+                            -sc * s2 * (float)g.ihz);
+          continue;
+        }
         float ax[S], ay[S], az[S], dd[S];
         rows_f32<S, TAB, false>(r.x, ta, td, ax, dd);
         rows_f32<S, TAB, false>(r.y, ta, td, ay, dd);
@@ -567,7 +608,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
-  gather_overflow<S, TAB, 0>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
+  gather_overflow<S, TAB, MODE>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
                              ovf_perm);
 }
 
@@ -920,6 +961,24 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
           const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
           k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
+                                  ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+          return 0;
+        });
+      }
+    }
+    if constexpr (MODE == 1) {
+      if (variant == GATHER_WS) {  // warp-specialized fieldforce_ad
+        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(float) +
+                           2 * (size_t)scap * (sizeof(float4) + 2 * sizeof(int));
+        return with_bool(tab, [&](auto T_) -> int {
+          constexpr bool TAB = decltype(T_)::value;
+          auto k = k_gather_ws<S, TAB, 1>;
+          allow_smem(k, dyn);
+          constexpr int NT = 32 * (kWsConsumerWarps + kWsProducerWarps);
+          int per_sm = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
+          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          k<<<grid, NT, dyn, s>>>(rec, counts, scap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
                                   ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
           return 0;
         });

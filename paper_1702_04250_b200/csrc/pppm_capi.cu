@@ -264,6 +264,7 @@ static int gather_eff(const pppm_ctx* c) {
     if (c->mode == 0 && gather_mma_ok(c->order)) return GATHER_MMA;
     return gather_split_ok(c->order, c->pd.hx) && c->mode == 0 ? GATHER_WS : GATHER_SORTED;
   }
+  if (c->mode == 1 && c->gather_variant == GATHER_WS) return GATHER_WS;  // warp-specialized fieldforce_ad
   if ((c->gather_variant == GATHER_SPLIT || c->gather_variant == GATHER_WS || c->gather_variant == GATHER_WSP) &&
       !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
     return GATHER_SORTED;
@@ -303,7 +304,8 @@ static int encode_maps(pppm_ctx* c) {
                           (cuuint64_t)c->nfields()};
     cuuint64_t strides[3] = {row, plane, vol};
     // split gather: one component per box, two extra rows (row shift per component)
-    const bool split = gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS || gather_eff(c) == GATHER_WSP;
+    const bool split = c->mode == 0 &&
+                       (gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS || gather_eff(c) == GATHER_WSP);
     // tensor-core gather: all fields, 16-float rows starting at the brick's lowest stencil node
     const bool mma = gather_eff(c) == GATHER_MMA;
     cuuint32_t box[4] = {(cuuint32_t)(mma ? 16 : txb), (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
