@@ -404,17 +404,14 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   if (warp < NPW) {
     // ---------------- producer
     int k = 0;
-    // dynamic scheduling: the brick after the current one is claimed one iteration ahead
-    int claim = (bk.sched && pt == 0) ? atomicAdd(bk.sched, 1) : 0;
+    // dynamic scheduling: a brick is claimed when its stage slot is free (claiming
+    // further ahead would let some CTAs hold two bricks while others idle)
     for (int b = blockIdx.x;; b += gridDim.x, ++k) {
       const int s = k & 1, use = k >> 1;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
-      if (bk.sched) {  // dynamic: the next unclaimed brick
+      if (bk.sched && k > 0) {  // dynamic after the first (static) brick: the next unclaimed one
         int nbk = 0;
-        if (pt == 0) {
-          nbk = claim;
-          if (claim < nb) claim = atomicAdd(bk.sched, 1);
-        }
+        if (pt == 0) nbk = gridDim.x + atomicAdd(bk.sched, 1);
         if (NPW > 1) {
           if (pt == 0) sbrick[s] = nbk;
           pbar();
@@ -426,6 +423,11 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
       }
       if (b >= nb) {  // end marker for the consumers
         if (pt == 0) sbrick[s] = -1;
+        // the last CTA done claiming resets the counters for the next launch (no memset node)
+        if (pt == 0 && bk.sched && atomicAdd(bk.sched + 1, 1) == (int)gridDim.x - 1) {
+          atomicExch(bk.sched, 0);
+          atomicExch(bk.sched + 1, 0);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[s]);
         break;

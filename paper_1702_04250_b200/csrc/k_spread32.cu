@@ -176,18 +176,20 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
   __shared__ int s_brick;
-  // dynamic scheduling: the brick after the current one is claimed one iteration ahead
-  int claim = (bk.sched && threadIdx.x == 0) ? atomicAdd(bk.sched + 32, 1) : 0;
-  for (int b = blockIdx.x;; b += gridDim.x) {
-    if (bk.sched) {  // dynamic: the next unclaimed brick
-      if (threadIdx.x == 0) {
-        s_brick = claim;
-        if (claim < nb) claim = atomicAdd(bk.sched + 32, 1);
-      }
+  for (int b = blockIdx.x, it = 0;; b += gridDim.x, ++it) {
+    if (bk.sched && it > 0) {  // dynamic after the first (static) brick: the next unclaimed one
+      if (threadIdx.x == 0) s_brick = gridDim.x + atomicAdd(bk.sched + 32, 1);
       __syncthreads();
       b = s_brick;
     }
-    if (b >= nb) break;
+    if (b >= nb) {
+      // the last CTA done claiming resets the counters for the next launch (no memset node)
+      if (bk.sched && threadIdx.x == 0 && atomicAdd(bk.sched + 33, 1) == (int)gridDim.x - 1) {
+        atomicExch(bk.sched + 32, 0);
+        atomicExch(bk.sched + 33, 0);
+      }
+      break;
+    }
     int cnt;
     if (resident) {
       cnt = res.start[b + 1] - res.start[b];

@@ -396,6 +396,15 @@ static Resident resident_of(pppm_ctx* c) {
   return r;
 }
 
+// brick-scheduling counters of the persistent make_rho / fieldforce: zeroed once
+// (first, eager run); each launch's last CTA resets them for the next
+static int ensure_sched(pppm_ctx* c) {
+  if (c->sched.p) return PPPM_OK;
+  TRY(c->sched.ensure(256));
+  CU(cudaMemsetAsync(c->sched.p, 0, 256, c->stream));
+  return PPPM_OK;
+}
+
 static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, bool resident = false) {
   const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
@@ -408,8 +417,7 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     // the persistent make_rho takes bricks from a counter (ints 32.., zeroed here, inside the graph)
     Bricks bks = c->bk;
     if (c->dyn_sched && c->spread_variant != SPREAD_WS) {
-      TRY(c->sched.ensure(256));
-      CU(cudaMemsetAsync(c->sched.as<char>() + 128, 0, 128, c->stream));
+      TRY(ensure_sched(c));
       bks.sched = c->sched.as<int>();
     }
     TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
@@ -525,8 +533,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     // the warp-specialized fieldforce takes bricks from a counter (zeroed here, inside the graph)
     Bricks bkg = c->bk;
     if (c->dyn_sched && gather_eff(c) == GATHER_WS) {
-      TRY(c->sched.ensure(256));
-      CU(cudaMemsetAsync(c->sched.p, 0, 128, c->stream));
+      TRY(ensure_sched(c));
       bkg.sched = c->sched.as<int>();
     }
     TRY(launch_gather_brick(gather_eff(c), c->order, c->n_points > 0, c->mode, out_f64, c->rec.as<float4>(),
