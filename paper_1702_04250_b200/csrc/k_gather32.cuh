@@ -612,6 +612,15 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   }
   gather_overflow<S, TAB, MODE>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
                              ovf_perm);
+  // resident step: the last CTA done with the per-step mover list clears it for the next
+  // make_rho (instead of a memset node before it)
+  if (bk.sched && rstart) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(bk.sched + 2, 1) == (int)gridDim.x - 1) {
+      atomicExch(const_cast<int*>(novf_res), 0);
+      atomicExch(bk.sched + 2, 0);
+    }
+  }
 }
 
 // fieldforce_ik, warp-specialized split variant with x-adjacent atom pairs:

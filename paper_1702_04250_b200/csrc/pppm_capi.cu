@@ -144,6 +144,7 @@ struct pppm_ctx {
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
   int res_maxcnt = 0;       // largest resident brick (staging capacity of the resident fieldforce)
   DevBuf sched;             // brick-scheduling counters of the persistent fieldforce / make_rho
+  bool novf_clean = false;  // the resident mover counter is zero (cleared by the last fieldforce CTA)
   bool dyn_sched = true;
   // resident step without a binning pass: make_rho maps the brick-ordered fp32
   // positions itself (Resident in pppm_types.h); bstart = per-brick ranges
@@ -1061,6 +1062,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   c->res_dtype = dtype;
   c->res_sorted = false;
   c->res_maxcnt = 0;
+  c->novf_clean = false;
   if (!c->fp64() && c->sort_resident && !c->slab) {  // single-mesh contexts only
     // keep the resident atoms in brick order (as an MD engine sorts its atoms):
     // bin once, then gather positions / charges into bucket order
@@ -1121,21 +1123,28 @@ static int run_subphase(pppm_ctx* c, int sp) {
       return PPPM_OK;
     case SP_SPREAD:
       if (resident_step(c)) {
-        // reset the per-step list of atoms that left their brick, then make_rho
-        CU(cudaMemsetAsync(c->res_novf.p, 0, sizeof(int), c->stream));
+        // the per-step list of atoms that left their brick is cleared before
+        // make_rho (launch_subphase: a memset outside the graph unless the last
+        // fieldforce cleared it)
+        c->novf_clean = false;
         return run_spread(c, p, q, n, c->res_dtype, true);
       }
       return run_spread(c, p, q, n, c->res_dtype);
     case SP_POISSON:
       return run_poisson(c);
     case SP_GATHER:
-      return do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64(), resident_step(c));
+      TRY(do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64(), resident_step(c)));
+      // k_gather_ws (dynamic scheduling) clears the mover counter at its end
+      c->novf_clean = resident_step(c) && c->dyn_sched && gather_eff(c) == GATHER_WS;
+      return PPPM_OK;
   }
   return PPPM_OK;
 }
 
 // eager on the first run of a sub-phase, then captured into a CUDA graph and replayed
 static int launch_subphase(pppm_ctx* c, int sp) {
+  if (sp == SP_SPREAD && resident_step(c) && !c->novf_clean)
+    CU(cudaMemsetAsync(c->res_novf.p, 0, sizeof(int), c->stream));
   if (!c->use_graphs) return run_subphase(c, sp);
   if (sp == SP_BIN && resident_step(c)) return PPPM_OK;  // nothing to launch
   if (c->gexec[sp]) {
