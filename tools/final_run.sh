@@ -19,3 +19,7 @@ done
 PPPM_B200_GATHER=4 timeout 120 python bench.py $A > /dev/null 2>&1 && PPPM_B200_GATHER=4 timeout 300 ncu --set full \
   --clock-control none --import-source on -k regex:k_gather_mma -s 1 -c 1 -o gpurun_out/r01_full_k_gather_mma \
   python bench.py $A > gpurun_out/ncu_mma.log 2>&1; echo "ncu mma=$?"
+# the multi-GPU (z-slab, NCCL) code path end to end with one slab
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 1 --force-slab --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/slab1.json 2> gpurun_out/slab1.err
+echo "slab=$?"
