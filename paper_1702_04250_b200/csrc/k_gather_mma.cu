@@ -434,9 +434,8 @@ int launch_gather_mma(int order, bool tab, bool out_f64, const float4* rec, cons
       using T = MmaTile<S>;
       const size_t dyn0 = 1024 + 2 * (size_t)T::kTileStride + 12 * (size_t)T::kBopBytes + kAR * 8192 +
                           kAR * 128 * (4 * ((T::D + 1) / 2) + 4) * sizeof(float);
-      // one CTA per SM: each CTA allocates all 512 TMEM columns
-      static const size_t floor_b = getenv("PPPM_MMA_SMEM_FLOOR") ? (size_t)atoi(getenv("PPPM_MMA_SMEM_FLOOR")) : 0;
-      const size_t dyn = std::max(dyn0, floor_b);
+      // at least half the SM's shared memory: one CTA per SM (each allocates all 512 TMEM columns)
+      const size_t dyn = std::max(dyn0, (size_t)116 * 1024);
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
