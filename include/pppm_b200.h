@@ -136,9 +136,11 @@ int pppm_ctx_get_energy(pppm_ctx* ctx, double* energy);
  * first eager run each sub-phase is captured into a CUDA graph and replayed. */
 int pppm_ctx_time_steps(pppm_ctx* ctx, int steps, int warmup, int flush_l2, double* ms);
 /* kernel variants for A/B measurement: kernel 0 = fp32 make_rho
- * (0: float CAS shared atomics, 1: int32 fixed-point shared atomics [default]),
- * kernel 1 = fp32 fieldforce (0: bucket order, 1: bank rounds, 2: one task per
- * (atom, component) [ik], 3: 2 + warp-specialized staging [ik default]) */
+ * (0: float CAS shared atomics, 1: int32 fixed-point shared atomics [default],
+ * 3: warp-specialized), kernel 1 = fp32 fieldforce (0: bucket order, 1: bank
+ * rounds, 2: one task per (atom, component) [ik], 3: warp-specialized staging
+ * [default; ik: per-component tasks, ad: one task per atom], 4: tcgen05 tensor
+ * cores [ik, orders 3-5], 5: x-adjacent atom pairs [ik]) */
 int pppm_ctx_set_variant(pppm_ctx* ctx, int kernel, int variant);
 /* z-slab decomposition over `nslabs` GPUs (no counterpart in the reference,
  * which is single-process).  Slab `rank` owns global planes
