@@ -362,8 +362,13 @@ template <int S> constexpr int kWsXl = PPPM_WS_XL < S ? PPPM_WS_XL : S;
 #endif
 constexpr int kWsU1 = PPPM_WS_U1, kWsU2 = PPPM_WS_U2;
 
+// producer warps / staging batch of the warp-specialized gather: fieldforce_ad's
+// consumers are ~3x faster per brick, so its staging runs on two warps
+template <int MODE> constexpr int kWsPw = MODE == 1 ? 2 : kWsProducerWarps;
+template <int MODE> constexpr int kWsU2m = MODE == 1 ? 2 : kWsU2;
+
 template <int S, bool TAB, int MODE = 0>
-__global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3) k_gather_ws(
+__global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), 3) k_gather_ws(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
     const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
     const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,
@@ -388,14 +393,14 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   const int nb = bk.count();
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&full[s], kWsProducerWarps);
+      mbar_init(&full[s], kWsPw<MODE>);
       mbar_init(&tmaf[s], 1);
       mbar_init(&empty[s], NCW);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  constexpr int NPW = kWsProducerWarps;
+  constexpr int NPW = kWsPw<MODE>;
   const int pt = threadIdx.x;  // producer thread (warps 0 .. NPW-1)
   auto pbar = [&]() {
     if (NPW > 1) asm volatile("bar.sync 1, %0;" ::"n"(NPW * 32) : "memory");
@@ -490,11 +495,11 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
       float4* sr = s_r + s * cap;
       int* sc = s_c + s * cap;
       int* sp = s_p + s * cap;
-      for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsU2) {
-        int4 m[kWsU2];
-        float4 r[kWsU2];
+      for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsU2m<MODE>) {
+        int4 m[kWsU2m<MODE>];
+        float4 r[kWsU2m<MODE>];
 #pragma unroll
-        for (int u = 0; u < kWsU2; ++u) {
+        for (int u = 0; u < kWsU2m<MODE>; ++u) {
           const int j = j0 + u * 32 * NPW + pt;
           m[u].x = -1;
           if (j < cnt) {
@@ -503,7 +508,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
           }
         }
 #pragma unroll
-        for (int u = 0; u < kWsU2; ++u) {
+        for (int u = 0; u < kWsU2m<MODE>; ++u) {
           if (m[u].x < 0) continue;
           const int lx = m[u].x & (kBrick - 1), ly = (m[u].x >> 3) & (kBrick - 1), lz = m[u].x >> 6;
           const int dst = atomicAdd(&cursor[((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
@@ -985,7 +990,7 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
           constexpr bool TAB = decltype(T_)::value;
           auto k = k_gather_ws<S, TAB, 1>;
           allow_smem(k, dyn);
-          constexpr int NT = 32 * (kWsConsumerWarps + kWsProducerWarps);
+          constexpr int NT = 32 * (kWsConsumerWarps + kWsPw<1>);
           int per_sm = 0;
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
           const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
