@@ -364,7 +364,10 @@ constexpr int kWsU1 = PPPM_WS_U1, kWsU2 = PPPM_WS_U2;
 
 // producer warps / staging batch of the warp-specialized gather: fieldforce_ad's
 // consumers are ~3x faster per brick, so its staging runs on two warps
-template <int MODE> constexpr int kWsPw = MODE == 1 ? 2 : kWsProducerWarps;
+#ifndef PPPM_WS_PW_AD
+#define PPPM_WS_PW_AD 2
+#endif
+template <int MODE> constexpr int kWsPw = MODE == 1 ? PPPM_WS_PW_AD : kWsProducerWarps;
 template <int MODE> constexpr int kWsU2m = MODE == 1 ? 2 : kWsU2;
 
 template <int S, bool TAB, int MODE = 0>
