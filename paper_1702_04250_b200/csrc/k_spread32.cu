@@ -84,8 +84,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
                                               int* __restrict__ ovf_perm, BankSmem sm, float4* __restrict__ t_r,
                                               int* __restrict__ t_c) {
   constexpr int PER = kCapMax / NT;
-  if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
-  __syncthreads();
+  // (bsize was reset by the caller before its brick barrier)
   // pass 1: map positions, write the slot records (fieldforce reads them at
   // the resident index), bank histogram; only bank / rank stay in registers
   int rk[PER], bank[PER];
@@ -176,12 +175,16 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
   __shared__ int s_brick;
+  bool prefetched = false;  // uniform: s_brick already holds the next claim (written before the last barrier)
   for (int b = blockIdx.x, it = 0;; b += gridDim.x, ++it) {
     if (bk.sched && it > 0) {  // dynamic after the first (static) brick: the next unclaimed one
-      if (threadIdx.x == 0) s_brick = gridDim.x + atomicAdd(bk.sched + 32, 1);
-      __syncthreads();
+      if (!prefetched) {
+        if (threadIdx.x == 0) s_brick = gridDim.x + atomicAdd(bk.sched + 32, 1);
+        __syncthreads();
+      }
       b = s_brick;
     }
+    prefetched = false;
     if (b >= nb) {
       // the last CTA done claiming resets the counters for the next launch (no memset node)
       if (bk.sched && threadIdx.x == 0 && atomicAdd(bk.sched + 33, 1) == (int)gridDim.x - 1) {
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     float* ftile = reinterpret_cast<float*>(tile);
     // all reduces but the most recent (other buffer) have finished reading
     if (threadIdx.x == 0) bulk_wait_read<1>();
+    if (RES && threadIdx.x < 32) bsize[threadIdx.x] = 0;  // stage_resident's histogram
     __syncthreads();
     for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
     float scale = inv_vcell, inv_scale = 1.f;
@@ -254,7 +258,9 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     if (FIX)
       for (int k = threadIdx.x; k < TN; k += blockDim.x) ftile[k] = (float)tile[k] * inv_scale;
     fence_proxy_async_smem();
+    if (bk.sched && threadIdx.x == 0) s_brick = gridDim.x + atomicAdd(bk.sched + 32, 1);  // next brick
     __syncthreads();
+    prefetched = bk.sched != nullptr;
     if (threadIdx.x == 0) {
       const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
       tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
