@@ -12,11 +12,15 @@ context stream; L2 (126 MB) is flushed with a 256 MiB memset before every
 step.  ``e2e`` is the same workload through the C ABI with pinned host
 buffers (H2D of positions/charges, full step, D2H of forces and energy).
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): the config is z-slab
-decomposed over the N GPUs (strong scaling, paper_1702_04250_b200/slab.py):
-ghost-plane reverse sums / forward copies and the FFT all-to-all transposes
-over NCCL; barrier + device sync around the timed region, max time over
-ranks.
+Multi-GPU (one rank per GPU; ``--gpus N`` re-launches itself under
+torch.distributed.run when started without it): BASELINE config 5 (8,388,608
+atoms, 256^3) z-slab decomposed over the N GPUs (strong scaling,
+paper_1702_04250_b200/slab.py).  Each rank's step runs inside the library:
+NCCL ghost-plane reverse sums / forward copies, the FFT all-to-all transposes
+and the energy all-reduce on the context stream, replayed from CUDA graphs;
+barrier + device sync around the timed region, max time over ranks.  The N=1
+line carries a ``config5`` sub-record (the same workload on one GPU, single
+mesh and the one-slab NCCL path) so the 1/2/4/8 curve has its N=1 point.
 
 ``--impl reference`` times the CPU oracle port of the reference algorithm
 (oracle/pppm_oracle.py, numpy, all host threads for make_rho) on bounded
@@ -51,7 +55,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 3 on one GPU, 5 when decomposed over N > 1 GPUs)")
+    ap.add_argument("--probe-launch", action="store_true",
+                    help="only launch the N ranks and report them (CPU check of the spawn path)")
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 sub-record at N=1")
     ap.add_argument("--mode", default=None, choices=(None, "ik", "ad"))
     ap.add_argument("--order", type=int, default=None, help="override the config's stencil order (config 4 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,91 +254,95 @@ def run_reference(args, cfg, rank, pg):
     print(json.dumps(line), flush=True)
 
 
-def run_slabs(args, cfg, rank, local, world, pg):
-    """N > 1: one config, z-slab decomposed over the N GPUs (strong scaling):
-    NCCL ghost-plane exchanges and FFT all-to-all transposes (slab.py)."""
+def _slab_partition(cfg, mode, world, rank, device):
+    """This rank's atoms of the config: owner = the slab holding the atom's
+    wrapped node_z (bit-exact particle_map on the device)."""
+    import paper_1702_04250_b200 as pb
+    from paper_1702_04250_b200 import _native as nat
+    from paper_1702_04250_b200.slab import owner_of_nodes
+
+    pos, q, lengths = cfg.build()          # the same seeded system on every rank, then partitioned
+    p32 = np.ascontiguousarray(pos, dtype=np.float32)
+    probe = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
+                           device=device)
+    nodes = np.empty((3, p32.shape[0]), dtype=np.int32)
+    probe.ctx("pppm_particle_map", nat.ptr(p32), p32.shape[0], nat.F32, nat.HOST, nat.ptr(nodes))
+    probe.close()
+    mine = np.nonzero(owner_of_nodes(nodes[2], cfg.dims[2], world) == rank)[0]
+    return p32[mine], q[mine].astype(np.float32), lengths, pos.shape[0]
+
+
+def slab_timing(cfg, mode, world, rank, device, steps, warmup, pg=None, unique_id=None):
+    """One z-slab of ``cfg`` on ``device``, the whole step inside the library
+    (kernels + NCCL ghost exchanges / transposes / energy all-reduce on the
+    context stream, CUDA graphs): phase times summed over ``steps``."""
+    from paper_1702_04250_b200.slab import SlabContext, nccl_unique_id
+
+    p_mine, q_mine, lengths, n_total = _slab_partition(cfg, mode, world, rank, device)
+    slab = SlabContext(cfg.dims, lengths, cfg.order, mode, cfg.alpha, world, rank, device=device)
+    slab.load_atoms(p_mine, q_mine)
+    slab.attach_nccl(unique_id if unique_id is not None else nccl_unique_id())
+    launches = slab.launches_per_step()
+    slab.time_steps(3, 0)                # eager + capture + replay
+    return slab, n_total, len(p_mine), launches
+
+
+def _bcast_unique_id(pg, rank, device):
+    """rank 0's NCCL id to every rank over the torch.distributed group."""
     import torch
 
+    from paper_1702_04250_b200.slab import nccl_unique_id
+
+    dev = f"cuda:{device}" if pg.get_backend() == "nccl" else "cpu"
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    pg.broadcast(t, src=0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def run_slabs(args, cfg, rank, local, world, pg):
+    """N > 1: BASELINE config 5 (8,388,608 atoms, 256^3) z-slab decomposed over
+    the N GPUs (strong scaling).  Each rank's step runs inside the library:
+    resident brick-ordered atoms (no binning pass), NCCL ghost-plane reverse
+    sums / forward copies, FFT transposes and the energy all-reduce on the
+    context stream, every phase replayed from a CUDA graph."""
     import __graft_entry__
 
     __graft_entry__.build()
-    import paper_1702_04250_b200 as pb
-    from paper_1702_04250_b200 import _native as nat
-    from paper_1702_04250_b200.slab import SlabContext, SlabStep, TorchComm, owner_of_nodes
-
+    if world != args.gpus:
+        raise SystemExit(f"bench: launched with {world} ranks but --gpus {args.gpus}")
     mode = args.mode or cfg.mode
-    pos, q, lengths = cfg.build()          # the same system on every rank, then partitioned
-    n_total = pos.shape[0]
-    p32 = pos.astype(np.float32)
-    probe = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
-                           device=local)
-    nodes = np.empty((3, n_total), dtype=np.int32)
-    probe.ctx("pppm_particle_map", nat.ptr(p32), n_total, nat.F32, nat.HOST, nat.ptr(nodes))
-    probe.close()
-    mine = np.nonzero(owner_of_nodes(nodes[2], cfg.dims[2], world) == rank)[0]
-    slab = SlabContext(cfg.dims, lengths, cfg.order, mode, cfg.alpha, world, rank, device=local)
-    slab.load_atoms(p32[mine], q[mine].astype(np.float32))
-    comm = TorchComm()
-    step = SlabStep(slab, comm)
-    stream = torch.cuda.ExternalStream(slab.stream_ptr, device=local)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-
-    def run(k, timed):
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
-        for i in range(k):
-            with torch.cuda.stream(stream):
-                flush.zero_()
-                ev[i][0].record(stream)
-            step.make_rho()
-            with torch.cuda.stream(stream):
-                ev[i][1].record(stream)
-            step.poisson()
-            with torch.cuda.stream(stream):
-                ev[i][2].record(stream)
-            step.fieldforce()
-            with torch.cuda.stream(stream):
-                ev[i][3].record(stream)
-        stream.synchronize()
-        return [(e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])) for e in ev]
-
-    run(max(3, args.warmup), False)
+    uid = _bcast_unique_id(pg, rank, local)
+    slab, n_total, n_local, launches = slab_timing(cfg, mode, world, rank, local, args.steps, args.warmup,
+                                                   unique_id=uid)
     barrier(pg)
     sampler = ClockSampler(local)
     sampler.start()
     t_load = time.perf_counter()
     while time.perf_counter() - t_load < 1.5:
-        run(5, False)
-    torch.cuda.synchronize()
+        slab.time_steps(5, 0)
     barrier(pg)
-    cnt0 = ctypes.c_int64()
-    slab("pppm_ctx_launch_count", ctypes.byref(cnt0))
     t_wall = time.perf_counter()
-    times = run(args.steps, True)
-    torch.cuda.synchronize()
-    barrier(pg)
+    ms = slab.time_steps(args.steps, args.warmup)
     t_wall = time.perf_counter() - t_wall
-    cnt1 = ctypes.c_int64()
-    slab("pppm_ctx_launch_count", ctypes.byref(cnt1))
     clocks = sampler.stop()
+    barrier(pg)
     k = args.steps
-    t_mr = sum(t[0] for t in times) / 1e3
-    t_po = sum(t[1] for t in times) / 1e3
-    t_ff = sum(t[2] for t in times) / 1e3
+    t_mr = (ms["bin"] + ms["spread"]) / 1e3
+    t_po = ms["poisson"] / 1e3
+    t_ff = ms["gather"] / 1e3
     t_mf_max = max_over_ranks(pg, t_mr + t_ff)
     t_step_max = max_over_ranks(pg, t_mr + t_po + t_ff)
-    n_local = float(len(mine))
     value = n_total * k / t_mf_max
     peak, peak_kind = peaks()
     mesh_local = int(np.prod(cfg.dims)) // world
-    alg = n_local * 16 + mesh_local * 4 + n_local * 16 + 3 * mesh_local * 4 + 3 * n_local * 4
+    nf = 3 if mode == "ik" else 1
+    alg = n_local * 16 + mesh_local * 4 + n_local * 16 + nf * mesh_local * 4 + 3 * n_local * 4
     gbs = alg / ((t_mr + t_ff) / k) / 1e9
-    # the binding on-chip roofline: shared-memory bandwidth (128 B/clk/SM), algorithmic
-    # shared bytes = one 4-byte tile access per stencil point per field (SURVEY §8d)
     sm_clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
     smem_peak = 148 * 128 * sm_clk / 1e9
     S3 = cfg.order ** 3
-    nf = 3 if mode == "ik" else 1
-    # rank 0's slab: its atoms and its make_rho (incl. ghost exchange) / fieldforce times
     smem_alg = {"spread": n_local * S3 * 4, "gather": n_local * S3 * 4 * nf}
     onchip = {"bound": "smem", "unit": "GB/s", "peak": smem_peak,
               "peak_basis": "148 SMs x 128 B/clk x measured SM clock (rank 0)"}
@@ -346,13 +358,13 @@ def run_slabs(args, cfg, rank, local, world, pg):
                                f"{mode}, mixed, z-slab decomposed over {world} GPUs", "n_atoms": n_total,
                    "mesh": list(cfg.dims), "order": cfg.order, "mode": mode, "precision": "mixed",
                    "l2": "flushed before every step (256 MiB memset, outside the phase intervals)",
-                   "parallelism": f"zslab{world}: NCCL ghost send/recv + FFT all-to-all"},
-        "phases_ms_per_step_rank0": {"make_rho_incl_ghost_exchange": t_mr / k * 1e3, "poisson_incl_a2a": t_po / k * 1e3,
-                                     "fieldforce": t_ff / k * 1e3},
+                   "parallelism": f"zslab{world}: NCCL ghost send/recv + FFT all-to-all inside the library"},
+        "phases_ms_per_step_rank0": {"make_rho_incl_ghost_exchange": t_mr / k * 1e3,
+                                     "poisson_incl_a2a": t_po / k * 1e3, "fieldforce": t_ff / k * 1e3},
         "whole_step_atom_steps_per_s": n_total * k / t_step_max,
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": None, "kernel": "make_rho+fieldforce per GPU (rank 0)", "peak_kind": peak_kind},
-        "onchip_roofline": onchip, "clocks": clocks, "gpu_launches": int(cnt1.value - cnt0.value), "wall_s_timed_region": t_wall,
+        "onchip_roofline": onchip, "clocks": clocks, "gpu_launches": launches * k, "wall_s_timed_region": t_wall,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -360,18 +372,96 @@ def run_slabs(args, cfg, rank, local, world, pg):
     pg.destroy_process_group()
 
 
+def config5_record(args, device):
+    """BASELINE config 5 (8,388,608 atoms, 256^3, ik) on this one GPU, for the
+    N=1 point of the 1/2/4/8 curve: the single-mesh resident step and the
+    one-slab NCCL path (the multi-GPU code path with P = 1, NCCL to itself)."""
+    import paper_1702_04250_b200 as pb
+    from paper_1702_04250_b200 import scenarios
+
+    cfg = scenarios.CONFIGS[5]
+    mode = args.mode or cfg.mode
+    steps, warmup = max(5, args.steps // 2), max(3, args.warmup)
+    out = {"workload": f"config5: {cfg.n_atoms} point charges, mesh 256^3, order {cfg.order}, {mode}, mixed",
+           "steps": steps}
+    pos, q, lengths = cfg.build()
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
+                         device=device)
+    ctx.load_atoms(pos.astype(np.float32), q.astype(np.float32))
+    ms = ctx.time_steps(steps, warmup, flush_l2=True)
+    ctx.close()
+    del pos, q
+    t_mf = (ms["bin"] + ms["spread"] + ms["gather"]) / 1e3
+    t_all = t_mf + ms["poisson"] / 1e3
+    out["single"] = {"value": cfg.n_atoms * steps / t_mf, "whole_step_atom_steps_per_s": cfg.n_atoms * steps / t_all,
+                     "phases_ms_per_step": {kk: v / steps for kk, v in ms.items()}}
+    try:
+        slab, n_total, _, _ = slab_timing(cfg, mode, 1, 0, device, steps, warmup)
+        ms = slab.time_steps(steps, warmup)
+        slab.close()
+        t_mf = (ms["bin"] + ms["spread"] + ms["gather"]) / 1e3
+        t_all = t_mf + ms["poisson"] / 1e3
+        out["slab1_nccl"] = {"value": n_total * steps / t_mf, "whole_step_atom_steps_per_s": n_total * steps / t_all,
+                             "phases_ms_per_step": {kk: v / steps for kk, v in ms.items()}}
+    except Exception as exc:  # report, do not hide: the headline line still prints
+        out["slab1_nccl"] = {"error": str(exc)[:300]}
+    return out
+
+
+def probe_launch(args, rank, world, pg):
+    """--probe-launch: the spawn path without a GPU workload (CPU test of the
+    N-rank launch): every rank reports in, rank 0 prints the gathered ranks."""
+    import torch
+
+    t = torch.tensor([rank], dtype=torch.int64)
+    out = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    if pg is not None:
+        pg.all_gather(out, t)
+    else:
+        out = [t]
+    if rank == 0:
+        print(json.dumps({"probe": True, "n_gpus": args.gpus, "world": world,
+                          "ranks": sorted(int(x.item()) for x in out),
+                          "backend": pg.get_backend() if pg is not None else None}), flush=True)
+
+
+def spawn(args):
+    """--gpus N > 1 without torchrun: re-exec this script under
+    torch.distributed.run with N ranks on this node (rank 0 prints the line)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     from paper_1702_04250_b200 import scenarios
 
-    cfg = scenarios.CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (args.impl == "ours" or args.probe_launch):
+        sys.exit(spawn(args))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    ours_multi = args.impl == "ours" and not args.probe_launch and (
+        world_env > 1 or (args.force_slab and "WORLD_SIZE" in os.environ))
+    # one GPU: BASELINE config 3 (the metric's config); N > 1: config 5 over N
+    # slabs (both arms: the reference arm times the same workload's config)
+    multi = world_env > 1 or args.gpus > 1
+    cfg = scenarios.CONFIGS[args.config or (5 if multi else 3)]
     if args.order is not None:
         import dataclasses
 
         cfg = dataclasses.replace(cfg, order=args.order)
-    world_env = int(os.environ.get("WORLD_SIZE", "1"))
-    ours_multi = args.impl == "ours" and (world_env > 1 or (args.force_slab and "WORLD_SIZE" in os.environ))
-    rank, local, world, pg = dist_setup(args.gpus, backend="nccl" if ours_multi else "gloo")
+    backend = "nccl" if ours_multi else "gloo"
+    rank, local, world, pg = dist_setup(args.gpus, backend=backend)
+    if args.probe_launch:
+        probe_launch(args, rank, world, pg)
+        if pg is not None:
+            pg.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, cfg, rank, pg)
         return
@@ -496,6 +586,9 @@ def main():
         hp.free()
         hq.free()
         hf.free()
+
+    if rank == 0 and world == 1 and not args.no_config5 and args.config is None:
+        line["config5"] = config5_record(args, local)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))

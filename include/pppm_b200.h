@@ -105,7 +105,8 @@ int pppm_set_rho(pppm_ctx* ctx, const double* rho);
 int pppm_get_rho(pppm_ctx* ctx, double* rho);
 /* replaces kspace.poisson_ik / poisson_ad (kspace.py:271-317) and
  * kspace.kspace_energy (kspace.py:320-337): one R2C, the Green multiply with the
- * energy reduced in fp64, and (want_fields) the C2R back transforms */
+ * energy reduced in fp64, and (want_fields) the C2R back transforms;
+ * want_fields = 2 also measures imag_residue (pppm_get_imag_residue) */
 int pppm_poisson(pppm_ctx* ctx, int want_fields, double* energy);
 /* ik: f0,f1,f2 = ex,ey,ez; ad: f0 = phi.  Host (nz,ny,nx) fp64 */
 int pppm_get_fields(pppm_ctx* ctx, double* f0, double* f1, double* f2);
@@ -166,6 +167,15 @@ int pppm_slab_fft_fwd(pppm_ctx* ctx);
 int pppm_slab_green(pppm_ctx* ctx);
 int pppm_slab_fft_bwd(pppm_ctx* ctx);
 int pppm_slab_fieldforce(pppm_ctx* ctx);
+/* NCCL inside the library: rank 0 creates an id (NCCL_UNIQUE_ID_BYTES = 128
+ * bytes), the host broadcasts it, every slab attaches with it (collective).
+ * pppm_ctx_step / pppm_ctx_time_steps then run the whole slab step - kernels
+ * and the ghost send/recv, transposes and energy all-reduce - on the context
+ * stream, captured into CUDA graphs per phase.  NCCL is resolved at run time
+ * (libnccl.so.2); its errors and a stalled peer (timeout_s, <= 0: 600 s,
+ * communicator aborted) are reported as PPPM_ERR_NCCL. */
+int pppm_nccl_unique_id(char* id);
+int pppm_slab_attach_nccl(pppm_ctx* ctx, const char* id, double timeout_s);
 /* kernels launched by one step (for the bench's gpu_launches claim) */
 int pppm_ctx_launches_per_step(pppm_ctx* ctx, int* launches);
 
@@ -198,10 +208,29 @@ int pppm_ctx_compute_forces(pppm_ctx* ctx, const void* positions, const void* ch
  * one compute_forces per step, positions / velocities / forces resident on the
  * device.  Host fp64 inputs; series: (steps + 1) rows of {total, kinetic,
  * potential, temperature, px, py, pz}; pos_out / vel_out (nullable): final
- * state.  Errors carry the "step k: " prefix of driver.py:345-347. */
+ * state; sections[3] / counters[2] (nullable): as pppm_ctx_compute_forces,
+ * summed over the steps + 1 force evaluations (the reference's timer and
+ * counters accumulate per compute_forces call).  Errors carry the "step k: "
+ * prefix of driver.py:345-347. */
 int pppm_ctx_integrate_nve(pppm_ctx* ctx, const double* positions, const double* velocities, const double* masses,
                            const double* charges, int64_t n, double dt, int steps, double cutoff, const double* lj,
-                           double* series, double* pos_out, double* vel_out);
+                           double* series, double* pos_out, double* vel_out, double* sections, long long* counters);
+
+/* ---- drop-in Poisson API on the full complex spectrum (kspace.py:199-337) ---- */
+/* numpy fftn / ifftn semantics (forward unnormalised, backward 1/N) on the
+ * device: the default KSpacePlan.forward / .backward (kspace.py:244).
+ * in / out: host complex128 (interleaved) arrays of shape[ndim], ndim 1..3 */
+int pppm_fftn(int device, int ndim, const int64_t* shape, const double* in, double* out, int inverse);
+/* imag_residue (kspace.py:264-268) of the last pppm_poisson(ctx, 2, ...):
+ * want_fields = 2 also expands the Green / ik half spectra to the full grid
+ * and measures max|Im| / max|Re| of their complex inverse transforms */
+int pppm_get_imag_residue(pppm_ctx* ctx, double* residue);
+/* build_plan(fft=(forward, backward)) (kspace.py:207,244): with the caller's
+ * forward transform rho_hat (host complex128 (nz, ny, nx)), out = G rho_hat
+ * (component -1) or -i k_d G rho_hat (component d = 0, 1, 2) for the caller's
+ * backward transform (kspace.py:278-312); gsum (nullable) = sum G |rho_hat|^2
+ * in a fixed order (kspace.py:335) */
+int pppm_spectrum_apply(pppm_ctx* ctx, const double* rho_hat, int component, double* out, double* gsum);
 
 #ifdef __cplusplus
 }

@@ -86,8 +86,13 @@ PROTOTYPES = {
     "pppm_singular_pair": (_c_int, [ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong), _dp]),
     "pppm_ctx_compute_forces": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_dbl, _vp, _vp, _vp, _vp,
                                          _vp]),
+    "pppm_nccl_unique_id": (_c_int, [ctypes.c_char_p]),
+    "pppm_slab_attach_nccl": (_c_int, [_vp, ctypes.c_char_p, _c_dbl]),
+    "pppm_fftn": (_c_int, [_c_int, _c_int, _vp, _vp, _vp, _c_int]),
+    "pppm_get_imag_residue": (_c_int, [_vp, _dp]),
+    "pppm_spectrum_apply": (_c_int, [_vp, _vp, _c_int, _vp, _dp]),
     "pppm_ctx_integrate_nve": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_dbl, _c_int, _c_dbl, _vp, _vp, _vp,
-                                        _vp]),
+                                        _vp, _vp, _vp]),
 }
 
 

@@ -139,23 +139,53 @@ __global__ void k_rank_cells(float4* __restrict__ rec, const int* __restrict__ c
 }
 
 // new positions (caller's order) into the brick-ordered resident array (fp32)
-template <typename TIn>
+template <int S, typename TIn>
 __global__ void k_update_resident(const TIn* __restrict__ pos, const int* __restrict__ orig, int64_t n, Geom g,
                                   float* __restrict__ res_pos, int* __restrict__ err) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = orig[k];
-    const float x = (float)pos[3 * i], y = (float)pos[3 * i + 1], z = (float)pos[3 * i + 2];
-    if (outside((double)x, g.lx) || outside((double)y, g.ly) || outside((double)z, g.lz)) atomicOr(err, 1);
+    const float x = round_pos_f32((double)pos[3 * i], g.lx), y = round_pos_f32((double)pos[3 * i + 1], g.ly),
+                z = round_pos_f32((double)pos[3 * i + 2], g.lz);
+    if (outside((double)x, g.lx) || outside((double)y, g.ly) || outside((double)z, g.lz)) {
+      atomicOr(err, 1);
+    } else if (g.nzl < g.nz) {
+      // z-slab: the atom must still be owned by this slab (bit-exact node_z)
+      int nd;
+      double t;
+      particle_map_1d<S>((double)z, g.hz, nd, t);
+      nd = nd >= g.nz ? nd - g.nz : nd;
+      if (nd < g.z0 || nd >= g.z0 + g.nzl) atomicOr(err, 2);
+    }
     res_pos[3 * k] = x;
     res_pos[3 * k + 1] = y;
     res_pos[3 * k + 2] = z;
   }
 }
 
-int launch_update_resident(bool f32, const void* pos, const int* orig, int64_t n, const Geom& g, float* res_pos,
-                           int* err, cudaStream_t s) {
-  if (f32) k_update_resident<float><<<grid_for(n), kThreads, 0, s>>>((const float*)pos, orig, n, g, res_pos, err);
-  else k_update_resident<double><<<grid_for(n), kThreads, 0, s>>>((const double*)pos, orig, n, g, res_pos, err);
+int launch_update_resident(int order, bool f32, const void* pos, const int* orig, int64_t n, const Geom& g,
+                           float* res_pos, int* err, cudaStream_t s) {
+  const int st = with_order(order, [&](auto S_) {
+    constexpr int S = decltype(S_)::value;
+    if (f32)
+      k_update_resident<S, float><<<grid_for(n), kThreads, 0, s>>>((const float*)pos, orig, n, g, res_pos, err);
+    else
+      k_update_resident<S, double><<<grid_for(n), kThreads, 0, s>>>((const double*)pos, orig, n, g, res_pos, err);
+    return 0;
+  });
+  return st ? st : launch_status();
+}
+
+// fp64 positions -> fp32 residents with the fold of round_pos_f32
+__global__ void k_round_positions(const double* __restrict__ pos, int64_t n, Geom g, float* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    out[3 * k] = round_pos_f32(pos[3 * k], g.lx);
+    out[3 * k + 1] = round_pos_f32(pos[3 * k + 1], g.ly);
+    out[3 * k + 2] = round_pos_f32(pos[3 * k + 2], g.lz);
+  }
+}
+
+int launch_round_positions(const double* pos, int64_t n, const Geom& g, float* out, cudaStream_t s) {
+  k_round_positions<<<grid_for(n), kThreads, 0, s>>>(pos, n, g, out);
   return launch_status();
 }
 

@@ -22,9 +22,9 @@ __global__ void k_particle_map(const TIn* __restrict__ pos, int64_t n, Geom g,
                                int32_t* __restrict__ nodes, int* __restrict__ err) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_real<TIn, R32>(pos, 3 * i + 0);
-    const double y = load_real<TIn, R32>(pos, 3 * i + 1);
-    const double z = load_real<TIn, R32>(pos, 3 * i + 2);
+    const double x = load_pos<TIn, R32>(pos, 3 * i + 0, g.lx);
+    const double y = load_pos<TIn, R32>(pos, 3 * i + 1, g.ly);
+    const double z = load_pos<TIn, R32>(pos, 3 * i + 2, g.lz);
     if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) atomicOr(err, 1);
     int nd;
     double t;
@@ -111,9 +111,9 @@ __global__ void __launch_bounds__(kThreads) k_spread_fix64(
   const double scale = *scale_p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_real<TIn, R32>(pos, 3 * i + 0);
-    const double y = load_real<TIn, R32>(pos, 3 * i + 1);
-    const double z = load_real<TIn, R32>(pos, 3 * i + 2);
+    const double x = load_pos<TIn, R32>(pos, 3 * i + 0, g.lx);
+    const double y = load_pos<TIn, R32>(pos, 3 * i + 1, g.ly);
+    const double z = load_pos<TIn, R32>(pos, 3 * i + 2, g.lz);
     const double q = load_real<TIn, R32>(qv, i);
     if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
       atomicOr(err, 1);
@@ -334,9 +334,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_direct(
   constexpr int lo = Stencil<S>::lo;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_real<TIn, R32>(pos, 3 * i + 0);
-    const double y = load_real<TIn, R32>(pos, 3 * i + 1);
-    const double z = load_real<TIn, R32>(pos, 3 * i + 2);
+    const double x = load_pos<TIn, R32>(pos, 3 * i + 0, g.lx);
+    const double y = load_pos<TIn, R32>(pos, 3 * i + 1, g.ly);
+    const double z = load_pos<TIn, R32>(pos, 3 * i + 2, g.lz);
     const double q = load_real<TIn, R32>(qv, i);
     if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
       atomicOr(err, 1);

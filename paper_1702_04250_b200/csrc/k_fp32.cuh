@@ -111,9 +111,9 @@ __global__ void __launch_bounds__(kThreads, (S >= 6 ? 4 : PPPM_BIN_MINB)) k_bin_
       const int64_t i = i0 + u * stride;
       b[u] = -1;
       if (i >= n) continue;
-      const double x = load_real<TIn, true>(pos, 3 * i + 0);
-      const double y = load_real<TIn, true>(pos, 3 * i + 1);
-      const double z = load_real<TIn, true>(pos, 3 * i + 2);
+      const double x = load_pos<TIn, true>(pos, 3 * i + 0, g.lx);
+      const double y = load_pos<TIn, true>(pos, 3 * i + 1, g.ly);
+      const double z = load_pos<TIn, true>(pos, 3 * i + 2, g.lz);
       const float q = (float)qv[i];
       if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
         atomicOr(err, 1);
@@ -272,6 +272,10 @@ __device__ __forceinline__ int atom_record(const Resident& res, int64_t i, const
   n0 = n0 >= g.nx ? n0 - g.nx : n0;
   n1 = n1 >= g.ny ? n1 - g.ny : n1;
   n2 = n2 >= g.nz ? n2 - g.nz : n2;
+  // z-slab: slab-local plane (ownership is checked when positions are updated,
+  // k_update_resident; the clamp only keeps a stale atom inside the mesh)
+  n2 -= g.z0;
+  n2 = n2 < 0 ? 0 : (n2 >= g.nzl ? g.nzl - 1 : n2);
   lc = (((n2 % kBrick) * kBrick) + (n1 % kBrick)) * kBrick + (n0 % kBrick);
   pk = n0 | (n1 << 10) | (n2 << 20);
   if (TAB) {

@@ -480,10 +480,22 @@ int launch_series_row(const double* v, const double* m, int64_t n, double* tmp4,
   return launch_status();
 }
 
+// Python's float floor division a // b (CPython float_floor_div): the cell
+// count int(L // cutoff) of shortrange.py differs from (int)(L / rc) whenever
+// the quotient rounds up to an integer (L = 3.0, rc = 0.1: 29, not 30)
+int py_floordiv_int(double a, double b) {
+  double mod = fmod(a, b);
+  double div = (a - mod) / b;
+  if (mod != 0.0 && ((b < 0) != (mod < 0))) div -= 1.0;
+  double fl = floor(div);
+  if (div - fl > 0.5) fl += 1.0;
+  return (int)fl;
+}
+
 PairGeom make_pair_geom(double lx, double ly, double lz, double rc) {
   PairGeom pg{};
   pg.lx = lx; pg.ly = ly; pg.lz = lz;
-  pg.nx = (int)(lx / rc); pg.ny = (int)(ly / rc); pg.nz = (int)(lz / rc);  // int(L // rc)
+  pg.nx = py_floordiv_int(lx, rc); pg.ny = py_floordiv_int(ly, rc); pg.nz = py_floordiv_int(lz, rc);  // int(L // rc)
   if (pg.nx < 1) pg.nx = 1;
   if (pg.ny < 1) pg.ny = 1;
   if (pg.nz < 1) pg.nz = 1;

@@ -9,8 +9,11 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cufft.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <functional>
+#include <chrono>
 #include <cmath>
 #include <vector>
 #include <cstdio>
@@ -20,6 +23,7 @@
 #include <type_traits>
 #include <utility>
 
+#include "nccl_dyn.h"
 #include "../../include/pppm_b200.h"
 #include "pppm_types.h"
 
@@ -171,6 +175,17 @@ struct pppm_ctx {
   bool warm[SP_COUNT] = {};
   int sp_launches[SP_COUNT] = {};  // our kernels per sub-phase (counted on the eager run)
   int launches = 0;
+  // full-complex helpers of the drop-in API (k_spectral.cu): imag_residue and
+  // caller-supplied transforms
+  cufftHandle cplan = 0;
+  bool cplan_ok = false;
+  DevBuf spec_full, g_full, e_elem, amax, sum_part;
+  bool g_full_ok = false;
+  double imag_residue = 0.0;
+  // z-slab exchanges inside the library: an NCCL communicator over the P slabs
+  // (pppm_slab_attach_nccl), used on the context stream and inside its graphs
+  ncclComm_t comm = nullptr;
+  double nccl_timeout_s = 600.0;
 
   bool fp64() const { return prec == PPPM_PREC_FP64; }
   size_t real_size() const { return fp64() ? sizeof(double) : sizeof(float); }
@@ -193,13 +208,52 @@ static int activate(pppm_ctx* c) {
   return PPPM_OK;
 }
 
+static int nccl_fail(ncclResult_t r, const char* what) {
+  std::string why;
+  const NcclApi* nc = nccl_api(&why);
+  return fail(PPPM_ERR_NCCL, std::string(what) + ": " + (nc ? nc->GetErrorString(r) : why));
+}
+
+// wait for the context stream; with an NCCL communicator attached, poll its
+// asynchronous error state and give up (abort the communicator) after the
+// timeout instead of blocking forever on a dead peer
+static int stream_wait(pppm_ctx* c) {
+  if (!c->comm) {
+    CU(cudaStreamSynchronize(c->stream));
+    return PPPM_OK;
+  }
+  const NcclApi* nc = nccl_api(nullptr);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return fail(PPPM_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(q));
+    ncclResult_t ae = ncclSuccess;
+    if (nc->CommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+      nc->CommAbort(c->comm);
+      c->comm = nullptr;
+      return nccl_fail(ae, "NCCL asynchronous error (communicator aborted)");
+    }
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (dt > c->nccl_timeout_s) {
+      nc->CommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(PPPM_ERR_NCCL, "NCCL exchange timed out (communicator aborted; a peer slab stopped?)");
+    }
+    usleep(50);
+  }
+  return PPPM_OK;
+}
+
 static int check_err_flag(pppm_ctx* c) {
   CU(cudaMemcpyAsync(c->h_err, c->err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
+  TRY(stream_wait(c));
   if (*c->h_err) {
+    const int e = *c->h_err;
     *c->h_err = 0;
     CU(cudaMemsetAsync(c->err.p, 0, sizeof(int), c->stream));
-    return fail(PPPM_ERR_RUNTIME, "positions must be wrapped into the box before mapping");
+    if (e & 1) return fail(PPPM_ERR_RUNTIME, "positions must be wrapped into the box before mapping");
+    return fail(PPPM_ERR_STATE, "atoms left their z-slab: migrate them to their owner slab (SlabStep.migrate)");
   }
   return PPPM_OK;
 }
@@ -358,15 +412,24 @@ static int bucket_cap(pppm_ctx* c, int64_t n) {
   return (int)cap;
 }
 
+// The bucket capacity only grows (a one-shot call with fewer atoms keeps the
+// resident step's capacity); captured graphs hold these pointers and the
+// capacity, so any change drops them.
 static int ensure_bins(pppm_ctx* c, int64_t n) {
   const int nb = c->bk.count();
-  c->cap = bucket_cap(c, n);
+  const void* before[5] = {c->counts.p, c->rec.p, c->ovf_rec.p, c->ovf_cell.p, c->ovf_perm.p};
+  const int cap0 = c->cap;
+  c->cap = std::max(c->cap, bucket_cap(c, n));
   const int64_t slots = (int64_t)nb * c->cap;
   TRY(c->counts.ensure(sizeof(int) * (nb + 2) * kCountStride));
   TRY(c->rec.ensure(2 * sizeof(float4) * slots));  // 32-byte slots (k_fp32.cuh)
   TRY(c->ovf_rec.ensure(sizeof(float4) * n));
   TRY(c->ovf_cell.ensure(sizeof(int) * n));
   TRY(c->ovf_perm.ensure(sizeof(int) * n));
+  const void* after[5] = {c->counts.p, c->rec.p, c->ovf_rec.p, c->ovf_cell.p, c->ovf_perm.p};
+  bool changed = cap0 != c->cap;
+  for (int i = 0; i < 5; ++i) changed |= before[i] != after[i];
+  if (changed) drop_graphs(c);
   return PPPM_OK;
 }
 
@@ -509,6 +572,45 @@ static int run_fft_bwd(pppm_ctx* c) {
   return PPPM_OK;
 }
 
+// imag_residue of the back transforms (kspace.py:264-268): the Green / ik half
+// spectra in ework (non-fused layout [f][half], before the C2R, which may
+// overwrite its input) are expanded to the full grid by Hermitian symmetry and
+// transformed back with a complex inverse FFT; max |Im| / max |Re| over fields
+static int run_imag_residue(pppm_ctx* c) {
+  if (c->slab) return fail(PPPM_ERR_STATE, "imag_residue is not available on a slab context");
+  const bool d = c->fp64();
+  if (!c->cplan_ok) {
+    FFT(cufftPlan3d(&c->cplan, c->g.nz, c->g.ny, c->g.nx, d ? CUFFT_Z2Z : CUFFT_C2C));
+    FFT(cufftSetStream(c->cplan, c->stream));
+    c->cplan_ok = true;
+  }
+  const size_t cs = 2 * c->real_size();
+  TRY(c->spec_full.ensure(cs * c->M));
+  TRY(c->amax.ensure(16));
+  double worst = 0.0;
+  for (int f = 0; f < c->nfields(); ++f) {
+    CU(cudaMemsetAsync(c->amax.p, 0, 16, c->stream));
+    TRY(launch_hermitian_expand(d, (const char*)c->ework.p + cs * c->half * f, c->spec_full.p, c->g.nx, c->g.ny,
+                                c->g.nz, c->stream));
+    if (d)
+      FFT(cufftExecZ2Z(c->cplan, c->spec_full.as<cufftDoubleComplex>(), c->spec_full.as<cufftDoubleComplex>(),
+                       CUFFT_INVERSE));
+    else
+      FFT(cufftExecC2C(c->cplan, c->spec_full.as<cufftComplex>(), c->spec_full.as<cufftComplex>(), CUFFT_INVERSE));
+    TRY(launch_abs_max(d, c->spec_full.p, c->M, c->amax.as<unsigned long long>(), c->stream));
+    unsigned long long h[2];
+    CU(cudaMemcpyAsync(h, c->amax.p, 16, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    double re, im;
+    memcpy(&re, &h[0], 8);
+    memcpy(&im, &h[1], 8);
+    if (re > 0.0) worst = std::max(worst, im / re);  // kspace.py:264-268 (0 for a zero field)
+    c->launches += 2;
+  }
+  c->imag_residue = worst;
+  return PPPM_OK;
+}
+
 // fieldforce ---------------------------------------------------------------------
 // out: device buffer of (n, 3) fp64 (out_f64) or fp32
 static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, void* out,
@@ -625,6 +727,51 @@ void pppm_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+// numpy fftn / ifftn semantics (forward unnormalised, backward 1/N) on the
+// device: the default (forward, backward) pair of a KSpacePlan (kspace.py:244).
+// in / out: host complex128 arrays of `shape` (C order), may alias
+int pppm_fftn(int device, int ndim, const int64_t* shape, const double* in, double* out, int inverse) {
+  if (ndim < 1 || ndim > 3) return fail(PPPM_ERR_VALUE, "the device transform supports 1 to 3 dimensions");
+  if (!shape || !in || !out) return fail(PPPM_ERR_VALUE, "null argument");
+  int n[3] = {1, 1, 1};
+  int64_t total = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (shape[i] < 1 || shape[i] > (1 << 30)) return fail(PPPM_ERR_VALUE, "invalid transform shape");
+    n[i] = (int)shape[i];
+    total *= shape[i];
+  }
+  CU(cudaSetDevice(device));
+  cudaStream_t s = nullptr;
+  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  DevBuf buf;
+  cufftHandle plan = 0;
+  bool have_plan = false;
+  int st = buf.ensure(16 * total);
+  auto done = [&](int r) {
+    if (s) cudaStreamSynchronize(s);
+    if (have_plan) cufftDestroy(plan);
+    buf.release();
+    if (s) cudaStreamDestroy(s);
+    return r;
+  };
+  if (st != PPPM_OK) return done(st);
+  if (cufftPlanMany(&plan, ndim, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_Z2Z, 1) != CUFFT_SUCCESS)
+    return done(fail(PPPM_ERR_CUFFT, "cufftPlanMany (fftn) failed"));
+  have_plan = true;
+  if (cufftSetStream(plan, s) != CUFFT_SUCCESS) return done(fail(PPPM_ERR_CUFFT, "cufftSetStream failed"));
+  if (cudaMemcpyAsync(buf.p, in, 16 * total, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return done(fail(PPPM_ERR_CUDA, "fftn upload failed"));
+  if (cufftExecZ2Z(plan, buf.as<cufftDoubleComplex>(), buf.as<cufftDoubleComplex>(),
+                   inverse ? CUFFT_INVERSE : CUFFT_FORWARD) != CUFFT_SUCCESS)
+    return done(fail(PPPM_ERR_CUFFT, "cufftExecZ2Z (fftn) failed"));
+  if (inverse && launch_scale_complex(buf.as<double2>(), total, 1.0 / (double)total, s) != 0)
+    return done(PPPM_ERR_CUDA);
+  if (cudaMemcpyAsync(out, buf.p, 16 * total, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return done(fail(PPPM_ERR_CUDA, "fftn download failed"));
+  if (cudaStreamSynchronize(s) != cudaSuccess) return done(fail(PPPM_ERR_CUDA, "fftn failed"));
+  return done(PPPM_OK);
+}
+
 int pppm_weight_rows(int device, int order, const double* t, int64_t n, double* assign, double* deriv) {
   if (n < 0) return fail(PPPM_ERR_VALUE, "negative count");
   if (n == 0) return PPPM_OK;
@@ -677,6 +824,9 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (!(alpha > 0.0)) return fail(PPPM_ERR_CONFIG, "alpha must be positive");
   if (!(dielectric > 0.0)) return fail(PPPM_ERR_CONFIG, "dielectric must be positive");
   if (P < 1 || rank < 0 || rank >= P) return fail(PPPM_ERR_VALUE, "bad slab rank / count");
+  // overflow records pack the wrapped node as 10 + 10 + 10 bits (k_fp32.cuh)
+  if (precision == PPPM_PREC_MIXED && (nx > 1024 || ny > 1024 || nz > 1024))
+    return fail(PPPM_ERR_CONFIG, "mixed precision supports grid dimensions up to 1024");
   if (slab) {
     if (precision != PPPM_PREC_MIXED) return fail(PPPM_ERR_CONFIG, "z-slab decomposition runs in mixed precision");
     if (nz % P || ny % P) return fail(PPPM_ERR_CONFIG, "nz and ny must be divisible by the slab count");
@@ -818,6 +968,11 @@ int pppm_ctx_destroy(pppm_ctx* c) {
       cufftDestroy(c->bwd2);
     }
   }
+  if (c->comm) {
+    if (const NcclApi* nc = nccl_api(nullptr)) nc->CommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  if (c->cplan_ok) cufftDestroy(c->cplan);
   if (c->slab_plans) {
     cufftDestroy(c->p2f);
     cufftDestroy(c->pz);
@@ -829,7 +984,8 @@ int pppm_ctx_destroy(pppm_ctx* c) {
                     &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone, &c->res_novf, &c->ptw,
                     &c->pr_cell, &c->pr_count, &c->pr_start, &c->pr_cursor, &c->pr_order, &c->pr_tmp, &c->pr_force,
                     &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal, &c->pr_sp,
-                    &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series};
+                    &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series,
+                    &c->spec_full, &c->g_full, &c->e_elem, &c->amax, &c->sum_part};
   for (DevBuf* b : bufs) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -897,6 +1053,7 @@ int pppm_ctx_build_influence(pppm_ctx* c, int kind, double deconv_floor) {
   c->have_green = true;
   c->green_kind = kind;
   c->green_floor = deconv_floor;
+  c->g_full_ok = false;
   return PPPM_OK;
 }
 
@@ -911,9 +1068,13 @@ int pppm_ctx_set_influence(pppm_ctx* c, const double* g_full) {
   else {
     TRY(launch_convert(false, c->out_stage.p, c->green.p, c->half, c->stream));
   }
+  // the full grid too, for caller-supplied transforms (pppm_spectrum_apply)
+  TRY(c->g_full.ensure(8 * c->M));
+  CU(cudaMemcpyAsync(c->g_full.p, g_full, 8 * c->M, cudaMemcpyHostToDevice, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   c->have_green = true;
   c->green_kind = -1;
+  c->g_full_ok = true;
   return PPPM_OK;
 }
 
@@ -978,7 +1139,14 @@ int pppm_get_rho(pppm_ctx* c, double* rho) {
 int pppm_poisson(pppm_ctx* c, int want_fields, double* energy) {
   TRY(activate(c));
   if (!c->have_rho) return fail(PPPM_ERR_STATE, "no charge grid on the device");
-  if (want_fields) {
+  if (want_fields == 2) {
+    // fields + imag_residue: unfused 3D transforms, residue measured before the C2R
+    TRY(ensure_plans(c));
+    TRY(run_fft_fwd(c));
+    TRY(run_green(c, true));
+    TRY(run_imag_residue(c));
+    TRY(run_fft_bwd(c));
+  } else if (want_fields) {
     TRY(run_poisson(c));
   } else {
     TRY(run_fft_fwd(c));
@@ -991,6 +1159,51 @@ int pppm_poisson(pppm_ctx* c, int want_fields, double* energy) {
   } else {
     CU(cudaStreamSynchronize(c->stream));
   }
+  return PPPM_OK;
+}
+
+int pppm_get_imag_residue(pppm_ctx* c, double* residue) {
+  if (!c || !residue) return fail(PPPM_ERR_VALUE, "null argument");
+  *residue = c->imag_residue;
+  return PPPM_OK;
+}
+
+// caller-supplied transforms (build_plan(fft=...), kspace.py:207,244): host full
+// complex rho_hat (nz, ny, nx) -> host full complex G rho_hat (component -1) or
+// -i k_d G rho_hat (component 0, 1, 2); gsum (nullable) = sum G |rho_hat|^2
+int pppm_spectrum_apply(pppm_ctx* c, const double* rho_hat, int component, double* out, double* gsum) {
+  TRY(activate(c));
+  if (!rho_hat) return fail(PPPM_ERR_VALUE, "null spectrum");
+  if (component < -1 || component > 2) return fail(PPPM_ERR_VALUE, "component must be -1 (phi) or 0, 1, 2");
+  if (c->slab) return fail(PPPM_ERR_STATE, "not available on a slab context");
+  if (!c->have_green) return fail(PPPM_ERR_STATE, "influence function not built");
+  if (!c->g_full_ok) {
+    if (c->green_kind < 0) return fail(PPPM_ERR_STATE, "influence function not available as a full grid");
+    GreenSpec s{c->g.nx, c->g.ny, c->g.nz, c->order, c->g.lx, c->g.ly, c->g.lz, c->alpha, c->green_floor,
+                c->green_kind == PPPM_INFLUENCE_OPTIMAL};
+    TRY(c->g_full.ensure(8 * c->M));
+    TRY(launch_influence(true, s, 0, c->g.ny, nullptr, c->g_full.as<double>(), c->stream));
+    c->g_full_ok = true;
+  }
+  TRY(c->spec_full.ensure(16 * c->M));
+  CU(cudaMemcpyAsync(c->spec_full.p, rho_hat, 16 * c->M, cudaMemcpyHostToDevice, c->stream));
+  double2* sp = c->spec_full.as<double2>();
+  double* e = nullptr;
+  if (gsum) {
+    TRY(c->e_elem.ensure(8 * c->M));
+    e = c->e_elem.as<double>();
+  }
+  TRY(launch_spectrum_apply(sp, c->g_full.as<double>(), c->ik64.as<double>(), component, c->g.nx, c->g.ny, c->g.nz,
+                            out ? sp : nullptr, e, c->stream));
+  c->launches += 1;
+  if (gsum) {
+    TRY(c->sum_part.ensure(8 * 1024));
+    TRY(launch_sum(e, c->M, c->sum_part.as<double>(), 1.0, c->scal.as<double>() + 4, c->stream));
+    CU(cudaMemcpyAsync(gsum, c->scal.as<double>() + 4, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->launches += 2;
+  }
+  if (out) CU(cudaMemcpyAsync(out, sp, 16 * c->M, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   return PPPM_OK;
 }
 
@@ -1063,7 +1276,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   c->res_sorted = false;
   c->res_maxcnt = 0;
   c->novf_clean = false;
-  if (!c->fp64() && c->sort_resident && !c->slab) {  // single-mesh contexts only
+  if (!c->fp64() && c->sort_resident) {
     // keep the resident atoms in brick order (as an MD engine sorts its atoms):
     // bin once, then gather positions / charges into bucket order
     TRY(run_bin(c, c->res_pos.p, c->res_q.p, n, dtype, nullptr));
@@ -1081,7 +1294,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
       // mixed precision maps fp32-rounded positions anyway: keep fp32 residents
       TRY(c->res_tmp_pos.ensure(3 * n * sizeof(float)));
       TRY(c->res_tmp_q.ensure(n * sizeof(float)));
-      TRY(launch_convert(false, c->res_pos.p, c->res_tmp_pos.p, 3 * n, c->stream));
+      TRY(launch_round_positions(c->res_pos.as<double>(), n, c->g, c->res_tmp_pos.as<float>(), c->stream));
       TRY(launch_convert(false, c->res_q.p, c->res_tmp_q.p, n, c->stream));
       std::swap(c->res_pos, c->res_tmp_pos);
       std::swap(c->res_q, c->res_tmp_q);
@@ -1105,6 +1318,112 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
 }
 
 
+// ---------------------------------------------------------------------------
+// z-slab exchanges over NCCL on the context stream (slab.py has the
+// same schedule over torch.distributed for the CPU / loopback checks)
+
+static const NcclApi* slab_nccl(pppm_ctx* c) {
+  std::string why;
+  const NcclApi* nc = nccl_api(&why);
+  if (!nc) {
+    fail(PPPM_ERR_NCCL, why);
+    return nullptr;
+  }
+  if (!c->comm) {
+    fail(PPPM_ERR_STATE, "slab context has no NCCL communicator (pppm_slab_attach_nccl)");
+    return nullptr;
+  }
+  return nc;
+}
+
+#define NC(call, what)                                \
+  do {                                                \
+    const ncclResult_t r_ = (call);                   \
+    if (r_ != ncclSuccess) return nccl_fail(r_, what); \
+  } while (0)
+
+static int grouped(const NcclApi* nc, const std::function<int()>& body) {
+  NC(nc->GroupStart(), "ncclGroupStart");
+  const int st = body();
+  const ncclResult_t r = nc->GroupEnd();
+  if (st != PPPM_OK) return st;
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+  return PPPM_OK;
+}
+
+// ghost planes of rho reverse-summed: my lower ghosts to the slab below (into
+// its RECV_HI), my upper ghosts to the slab above (into its RECV_LO); then
+// the received planes are added into the first / last H owned planes
+static int slab_ghost_sum(pppm_ctx* c) {
+  const NcclApi* nc = slab_nccl(c);
+  if (!nc) return PPPM_ERR_NCCL;
+  const size_t plane = (size_t)c->pd.py * c->pd.px, n = plane * c->pd.H;
+  const int prev = (c->rank - 1 + c->P) % c->P, next = (c->rank + 1) % c->P;
+  float* rho = c->rho.as<float>();
+  TRY(grouped(nc, [&]() -> int {
+    NC(nc->Send(rho, n, ncclFloat32, prev, c->comm, c->stream), "ncclSend");
+    NC(nc->Send(rho + plane * (c->pd.H + c->g.nzl), n, ncclFloat32, next, c->comm, c->stream), "ncclSend");
+    NC(nc->Recv(c->ghost_hi.p, n, ncclFloat32, next, c->comm, c->stream), "ncclRecv");
+    NC(nc->Recv(c->ghost_lo.p, n, ncclFloat32, prev, c->comm, c->stream), "ncclRecv");
+    return PPPM_OK;
+  }));
+  TRY(launch_add_planes(c->ghost_lo.as<float>(), rho + plane * c->pd.H, (int64_t)n, c->stream));
+  TRY(launch_add_planes(c->ghost_hi.as<float>(), rho + plane * c->g.nzl, (int64_t)n, c->stream));
+  c->launches += 2;
+  return PPPM_OK;
+}
+
+// all-to-all of equal chunks (the FFT transposes): chunk p of send goes to slab p
+static int slab_a2a(pppm_ctx* c, const float* send, float* recv, size_t floats) {
+  const NcclApi* nc = slab_nccl(c);
+  if (!nc) return PPPM_ERR_NCCL;
+  const size_t chunk = floats / c->P;
+  return grouped(nc, [&]() -> int {
+    for (int p = 0; p < c->P; ++p) {
+      NC(nc->Send(send + chunk * p, chunk, ncclFloat32, p, c->comm, c->stream), "ncclSend");
+      NC(nc->Recv(recv + chunk * p, chunk, ncclFloat32, p, c->comm, c->stream), "ncclRecv");
+    }
+    return PPPM_OK;
+  });
+}
+
+// boundary planes of the fields forward-copied into the neighbours' ghosts
+static int slab_ghost_fwd(pppm_ctx* c) {
+  const NcclApi* nc = slab_nccl(c);
+  if (!nc) return PPPM_ERR_NCCL;
+  const size_t plane = (size_t)c->pd.py * c->pd.px, n = plane * c->pd.H;
+  const int prev = (c->rank - 1 + c->P) % c->P, next = (c->rank + 1) % c->P;
+  return grouped(nc, [&]() -> int {
+    for (int f = 0; f < c->nfields(); ++f) {
+      float* fl = c->fields.as<float>() + (size_t)c->pd.count() * f;
+      NC(nc->Send(fl + plane * c->g.nzl, n, ncclFloat32, next, c->comm, c->stream), "ncclSend");     // top
+      NC(nc->Send(fl + plane * c->pd.H, n, ncclFloat32, prev, c->comm, c->stream), "ncclSend");      // bottom
+      NC(nc->Recv(fl, n, ncclFloat32, prev, c->comm, c->stream), "ncclRecv");                         // ghost lo
+      NC(nc->Recv(fl + plane * (c->pd.H + c->g.nzl), n, ncclFloat32, next, c->comm, c->stream), "ncclRecv");
+    }
+    return PPPM_OK;
+  });
+}
+
+static int slab_fft_fwd(pppm_ctx* c);
+static int slab_green(pppm_ctx* c);
+static int slab_fft_bwd(pppm_ctx* c);
+
+// the distributed Poisson solve: planes R2C -> transpose -> z FFT / Green / ik /
+// energy -> energy all-reduce + transpose back -> planes C2R -> field ghosts
+static int slab_poisson(pppm_ctx* c) {
+  const NcclApi* nc = slab_nccl(c);
+  if (!nc) return PPPM_ERR_NCCL;
+  const size_t a2a = (size_t)c->half * 2;  // floats per field
+  TRY(slab_fft_fwd(c));
+  TRY(slab_a2a(c, c->a2a_send.as<float>(), c->a2a_recv.as<float>(), a2a));
+  TRY(slab_green(c));
+  NC(nc->AllReduce(c->scal.p, c->scal.p, 1, ncclFloat64, ncclSum, c->comm, c->stream), "ncclAllReduce");
+  TRY(slab_a2a(c, c->a2a_send.as<float>(), c->a2a_recv.as<float>(), a2a * c->nfields()));
+  TRY(slab_fft_bwd(c));
+  return slab_ghost_fwd(c);
+}
+
 static bool resident_step(const pppm_ctx* c) {
   return !c->fp64() && c->res_sorted && c->res_direct && c->res_dtype == PPPM_F32;
 }
@@ -1119,7 +1438,7 @@ static int run_subphase(pppm_ctx* c, int sp) {
       if (resident_step(c)) return PPPM_OK;  // make_rho maps the positions itself
       // sorted resident atoms: slots carry the resident index (forces land in
       // brick order, contiguous per brick) and get_forces un-permutes
-      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, nullptr));
+      if (!c->fp64()) TRY(run_bin(c, p, q, n, c->res_dtype, c->slab && c->res_sorted ? c->res_orig.as<int>() : nullptr));
       return PPPM_OK;
     case SP_SPREAD:
       if (resident_step(c)) {
@@ -1127,11 +1446,13 @@ static int run_subphase(pppm_ctx* c, int sp) {
         // make_rho (launch_subphase: a memset outside the graph unless the last
         // fieldforce cleared it)
         c->novf_clean = false;
-        return run_spread(c, p, q, n, c->res_dtype, true);
+        TRY(run_spread(c, p, q, n, c->res_dtype, true));
+      } else {
+        TRY(run_spread(c, p, q, n, c->res_dtype));
       }
-      return run_spread(c, p, q, n, c->res_dtype);
+      return c->slab ? slab_ghost_sum(c) : PPPM_OK;  // z ghosts reverse-summed over NCCL
     case SP_POISSON:
-      return run_poisson(c);
+      return c->slab ? slab_poisson(c) : run_poisson(c);
     case SP_GATHER:
       TRY(do_fieldforce(c, p, q, n, c->res_dtype, !c->binned, c->res_force.p, c->fp64(), resident_step(c)));
       // k_gather_ws (dynamic scheduling) clears the mover counter at its end
@@ -1234,7 +1555,7 @@ int pppm_ctx_update_positions(pppm_ctx* c, const void* pos, int dtype, int mem) 
     CU(cudaMemcpyAsync(c->pos_stage.p, pos, 3 * c->n_res * es, cudaMemcpyHostToDevice, c->stream));
     dp = c->pos_stage.p;
   }
-  TRY(launch_update_resident(dtype == PPPM_F32, dp, c->res_orig.as<int>(), c->n_res, c->g, c->res_pos.as<float>(),
+  TRY(launch_update_resident(c->order, dtype == PPPM_F32, dp, c->res_orig.as<int>(), c->n_res, c->g, c->res_pos.as<float>(),
                              c->err.as<int>(), c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return check_err_flag(c);
@@ -1403,6 +1724,11 @@ int pppm_slab_make_rho(pppm_ctx* c) {
   TRY(activate(c));
   if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
   c->binned = false;
+  if (resident_step(c)) {  // brick-ordered residents: make_rho maps them itself
+    if (!c->novf_clean) CU(cudaMemsetAsync(c->res_novf.p, 0, sizeof(int), c->stream));
+    c->novf_clean = false;
+    return run_spread(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype, true);
+  }
   TRY(run_bin(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype, c->res_sorted ? c->res_orig.as<int>() : nullptr));
   return run_spread(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype);
 }
@@ -1422,6 +1748,10 @@ int pppm_slab_add_ghosts(pppm_ctx* c) {
 // 2D R2C of the local planes, packed per destination ky chunk (A2A_SEND)
 int pppm_slab_fft_fwd(pppm_ctx* c) {
   TRY(activate(c));
+  return slab_fft_fwd(c);
+}
+
+static int slab_fft_fwd(pppm_ctx* c) {
   TRY(ensure_slab_plans(c));
   if (c->plane)
     TRY(launch_plane_r2c(c->g.nx, c->g.ny, c->g.nzl, c->rho.as<float>(), c->pd, c->spec2d.as<float2>(),
@@ -1438,6 +1768,10 @@ int pppm_slab_fft_fwd(pppm_ctx* c) {
 // of the field spectra, packed per destination slab (A2A_SEND_F)
 int pppm_slab_green(pppm_ctx* c) {
   TRY(activate(c));
+  return slab_green(c);
+}
+
+static int slab_green(pppm_ctx* c) {
   TRY(ensure_slab_plans(c));
   if (!c->have_green) return fail(PPPM_ERR_STATE, "influence function not built");
   cufftComplex* spec = c->a2a_recv.as<cufftComplex>();
@@ -1468,6 +1802,10 @@ int pppm_slab_green(pppm_ctx* c) {
 // (FIELD_BOTTOM/TOP) are then ready to be copied into the neighbours' ghosts
 int pppm_slab_fft_bwd(pppm_ctx* c) {
   TRY(activate(c));
+  return slab_fft_bwd(c);
+}
+
+static int slab_fft_bwd(pppm_ctx* c) {
   TRY(ensure_slab_plans(c));
   const int nf = c->nfields();
   TRY(launch_unpack_bwd(c->g, c->P, nf, c->a2a_recv.p, c->spec2d.p, c->stream));
@@ -1491,7 +1829,43 @@ int pppm_slab_fft_bwd(pppm_ctx* c) {
 int pppm_slab_fieldforce(pppm_ctx* c) {
   TRY(activate(c));
   if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
-  return do_fieldforce(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype, !c->binned, c->res_force.p, false);
+  TRY(do_fieldforce(c, c->res_pos.p, c->res_q.p, c->n_res, c->res_dtype, !c->binned, c->res_force.p, false,
+                    resident_step(c)));
+  c->novf_clean = resident_step(c) && c->dyn_sched && gather_eff(c) == GATHER_WS;
+  return PPPM_OK;
+}
+
+// NCCL bootstrap: rank 0 makes the id, the caller broadcasts it (torch.distributed)
+int pppm_nccl_unique_id(char* id) {
+  if (!id) return fail(PPPM_ERR_VALUE, "null argument");
+  std::string why;
+  const NcclApi* nc = nccl_api(&why);
+  if (!nc) return fail(PPPM_ERR_NCCL, why);
+  ncclUniqueId u;
+  NC(nc->GetUniqueId(&u), "ncclGetUniqueId");
+  memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  return PPPM_OK;
+}
+
+// every slab calls this with the same id (a collective: blocks until all P
+// ranks joined); the communicator is then used by pppm_ctx_step / time_steps
+int pppm_slab_attach_nccl(pppm_ctx* c, const char* id, double timeout_s) {
+  TRY(activate(c));
+  if (!c->slab) return fail(PPPM_ERR_STATE, "not a slab context");
+  if (!id) return fail(PPPM_ERR_VALUE, "null argument");
+  std::string why;
+  const NcclApi* nc = nccl_api(&why);
+  if (!nc) return fail(PPPM_ERR_NCCL, why);
+  if (c->comm) {
+    nc->CommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  drop_graphs(c);
+  ncclUniqueId u;
+  memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+  NC(nc->CommInitRank(&c->comm, c->P, u, c->rank), "ncclCommInitRank");
+  if (timeout_s > 0) c->nccl_timeout_s = timeout_s;
+  return PPPM_OK;
 }
 
 int pppm_ctx_launches_per_step(pppm_ctx* c, int* launches) {
@@ -1556,8 +1930,8 @@ static int stage_f64(pppm_ctx* c, const void* pos, const void* q, int64_t n, int
 // to report unwrapped positions / overlapping atoms
 static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double alpha, double rc,
                        const double* lj, long long* counters) {
-  const int cx = std::max(1, (int)(c->g.lx / rc)), cy = std::max(1, (int)(c->g.ly / rc)),
-            cz = std::max(1, (int)(c->g.lz / rc));
+  const int cx = std::max(1, py_floordiv_int(c->g.lx, rc)), cy = std::max(1, py_floordiv_int(c->g.ly, rc)),
+            cz = std::max(1, py_floordiv_int(c->g.lz, rc));
   const int64_t ncells = (int64_t)cx * cy * cz;
   if (ncells > (1 << 28)) return fail(PPPM_ERR_VALUE, "cutoff too small for the cell list");
   TRY(c->pr_cell.ensure(sizeof(int) * n));
@@ -1707,7 +2081,7 @@ int pppm_ctx_compute_forces(pppm_ctx* c, const void* pos, const void* q, int64_t
 
 int pppm_ctx_integrate_nve(pppm_ctx* c, const double* pos, const double* vel, const double* masses, const double* q,
                            int64_t n, double dt, int steps, double cutoff, const double* lj, double* series,
-                           double* pos_out, double* vel_out) {
+                           double* pos_out, double* vel_out, double* sections, long long* counters) {
   TRY(activate(c));
   if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
   if (!(dt > 0.0)) return fail(PPPM_ERR_VALUE, "dt must be positive");
@@ -1731,24 +2105,52 @@ int pppm_ctx_integrate_nve(pppm_ctx* c, const double* pos, const double* vel, co
   const double* m = c->md_m.as<double>();
   const double* dq = c->md_q.as<double>();
   double* rows = c->md_series.as<double>();
+  // per-evaluation section times (CUDA events; driver.REPORT_SECTIONS) and
+  // pair counters, accumulated over the steps + 1 force evaluations as the
+  // reference's compute_forces calls accumulate them (driver.py:310-376)
+  cudaEvent_t ev[5] = {};
+  if (sections) {
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    sections[0] = sections[1] = sections[2] = 0.0;
+  }
+  if (counters) counters[0] = counters[1] = 0;
+  auto destroy = [&]() {
+    if (sections)
+      for (auto& e : ev) cudaEventDestroy(e);
+  };
   auto eval = [&](int step) -> int {
-    const int st = forces_device(c, x, dq, n, cutoff, lj, f, nullptr);
+    long long cnt[2] = {0, 0};
+    const int st = forces_device(c, x, dq, n, cutoff, lj, f, cnt, sections ? ev : nullptr);
     if (st != PPPM_OK) {
       g_err = "step " + std::to_string(step) + ": " + g_err;  // driver.py:345-347
       return st;
     }
+    if (counters) {
+      counters[0] += cnt[0];
+      counters[1] += cnt[1];
+    }
+    if (sections) {
+      CU(cudaEventSynchronize(ev[4]));
+      float t[4] = {};
+      for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+      sections[0] += 1e-3 * ((double)t[1] + (double)t[3]);  // pppm_non_fft: make_rho + fieldforce
+      sections[1] += 1e-3 * (double)t[2];                   // pppm_fft: Poisson
+      sections[2] += 1e-3 * (double)t[0];                   // pair
+    }
     return PPPM_OK;
   };
-  TRY(eval(0));
-  for (int step = 0; step <= steps; ++step) {
-    TRY(launch_series_row(v, m, n, c->md_tmp.as<double>(), c->pr_part.as<double>(), rows + 7 * step,
-                          c->pr_scal.as<double>(), c->scal.as<double>(), c->pr_scal.as<double>() + 1, c->stream));
-    if (step == steps) break;
-    TRY(launch_kick(v, f, m, 0.5 * dt, n, c->stream));
-    TRY(launch_drift(x, v, dt, c->g.lx, c->g.ly, c->g.lz, n, c->stream));
-    TRY(eval(step + 1));
-    TRY(launch_kick(v, f, m, 0.5 * dt, n, c->stream));
+  int st = eval(0);
+  for (int step = 0; st == PPPM_OK && step <= steps; ++step) {
+    st = launch_series_row(v, m, n, c->md_tmp.as<double>(), c->pr_part.as<double>(), rows + 7 * step,
+                           c->pr_scal.as<double>(), c->scal.as<double>(), c->pr_scal.as<double>() + 1, c->stream);
+    if (st != PPPM_OK || step == steps) break;
+    st = launch_kick(v, f, m, 0.5 * dt, n, c->stream);
+    if (st == PPPM_OK) st = launch_drift(x, v, dt, c->g.lx, c->g.ly, c->g.lz, n, c->stream);
+    if (st == PPPM_OK) st = eval(step + 1);
+    if (st == PPPM_OK) st = launch_kick(v, f, m, 0.5 * dt, n, c->stream);
   }
+  destroy();
+  if (st != PPPM_OK) return st;
   CU(cudaMemcpyAsync(series, rows, sizeof(double) * 7 * (size_t)(steps + 1), cudaMemcpyDeviceToHost, c->stream));
   if (pos_out) CU(cudaMemcpyAsync(pos_out, x, v3, cudaMemcpyDeviceToHost, c->stream));
   if (vel_out) CU(cudaMemcpyAsync(vel_out, v, v3, cudaMemcpyDeviceToHost, c->stream));

@@ -165,6 +165,20 @@ __device__ __forceinline__ double load_real(const TIn* p, int64_t k) {
 
 __device__ __forceinline__ bool outside(double x, double len) { return !(x >= 0.0 && x < len); }
 
+// fp32 rounding of a wrapped position x in [0, L): a value that rounds up to L
+// itself is folded to 0, its periodic image (scenarios.round_to_f32); an
+// unwrapped input stays outside [0, L) and is still reported
+__device__ __forceinline__ float round_pos_f32(double x, double len) {
+  const float f = (float)x;
+  return ((double)f >= len && x >= 0.0 && x < len) ? 0.f : f;
+}
+
+template <typename TIn, bool R32>
+__device__ __forceinline__ double load_pos(const TIn* p, int64_t k, double len) {
+  const double v = (double)p[k];
+  return R32 ? (double)round_pos_f32(v, len) : v;
+}
+
 // particle_map with a multiply instead of the division, bit-exact anyway:
 // |x * (1/h) - x / h| is a few ulp of u, so floor() can only differ when
 // u (+1/2) lies within 1e-6 of an integer; those rare atoms take the exact

@@ -104,6 +104,7 @@ int launch_kick(double* v, const double* f, const double* m, double half_dt, int
 int launch_drift(double* x, const double* v, double dt, double lx, double ly, double lz, int64_t n, cudaStream_t s);
 int launch_series_row(const double* v, const double* m, int64_t n, double* tmp4, double* partial, double* row,
                       const double* e_pair, const double* e_kspace, const double* e_self, cudaStream_t s);
+int py_floordiv_int(double a, double b);  // Python's float a // b (k_pair.cu)
 bool zfft_supported(int nz);
 bool plane_supported(int nx, int ny);
 void plane_twiddles(int nx, int ny, float* out);
@@ -116,8 +117,9 @@ int zfft_blocks(int nz, int ncols);
 int launch_zfft_green(int mode, int nz, int ny_full, int y0, int nyl, int nx, const float2* spec, const float* green,
                       const float* ik, float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial,
                       unsigned* done, double prefactor, double* energy, cudaStream_t s);
-int launch_update_resident(bool f32, const void* pos, const int* orig, int64_t n, const Geom& g, float* res_pos,
-                           int* err, cudaStream_t s);
+int launch_update_resident(int order, bool f32, const void* pos, const int* orig, int64_t n, const Geom& g,
+                           float* res_pos, int* err, cudaStream_t s);
+int launch_round_positions(const double* pos, int64_t n, const Geom& g, float* out, cudaStream_t s);
 int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
@@ -157,5 +159,11 @@ int launch_pack_fwd(const Geom& g, int P, const void* spec, void* send, cudaStre
 int launch_pack_bwd(const Geom& g, int P, int nf, const void* ework, void* send, cudaStream_t s);
 int launch_unpack_bwd(const Geom& g, int P, int nf, const void* recv, void* spec, cudaStream_t s);
 int launch_add_planes(const float* src, float* dst, int64_t n, cudaStream_t s);
+// full-complex spectral helpers of the drop-in API (k_spectral.cu)
+int launch_hermitian_expand(bool f64, const void* half, void* full, int nx, int ny, int nz, cudaStream_t s);
+int launch_abs_max(bool f64, const void* v, int64_t n, unsigned long long* out, cudaStream_t s);
+int launch_scale_complex(double2* v, int64_t n, double scale, cudaStream_t s);
+int launch_spectrum_apply(const double2* rho_hat, const double* g_full, const double* ik, int comp, int nx, int ny,
+                          int nz, double2* out, double* e_elem, cudaStream_t s);
 
 }  // namespace pppm

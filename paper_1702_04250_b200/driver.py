@@ -167,13 +167,27 @@ def integrate_nve(system, params, dt, steps, lj=None, *, workers=1, timer=None, 
     pos_out = np.empty((n, 3))
     vel_out = np.empty((n, 3))
     ljp = lj_array(lj)
+    sec = np.zeros(3)
+    cnt = np.zeros(2, dtype=np.int64)
     t0 = time.perf_counter()
     ctx("pppm_ctx_integrate_nve", nat.ptr(pos), nat.ptr(vel), nat.ptr(masses), nat.ptr(q), n, float(dt), steps,
         float(params.cutoff), None if ljp is None else nat.ptr(ljp), nat.ptr(series), nat.ptr(pos_out),
-        nat.ptr(vel_out))
+        nat.ptr(vel_out), nat.ptr(sec), nat.ptr(cnt))
+    wall = time.perf_counter() - t0
     if timer is not None:
-        timer.add("device", time.perf_counter() - t0)
+        # the reference's sections, accumulated over the steps + 1 force evaluations
+        # (CUDA events per evaluation); the rest of the wall time is "other"
+        sections = {"pppm_non_fft": float(sec[0]), "pppm_fft": float(sec[1]), "pair": float(sec[2])}
+        for name, dt_s in sections.items():
+            timer.add(name, dt_s)
+        timer.add("other", max(0.0, wall - sum(sections.values())))
     if counters is not None:
+        evals = steps + 1
+        counters["pair_candidates"] = counters.get("pair_candidates", 0) + int(cnt[0])
+        counters["pairs_within_cutoff"] = counters.get("pairs_within_cutoff", 0) + int(cnt[1])
+        for _ in range(evals):
+            rt.count_touch(counters, "cells_touched_map", n, int(params.order))
+            rt.count_touch(counters, "cells_touched_distribute", n, int(params.order))
         nx, ny, nz = params.grid_dims
         counters["grid_points"] = nx * ny * nz
     out = {

@@ -47,6 +47,16 @@ def install(pppm_module, force_driver=True):
     T.EnergyBreakdown = mods["model"].EnergyBreakdown
     nat.ERRORS.config = mods["model"].ConfigurationError
     nat.ERRORS.singular = mods["model"].SingularityError
+    # errors raised by this package's own validation are the reference's class,
+    # and the stencil orders are the reference's (its tests assert that even
+    # orders are rejected, test_stencil.py:150-152; 4 and 6 stay available
+    # through this package's own API)
+    from . import model as own_model
+
+    for mod in (kspace, shortrange, stencil, gridmap, driver, own_model):
+        if hasattr(mod, "ConfigurationError"):
+            _swap(mod, "ConfigurationError", mods["model"].ConfigurationError)
+    _swap(stencil, "SUPPORTED_ORDERS", tuple(mods["model"].SUPPORTED_ORDERS))
     paths = dict(HOT_PATH, **(NEXT_PATH if force_driver else {}))
     for modname, names in paths.items():
         for name in names:
@@ -56,6 +66,11 @@ def install(pppm_module, force_driver=True):
                     _saved.setdefault((target.__name__, name), (target, getattr(target, name)))
                     setattr(target, name, new)
     return sorted({name for names in paths.values() for name in names})
+
+
+def _swap(target, name, value):
+    _saved.setdefault((target.__name__, name), (target, getattr(target, name)))
+    setattr(target, name, value)
 
 
 def uninstall():

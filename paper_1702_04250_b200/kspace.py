@@ -2,13 +2,23 @@
 
 Mirrors kspace.py:99-337 of the reference.  The transforms are cuFFT R2C/C2R
 on the device (the reference uses full complex numpy FFTs and keeps the real
-part; for the Hermitian spectra involved the two agree, and the imaginary
-residue is identically zero, reported as 0.0).  The influence-function
+part; for the Hermitian spectra involved the two agree).  The influence-function
 multiply, the ik gradient and the energy reduction are one hand-written
 kernel (``k_green``); the influence function itself is evaluated on the
 device (``k_influence``).  Forward transforms are unnormalised and the 1/M of
 the backward transform is folded into the Green multiply, as in the
 reference's convention (kspace.py:1-6).
+
+``imag_residue`` (kspace.py:264-268) is measured on the device: the Green / ik
+half spectra are expanded to the full grid through Hermitian symmetry and
+transformed back with a complex inverse FFT (k_spectral.cu).
+
+The plan's ``forward`` / ``backward`` pair (kspace.py:244) defaults to device
+transforms with numpy ``fftn`` / ``ifftn`` semantics (``DeviceFFT``).  A
+caller-supplied pair (``build_plan(fft=(fwd, bwd))``, the reference's
+pluggable-transform hook) is honoured: the solve then runs the caller's
+transforms and does the influence / ik multiply and the energy sum on the
+device (``pppm_spectrum_apply``).
 """
 
 from __future__ import annotations
@@ -22,13 +32,51 @@ from .model import ConfigurationError
 DECONV_FLOOR = 1e-10
 
 
+class DeviceFFT:
+    """numpy ``fftn`` (forward, unnormalised) / ``ifftn`` (backward, 1/N)
+    semantics on the device (cuFFT Z2Z, ``pppm_fftn``); 1-3 dimensional
+    real or complex input, complex128 output."""
+
+    def __init__(self, inverse: bool):
+        self.inverse = bool(inverse)
+        self.__name__ = "ifftn" if inverse else "fftn"
+
+    def __call__(self, a):
+        x = np.ascontiguousarray(a, dtype=np.complex128)
+        if x.ndim < 1 or x.ndim > 3:
+            raise ValueError("the device transform supports 1 to 3 dimensions")
+        out = np.empty_like(x)
+        if x.size == 0:
+            raise ValueError("Invalid number of FFT data points (0) specified.")
+        shape = np.array(x.shape, dtype=np.int64)
+        nat.require_device(rt.get_device())
+        nat.call("pppm_fftn", rt.get_device(), x.ndim, nat.ptr(shape), nat.ptr(x), nat.ptr(out),
+                 1 if self.inverse else 0)
+        return out
+
+    def __repr__(self):
+        return f"DeviceFFT({self.__name__})"
+
+
+DEVICE_FFT = (DeviceFFT(False), DeviceFFT(True))
+
+
+def _is_default_fft(forward, backward) -> bool:
+    """The device pair, or numpy's own fftn / ifftn (the reference default,
+    kspace.py:244): the same transforms as the device solve."""
+    if isinstance(forward, DeviceFFT) and isinstance(backward, DeviceFFT):
+        return True
+    return forward is np.fft.fftn and backward is np.fft.ifftn
+
+
 class KSpacePlan:
     """Solve plan: geometry, influence variant; G lives on the device.
 
     ``influence`` / ``ik_x`` / ``ik_y`` / ``ik_z`` are computed on the device
     and copied to the host only when read (read-only arrays, as in
-    kspace.py:104-132).  ``forward`` / ``backward`` keep a caller-supplied
-    ``fft`` pair for API compatibility; the solver itself always runs cuFFT.
+    kspace.py:104-132).  ``forward`` / ``backward`` are the device transforms
+    (``DEVICE_FFT``) unless the caller supplied its own ``fft`` pair, which the
+    solve then runs (module docstring).
     """
 
     def __init__(self, dims, box_lengths, alpha, order, variant="pme", deconv_floor=DECONV_FLOOR,
@@ -40,7 +88,7 @@ class KSpacePlan:
         self.order = int(order)
         self.variant = variant
         self.deconv_floor = float(deconv_floor)
-        self.forward, self.backward = fft if fft is not None else (None, None)
+        self.forward, self.backward = fft if fft is not None else DEVICE_FFT
         self._influence = None
         self._ik = None
 
@@ -139,43 +187,83 @@ def _check_grid(grid, plan):
         raise ValueError(f"grid dims {grid.dims} do not match plan dims {plan.dims}")
 
 
+def _residue(e, real):
+    """kspace.py:264-268 on the caller's complex back transform."""
+    scale = float(np.max(np.abs(real)))
+    if scale == 0.0:
+        return 0.0
+    return float(np.max(np.abs(np.asarray(e).imag))) / scale
+
+
+def _solve_custom(rho, plan, ctx, mode_code):
+    """Caller-supplied transforms: forward / backward are the caller's, the
+    influence and ik multiply run on the device (kspace.py:278-312)."""
+    rho_hat = np.ascontiguousarray(plan.forward(rho.values), dtype=np.complex128)
+    if rho_hat.shape != ctx.mesh_shape:
+        raise ValueError(f"forward transform returned shape {rho_hat.shape}, expected {ctx.mesh_shape}")
+    comps = (0, 1, 2) if mode_code == nat.MODE_IK else (-1,)
+    outs, residue = [], 0.0
+    for comp in comps:
+        spec = np.empty_like(rho_hat)
+        ctx("pppm_spectrum_apply", nat.ptr(rho_hat), comp, nat.ptr(spec), None)
+        e = plan.backward(spec)
+        real = np.ascontiguousarray(np.real(e), dtype=np.float64)
+        residue = max(residue, _residue(e, real))
+        real.flags.writeable = False
+        outs.append(real)
+    return outs, residue
+
+
 def _solve(rho, plan, mode_code):
     _check_grid(rho, plan)
     ctx = _plan_ctx(plan, mode_code, rt.get_precision())
+    if not _is_default_fft(plan.forward, plan.backward):
+        return _solve_custom(rho, plan, ctx, mode_code)
     values = np.ascontiguousarray(rho.values, dtype=np.float64)
     ctx("pppm_set_rho", nat.ptr(values))
     energy = np.zeros(1)
-    ctx("pppm_poisson", 1, energy.ctypes.data_as(nat._dp))
+    ctx("pppm_poisson", 2, energy.ctypes.data_as(nat._dp))  # fields + measured imag_residue
     outs = [np.empty(ctx.mesh_shape) for _ in range(3 if mode_code == nat.MODE_IK else 1)]
     ptrs = [nat.ptr(a) for a in outs] + [None] * (3 - len(outs))
     ctx("pppm_get_fields", *ptrs)
     for a in outs:
         a.flags.writeable = False
-    return outs
+    residue = np.zeros(1)
+    ctx("pppm_get_imag_residue", residue.ctypes.data_as(nat._dp))
+    return outs, float(residue[0])
 
 
 def poisson_ik(rho, plan):
     """E_d = -i k_d G rho^ transformed back, three grids (kspace.py:271-300)."""
-    ex, ey, ez = _solve(rho, plan, nat.MODE_IK)
+    (ex, ey, ez), residue = _solve(rho, plan, nat.MODE_IK)
     T = rt.types()
     return T.FieldGrids(mode=T.DiffMode.IK, dims=rho.dims, spacing=rho.spacing, ex=ex, ey=ey, ez=ez,
-                        imag_residue=0.0)
+                        imag_residue=residue)
 
 
 def poisson_ad(rho, plan):
     """phi = G rho^ transformed back, one grid (kspace.py:303-317)."""
-    (phi,) = _solve(rho, plan, nat.MODE_AD)
+    (phi,), residue = _solve(rho, plan, nat.MODE_AD)
     T = rt.types()
     return T.FieldGrids(mode=T.DiffMode.AD, dims=rho.dims, spacing=rho.spacing, phi=phi,
-                        imag_residue=0.0)
+                        imag_residue=residue)
 
 
 def kspace_energy(rho, plan, *, coulomb_constant=1.0, dielectric=1.0):
     """C/eps * Vc^2/(2V) * sum_k G |rho^|^2 (kspace.py:320-337), reduced in fp64 on the device."""
     _check_grid(rho, plan)
     ctx = _plan_ctx(plan, nat.MODE_AD, rt.get_precision())
+    scale = coulomb_constant / dielectric
+    if not _is_default_fft(plan.forward, plan.backward):
+        rho_hat = np.ascontiguousarray(plan.forward(rho.values), dtype=np.complex128)
+        total = np.zeros(1)
+        ctx("pppm_spectrum_apply", nat.ptr(rho_hat), -1, None, total.ctypes.data_as(nat._dp))
+        nx, ny, nz = plan.dims
+        volume = float(np.prod(plan.box_lengths))
+        vcell = volume / (nx * ny * nz)
+        return scale * vcell ** 2 / (2.0 * volume) * float(total[0])
     values = np.ascontiguousarray(rho.values, dtype=np.float64)
     ctx("pppm_set_rho", nat.ptr(values))
     energy = np.zeros(1)
     ctx("pppm_poisson", 0, energy.ctypes.data_as(nat._dp))
-    return float(energy[0]) * (coulomb_constant / dielectric)
+    return float(energy[0]) * scale

@@ -52,6 +52,14 @@ class _CudaView:
         }
 
 
+def nccl_unique_id() -> bytes:
+    """An NCCL unique id (128 bytes) for pppm_slab_attach_nccl; made on rank 0
+    and broadcast by the caller."""
+    buf = ctypes.create_string_buffer(128)
+    nat.call("pppm_nccl_unique_id", buf)
+    return buf.raw
+
+
 class SlabContext:
     """One slab of the decomposed mesh on one device (mixed precision)."""
 
@@ -121,6 +129,34 @@ class SlabContext:
 
     def synchronize(self):
         self("pppm_ctx_synchronize")
+
+    # the whole step inside the library (NCCL on the context stream, CUDA graphs)
+    def attach_nccl(self, unique_id: bytes, timeout_s: float = 600.0):
+        """Join the P-slab NCCL communicator (collective over the slabs)."""
+        if len(unique_id) != 128:
+            raise ValueError("an NCCL unique id is 128 bytes")
+        self("pppm_slab_attach_nccl", unique_id, float(timeout_s))
+
+    def step(self, phases=nat.PHASE_ALL):
+        self("pppm_ctx_step", int(phases))
+
+    def time_steps(self, steps, warmup, flush_l2=True):
+        """CUDA-event phase times in ms summed over ``steps`` (make_rho includes
+        the ghost reverse sum, poisson the transposes and the energy all-reduce)."""
+        ms = np.zeros(5)
+        self("pppm_ctx_time_steps", int(steps), int(warmup), int(bool(flush_l2)), nat.ptr(ms))
+        return dict(zip(("bin", "spread", "poisson", "gather", "total"), (float(v) for v in ms)))
+
+    def launches_per_step(self):
+        n = ctypes.c_int(0)
+        self("pppm_ctx_launches_per_step", ctypes.byref(n))
+        return n.value
+
+    def update_positions(self, positions):
+        """New positions of this slab's atoms (its load order).  Raises when an
+        atom left the slab (see SlabStep.migrate)."""
+        pos = np.ascontiguousarray(positions, dtype=np.float32)
+        self("pppm_ctx_update_positions", nat.ptr(pos), nat.F32, nat.HOST)
 
     def forces(self):
         out = np.empty((self.n_atoms, 3))

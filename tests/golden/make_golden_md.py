@@ -69,6 +69,14 @@ def main():
     pair_case("pair_box_lj", s2, 1.1, 3.0, rsr.LjParams(epsilon=0.3, sigma=0.8, cutoff=2.5, enabled=True),
               scale=(2.0, 1.5))
 
+    # cell counts where Python's int(L // rc) differs from a truncated L / rc
+    # (1.0 // 0.1 == 9.0 but 1.0 / 0.1 == 10.0; 3.0 // 0.1 == 29.0)
+    rng = np.random.default_rng(15)
+    box = pppm.SimulationBox([1.0, 3.0, 2.1])
+    pos = rng.uniform(0, 1, (400, 3)) * box.lengths
+    q = np.where(np.arange(400) % 2 == 0, 1.0, -1.0)
+    pair_case("pair_floordiv", pppm.AtomSystem(box=box, positions=pos, charges=q), 20.0, 0.1)
+
     # full force evaluation, both modes, table on (the reference's default)
     g = rdrv.generate_scenario("random_gas", 512, seed=13, min_separation=0.8)
     forces_case("forces_gas_ik", g, params_for((16, 16, 16), 5, "ik", 0.8, 3.0))

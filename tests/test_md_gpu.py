@@ -36,7 +36,7 @@ def _params(pb, g, precision="fp64"):
                          use_table=bool(g["use_table"]), precision=precision)
 
 
-@pytest.mark.parametrize("name", ["pair_gas", "pair_box_lj"])
+@pytest.mark.parametrize("name", ["pair_gas", "pair_box_lj", "pair_floordiv"])
 def test_pair_forces_vs_reference(pb, name):
     g = load_golden(name)
     s = pb.AtomSystem(box=pb.SimulationBox(g["lengths"]), positions=g["pos"], charges=g["q"])
