@@ -54,6 +54,18 @@ template <int S> struct Tile {
 
 // largest 1D weight of the order-S spline (t = 0 for odd S, w = 0 for even S)
 template <int S> struct WMax;
+// (sum over stencil nodes d of max_t w_d(t))^3: the most one atom deposits, in
+// total, into any single cell summed over all its possible positions relative
+// to the cell (per axis separable).  A cell receiving from atoms in cells with
+// at most m atoms each holds at most m * max|q| * WSum3 (rigorous bound on the
+// final fixed-point cell value; oracle bspline_rows maxima, rounded up)
+template <int S> struct WSum3;
+template <> struct WSum3<3> { static constexpr float v = 5.3594f; };
+template <> struct WSum3<4> { static constexpr float v = 4.6297f; };
+template <> struct WSum3<5> { static constexpr float v = 4.0880f; };
+template <> struct WSum3<6> { static constexpr float v = 3.7239f; };
+template <> struct WSum3<7> { static constexpr float v = 3.4500f; };
+
 template <> struct WMax<3> { static constexpr float v = 0.75f; };
 template <> struct WMax<4> { static constexpr float v = 0.6666667f; };
 template <> struct WMax<5> { static constexpr float v = 0.5989584f; };
@@ -402,7 +414,16 @@ struct BankSmem {
   int* p;
   int* bsize;   // 32
   int* bstart;  // 33 (bstart[32] = rounds)
+  int* occ = nullptr;  // optional: kBrick^3 per-cell atom counts + [kBrick^3] = max count (zeroed by the caller)
 };
+
+// per-cell occupancy of the staged atoms; occ[kBrick^3] = the largest count
+__device__ __forceinline__ void occ_count(int* occ, bool valid, int cell) {
+  int m = valid ? atomicAdd(occ + cell, 1) + 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(occ + kBrick * kBrick * kBrick, m);
+}
 
 template <bool PERM, int D, int TXB, int SH, int NT = kThreads>
 __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, const int* __restrict__ rcell,
@@ -429,6 +450,7 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
       }
     }
+    if (sm.occ) occ_count(sm.occ, j < cnt && bank[k] >= 0, j < cnt ? c[k] : 0);
   }
   __syncthreads();
   if (threadIdx.x < 32) {

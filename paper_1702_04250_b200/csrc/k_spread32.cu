@@ -93,6 +93,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
   for (int k = 0; k < PER; ++k) {
     const int j = threadIdx.x + k * NT;
     bank[k] = -1;
+    int occ_cell = 0;
     if (j < cnt) {
       const int64_t i = base + j;
       float4 r;
@@ -103,6 +104,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
         reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(lc, (int)i, 0, 0);
         t_r[j] = r;  // unsorted copy in shared memory for pass 2
         t_c[j] = lc;
+        occ_cell = lc;
         const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
         bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
@@ -115,6 +117,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
         ovf_perm[o] = (int)i;
       }
     }
+    if (sm.occ) occ_count(sm.occ, bank[k] >= 0, occ_cell);
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -166,12 +169,13 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   int* tiles0 = dyn_i;
   float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
   __shared__ int bsize[32], bstart[33];
+  constexpr int kCells = kBrick * kBrick * kBrick;
+  __shared__ int s_occ[kCells + 1];  // per-cell atom counts of the staged brick, [kCells] = max (FIX scale)
   // staged atoms: s_r[cap] | (resident: t_r[cap]) | s_c[cap] | (resident: t_c[cap])
-  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + (RES ? 2 * cap : cap)), nullptr, bsize, bstart};
+  BankSmem sm{s_r, reinterpret_cast<int*>(s_r + (RES ? 2 * cap : cap)), nullptr, bsize, bstart,
+              FIX ? s_occ : nullptr};
   const int nb = bk.count();
   const float qmax = resident ? res.qmax : __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
-  const float w3 = WMax<S>::v * WMax<S>::v * WMax<S>::v * 1.01f;
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
   __shared__ int s_brick;
@@ -206,21 +210,10 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     // all reduces but the most recent (other buffer) have finished reading
     if (threadIdx.x == 0) bulk_wait_read<1>();
     if (RES && threadIdx.x < 32) bsize[threadIdx.x] = 0;  // stage_resident's histogram
+    if (FIX)
+      for (int k = threadIdx.x; k <= kCells; k += blockDim.x) s_occ[k] = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
-    float scale = inv_vcell, inv_scale = 1.f;
-    if (FIX) {
-      // int32 fixed point, power-of-two scale: every cell sum below 2^30
-      // (|cell| <= count * max|q| * wmax^3) and every contribution below 2^22,
-      // so float->int is one FFMA with the 1.5*2^23 magic number (round to
-      // nearest) instead of an F2I on the quarter-rate conversion pipe.
-      int e_sum = 0, e_one = 0;
-      frexpf(qmax > 0.f ? (float)cnt * qmax * w3 : 1.f, &e_sum);
-      frexpf(qmax > 0.f ? qmax * w3 : 1.f, &e_one);
-      const int sc = min(30 - e_sum, 22 - e_one);
-      scale = ldexpf(1.f, sc);
-      inv_scale = ldexpf(1.f, -sc) * inv_vcell;
-    }
     int rounds;
     if constexpr (RES)
       rounds = stage_resident<S, TAB, D, TXB, T::SH, NT>(res, b, cnt, g, bk, pd, n_points, ta, inv_vcell, rho,
@@ -228,6 +221,23 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
                                                             s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap);
     else
       rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
+    float scale = inv_vcell, inv_scale = 1.f;
+    if (FIX) {
+      // int32 fixed point, power-of-two scale 2^sc.  Integer adds wrap, so only
+      // the final cell value has to fit: with at most m atoms in any cell of the
+      // brick, |cell| <= m * max|q| * WSum3 < 2^31 (s_occ[kCells] = m, counted
+      // while staging; the 1.01 margin covers the per-contribution rounding).
+      // Contributions are formed in fp64 and rounded to integers by one DFMA
+      // with the 1.5*2^52 magic number (B200 fp64 runs at half the fp32 rate):
+      // the low word of the result is the integer modulo 2^32, for any
+      // contribution size, so the scale is limited by the cell bound alone.
+      int e_sum = 0;
+      const int m = s_occ[kCells];
+      frexpf(qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f, &e_sum);
+      const int sc = 31 - e_sum;
+      scale = ldexpf(1.f, sc);
+      inv_scale = ldexpf(1.f, -sc) * inv_vcell;
+    }
     for (int rr = warp; rr < rounds; rr += nwarp) {
       if (rr >= bsize[lane]) continue;
       const int j = bstart[lane] + rr;
@@ -238,18 +248,34 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
       rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
       rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
       rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
-      const float qs = r.w * scale;
+      if (FIX) {
+        constexpr double kMagic52 = 6755399441055744.0;  // 1.5 * 2^52
+        double dx[S];
 #pragma unroll
-      for (int a = 0; a < S; ++a) {
-        const float qa = qs * wz[a];
+        for (int c = 0; c < S; ++c) dx[c] = (double)wx[c];
+        const double qs = (double)r.w * (double)scale;
 #pragma unroll
-        for (int bb = 0; bb < S; ++bb) {
-          const float qab = qa * wy[bb];
-          const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+        for (int a = 0; a < S; ++a) {
+          const double qa = qs * (double)wz[a];
 #pragma unroll
-          for (int c = 0; c < S; ++c) {
-            if (FIX) atomicAdd(tile + row + c, __float_as_int(fmaf(qab, wx[c], kMagic)) - 0x4B400000);
-            else atomicAdd(ftile + row + c, qab * wx[c]);
+          for (int bb = 0; bb < S; ++bb) {
+            const double qab = qa * (double)wy[bb];
+            const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+#pragma unroll
+            for (int c = 0; c < S; ++c) atomicAdd(tile + row + c, __double2loint(fma(qab, dx[c], kMagic52)));
+          }
+        }
+      } else {
+        const float qs = r.w * scale;
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          const float qa = qs * wz[a];
+#pragma unroll
+          for (int bb = 0; bb < S; ++bb) {
+            const float qab = qa * wy[bb];
+            const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+#pragma unroll
+            for (int c = 0; c < S; ++c) atomicAdd(ftile + row + c, qab * wx[c]);
           }
         }
       }
