@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--probe-launch", action="store_true",
                     help="only launch the N ranks and report them (CPU check of the spawn path)")
     ap.add_argument("--no-config5", action="store_true", help="skip the config-5 sub-record at N=1")
+    ap.add_argument("--no-extra", action="store_true", help="skip the md / binned / fp64 sub-records at N=1")
     ap.add_argument("--mode", default=None, choices=(None, "ik", "ad"))
     ap.add_argument("--order", type=int, default=None, help="override the config's stencil order (config 4 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -408,6 +409,104 @@ def config5_record(args, device):
     return out
 
 
+def extra_records(args, cfg, device, pos, q, lengths):
+    """Next to the headline (resident atoms, no binning pass, no motion):
+    * md: an MD-like step - every step the atoms move (~0.1 A rms), the new
+      positions are scattered into the brick-ordered residents on the device
+      (update_positions_async), atoms outside their brick take the direct
+      path, and the residents are re-sorted automatically once 5 % of them
+      left their brick; the re-sorts are inside the timed steps;
+    * binned: the one-shot path's work - atoms in the caller's order, binned
+      into bricks every step;
+    * fp64: the reference's arithmetic (fp64 mesh, int64 fixed-point make_rho,
+      fp64 gather) on the same workload."""
+    import torch
+
+    import paper_1702_04250_b200 as pb
+    from paper_1702_04250_b200 import _native as nat
+    from paper_1702_04250_b200 import scenarios
+
+    mode = args.mode or cfg.mode
+    n = pos.shape[0]
+    k, w = args.steps, max(3, args.warmup)
+    out = {}
+    p32 = pos.astype(np.float32)
+    q32 = q.astype(np.float32)
+    # --- md
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
+                         device=device)
+    ctx.load_atoms(p32, q32)
+    rng = np.random.default_rng(7)
+    cur = pos.astype(np.float64)
+    traj = np.empty((k + w, n, 3), dtype=np.float32)
+    for i in range(k + w):
+        cur = scenarios.wrap(cur + rng.normal(0.0, 0.1 / np.sqrt(3.0), cur.shape), lengths)
+        traj[i] = scenarios.round_to_f32(cur, lengths)
+    dev = torch.from_numpy(traj).to(f"cuda:{device}")
+    del traj
+    sp = ctypes.c_void_p()
+    ctx.ctx("pppm_ctx_stream", ctypes.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(k)]
+
+    def mark(j, idx):
+        if j >= 0:
+            with torch.cuda.stream(stream):
+                ev[j][idx].record(stream)
+
+    for i in range(k + w):
+        j = i - w
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xff)
+        mark(j, 0)
+        ctx.update_positions_async(dev[i].data_ptr(), mem=nat.DEVICE)
+        mark(j, 1)
+        ctx.step(nat.PHASE_MAKE_RHO)
+        mark(j, 2)
+        ctx.step(nat.PHASE_POISSON)
+        mark(j, 3)
+        ctx.step(nat.PHASE_FIELDFORCE)
+        mark(j, 4)
+    ctx.synchronize()
+    ph = np.array([[e[a].elapsed_time(e[a + 1]) for a in range(4)] for e in ev]).sum(axis=0)
+    info = ctx.resident_info()
+    ctx.close()
+    del dev
+    out["md"] = {"value": n * k / (ph.sum() / 1e3), "unit": UNIT, "ms_per_step": ph.sum() / k,
+                 "value_make_rho_fieldforce": n * k / ((ph[1] + ph[3]) / 1e3),
+                 "phases_ms_per_step": {"update": ph[0] / k, "make_rho": ph[1] / k, "poisson": ph[2] / k,
+                                        "fieldforce": ph[3] / k},
+                 "what": "update_positions_async (device, ~0.1 A rms displacement per step) + full step, "
+                         "automatic re-sort at 5 % movers; value = whole MD PPPM step (update, make_rho, "
+                         "Poisson, fieldforce)",
+                 "resorts": info["resorts"], "movers_last_update": info["movers"], "steps": k}
+    # --- binned one-shot path
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
+                         device=device)
+    ctx.set_variant(2, 0)
+    ctx.load_atoms(p32, q32)
+    ms = ctx.time_steps(k, w, flush_l2=True)
+    ctx.close()
+    t_mf = (ms["bin"] + ms["spread"] + ms["gather"]) / 1e3
+    out["binned"] = {"value": n * k / t_mf, "unit": UNIT,
+                     "what": "atoms in the caller's order, binned every step (bin + make_rho + fieldforce)",
+                     "phases_ms_per_step": {kk: v / k for kk, v in ms.items()}}
+    # --- fp64
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="fp64", alpha=cfg.alpha,
+                         device=device)
+    ctx.load_atoms(pos.astype(np.float64), q.astype(np.float64))
+    ms = ctx.time_steps(max(3, k // 4), w, flush_l2=True)
+    kk4 = max(3, k // 4)
+    ctx.close()
+    t_mf = (ms["bin"] + ms["spread"] + ms["gather"]) / 1e3
+    out["fp64"] = {"value": n * kk4 / t_mf, "unit": UNIT, "dtype": "f64",
+                   "what": "fp64 mesh / stencil / forces (the reference's arithmetic): make_rho + fieldforce",
+                   "whole_step_atom_steps_per_s": n * kk4 / (t_mf + ms["poisson"] / 1e3),
+                   "phases_ms_per_step": {kx: v / kk4 for kx, v in ms.items()}}
+    return out
+
+
 def probe_launch(args, rank, world, pg):
     """--probe-launch: the spawn path without a GPU workload (CPU test of the
     N-rank launch): every rank reports in, rank 0 prints the gathered ranks."""
@@ -564,29 +663,46 @@ def main():
     }
 
     if not args.no_e2e:
-        # end to end through the C ABI: pinned host fp32 inputs -> H2D -> full step -> D2H forces (fp64) + energy
+        # end to end through the C ABI: pinned host fp32 inputs -> H2D (chunked,
+        # overlapped with binning) -> full step -> D2H forces + energy, forces in
+        # the path's own precision (fp32 on the mixed path; fp64 also reported)
         hp = pb.PinnedArray(posd.shape, posd.dtype)
         hq = pb.PinnedArray(qd.shape, qd.dtype)
-        hf = pb.PinnedArray((n, 3), np.float64)
         hp.array[...] = posd
         hq.array[...] = qd
-        for _ in range(max(2, args.warmup)):
-            ctx.compute(hp.array, hq.array, out=hf.array)
-        barrier(pg)
-        times = []
-        for _ in range(k):
-            t0 = time.perf_counter()
-            ctx.compute(hp.array, hq.array, out=hf.array)
-            times.append(time.perf_counter() - t0)
-        t_e2e = max_over_ranks(pg, sum(times))
-        line["e2e"] = {"value": atoms_total * k / t_e2e, "unit": UNIT,
-                       "h2d_bytes_per_step": int(posd.nbytes + qd.nbytes), "d2h_bytes_per_step": int(n * 3 * 8 + 8),
-                       "what": "pppm_compute: H2D pos+q (pinned), make_rho, poisson, fieldforce, D2H forces (pinned) + energy; "
-                               "wall clock per synchronous call"}
+        e2e = {}
+        for fdt in ((np.float32, np.float64) if fp32 else (np.float64,)):
+            hf = pb.PinnedArray((n, 3), fdt)
+            for _ in range(max(2, args.warmup)):
+                ctx.compute(hp.array, hq.array, out=hf.array)
+            barrier(pg)
+            times = []
+            for _ in range(k):
+                t0 = time.perf_counter()
+                ctx.compute(hp.array, hq.array, out=hf.array)
+                times.append(time.perf_counter() - t0)
+            t_e2e = max_over_ranks(pg, sum(times))
+            e2e[np.dtype(fdt).name] = (atoms_total * k / t_e2e, int(n * 3 * np.dtype(fdt).itemsize + 8))
+            hf.free()
+        main_dt = "float32" if fp32 else "float64"
+        line["e2e"] = {"value": e2e[main_dt][0], "unit": UNIT,
+                       "h2d_bytes_per_step": int(posd.nbytes + qd.nbytes), "d2h_bytes_per_step": e2e[main_dt][1],
+                       "forces_dtype": main_dt,
+                       "what": "PppmContext.compute -> pppm_compute_ex: H2D pos+q from pinned memory (8 chunks on a "
+                               "copy stream, each binned as it lands), make_rho, poisson, fieldforce, D2H forces "
+                               "(pinned) + energy; wall clock per synchronous call"}
+        if "float64" in e2e and fp32:
+            line["e2e"]["value_f64_forces"] = e2e["float64"][0]
+            line["e2e"]["d2h_bytes_per_step_f64_forces"] = e2e["float64"][1]
         hp.free()
         hq.free()
-        hf.free()
 
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = extra_records(args, cfg, local, pos, q, lengths)
+        line["value_md"] = extra["md"]["value"]
+        line["value_binned"] = extra["binned"]["value"]
+        line["value_fp64"] = extra["fp64"]["value"]
+        line["extra"] = extra
     if rank == 0 and world == 1 and not args.no_config5 and args.config is None:
         line["config5"] = config5_record(args, local)
 

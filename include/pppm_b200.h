@@ -118,6 +118,13 @@ int pppm_fieldforce(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, in
 int pppm_compute(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int dtype, int mem,
                  double* forces, double* energy);
 
+/* pppm_compute with the forces' element type chosen by the caller (PPPM_F64,
+ * or PPPM_F32 on a mixed-precision context: the path's own precision, half the
+ * device->host bytes).  Host fp32 atoms on the mixed path are copied in chunks
+ * on a second stream, each chunk binned as soon as it has landed. */
+int pppm_compute_ex(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int dtype, int mem,
+                    void* forces, int forces_dtype, double* energy);
+
 /* device-resident performance path ---------------------------------------- */
 int pppm_ctx_load_atoms(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int dtype);
 int pppm_ctx_step(pppm_ctx* ctx, int phases);            /* async on the context stream */
@@ -126,9 +133,18 @@ int pppm_ctx_get_forces(pppm_ctx* ctx, double* forces);
 /* new positions of the resident atoms (caller's order, same count), kept in the
  * context's brick order: a time-stepping caller (driver.integrate_nve's
  * position update, driver.py:369) moves atoms without re-sorting; make_rho /
- * fieldforce send atoms that left their brick down a direct path until the
- * next pppm_ctx_load_atoms re-sorts them. */
+ * fieldforce send atoms that left their brick down a direct path until they
+ * are re-sorted (automatically, see below, or by pppm_ctx_load_atoms). */
 int pppm_ctx_update_positions(pppm_ctx* ctx, const void* positions, int dtype, int mem);  /* host (n,3) fp64 */
+/* The update counts the atoms outside their sorted brick; above a fraction of
+ * the atoms (pppm_ctx_set_resort, default 0.05) the residents are re-sorted in
+ * place.  The async form does not wait: errors surface at the next
+ * pppm_ctx_synchronize and the previous update's mover count decides the
+ * re-sort (an MD loop: update_positions_async + step per time step). */
+int pppm_ctx_update_positions_async(pppm_ctx* ctx, const void* positions, int dtype, int mem);
+int pppm_ctx_set_resort(pppm_ctx* ctx, double fraction);
+/* info[4]: movers at the last counted update, re-sorts so far, largest brick, resident atoms */
+int pppm_ctx_resident_info(pppm_ctx* ctx, int64_t* info);
 int pppm_ctx_get_energy(pppm_ctx* ctx, double* energy);
 /* CUDA-event timing of `steps` full steps after `warmup`; flush_l2 writes a
  * 256 MiB buffer before each step (outside the phase intervals).
@@ -141,7 +157,10 @@ int pppm_ctx_time_steps(pppm_ctx* ctx, int steps, int warmup, int flush_l2, doub
  * 3: warp-specialized), kernel 1 = fp32 fieldforce (0: bucket order, 1: bank
  * rounds, 2: one task per (atom, component) [ik], 3: warp-specialized staging
  * [default; ik: per-component tasks, ad: one task per atom], 4: tcgen05 tensor
- * cores [ik, orders 3-5], 5: x-adjacent atom pairs [ik]) */
+ * cores [ik, orders 3-5], 5: x-adjacent atom pairs [ik]), kernel 2 =
+ * resident atoms at the next load (0: caller's order, binned every step as the
+ * one-shot calls do; 1: brick order, binned every step; 2: brick order, no
+ * binning pass [default]) */
 int pppm_ctx_set_variant(pppm_ctx* ctx, int kernel, int variant);
 /* z-slab decomposition over `nslabs` GPUs (no counterpart in the reference,
  * which is single-process).  Slab `rank` owns global planes

@@ -60,11 +60,15 @@ PROTOTYPES = {
     "pppm_set_fields": (_c_int, [_vp, _vp, _vp, _vp]),
     "pppm_fieldforce": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _vp]),
     "pppm_compute": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _vp, _dp]),
+    "pppm_compute_ex": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _vp, _c_int, _dp]),
     "pppm_ctx_load_atoms": (_c_int, [_vp, _vp, _vp, _c_i64, _c_int]),
     "pppm_ctx_step": (_c_int, [_vp, _c_int]),
     "pppm_ctx_synchronize": (_c_int, [_vp]),
     "pppm_ctx_get_forces": (_c_int, [_vp, _vp]),
     "pppm_ctx_update_positions": (_c_int, [_vp, _vp, _c_int, _c_int]),
+    "pppm_ctx_update_positions_async": (_c_int, [_vp, _vp, _c_int, _c_int]),
+    "pppm_ctx_set_resort": (_c_int, [_vp, _c_dbl]),
+    "pppm_ctx_resident_info": (_c_int, [_vp, ctypes.POINTER(_c_i64)]),
     "pppm_ctx_get_energy": (_c_int, [_vp, _dp]),
     "pppm_ctx_time_steps": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp]),
     "pppm_ctx_launches_per_step": (_c_int, [_vp, ctypes.POINTER(_c_int)]),

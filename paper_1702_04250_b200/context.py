@@ -60,6 +60,29 @@ class PppmContext:
         dtype = nat.F32 if pos.dtype == np.float32 else nat.F64
         self.ctx("pppm_ctx_update_positions", nat.ptr(pos), dtype, nat.HOST)
 
+    def update_positions_async(self, positions, mem=nat.HOST):
+        """MD position update without waiting (device pointers: ``mem=DEVICE``
+        with an integer address); errors surface at the next synchronize."""
+        if mem == nat.DEVICE:
+            self.ctx("pppm_ctx_update_positions_async", ctypes.c_void_p(int(positions)), nat.F32, nat.DEVICE)
+            return
+        pos = np.ascontiguousarray(positions)
+        dtype = nat.F32 if pos.dtype == np.float32 else nat.F64
+        self._pending = pos  # keep the host buffer alive until the copy ran
+        self.ctx("pppm_ctx_update_positions_async", nat.ptr(pos), dtype, nat.HOST)
+
+    def set_resort(self, fraction):
+        """Re-sort the residents when more than ``fraction`` of them left their brick."""
+        self.ctx("pppm_ctx_set_resort", float(fraction))
+
+    def resident_info(self):
+        info = (ctypes.c_int64 * 4)()
+        self.ctx("pppm_ctx_resident_info", info)
+        return dict(zip(("movers", "resorts", "max_brick", "n"), list(info)))
+
+    def set_variant(self, kernel, variant):
+        self.ctx("pppm_ctx_set_variant", int(kernel), int(variant))
+
     def step(self, phases=nat.PHASE_ALL):
         self.ctx("pppm_ctx_step", int(phases))
 
@@ -103,7 +126,8 @@ class PppmContext:
 
     def compute(self, positions, charges, mem=nat.HOST, out=None):
         """One full evaluation through the C ABI with host buffers (H2D, step, D2H).
-        ``out``: optional (n, 3) float64 destination (e.g. a pinned PinnedArray view)."""
+        ``out``: optional (n, 3) float64 destination (e.g. a pinned PinnedArray
+        view), or float32 on a mixed-precision context (the path's own precision)."""
         pos = np.ascontiguousarray(positions)
         q = np.ascontiguousarray(charges)
         dtype = nat.F32 if pos.dtype == np.float32 else nat.F64
@@ -111,10 +135,12 @@ class PppmContext:
             forces = np.empty((pos.shape[0], 3))
         else:
             forces = out
-            if forces.shape != (pos.shape[0], 3) or forces.dtype != np.float64 or not forces.flags.c_contiguous:
-                raise ValueError("out must be a C-contiguous (n, 3) float64 array")
+            if (forces.shape != (pos.shape[0], 3) or forces.dtype not in (np.float64, np.float32)
+                    or not forces.flags.c_contiguous):
+                raise ValueError("out must be a C-contiguous (n, 3) float64 or float32 array")
         e = np.zeros(1)
-        self.ctx("pppm_compute", nat.ptr(pos), nat.ptr(q), pos.shape[0], dtype, mem, nat.ptr(forces),
+        fdt = nat.F64 if forces.dtype == np.float64 else nat.F32
+        self.ctx("pppm_compute_ex", nat.ptr(pos), nat.ptr(q), pos.shape[0], dtype, mem, nat.ptr(forces), fdt,
                  e.ctypes.data_as(nat._dp))
         return forces, float(e[0])
 

@@ -6,8 +6,11 @@ namespace pppm {
 
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
-               int* err, const int* orig, cudaStream_t s) {
-  if (cudaMemsetAsync(counts, 0, sizeof(int) * (bk.count() + 2) * kCountStride, s) != cudaSuccess) return launch_status();
+               int* err, const int* orig, cudaStream_t s, int64_t ibase, bool reset) {
+  // ibase: caller index of a[0] (a chunk of a larger input binned by several
+  // launches); reset: zero the bucket counters first (the first chunk)
+  if (reset && cudaMemsetAsync(counts, 0, sizeof(int) * (bk.count() + 2) * kCountStride, s) != cudaSuccess)
+    return launch_status();
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
@@ -27,11 +30,11 @@ int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Brick
       if (!a.f32)
         k_bin_fixed<S, TAB, double><<<grid, kThreads, 0, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, bk,
                                                               cap, n_points, counts, rec, rcell, perm, ovf_rec,
-                                                              ovf_cell, ovf_perm, err, orig);
+                                                              ovf_cell, ovf_perm, err, orig, ibase);
       else
         k_bin_fixed<S, TAB, float><<<grid, kThreads, 0, s>>>((const float*)a.pos, (const float*)a.q, a.n, g, bk,
                                                              cap, n_points, counts, rec, rcell, perm, ovf_rec,
-                                                             ovf_cell, ovf_perm, err, orig);
+                                                             ovf_cell, ovf_perm, err, orig, ibase);
       return 0;
     });
   });
@@ -141,35 +144,88 @@ __global__ void k_rank_cells(float4* __restrict__ rec, const int* __restrict__ c
 // new positions (caller's order) into the brick-ordered resident array (fp32)
 template <int S, typename TIn>
 __global__ void k_update_resident(const TIn* __restrict__ pos, const int* __restrict__ orig, int64_t n, Geom g,
-                                  float* __restrict__ res_pos, int* __restrict__ err) {
+                                  Bricks bk, const int* __restrict__ res_brick, float* __restrict__ res_pos,
+                                  int* __restrict__ err, int* __restrict__ movers) {
+  int mv = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = orig[k];
     const float x = round_pos_f32((double)pos[3 * i], g.lx), y = round_pos_f32((double)pos[3 * i + 1], g.ly),
                 z = round_pos_f32((double)pos[3 * i + 2], g.lz);
     if (outside((double)x, g.lx) || outside((double)y, g.ly) || outside((double)z, g.lz)) {
       atomicOr(err, 1);
-    } else if (g.nzl < g.nz) {
-      // z-slab: the atom must still be owned by this slab (bit-exact node_z)
-      int nd;
+    } else {
+      // brick of the new position (bit-exact nodes): atoms outside the brick
+      // they were sorted into take make_rho's / fieldforce's direct path;
+      // their count drives the automatic re-sort
+      int n0, n1, n2;
       double t;
-      particle_map_1d<S>((double)z, g.hz, nd, t);
-      nd = nd >= g.nz ? nd - g.nz : nd;
-      if (nd < g.z0 || nd >= g.z0 + g.nzl) atomicOr(err, 2);
+      particle_map_1d<S>((double)x, g.hx, n0, t);
+      particle_map_1d<S>((double)y, g.hy, n1, t);
+      particle_map_1d<S>((double)z, g.hz, n2, t);
+      n0 = n0 >= g.nx ? n0 - g.nx : n0;
+      n1 = n1 >= g.ny ? n1 - g.ny : n1;
+      n2 = n2 >= g.nz ? n2 - g.nz : n2;
+      if (g.nzl < g.nz && (n2 < g.z0 || n2 >= g.z0 + g.nzl)) atomicOr(err, 2);  // left this z-slab
+      n2 -= g.z0;
+      const int b = ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
+      if (res_brick && b != res_brick[k]) ++mv;
     }
     res_pos[3 * k] = x;
     res_pos[3 * k + 1] = y;
     res_pos[3 * k + 2] = z;
   }
+  if (movers) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mv += __shfl_xor_sync(0xffffffffu, mv, o);
+    if ((threadIdx.x & 31) == 0 && mv) atomicAdd(movers, mv);
+  }
+}
+
+// brick of every resident slot from the per-brick ranges (after a sort)
+__global__ void k_slot_bricks(const int* __restrict__ start, int nb, int64_t n, int* __restrict__ res_brick) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nb;  // last b with start[b] <= k (k >= start[nb]: overflowed at the sort, -1)
+    if (k >= start[nb]) {
+      res_brick[k] = -1;
+      continue;
+    }
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (start[mid] <= k) lo = mid;
+      else hi = mid;
+    }
+    res_brick[k] = lo;
+  }
+}
+
+int launch_slot_bricks(const int* start, int nb, int64_t n, int* res_brick, cudaStream_t s) {
+  k_slot_bricks<<<grid_for(n), kThreads, 0, s>>>(start, nb, n, res_brick);
+  return launch_status();
+}
+
+// new caller index of every resident slot after a re-sort: orig_new[k] = orig_old[perm[k]]
+__global__ void k_compose(const int* __restrict__ orig_old, const int* __restrict__ perm, int64_t n,
+                          int* __restrict__ orig_new) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    orig_new[k] = orig_old[perm[k]];
+}
+
+int launch_compose(const int* orig_old, const int* perm, int64_t n, int* orig_new, cudaStream_t s) {
+  k_compose<<<grid_for(n), kThreads, 0, s>>>(orig_old, perm, n, orig_new);
+  return launch_status();
 }
 
 int launch_update_resident(int order, bool f32, const void* pos, const int* orig, int64_t n, const Geom& g,
-                           float* res_pos, int* err, cudaStream_t s) {
+                           const Bricks& bk, const int* res_brick, float* res_pos, int* err, int* movers,
+                           cudaStream_t s) {
   const int st = with_order(order, [&](auto S_) {
     constexpr int S = decltype(S_)::value;
     if (f32)
-      k_update_resident<S, float><<<grid_for(n), kThreads, 0, s>>>((const float*)pos, orig, n, g, res_pos, err);
+      k_update_resident<S, float><<<grid_for(n), kThreads, 0, s>>>((const float*)pos, orig, n, g, bk, res_brick,
+                                                                   res_pos, err, movers);
     else
-      k_update_resident<S, double><<<grid_for(n), kThreads, 0, s>>>((const double*)pos, orig, n, g, res_pos, err);
+      k_update_resident<S, double><<<grid_for(n), kThreads, 0, s>>>((const double*)pos, orig, n, g, bk, res_brick,
+                                                                    res_pos, err, movers);
     return 0;
   });
   return st ? st : launch_status();

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, (S >= 6 ? 4 : PPPM_BIN_MINB)) k_bin_
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk, int cap,
     int n_points, int* __restrict__ counts, float4* __restrict__ rec, int* __restrict__ rcell,
     int* __restrict__ perm, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell, int* __restrict__ ovf_perm,
-    int* __restrict__ err, const int* __restrict__ orig) {
+    int* __restrict__ err, const int* __restrict__ orig, int64_t ibase) {
   const int nb = bk.count();
   int* ovf_count = counts + (int64_t)nb * kCountStride;
   float qmax = 0.f;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, (S >= 6 ? 4 : PPPM_BIN_MINB)) k_bin_
     for (int u = 0; u < kBinUnroll; ++u) {
       if (b[u] < 0) continue;
       const int64_t i = i0 + u * stride;
-      const int oi = orig ? orig[i] : (int)i;  // index in the caller's atom order
+      const int oi = orig ? orig[i] : (int)(i + ibase);  // index in the caller's atom order
       if (slot[u] < cap) {
         // one 32-byte slot per atom (full-sector write): {tx, ty, tz, q}, {cell, input index}
         const int64_t k = (int64_t)b[u] * cap + slot[u];

@@ -186,6 +186,18 @@ struct pppm_ctx {
   // (pppm_slab_attach_nccl), used on the context stream and inside its graphs
   ncclComm_t comm = nullptr;
   double nccl_timeout_s = 600.0;
+  // pppm_compute_ex: host atoms copied in chunks on a second stream
+  // automatic re-sort of the resident atoms (MD): movers counted by each
+  // position update, re-sorted when they exceed resort_frac of the atoms
+  DevBuf res_brick, res_movers, res_perm, res_orig_tmp;
+  int* h_movers = nullptr;
+  cudaEvent_t movers_ev = nullptr;
+  bool movers_pending = false;
+  double resort_frac = 0.05;
+  int64_t resorts = 0, last_movers = 0;
+  static constexpr int kChunks = 8;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[kChunks] = {};
 
   bool fp64() const { return prec == PPPM_PREC_FP64; }
   size_t real_size() const { return fp64() ? sizeof(double) : sizeof(float); }
@@ -925,6 +937,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_PLANE")) c->use_plane = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_RESORT")) c->resort_frac = atof(v);
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
   return PPPM_OK;
@@ -950,7 +963,13 @@ int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
   else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_WSP)
     c->gather_variant = variant;
-  else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
+  else if (kernel == 2 && variant >= 0 && variant <= 2) {
+    // resident atoms (takes effect at the next pppm_ctx_load_atoms): 0 = caller's
+    // order, binned every step (the one-shot path's work); 1 = brick order,
+    // binned every step; 2 = brick order, no binning pass [default]
+    c->sort_resident = variant >= 1;
+    c->res_direct = variant == 2;
+  } else return fail(PPPM_ERR_VALUE, "unknown kernel variant");
   if (!c->fp64() && c->fields.p) TRY(encode_maps(c));
   return PPPM_OK;
 }
@@ -991,6 +1010,15 @@ int pppm_ctx_destroy(pppm_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_scal) cudaFreeHost(c->h_scal);
+  for (auto& e : c->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->movers_ev) cudaEventDestroy(c->movers_ev);
+  if (c->h_movers) cudaFreeHost(c->h_movers);
+  c->res_brick.release();
+  c->res_movers.release();
+  c->res_perm.release();
+  c->res_orig_tmp.release();
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return PPPM_OK;
@@ -1261,6 +1289,105 @@ int pppm_compute(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dty
   return PPPM_OK;
 }
 
+// pppm_compute with the output type chosen by the caller, and for host fp32
+// inputs on the mixed path the H2D copy overlapped with binning: the atoms
+// travel in chunks on a copy stream and each chunk is binned as soon as it
+// has landed (the slot records carry the caller's index, so chunks bin
+// independently into the same buckets)
+int pppm_compute_ex(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, void* forces,
+                    int forces_dtype, double* energy) {
+  TRY(activate(c));
+  if (forces_dtype != PPPM_F64 && forces_dtype != PPPM_F32) return fail(PPPM_ERR_VALUE, "unknown forces dtype");
+  if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
+  if (dtype != PPPM_F64 && dtype != PPPM_F32) return fail(PPPM_ERR_VALUE, "unknown dtype");
+  const bool f64_out = forces_dtype == PPPM_F64;
+  if (c->fp64() && !f64_out) return fail(PPPM_ERR_VALUE, "fp64 contexts return fp64 forces");
+  const size_t es = dtype == PPPM_F64 ? 8 : 4;
+  if (c->fp64() || mem == PPPM_DEVICE || c->slab) {
+    const void *dpos, *dq;
+    TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
+    TRY(do_make_rho(c, dpos, dq, n, dtype));
+    TRY(run_poisson(c));
+    TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
+    TRY(do_fieldforce(c, dpos, dq, n, dtype, false, c->out_stage.p, f64_out));
+  } else {
+    TRY(c->pos_stage.ensure(3 * n * es));
+    TRY(c->q_stage.ensure(n * es));
+    TRY(ensure_bins(c, n));
+    if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : c->chunk_ev)
+      if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const int64_t per = std::max<int64_t>(1 << 17, (n + pppm_ctx::kChunks - 1) / pppm_ctx::kChunks);
+    c->binned = false;
+    int k = 0;
+    for (int64_t off = 0; off < n; off += per, ++k) {
+      const int64_t m = std::min(per, n - off);
+      char* dp = (char*)c->pos_stage.p + 3 * off * es;
+      char* dq = (char*)c->q_stage.p + off * es;
+      CU(cudaMemcpyAsync(dp, (const char*)pos + 3 * off * es, 3 * m * es, cudaMemcpyHostToDevice, c->copy_stream));
+      CU(cudaMemcpyAsync(dq, (const char*)q + off * es, m * es, cudaMemcpyHostToDevice, c->copy_stream));
+      CU(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
+      CU(cudaStreamWaitEvent(c->stream, c->chunk_ev[k], 0));
+      TRY(launch_bin(c->order, c->n_points > 0, atoms_in(dp, dq, m, dtype), c->g, c->bk, c->cap, c->n_points,
+                     c->counts.as<int>(), c->rec.as<float4>(), c->rcell.as<int>(), c->perm.as<int>(),
+                     c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->err.as<int>(), nullptr,
+                     c->stream, off, off == 0));
+      c->launches += 1;
+    }
+    c->binned = true;
+    TRY(run_spread(c, c->pos_stage.p, c->q_stage.p, n, dtype));
+    TRY(run_poisson(c));
+    TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
+    TRY(run_gather(c, c->pos_stage.p, c->q_stage.p, n, dtype, c->out_stage.p, f64_out));
+  }
+  CU(cudaMemcpyAsync(forces, c->out_stage.p, (f64_out ? 8 : 4) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(c->h_scal, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  TRY(check_err_flag(c));
+  if (energy) *energy = c->h_scal[0];
+  return PPPM_OK;
+}
+
+// after a brick sort: the largest brick (staging capacity of the resident
+// fieldforce; only grows, a larger capacity than needed is safe and keeps the
+// captured graphs valid) and every slot's brick (mover detection)
+static int after_sort(pppm_ctx* c) {
+  std::vector<int> st(c->bk.count() + 1);
+  CU(cudaMemcpyAsync(st.data(), c->bstart.as<int>(), sizeof(int) * st.size(), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  int mx = 1;
+  for (int b = 0; b < c->bk.count(); ++b) mx = std::max(mx, st[b + 1] - st[b]);
+  if (mx > c->res_maxcnt) {
+    if (c->res_maxcnt > 0) drop_graphs(c);
+    c->res_maxcnt = mx;
+  }
+  TRY(c->res_brick.ensure(sizeof(int) * c->n_res));
+  TRY(launch_slot_bricks(c->bstart.as<int>(), c->bk.count(), c->n_res, c->res_brick.as<int>(), c->stream));
+  return PPPM_OK;
+}
+
+// re-sort the (fp32, brick-ordered) resident atoms in place: bin them again,
+// reorder into the scratch arrays, copy back (the captured graphs keep their
+// pointers) and compose the caller-index map
+static int resort_residents(pppm_ctx* c) {
+  const int64_t n = c->n_res;
+  TRY(run_bin(c, c->res_pos.p, c->res_q.p, n, PPPM_F32, nullptr));
+  TRY(c->res_tmp_pos.ensure(3 * n * sizeof(float)));
+  TRY(c->res_tmp_q.ensure(n * sizeof(float)));
+  TRY(c->res_perm.ensure(sizeof(int) * n));
+  TRY(c->res_orig_tmp.ensure(sizeof(int) * n));
+  TRY(launch_reorder_resident(true, c->bk, c->cap, c->rec.as<float4>(), c->counts.as<int>(), c->bstart.as<int>(),
+                              c->ovf_perm.as<int>(), n, c->res_pos.p, c->res_q.p, c->res_tmp_pos.p, c->res_tmp_q.p,
+                              c->res_perm.as<int>(), c->stream));
+  TRY(launch_compose(c->res_orig.as<int>(), c->res_perm.as<int>(), n, c->res_orig_tmp.as<int>(), c->stream));
+  CU(cudaMemcpyAsync(c->res_pos.p, c->res_tmp_pos.p, 3 * n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->res_q.p, c->res_tmp_q.p, n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->res_orig.p, c->res_orig_tmp.p, n * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+  c->launches += 5;
+  c->resorts += 1;
+  c->binned = false;
+  return after_sort(c);
+}
+
 int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
   TRY(activate(c));
   drop_graphs(c);
@@ -1269,8 +1396,9 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   TRY(c->res_pos.ensure(3 * n * es));
   TRY(c->res_q.ensure(n * es));
   TRY(c->res_force.ensure(3 * n * (c->fp64() ? 8 : 4)));
-  CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * n * es, cudaMemcpyHostToDevice, c->stream));
-  CU(cudaMemcpyAsync(c->res_q.p, q, n * es, cudaMemcpyHostToDevice, c->stream));
+  // host or device buffers (unified addressing)
+  CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * n * es, cudaMemcpyDefault, c->stream));
+  CU(cudaMemcpyAsync(c->res_q.p, q, n * es, cudaMemcpyDefault, c->stream));
   c->n_res = n;
   c->res_dtype = dtype;
   c->res_sorted = false;
@@ -1307,11 +1435,8 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
     CU(cudaStreamSynchronize(c->stream));
     memcpy(&c->res_qmax, &qbits, sizeof(float));
     TRY(c->res_novf.ensure(sizeof(int)));
-    // largest resident brick: shared-memory staging capacity of the resident fieldforce
-    std::vector<int> st(c->bk.count() + 1);
-    CU(cudaMemcpy(st.data(), c->bstart.as<int>(), sizeof(int) * st.size(), cudaMemcpyDeviceToHost));
-    c->res_maxcnt = 1;
-    for (int b = 0; b < c->bk.count(); ++b) c->res_maxcnt = std::max(c->res_maxcnt, st[b + 1] - st[b]);
+    // largest resident brick (staging capacity of the resident fieldforce), slot bricks
+    TRY(after_sort(c));
   }
   CU(cudaStreamSynchronize(c->stream));
   return check_err_flag(c);
@@ -1535,7 +1660,13 @@ int pppm_ctx_synchronize(pppm_ctx* c) {
   return check_err_flag(c);
 }
 
-int pppm_ctx_update_positions(pppm_ctx* c, const void* pos, int dtype, int mem) {
+// new positions of the resident atoms: scattered into brick order on the
+// device; atoms outside their sorted brick are counted, and when they exceed
+// resort_frac of the atoms (PPPM_B200_RESORT, default 0.05) the residents are
+// re-sorted.  sync: wait and check (errors, the mover count of this update);
+// async: nothing waits - errors surface at the next synchronize, and the mover
+// count of the previous update decides the re-sort.
+static int update_positions(pppm_ctx* c, const void* pos, int dtype, int mem, bool sync) {
   TRY(activate(c));
   if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
   if (!c->res_sorted || c->res_dtype != PPPM_F32) {
@@ -1545,8 +1676,19 @@ int pppm_ctx_update_positions(pppm_ctx* c, const void* pos, int dtype, int mem) 
     CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * c->n_res * es, mem == PPPM_DEVICE ? cudaMemcpyDeviceToDevice
                                                                                  : cudaMemcpyHostToDevice,
                        c->stream));
-    CU(cudaStreamSynchronize(c->stream));
+    if (sync) CU(cudaStreamSynchronize(c->stream));
     return PPPM_OK;
+  }
+  if (!c->h_movers) {
+    CU(cudaHostAlloc(&c->h_movers, sizeof(int), 0));
+    CU(cudaEventCreateWithFlags(&c->movers_ev, cudaEventDisableTiming));
+    TRY(c->res_movers.ensure(sizeof(int)));
+  }
+  // the previous update's movers (async path): re-sort before moving on
+  if (!sync && c->movers_pending && cudaEventQuery(c->movers_ev) == cudaSuccess) {
+    c->movers_pending = false;
+    c->last_movers = *c->h_movers;
+    if (c->last_movers > c->resort_frac * (double)c->n_res) TRY(resort_residents(c));
   }
   const void* dp = pos;
   if (mem == PPPM_HOST) {
@@ -1555,10 +1697,47 @@ int pppm_ctx_update_positions(pppm_ctx* c, const void* pos, int dtype, int mem) 
     CU(cudaMemcpyAsync(c->pos_stage.p, pos, 3 * c->n_res * es, cudaMemcpyHostToDevice, c->stream));
     dp = c->pos_stage.p;
   }
-  TRY(launch_update_resident(c->order, dtype == PPPM_F32, dp, c->res_orig.as<int>(), c->n_res, c->g, c->res_pos.as<float>(),
-                             c->err.as<int>(), c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  return check_err_flag(c);
+  CU(cudaMemsetAsync(c->res_movers.p, 0, sizeof(int), c->stream));
+  TRY(launch_update_resident(c->order, dtype == PPPM_F32, dp, c->res_orig.as<int>(), c->n_res, c->g, c->bk,
+                             c->res_brick.as<int>(), c->res_pos.as<float>(), c->err.as<int>(),
+                             c->res_movers.as<int>(), c->stream));
+  CU(cudaMemcpyAsync(c->h_movers, c->res_movers.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaEventRecord(c->movers_ev, c->stream));
+  c->launches += 1;
+  if (!sync) {
+    c->movers_pending = true;
+    return PPPM_OK;
+  }
+  TRY(check_err_flag(c));
+  c->movers_pending = false;
+  c->last_movers = *c->h_movers;
+  if (c->last_movers > c->resort_frac * (double)c->n_res) TRY(resort_residents(c));
+  return PPPM_OK;
+}
+
+int pppm_ctx_update_positions(pppm_ctx* c, const void* pos, int dtype, int mem) {
+  return update_positions(c, pos, dtype, mem, true);
+}
+
+int pppm_ctx_update_positions_async(pppm_ctx* c, const void* pos, int dtype, int mem) {
+  return update_positions(c, pos, dtype, mem, false);
+}
+
+// info[4]: movers at the last counted update, re-sorts so far, largest brick, resident atoms
+int pppm_ctx_resident_info(pppm_ctx* c, int64_t* info) {
+  if (!c || !info) return fail(PPPM_ERR_VALUE, "null argument");
+  info[0] = c->last_movers;
+  info[1] = c->resorts;
+  info[2] = c->res_maxcnt;
+  info[3] = c->n_res;
+  return PPPM_OK;
+}
+
+// fraction of the resident atoms outside their brick that triggers a re-sort (<= 0: never)
+int pppm_ctx_set_resort(pppm_ctx* c, double fraction) {
+  if (!c) return fail(PPPM_ERR_VALUE, "null context");
+  c->resort_frac = fraction > 0 ? fraction : 1e30;
+  return PPPM_OK;
 }
 
 int pppm_ctx_get_forces(pppm_ctx* c, double* forces) {
@@ -2013,17 +2192,35 @@ int pppm_ctx_pair_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n,
 // full force evaluation on device atoms: pair forces + mesh forces -> out (n, 3)
 // fp64, energies -> pr_scal[0] (pair), scal[0] (kspace), pr_scal[1] (self).
 // ev (nullable): 5 events bracketing pair | make_rho | Poisson | fieldforce
+// md_step >= 0 on a mixed-precision context: the mesh part of an MD step on
+// the resident path - the atoms are loaded (and brick-sorted) at step 0 and
+// afterwards only moved (update_positions_async: scatter into brick order,
+// automatic re-sort), so make_rho has no binning pass; the brick-ordered fp32
+// forces are un-permuted into `out` (fp64, caller order)
 static int forces_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double rc, const double* lj,
-                         double* out, long long* counters, cudaEvent_t* ev = nullptr) {
+                         double* out, long long* counters, cudaEvent_t* ev = nullptr, int md_step = -1) {
   if (ev) cudaEventRecord(ev[0], c->stream);
   TRY(pair_device(c, dpos, dq, n, c->alpha, rc, lj, counters));
   if (ev) cudaEventRecord(ev[1], c->stream);
-  TRY(do_make_rho(c, dpos, dq, n, PPPM_F64));
-  if (ev) cudaEventRecord(ev[2], c->stream);
-  TRY(run_poisson(c));
-  if (ev) cudaEventRecord(ev[3], c->stream);
-  TRY(do_fieldforce(c, dpos, dq, n, PPPM_F64, false, out, true));
-  if (ev) cudaEventRecord(ev[4], c->stream);
+  if (!c->fp64() && md_step >= 0 && c->sort_resident && !c->slab) {
+    if (md_step == 0 || c->n_res != n) TRY(pppm_ctx_load_atoms(c, dpos, dq, n, PPPM_F64));
+    else TRY(update_positions(c, dpos, PPPM_F64, PPPM_DEVICE, false));
+    TRY(step_phases(c, PPPM_PHASE_MAKE_RHO, false));
+    if (ev) cudaEventRecord(ev[2], c->stream);
+    TRY(step_phases(c, PPPM_PHASE_POISSON, false));
+    if (ev) cudaEventRecord(ev[3], c->stream);
+    TRY(step_phases(c, PPPM_PHASE_FIELDFORCE, false));
+    TRY(launch_unpermute_forces(c->res_force.as<float>(), c->res_orig.as<int>(), n, out, c->stream));
+    c->launches += 1;
+    if (ev) cudaEventRecord(ev[4], c->stream);
+  } else {
+    TRY(do_make_rho(c, dpos, dq, n, PPPM_F64));
+    if (ev) cudaEventRecord(ev[2], c->stream);
+    TRY(run_poisson(c));
+    if (ev) cudaEventRecord(ev[3], c->stream);
+    TRY(do_fieldforce(c, dpos, dq, n, PPPM_F64, false, out, true));
+    if (ev) cudaEventRecord(ev[4], c->stream);
+  }
   TRY(launch_add3(c->pr_force.as<double>(), out, 3 * n, c->stream));
   // self energy -C alpha / sqrt(pi) sum q^2 (shortrange.py:270-278)
   TRY(launch_square(dq, n, c->pr_e.as<double>(), c->stream));
@@ -2120,7 +2317,7 @@ int pppm_ctx_integrate_nve(pppm_ctx* c, const double* pos, const double* vel, co
   };
   auto eval = [&](int step) -> int {
     long long cnt[2] = {0, 0};
-    const int st = forces_device(c, x, dq, n, cutoff, lj, f, cnt, sections ? ev : nullptr);
+    const int st = forces_device(c, x, dq, n, cutoff, lj, f, cnt, sections ? ev : nullptr, step);
     if (st != PPPM_OK) {
       g_err = "step " + std::to_string(step) + ": " + g_err;  // driver.py:345-347
       return st;

@@ -89,7 +89,7 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
                         double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s);
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
-               int* err, const int* orig, cudaStream_t s);
+               int* err, const int* orig, cudaStream_t s, int64_t ibase = 0, bool reset = true);
 int launch_pair(const double* pos, const double* q, int64_t n, double lx, double ly, double lz, double alpha,
                 double rc, double scale, const double* lj, int* cell, int* count, int* start, int* cursor,
                 int* order, int* tmp, double4* sp, double* force, double* e_atom, unsigned long long* cnt,
@@ -118,7 +118,10 @@ int launch_zfft_green(int mode, int nz, int ny_full, int y0, int nyl, int nx, co
                       const float* ik, float inv_m, const float2* tw, float2* out, int64_t fstride, double* partial,
                       unsigned* done, double prefactor, double* energy, cudaStream_t s);
 int launch_update_resident(int order, bool f32, const void* pos, const int* orig, int64_t n, const Geom& g,
-                           float* res_pos, int* err, cudaStream_t s);
+                           const Bricks& bk, const int* res_brick, float* res_pos, int* err, int* movers,
+                           cudaStream_t s);
+int launch_slot_bricks(const int* start, int nb, int64_t n, int* res_brick, cudaStream_t s);
+int launch_compose(const int* orig_old, const int* perm, int64_t n, int* orig_new, cudaStream_t s);
 int launch_round_positions(const double* pos, int64_t n, const Geom& g, float* out, cudaStream_t s);
 int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,

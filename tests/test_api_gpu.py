@@ -170,3 +170,38 @@ def test_one_shot_call_regrowing_bins_keeps_resident_step(pb):
 def test_mixed_grid_limit(pb):
     with pytest.raises(pb.ConfigurationError, match="1024"):
         pb.PppmContext((2048, 8, 8), (2048.0, 8.0, 8.0), order=5, mode="ik", precision="mixed", alpha=0.3)
+
+
+@pytest.mark.parametrize("mode", ["ik", "ad"])
+def test_compute_chunked_h2d_and_fp32_forces(pb, mode):
+    """pppm_compute_ex: host atoms binned chunk by chunk as they land (several
+    chunks of 2^17), forces returned as fp64 or fp32; same result as the
+    resident step and the oracle."""
+    from paper_1702_04250_b200 import scenarios
+
+    pos, q, lengths = scenarios.random_gas(400000, 41, 160.0)
+    p32 = scenarios.round_to_f32(pos, lengths)
+    q32 = q.astype(np.float32)
+    ctx = pb.PppmContext((64, 64, 64), lengths, order=5, mode=mode, precision="mixed", alpha=0.25)
+    try:
+        f64, e64 = ctx.compute(p32, q32)
+        f32, e32 = ctx.compute(p32, q32, out=np.empty((q.size, 3), dtype=np.float32))
+        ctx.load_atoms(p32, q32)
+        ctx.step()
+        ctx.synchronize()
+        fr = ctx.forces()
+    finally:
+        ctx.close()
+    assert f32.dtype == np.float32
+    assert rel_rms(f32, f64) <= 1e-6 and abs(e32 - e64) <= 1e-6 * abs(e64)
+    assert rel_rms(f64, fr) <= 1e-6
+    sub = np.random.default_rng(3).choice(q.size, 4096, replace=False)
+    rho_ref = orc.map_charge(p32.astype(np.float64), q, lengths, (64, 64, 64), 5, workers=8)
+    g = orc.influence_pme((64, 64, 64), lengths, 0.25, 5)
+    if mode == "ik":
+        fields = orc.poisson_ik(rho_ref, g, orc.ik_vectors((64, 64, 64), lengths))
+        f_ref = orc.fieldforce_ik(fields, p32[sub].astype(np.float64), q[sub], lengths, (64, 64, 64), 5)
+    else:
+        phi = orc.poisson_ad(rho_ref, g)
+        f_ref = orc.fieldforce_ad(phi, p32[sub].astype(np.float64), q[sub], lengths, (64, 64, 64), 5)
+    assert rel_rms(f64[sub], f_ref) <= 1e-5

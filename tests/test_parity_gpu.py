@@ -554,8 +554,10 @@ def test_resident_direct_movers_and_overflow(pb, mode):
         ctx.synchronize()
         f, e = ctx.forces(), ctx.energy()
         fr, er = ref.compute(p32, q32)
-        assert rel_rms(f, fr) <= 1e-6
-        assert abs(e - er) <= 1e-6 * abs(er)
+        # movers take the direct fp32 path in the resident step, their brick
+        # tile's fixed point in the binned one: rounding-level differences
+        assert rel_rms(f, fr) <= 3e-6
+        assert abs(e - er) <= 3e-6 * abs(er)
         # move every atom by up to ~1.5 mesh cells: many leave their brick
         p32 = scenarios.round_to_f32(np.mod(p32.astype(np.float64) + rng.uniform(-2.3, 2.3, p32.shape), edge),
                                      lengths)
