@@ -19,12 +19,8 @@ int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Brick
 #ifdef PPPM_BIN_PERSIST
       {
         // one resident wave (grid-stride), no tail wave
-        int per_sm = 0, dev = 0, sms = 148;
-        if (a.f32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bin_fixed<S, TAB, float>, kThreads, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bin_fixed<S, TAB, double>, kThreads, 0);
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = std::min(grid, std::max(1, per_sm) * sms);
+        grid = a.f32 ? persistent_grid(k_bin_fixed<S, TAB, float>, kThreads, 0, grid)
+                     : persistent_grid(k_bin_fixed<S, TAB, double>, kThreads, 0, grid);
       }
 #endif
       if (!a.f32)

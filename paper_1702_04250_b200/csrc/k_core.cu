@@ -13,9 +13,70 @@
 // order, and the energy reduction uses a fixed grid with an ordered final sum.
 #include <cuComplex.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "pppm_device.cuh"
+#include "k_fp32.cuh"
 
 namespace pppm {
+
+// ---------------------------------------------------------------------------
+// launch-configuration cache (persistent_grid, k_fp32.cuh): the SM count per
+// device and the occupancy per (kernel, threads, dynamic smem), queried once
+namespace {
+struct OccKey {
+  const void* k;
+  int threads;
+  size_t dyn;
+  int dev;
+  bool operator<(const OccKey& o) const {
+    return std::tie(k, threads, dyn, dev) < std::tie(o.k, o.threads, o.dyn, o.dev);
+  }
+};
+std::mutex g_occ_mu;
+std::map<OccKey, int> g_occ;
+int g_sms[64] = {};
+}  // namespace
+
+bool occ_cached(const void* kernel, int threads, size_t dyn, int* sms, int* per_sm) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_occ_mu);
+  if (dev >= 0 && dev < 64) {
+    if (!g_sms[dev]) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    *sms = g_sms[dev] > 0 ? g_sms[dev] : 148;
+  }
+  auto it = g_occ.find(OccKey{kernel, threads, dyn, dev});
+  if (it == g_occ.end()) return false;
+  *per_sm = it->second;
+  return true;
+}
+
+bool smem_raise(const void* kernel, size_t dyn) {
+  static std::map<std::pair<const void*, int>, size_t> attr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_occ_mu);
+  size_t& cur = attr[{kernel, dev}];
+  if (dyn <= cur) return false;
+  cur = dyn;
+  return true;
+}
+
+int device_sm_count() {
+  int sms = 148, per_sm = 0;
+  occ_cached(nullptr, 0, 0, &sms, &per_sm);
+  return sms;
+}
+
+void occ_store(const void* kernel, int threads, size_t dyn, int per_sm) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_occ_mu);
+  g_occ[OccKey{kernel, threads, dyn, dev}] = per_sm;
+}
 
 template <int S, typename TIn, bool R32>
 __global__ void k_particle_map(const TIn* __restrict__ pos, int64_t n, Geom g,

@@ -84,6 +84,39 @@ inline void allow_smem(K kernel, size_t bytes) {
   if (PPPM_CARVEOUT >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, PPPM_CARVEOUT);
 }
 
+// Grid of a persistent kernel: min(work items, SMs x resident CTAs per SM).
+// The SM count and each (kernel, threads, dynamic smem) occupancy are queried
+// once and cached (launch_cache in k_core.cu), so the launchers - which run
+// every step on the eager / one-shot paths - make no device queries.
+bool occ_cached(const void* kernel, int threads, size_t dyn, int* sms, int* per_sm);
+void occ_store(const void* kernel, int threads, size_t dyn, int per_sm);
+// true when `dyn` exceeds the largest dynamic smem opted in for `kernel` so far
+// (the attribute is a per-function maximum: lowering it would break a later
+// launch with a larger size that hits the occupancy cache)
+bool smem_raise(const void* kernel, size_t dyn);
+
+// PPPM_B200_DEBUG: report a failed launch of a persistent kernel with its configuration
+inline void debug_launch(const char* what, int grid, int threads, size_t dyn) {
+  static const bool on = getenv("PPPM_B200_DEBUG") != nullptr;
+  if (!on) return;
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess)
+    fprintf(stderr, "pppm_b200: %s launch failed: %s (grid %d, threads %d, dyn smem %zu)\n", what,
+            cudaGetErrorString(e), grid, threads, dyn);
+}
+
+template <typename K>
+inline int persistent_grid(K kernel, int threads, size_t dyn, int items) {
+  int sms = 148, per_sm = 0;
+  if (smem_raise((const void*)kernel, dyn)) allow_smem(kernel, dyn);
+  if (!occ_cached((const void*)kernel, threads, dyn, &sms, &per_sm)) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn);
+    occ_store((const void*)kernel, threads, dyn, per_sm);
+  }
+  const int cap = sms * (per_sm > 0 ? per_sm : 1);
+  return items < 1 ? 1 : (items < cap ? items : cap);
+}
+
 // ---------------------------------------------------------------------------
 // binning
 

@@ -223,6 +223,7 @@ template <int S> struct SplitTile {
   static constexpr bool ok = (TXB % 32 == 12 || TXB % 32 == 20);
 };
 
+#ifdef PPPM_AB_VARIANTS  // A/B variant (measured slower)
 template <int S, bool TAB, int NT>
 __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
   gather_overflow<S, TAB, 0>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell,
                              ovf_perm);
 }
+#endif
 
 // fieldforce_ik, warp-specialized split variant: warp 0 stages brick i+1
 // (bank-bucketed counting sort of its records into shared memory, TMA loads of
@@ -639,6 +641,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), 3) k_ga
 // 0.5 atoms / cell.  Singles and pairs are bank-bucketed separately and run as
 // two round sets.  Same per-atom arithmetic (and bitwise the same forces) as
 // k_gather_ws.
+#ifdef PPPM_AB_VARIANTS  // A/B variant (measured slower)
 template <int S, bool TAB>
 __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3) k_gather_wsp(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, int scap, Geom g, Bricks bk, Pad pd,
@@ -920,6 +923,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
   gather_overflow<S, TAB, 0>(rstart ? novf_res : counts + (int64_t)nb * kCountStride, g, pd, ta, td, fields, cscale,
                              force, out_f64, ovf_rec, ovf_cell, ovf_perm);
 }
+#endif
 
 template <int MODE>
 int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const float4* rec, const int* rcell,
@@ -930,10 +934,8 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if constexpr (MODE == 0 && SplitTile<S>::ok) {
+#ifdef PPPM_AB_VARIANTS
       if (variant == GATHER_WSP) {
         const int hc = (scap + 1) / 2;
         const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
@@ -942,32 +944,30 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
         return with_bool(tab, [&](auto T_) -> int {
           constexpr bool TAB = decltype(T_)::value;
           auto k = k_gather_wsp<S, TAB>;
-          allow_smem(k, dyn);
           constexpr int NT = 32 * (kWsConsumerWarps + kWsProducerWarps);
-          int per_sm = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          const int grid = persistent_grid(k, NT, dyn, bk.count());
           k<<<grid, NT, dyn, s>>>(rec, counts, cap, scap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
                                   ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+          debug_launch("gather", grid, NT, dyn);
           return 0;
         });
       }
+#endif
       if (variant == GATHER_WS) {
         const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
                            2 * (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
         return with_bool(tab, [&](auto T_) -> int {
           constexpr bool TAB = decltype(T_)::value;
           auto k = k_gather_ws<S, TAB>;
-          allow_smem(k, dyn);
           constexpr int NT = 32 * (kWsConsumerWarps + kWsProducerWarps);
-          int per_sm = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          const int grid = persistent_grid(k, NT, dyn, bk.count());
           k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
                                   ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+          debug_launch("gather", grid, NT, dyn);
           return 0;
         });
       }
+#ifdef PPPM_AB_VARIANTS
       if (variant == GATHER_SPLIT) {
         const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
                            (size_t)cap * (sizeof(float4) + 2 * sizeof(int));
@@ -975,15 +975,14 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
           constexpr bool TAB = decltype(T_)::value;
           constexpr int NT = kGatherThreads;
           auto k = k_gather_split<S, TAB, NT>;
-          allow_smem(k, dyn);
-          int per_sm = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          const int grid = persistent_grid(k, NT, dyn, bk.count());
           k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
                                   ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+          debug_launch("gather", grid, NT, dyn);
           return 0;
         });
       }
+#endif
     }
     if constexpr (MODE == 1) {
       if (variant == GATHER_WS) {  // warp-specialized fieldforce_ad
@@ -992,13 +991,11 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
         return with_bool(tab, [&](auto T_) -> int {
           constexpr bool TAB = decltype(T_)::value;
           auto k = k_gather_ws<S, TAB, 1>;
-          allow_smem(k, dyn);
           constexpr int NT = 32 * (kWsConsumerWarps + kWsPw<1>);
-          int per_sm = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-          const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+          const int grid = persistent_grid(k, NT, dyn, bk.count());
           k<<<grid, NT, dyn, s>>>(rec, counts, scap, g, bk, pd, ta, td, fmap, fields, cscale, force, out_f64,
                                   ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+          debug_launch("gather", grid, NT, dyn);
           return 0;
         });
       }
@@ -1008,12 +1005,10 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
       constexpr bool TAB = decltype(T_)::value;
       constexpr int NT = kGatherThreads;
       auto k = k_gather_tma<S, TAB, MODE, NT>;
-      allow_smem(k, dyn);
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-      const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+      const int grid = persistent_grid(k, NT, dyn, bk.count());
       k<<<grid, NT, dyn, s>>>(rec, rcell, perm, counts, cap, g, bk, pd, ta, td, fmap, fields, cscale, force,
                                     out_f64, variant != GATHER_PLAIN, ovf_rec, ovf_cell, ovf_perm, rstart, novf_res);
+      debug_launch("gather", grid, NT, dyn);
       return 0;
     });
   });

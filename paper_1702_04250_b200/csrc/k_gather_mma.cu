@@ -34,6 +34,8 @@
 
 namespace pppm {
 
+#ifdef PPPM_AB_VARIANTS  // A/B variant (measured slower than k_gather_ws)
+
 template <int S> struct MmaTile {
   static constexpr int D = kBrick + S - 1;   // tile edge (y, z); x rows are 16 wide (K)
   static constexpr int NR = D * D;           // (z, y) rows per field in the TMA box
@@ -436,9 +438,7 @@ int launch_gather_mma(int order, bool tab, bool out_f64, const float4* rec, cons
                           kAR * 128 * (4 * ((T::D + 1) / 2) + 4) * sizeof(float);
       // at least half the SM's shared memory: one CTA per SM (each allocates all 512 TMEM columns)
       const size_t dyn = std::max(dyn0, (size_t)116 * 1024);
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int sms = device_sm_count();
       return with_bool(tab, [&](auto T_) -> int {
         constexpr bool TAB = decltype(T_)::value;
         auto k = k_gather_mma<S, TAB>;
@@ -452,5 +452,18 @@ int launch_gather_mma(int order, bool tab, bool out_f64, const float4* rec, cons
   });
   return st ? st : launch_status();
 }
+
+#else  // default build: the tensor-core fieldforce is not compiled (tools/build_variant.py -DPPPM_AB_VARIANTS)
+
+bool gather_mma_ok(int) { return false; }
+
+int launch_gather_mma(int, bool, bool, const float4*, const int*, int, const float4*, const int*, const int*,
+                      const Geom&, const Bricks&, const Pad&, const CUtensorMap&, const float*, const float*,
+                      const float*, float, void*, const int*, const int*, cudaStream_t) {
+  set_error(2, "tensor-core fieldforce not built (A/B variant: -DPPPM_AB_VARIANTS)");
+  return 2;
+}
+
+#endif
 
 }  // namespace pppm

@@ -526,9 +526,7 @@ int launch_pair(const double* pos, const double* q, int64_t n, double lx, double
     pp.lj_rc = lj[2];
   }
   k_pair_sorted<<<grid_for(n), kThreads, 0, s>>>(pos, q, order, n, sp, spf);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sm_count();
   const int64_t want = (n + kPairWarps - 1) / kPairWarps;
   const int grid = (int)std::min<int64_t>(want, (int64_t)sms * 8);
   if (lj)

@@ -197,6 +197,7 @@ __device__ __forceinline__ void warp_fft(float2 (&v)[P], const float2 (&tn)[P], 
   }
 }
 
+#ifdef PPPM_AB_VARIANTS  // warp-register plane FFTs: A/B variant (measured slower)
 constexpr int kPlaneWThreads = 512;
 
 template <int NX, int NY>
@@ -363,6 +364,7 @@ static bool plane_w_ok(int nx, int ny, bool c2r) {
   const int m = v ? atoi(v) : 0;
   return nx >= 64 && ny >= 32 && (m == 1 || (m == 2 && c2r) || (m == 3 && !c2r));
 }
+#endif
 
 bool plane_supported(int nx, int ny) {
   auto p2 = [](int v) { return v >= 16 && v <= 128 && (v & (v - 1)) == 0; };
@@ -407,6 +409,7 @@ int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, fl
                      cudaStream_t s) {
   int st = with_plane(nx, ny, [&](auto NX_, auto NY_) -> int {
     constexpr int NX = decltype(NX_)::value, NY = decltype(NY_)::value;
+#ifdef PPPM_AB_VARIANTS
     if constexpr (NX >= 64 && NY >= 32) {
       if (plane_w_ok(nx, ny, false)) {
         auto kw = k_plane_r2c_w<NX, NY>;
@@ -416,6 +419,7 @@ int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, fl
         return 0;
       }
     }
+#endif
     auto k = k_plane_r2c<NX, NY>;
     constexpr size_t dyn = PlaneDims<NX, NY>::smem;
     if (dyn > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -429,6 +433,7 @@ int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, in
                      const Pad& pd, float* fields, const float2* tw, cudaStream_t s) {
   int st = with_plane(nx, ny, [&](auto NX_, auto NY_) -> int {
     constexpr int NX = decltype(NX_)::value, NY = decltype(NY_)::value;
+#ifdef PPPM_AB_VARIANTS
     if constexpr (NX >= 64 && NY >= 32) {
       if (plane_w_ok(nx, ny, true)) {
         auto kw = k_plane_c2r_w<NX, NY>;
@@ -438,6 +443,7 @@ int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, in
         return 0;
       }
     }
+#endif
     auto k = k_plane_c2r<NX, NY>;
     constexpr size_t dyn = PlaneDims<NX, NY>::smem;
     if (dyn > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);

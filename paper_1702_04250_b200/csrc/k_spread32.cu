@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
 }
 
 
+#ifdef PPPM_AB_VARIANTS  // A/B variant (measured slower)
 // make_rho, warp-specialized: warp 0 stages brick i+1 (two-pass bank-bucketed
 // counting sort of its slots into one of two stage slots) and finishes brick
 // i-1 (int32 tile -> fp32, TMA reduce-add into the padded rho, re-zero once
@@ -479,6 +480,8 @@ __global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
   spread_overflow<S, TAB>(counts, nb, g, pd, ta, inv_vcell, rho, ovf_rec, ovf_cell);
 }
 
+#endif
+
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, const Resident& res,
@@ -489,35 +492,37 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
+#ifdef PPPM_AB_VARIANTS
       if (variant == SPREAD_WS && !res.pos) {
         auto k = k_spread_ws<S, TAB>;
         const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + 2 * (size_t)cap * (sizeof(float4) + sizeof(int));
-        allow_smem(k, dyn);
         constexpr int NT = 32 * (kSpreadWsWarps + 1);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+        const int grid = persistent_grid(k, NT, dyn, bk.count());
         k<<<grid, NT, dyn, s>>>(rec, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell);
         return 0;
       }
+#endif
+#ifdef PPPM_AB_VARIANTS
       return with_bool(variant == SPREAD_FIX32, [&](auto F_) -> int {
         constexpr bool FIX = decltype(F_)::value;
+#else
+      return with_bool(true, [&](auto F_) -> int {  // int32 fixed point only (float CAS: A/B builds)
+        constexpr bool FIX = true;
+        (void)F_;
+#endif
         constexpr int NT = kSpreadThreads;
         auto k = res.pos ? k_spread_tma<S, TAB, FIX, NT, true> : k_spread_tma<S, TAB, FIX, NT, false>;
         const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) +
                            (res.pos ? 2 : 1) * (size_t)cap * (sizeof(float4) + sizeof(int));
-        allow_smem(k, dyn);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int grid = std::max(1, std::min(bk.count(), sms * std::max(1, per_sm)));
+        const int grid = persistent_grid(k, NT, dyn, bk.count());
         k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
                                 ovf_perm, res, n_points, rec_out);
+        if (getenv("PPPM_B200_DEBUG")) {
+          const cudaError_t e = cudaPeekAtLastError();
+          if (e != cudaSuccess)
+            fprintf(stderr, "spread launch failed: %s grid %d NT %d dyn %zu cap %d nb %d res %d\n",
+                    cudaGetErrorString(e), grid, NT, dyn, cap, bk.count(), res.pos != nullptr);
+        }
         return 0;
       });
     });

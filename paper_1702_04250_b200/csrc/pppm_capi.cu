@@ -215,10 +215,22 @@ static void drop_graphs(pppm_ctx* c) {
   }
 }
 
-static int activate(pppm_ctx* c) {
+// every C-ABI entry with a context starts here: bind its device and clear the
+// thread's last (non-sticky) runtime error, so a failed call made earlier on
+// this thread is not reported again by the launch checks of a later call
+// (they peek at the last error).  PPPM_B200_DEBUG=1 prints such leftovers.
+static thread_local const char* tl_prev_entry = "(none)";
+static int activate_at(pppm_ctx* c, const char* entry) {
+  if (!c) return fail(PPPM_ERR_VALUE, "null context");
+  const cudaError_t stale = cudaGetLastError();
+  if (stale != cudaSuccess && getenv("PPPM_B200_DEBUG"))
+    fprintf(stderr, "pppm_b200: stale CUDA error '%s' at %s (previous entry %s)\n", cudaGetErrorString(stale), entry,
+            tl_prev_entry);
+  tl_prev_entry = entry;
   CU(cudaSetDevice(c->device));
   return PPPM_OK;
 }
+#define activate(c) activate_at(c, __func__)
 
 static int nccl_fail(ncclResult_t r, const char* what) {
   std::string why;
@@ -322,6 +334,19 @@ static int ensure_plans(pppm_ctx* c) {
   }
   c->plans = true;
   return PPPM_OK;
+}
+
+// the measured-and-rejected variants are compiled only with -DPPPM_AB_VARIANTS
+static bool variant_built(int kernel, int variant) {
+#ifdef PPPM_AB_VARIANTS
+  (void)kernel;
+  (void)variant;
+  return true;
+#else
+  if (kernel == 0) return variant == SPREAD_FIX32;
+  if (kernel == 1) return variant == GATHER_PLAIN || variant == GATHER_SORTED || variant == GATHER_WS;
+  return true;
+#endif
 }
 
 // gather kernel actually used: the split (per-component) fieldforce needs ik
@@ -929,8 +954,10 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   }
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess)
     return cleanup(fail(PPPM_ERR_CUDA, "context setup kernels failed"));
-  if (const char* v = getenv("PPPM_B200_SPREAD")) c->spread_variant = atoi(v);
-  if (const char* v = getenv("PPPM_B200_GATHER")) c->gather_variant = atoi(v);
+  if (const char* v = getenv("PPPM_B200_SPREAD"))
+    if (variant_built(0, atoi(v))) c->spread_variant = atoi(v);
+  if (const char* v = getenv("PPPM_B200_GATHER"))
+    if (variant_built(1, atoi(v))) c->gather_variant = atoi(v);
   if (const char* v = getenv("PPPM_B200_GRAPHS")) c->use_graphs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_SORT_RESIDENT")) c->sort_resident = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_ZFFT")) c->use_zfft = atoi(v) != 0;
@@ -960,6 +987,8 @@ int pppm_ctx_create_slab(pppm_ctx** out, int device, int nx, int ny, int nz, dou
 int pppm_ctx_set_variant(pppm_ctx* c, int kernel, int variant) {
   if (!c) return fail(PPPM_ERR_VALUE, "null context");
   drop_graphs(c);
+  if (!variant_built(kernel, variant))
+    return fail(PPPM_ERR_VALUE, "kernel variant not built (A/B variants: -DPPPM_AB_VARIANTS, tools/build_variant.py)");
   if (kernel == 0 && variant >= 0 && variant <= 3) c->spread_variant = variant;
   else if (kernel == 1 && variant >= GATHER_PLAIN && variant <= GATHER_WSP)
     c->gather_variant = variant;

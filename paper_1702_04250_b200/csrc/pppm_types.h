@@ -81,6 +81,7 @@ inline bool gather_split_ok(int order, int hx) {
 
 // launchers: return 0, or a pppm_status code with the message set via set_error()
 void set_error(int code, const char* msg);
+int device_sm_count();  // cached per device (k_core.cu)
 int launch_particle_map(int order, bool r32, const AtomsIn& a, const Geom& g, int32_t* nodes, int* err,
                         cudaStream_t s);
 int launch_table_rows(int order, int n_points, double* assign, double* deriv, cudaStream_t s);

@@ -521,14 +521,21 @@ def test_kernel_variants_agree(pb, mode):
     ctx.step()
     ctx.synchronize()
     rho0, f0 = ctx.rho(), ctx.forces()
+    tried = 0
     for kernel, variant in ((0, 3), (1, 4), (1, 5), (1, 1), (1, 2), (1, 0), (0, 0)):
-        ctx.ctx("pppm_ctx_set_variant", kernel, variant)
+        try:
+            ctx.ctx("pppm_ctx_set_variant", kernel, variant)
+        except ValueError as exc:  # A/B variants are compiled only with -DPPPM_AB_VARIANTS
+            assert "not built" in str(exc)
+            continue
+        tried += 1
         ctx.step()
         ctx.synchronize()
         rho, f = ctx.rho(), ctx.forces()
         assert rel_rms(rho, rho0) <= 1e-5
         assert rel_rms(f, f0) <= 1e-5
     ctx.close()
+    assert tried >= 2
 
 
 @pytest.mark.parametrize("mode", ["ik", "ad"])
