@@ -30,18 +30,32 @@ __device__ __forceinline__ void store_force(void* force, bool out_f64, int64_t i
   }
 }
 
-// overflow atoms (full buckets): gather straight from the padded fields
+// overflow atoms (full buckets) and resident atoms that left their brick:
+// gathered straight from the padded fields (L2), one warp per atom - each lane
+// takes stencil points lane, lane + 32, ... (independent loads in flight
+// instead of one thread walking all S^3 points), then a shuffle reduction in a
+// fixed order (deterministic)
+template <int S>
+__device__ __forceinline__ float pick(const float (&v)[S], int i) {
+  float r = v[0];
+#pragma unroll
+  for (int t = 1; t < S; ++t) r = i == t ? v[t] : r;
+  return r;
+}
+
 template <int S, bool TAB, int MODE>
 __device__ __forceinline__ void gather_overflow(const int* __restrict__ novf_ptr, const Geom& g, const Pad& pd,
                                                 const float* __restrict__ ta, const float* __restrict__ td,
                                                 const float* __restrict__ fields, float cscale, void* force,
                                                 bool out_f64, const float4* __restrict__ ovf_rec,
                                                 const int* __restrict__ ovf_cell, const int* __restrict__ ovf_perm) {
-  constexpr int lo = Stencil<S>::lo;
+  constexpr int lo = Stencil<S>::lo, S3 = S * S * S, PER = (S3 + 31) / 32;
   const float ihx = (float)g.ihx, ihy = (float)g.ihy, ihz = (float)g.ihz;
   const int64_t mesh = pd.count();
   const int novf = *novf_ptr;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < novf; k += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < novf; k += nwarps) {
     const float4 r = ovf_rec[k];
     const int cc = ovf_cell[k];
     const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
@@ -50,27 +64,36 @@ __device__ __forceinline__ void gather_overflow(const int* __restrict__ novf_ptr
     rows_f32<S, TAB, MODE == 1>(r.y, ta, td, ay, dy);
     rows_f32<S, TAB, MODE == 1>(r.z, ta, td, az, dz);
     float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    for (int a = 0; a < S; ++a) {
-      for (int bb = 0; bb < S; ++bb) {
-        for (int c = 0; c < S; ++c) {
-          const int64_t gi = pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a);  // halos / ghosts filled
-          if (MODE == 0) {
-            const float w = az[a] * ay[bb] * ax[c];
-            s0 += w * __ldg(fields + gi);
-            s1 += w * __ldg(fields + mesh + gi);
-            s2 += w * __ldg(fields + 2 * mesh + gi);
-          } else {
-            const float p = __ldg(fields + gi);
-            s0 += az[a] * ay[bb] * dx[c] * p;
-            s1 += az[a] * dy[bb] * ax[c] * p;
-            s2 += dz[a] * ay[bb] * ax[c] * p;
-          }
-        }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int pnt = lane + 32 * u;
+      if (pnt >= S3) break;
+      const int a = pnt / (S * S), bb = (pnt / S) % S, c = pnt % S;
+      const int64_t gi = pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a);  // halos / ghosts filled
+      if (MODE == 0) {
+        const float w = pick(az, a) * pick(ay, bb) * pick(ax, c);
+        s0 += w * __ldg(fields + gi);
+        s1 += w * __ldg(fields + mesh + gi);
+        s2 += w * __ldg(fields + 2 * mesh + gi);
+      } else {
+        const float p = __ldg(fields + gi);
+        const float wa = pick(az, a), wb = pick(ay, bb), wc = pick(ax, c);
+        s0 += wa * wb * pick(dx, c) * p;
+        s1 += wa * pick(dy, bb) * wc * p;
+        s2 += pick(dz, a) * wb * wc * p;
       }
     }
-    const float sc = cscale * r.w;
-    if (MODE == 0) store_force<S, MODE>(force, out_f64, ovf_perm[k], sc * s0, sc * s1, sc * s2);
-    else store_force<S, MODE>(force, out_f64, ovf_perm[k], -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      const float sc = cscale * r.w;
+      if (MODE == 0) store_force<S, MODE>(force, out_f64, ovf_perm[k], sc * s0, sc * s1, sc * s2);
+      else store_force<S, MODE>(force, out_f64, ovf_perm[k], -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
+    }
   }
 }
 

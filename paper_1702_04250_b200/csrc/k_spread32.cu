@@ -73,6 +73,40 @@ __device__ __forceinline__ void spread_direct(const float4& r, int cc, const Pad
   }
 }
 
+// one atom straight into the padded mesh, one warp: lanes take stencil points
+// lane, lane + 32, ... (movers, processed after the CTA's bricks so that the
+// staging of a brick does not wait on one thread's S^3 global atomics)
+template <int S>
+__device__ __forceinline__ float pick_w(const float (&v)[S], int i) {
+  float r = v[0];
+#pragma unroll
+  for (int t = 1; t < S; ++t) r = i == t ? v[t] : r;
+  return r;
+}
+
+template <int S, bool TAB>
+__device__ __forceinline__ void spread_direct_warp(const float4& r, int cc, const Pad& pd, const float* __restrict__ ta,
+                                                   float inv_vcell, float* __restrict__ rho) {
+  constexpr int lo = Stencil<S>::lo, S3 = S * S * S, PER = (S3 + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
+  float wx[S], wy[S], wz[S], dd[S];
+  rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+  rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+  rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+  const float q = r.w * inv_vcell;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int pnt = lane + 32 * u;
+    if (pnt >= S3) break;
+    const int a = pnt / (S * S), bb = (pnt / S) % S, c = pnt % S;
+    // same product order as spread_direct: ((q wz) wy) wx
+    atomicAdd(rho + pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a), q * pick_w(wz, a) * pick_w(wy, bb) * pick_w(wx, c));
+  }
+}
+
+constexpr int kMoverQueue = 256;  // movers queued per CTA for the warp-cooperative direct spread
+
 // resident mode: stage brick b's atoms from their positions (the binning
 // pass folded into make_rho), write their slot records at the resident index
 // for fieldforce, send movers down the direct path; returns the rounds
@@ -82,7 +116,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
                                               float inv_vcell, float* __restrict__ rho, float4* __restrict__ rec,
                                               float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
                                               int* __restrict__ ovf_perm, BankSmem sm, float4* __restrict__ t_r,
-                                              int* __restrict__ t_c) {
+                                              int* __restrict__ t_c, int* __restrict__ mq, int* __restrict__ nmq) {
   constexpr int PER = kCapMax / NT;
   // (bsize was reset by the caller before its brick barrier)
   // pass 1: map positions, write the slot records (fieldforce reads them at
@@ -110,11 +144,14 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
       } else {
         reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(-1, (int)i, 0, 0);
-        spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
         const int o = atomicAdd(res.novf, 1);
         ovf_rec[o] = r;
         ovf_cell[o] = pk;
         ovf_perm[o] = (int)i;
+        // spread after the CTA's bricks (warp per atom); inline when the queue is full
+        const int slot = atomicAdd(nmq, 1);
+        if (slot < kMoverQueue) mq[slot] = o;
+        else spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
       }
     }
     if (sm.occ) occ_count(sm.occ, bank[k] >= 0, occ_cell);
@@ -179,6 +216,8 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
   __shared__ int s_brick;
+  __shared__ int s_mq[RES ? kMoverQueue : 1], s_nmq;
+  if (threadIdx.x == 0) s_nmq = 0;  // ordered before its first use by the brick loop's barriers
   bool prefetched = false;  // uniform: s_brick already holds the next claim (written before the last barrier)
   for (int b = blockIdx.x, it = 0;; b += gridDim.x, ++it) {
     if (bk.sched && it > 0) {  // dynamic after the first (static) brick: the next unclaimed one
@@ -218,7 +257,8 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
     if constexpr (RES)
       rounds = stage_resident<S, TAB, D, TXB, T::SH, NT>(res, b, cnt, g, bk, pd, n_points, ta, inv_vcell, rho,
                                                             rec_out, ovf_rec, ovf_cell, ovf_perm, sm,
-                                                            s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap);
+                                                            s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap,
+                                                            s_mq, &s_nmq);
     else
       rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     float scale = inv_vcell, inv_scale = 1.f;
@@ -296,6 +336,13 @@ __global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
   }
   if (threadIdx.x == 0) bulk_wait_read<0>();
   if constexpr (RES) {
+    // this CTA's movers (atoms outside their sorted brick), one warp each
+    __syncthreads();
+    const int nmq = s_nmq < kMoverQueue ? s_nmq : kMoverQueue;
+    for (int m = warp; m < nmq; m += nwarp) {
+      const int o = s_mq[m];
+      spread_direct_warp<S, TAB>(ovf_rec[o], ovf_cell[o], pd, ta, inv_vcell, rho);
+    }
     // atoms that overflowed their bucket at load: direct path, and on the list for fieldforce
     for (int64_t i = res.start[nb] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < res.n;
          i += (int64_t)gridDim.x * blockDim.x) {
