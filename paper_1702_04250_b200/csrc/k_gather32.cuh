@@ -239,8 +239,15 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
 // lane k serves the concatenation over f of the atom buckets k - f*TXB, whose
 // total is a sum of three bucket sizes - fuller conflict-free rounds than one
 // task per atom (SplitTile<S>::ok: TXB = 12 or 20 mod 32).
+// Field tiles of the per-component (split) fieldforce_ik.  Component f's tile
+// is loaded with its rows shifted by f, so a task's bank is its corner bank +
+// f * TXB; the three bank buckets are disjoint rotations only when TXB is 12 or
+// 20 mod 32.  Orders 6 and 7 (TmaTile TXB = 16) load 20-wide boxes instead (the
+// extra columns are never read).
 template <int S> struct SplitTile {
-  static constexpr int TXB = TmaTile<S>::TXB, D = TmaTile<S>::D, DY = D + 2;
+  static constexpr int TXB0 = TmaTile<S>::TXB, D = TmaTile<S>::D, DY = D + 2;
+  static constexpr int TXB = (TXB0 % 32 == 12 || TXB0 % 32 == 20) ? TXB0 : 20;
+  static_assert(TmaTile<S>::D + TmaTile<S>::SH <= TXB, "split field box narrower than the stencil tile");
   static constexpr int FTN = TXB * DY * D;          // floats per field box
   static constexpr int FT = (FTN + 31) / 32 * 32;   // 128-byte aligned field stride
   static constexpr bool ok = (TXB % 32 == 12 || TXB % 32 == 20);
@@ -406,7 +413,8 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), 3) k_ga
   using ST = SplitTile<S>;
   // ik (MODE 0): three component tiles, rows shifted by the component (DY = D + 2);
   // ad (MODE 1): one potential tile (DY = D), one task per atom, three derivative sums
-  constexpr int TXB = T::TXB, DY = MODE == 0 ? ST::DY : T::D, FT = MODE == 0 ? ST::FT : T::NP, lo = Stencil<S>::lo;
+  constexpr int TXB = MODE == 0 ? ST::TXB : T::TXB, DY = MODE == 0 ? ST::DY : T::D, FT = MODE == 0 ? ST::FT : T::NP,
+                lo = Stencil<S>::lo;
   constexpr int BUF = MODE == 0 ? 3 * FT : FT;
   constexpr int NCW = kWsConsumerWarps;
   constexpr uint32_t kBytes = MODE == 0 ? 3u * ST::FTN * sizeof(float) : (uint32_t)T::N * sizeof(float);

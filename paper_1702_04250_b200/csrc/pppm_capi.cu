@@ -400,7 +400,8 @@ static int encode_maps(pppm_ctx* c) {
                        (gather_eff(c) == GATHER_SPLIT || gather_eff(c) == GATHER_WS || gather_eff(c) == GATHER_WSP);
     // tensor-core gather: all fields, 16-float rows starting at the brick's lowest stencil node
     const bool mma = gather_eff(c) == GATHER_MMA;
-    cuuint32_t box[4] = {(cuuint32_t)(mma ? 16 : txb), (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
+    const int bx = mma ? 16 : (split ? split_txb(c->order, c->pd.hx) : txb);
+    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D,
                          (cuuint32_t)(split ? 1 : c->nfields())};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(&c->field_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->fields.p, dims, strides, box, es,

@@ -72,11 +72,16 @@ struct Resident {
 // kernel variants (selectable per context for A/B measurement)
 enum SpreadVariant { SPREAD_CAS_F32 = 0, SPREAD_FIX32 = 1, SPREAD_WS = 3 };  // WS: FIX32, warp-specialized
 enum GatherVariant { GATHER_PLAIN = 0, GATHER_SORTED = 1, GATHER_SPLIT = 2, GATHER_WS = 3, GATHER_MMA = 4, GATHER_WSP = 5 };  // SPLIT, WS, MMA, WSP: ik only
-// field tiles of the split gather: rows shifted per component (TXB = 12 or 20 mod 32)
-inline bool gather_split_ok(int order, int hx) {
+// field box width of the split gather (SplitTile<S>::TXB, k_gather32.cuh): the
+// brick tile's TXB when it is 12 or 20 mod 32, else 20 (orders 6, 7)
+inline int split_txb(int order, int hx) {
   const int D = 8 + order - 1, lo = (order - 1) / 2;
   const int sh = ((hx - lo) % 4 + 4) % 4, txb = (D + sh + 3) / 4 * 4;
-  return txb % 32 == 12 || txb % 32 == 20;
+  return (txb % 32 == 12 || txb % 32 == 20) ? txb : 20;
+}
+inline bool gather_split_ok(int order, int hx) {
+  const int t = split_txb(order, hx);
+  return t % 32 == 12 || t % 32 == 20;
 }
 
 // launchers: return 0, or a pppm_status code with the message set via set_error()
