@@ -126,7 +126,7 @@ inline int persistent_grid(K kernel, int threads, size_t dyn, int items) {
 #define PPPM_BIN_UNROLL 2
 #endif
 #ifndef PPPM_BIN_MINB
-#define PPPM_BIN_MINB 6
+#define PPPM_BIN_MINB 4  // 6 spilled (56 B) with the fixed-point bound; the binning pass only runs at load and on the one-shot path
 #endif
 #ifndef PPPM_BIN_NO_PERSIST
 #define PPPM_BIN_PERSIST

@@ -102,7 +102,7 @@ __device__ __forceinline__ void gather_overflow(const int* __restrict__ novf_ptr
 // i+1's (TXB, D, D, F) box from the halo-padded fields into the other buffer
 // (mbarrier transaction barriers; the halo makes every box in bounds).
 template <int S, bool TAB, int MODE, int NT>
-__global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_tma(
+__global__ void __launch_bounds__(NT, (S >= 4 ? (PPPM_GATHER_MINB > 2 ? PPPM_GATHER_MINB - 1 : PPPM_GATHER_MINB) : PPPM_GATHER_MINB)) k_gather_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ perm,
     const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
     const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,
@@ -403,7 +403,7 @@ template <int MODE> constexpr int kWsPw = MODE == 1 ? PPPM_WS_PW_AD : kWsProduce
 template <int MODE> constexpr int kWsU2m = MODE == 1 ? 2 : kWsU2;
 
 template <int S, bool TAB, int MODE = 0>
-__global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), 3) k_gather_ws(
+__global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6 ? 2 : 3)) k_gather_ws(
     const float4* __restrict__ rec, const int* __restrict__ counts, int cap, Geom g, Bricks bk, Pad pd,
     const float* __restrict__ ta, const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap,
     const float* __restrict__ fields, float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec,

@@ -190,8 +190,11 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
 // in place and added to the padded mesh with ONE TMA reduce-add of the
 // (TXB, D, D) box at the brick origin - lo (always in bounds: the mesh carries
 // an H-cell halo, folded back periodically by k_halo.cu afterwards).
+// (min CTAs per SM: fewer where the fixed-point (fp64 DFMA) deposit loop or
+// the binned staging would otherwise spill; ptxas -warn-spills clean)
 template <int S, bool TAB, bool FIX, int NT, bool RES>
-__global__ void __launch_bounds__(NT, PPPM_SPREAD_MINB) k_spread_tma(
+__global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PPPM_SPREAD_MINB - 1 : PPPM_SPREAD_MINB)))
+    k_spread_tma(
     const float4* __restrict__ rec, const int* __restrict__ rcell, const int* __restrict__ counts, int cap,
     Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
     const __grid_constant__ CUtensorMap rmap, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
