@@ -220,6 +220,51 @@ def cpu_sample_rate(pos, q, lengths, dims, order, mode, sample, workers, reps=1)
     return sample * reps / sum(times), times
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_package_rates(pos, q, lengths, cfg, mode, sample, cores):
+    """The as-shipped reference package (baseline/_ref: pip install of
+    /root/reference/pkg, staged with tests/run_reference_suite.py's recipe) on
+    a bounded sample of the workload: map_charge + distribute_force_{mode},
+    padded_rows=True (as shipped), table and exact weights, workers=1 and
+    workers=cores.  None when the package is not staged."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "pppm")):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    import pppm
+
+    box = pppm.SimulationBox(np.asarray(lengths, dtype=np.float64))
+    system = pppm.AtomSystem(box=box, positions=np.asarray(pos[:sample], dtype=np.float64),
+                             charges=np.asarray(q[:sample], dtype=np.float64), allow_net_charge=True)
+    out = {"package": os.path.relpath(pppm.__file__, ROOT), "sample_atoms": int(sample), "padded_rows": True}
+    for use_table in (True, False):
+        params = pppm.PppmParams(cutoff=10.0, accuracy=1e-4, order=cfg.order, mode=pppm.DiffMode(mode),
+                                 alpha=cfg.alpha, grid_dims=tuple(cfg.dims), use_table=use_table)
+        table = pppm.build_table(cfg.order, params.table_points) if use_table else None
+        rho = pppm.map_charge(system, params, table)
+        plan = pppm.build_plan(params.grid_dims, box, params.alpha, params.order)
+        fields = pppm.poisson_ik(rho, plan) if mode == "ik" else pppm.poisson_ad(rho, plan)
+        dist = pppm.distribute_force_ik if mode == "ik" else pppm.distribute_force_ad
+        for workers in (1, cores):
+            t0 = time.perf_counter()
+            pppm.map_charge(system, params, table, workers=workers)
+            dist(fields, system, params, table, workers=workers)
+            dt = time.perf_counter() - t0
+            out[f"{'table' if use_table else 'exact'}_workers{workers}"] = sample / dt
+    return out
+
+
 def run_reference(args, cfg, rank, pg):
     if rank != 0:
         return
@@ -713,10 +758,18 @@ def main():
         sample = int(min(n, max(16384, cal * 12.0)))   # ~12 s of CPU work per pass ...
         reps = max(1, int(np.ceil(12.0 / max(sample / cal, 1e-3))))  # ... repeated to >= ~12 s
         rate, times = cpu_sample_rate(p64, q, lengths, cfg.dims, cfg.order, mode, sample, cores, reps=reps)
+        rate1, _ = cpu_sample_rate(p64, q, lengths, cfg.dims, cfg.order, mode, min(sample, 65536), 1)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"make_rho(workers={cores}) + fieldforce_{mode} on the first {sample} atoms "
                                           f"of config {cfg.index}, {reps} pass(es) (numpy oracle port, fp64), "
-                                          f"{sum(times):.1f} s total"}
+                                          f"{sum(times):.1f} s total",
+                                "cpu_model": cpu_model(), "value_workers1": rate1}
+        try:
+            refp = reference_package_rates(p64, q, lengths, cfg, mode, 32768, cores)
+        except Exception as exc:  # reported, the headline line still prints
+            refp = {"error": str(exc)[:300]}
+        if refp is not None:
+            line["cpu_baseline"]["reference_package"] = refp
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)

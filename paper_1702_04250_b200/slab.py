@@ -41,6 +41,54 @@ def owner_of_nodes(nodes_z, nz, nslabs):
     return (nodes_z % nz) // (nz // nslabs)
 
 
+def migrate_atoms(owner, arrays, group=None):
+    """Atom migration between slabs (an all-to-all-v of atoms).
+
+    ``owner`` (n,) int: the slab each of this rank's atoms belongs to after
+    the move (``owner_of_nodes`` of the bit-exact node_z; SlabContext.owners
+    computes it on the device).  ``arrays``: per-atom numpy arrays (positions,
+    charges, velocities, global ids, ...), first axis n.  Every rank calls it
+    (collective over ``group``).  Returns the rank's new arrays: the atoms it
+    kept, in their order, followed by the atoms received from slab 0, 1, ...
+    in the senders' order (deterministic).  Counts travel with all_gather,
+    the payload with point-to-point sends / receives (NCCL on CUDA, gloo on
+    CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    owner = np.asarray(owner, dtype=np.int64)
+    if owner.size and (owner.min() < 0 or owner.max() >= world):
+        raise ValueError("owner slab out of range")
+    counts = np.bincount(owner, minlength=world).astype(np.int64)
+    allc = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, torch.from_numpy(counts), group=group)
+    recv_counts = [int(allc[src][rank]) for src in range(world)]
+    out = []
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        keep = a[owner == rank]
+        flat = a.reshape(a.shape[0], -1)
+        width = flat.shape[1]
+        ops, recv_bufs = [], {}
+        for dst in range(world):
+            if dst != rank and counts[dst]:
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(flat[owner == dst])),
+                                      dst, group))
+        for src in range(world):
+            if src != rank and recv_counts[src]:
+                buf = torch.empty((recv_counts[src], width), dtype=torch.from_numpy(flat[:0]).dtype)
+                recv_bufs[src] = buf
+                ops.append(dist.P2POp(dist.irecv, buf, src, group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        parts = [keep.reshape(-1, *a.shape[1:])]
+        parts += [recv_bufs[src].numpy().reshape(-1, *a.shape[1:]) for src in range(world) if src in recv_bufs]
+        out.append(np.concatenate(parts) if parts else keep)
+    return out
+
+
 class _CudaView:
     """__cuda_array_interface__ over a raw device pointer (no ownership)."""
 
@@ -152,9 +200,16 @@ class SlabContext:
         self("pppm_ctx_launches_per_step", ctypes.byref(n))
         return n.value
 
+    def owners(self, positions):
+        """Owning slab of each position (bit-exact particle_map on the device)."""
+        pos = np.ascontiguousarray(positions, dtype=np.float32)
+        nodes = np.empty((3, pos.shape[0]), dtype=np.int32)
+        self("pppm_particle_map", nat.ptr(pos), pos.shape[0], nat.F32, nat.HOST, nat.ptr(nodes))
+        return owner_of_nodes(nodes[2], self.dims[2], self.P)
+
     def update_positions(self, positions):
         """New positions of this slab's atoms (its load order).  Raises when an
-        atom left the slab (see SlabStep.migrate)."""
+        atom left the slab: exchange them with ``migrate_atoms`` and reload."""
         pos = np.ascontiguousarray(positions, dtype=np.float32)
         self("pppm_ctx_update_positions", nat.ptr(pos), nat.F32, nat.HOST)
 
