@@ -450,9 +450,12 @@ struct BankSmem {
   int* occ = nullptr;  // optional: kBrick^3 per-cell atom counts + [kBrick^3] = max count (zeroed by the caller)
 };
 
-// per-cell occupancy of the staged atoms; occ[kBrick^3] = the largest count
-__device__ __forceinline__ void occ_count(int* occ, bool valid, int cell) {
-  int m = valid ? atomicAdd(occ + cell, 1) + 1 : 0;
+// per-cell occupancy of the staged atoms: count one atom (returns the cell's
+// count so far), then occ_publish the thread's largest count once per brick;
+// occ[kBrick^3] = the largest count
+__device__ __forceinline__ int occ_count(int* occ, int cell) { return atomicAdd(occ + cell, 1) + 1; }
+
+__device__ __forceinline__ void occ_publish(int* occ, int m) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(occ + kBrick * kBrick * kBrick, m);
@@ -467,6 +470,7 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
   __syncthreads();
   float4 r[PER];
   int c[PER], rk[PER], p[PER], bank[PER];
+  int occ_max = 0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int j = threadIdx.x + k * NT;
@@ -481,10 +485,11 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
         const int lx = c[k] & (kBrick - 1), ly = (c[k] >> 3) & (kBrick - 1), lz = c[k] >> 6;
         bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
+        if (sm.occ) occ_max = max(occ_max, occ_count(sm.occ, c[k]));
       }
     }
-    if (sm.occ) occ_count(sm.occ, j < cnt && bank[k] >= 0, j < cnt ? c[k] : 0);
   }
+  if (sm.occ) occ_publish(sm.occ, occ_max);
   __syncthreads();
   if (threadIdx.x < 32) {
     const int v = sm.bsize[threadIdx.x];

@@ -123,11 +123,11 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
   // the resident index), bank histogram; only bank / rank stay in registers
   int rk[PER], bank[PER];
   const int64_t base = res.start[b];
+  int occ_max = 0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int j = threadIdx.x + k * NT;
     bank[k] = -1;
-    int occ_cell = 0;
     if (j < cnt) {
       const int64_t i = base + j;
       float4 r;
@@ -138,7 +138,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
         reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(lc, (int)i, 0, 0);
         t_r[j] = r;  // unsorted copy in shared memory for pass 2
         t_c[j] = lc;
-        occ_cell = lc;
+        if (sm.occ) occ_max = max(occ_max, occ_count(sm.occ, lc));
         const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
         bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
@@ -154,8 +154,8 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
         else spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
       }
     }
-    if (sm.occ) occ_count(sm.occ, bank[k] >= 0, occ_cell);
   }
+  if (sm.occ) occ_publish(sm.occ, occ_max);
   __syncthreads();
   if (threadIdx.x < 32) {
     const int v = sm.bsize[threadIdx.x];
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
   float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
   __shared__ int bsize[32], bstart[33];
   constexpr int kCells = kBrick * kBrick * kBrick;
-  __shared__ int s_occ[kCells + 1];  // per-cell atom counts of the staged brick, [kCells] = max (FIX scale)
+  __shared__ __align__(16) int s_occ[kCells + 4];  // per-cell atom counts of the staged brick, [kCells] = max (FIX scale)
   // staged atoms: s_r[cap] | (resident: t_r[cap]) | s_c[cap] | (resident: t_c[cap])
   BankSmem sm{s_r, reinterpret_cast<int*>(s_r + (RES ? 2 * cap : cap)), nullptr, bsize, bstart,
               FIX ? s_occ : nullptr};
@@ -252,10 +252,13 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
     // all reduces but the most recent (other buffer) have finished reading
     if (threadIdx.x == 0) bulk_wait_read<1>();
     if (RES && threadIdx.x < 32) bsize[threadIdx.x] = 0;  // stage_resident's histogram
-    if (FIX)
-      for (int k = threadIdx.x; k <= kCells; k += blockDim.x) s_occ[k] = 0;
+    if (FIX) {
+      for (int k = threadIdx.x; k < kCells / 4; k += blockDim.x) reinterpret_cast<int4*>(s_occ)[k] = make_int4(0, 0, 0, 0);
+      if (threadIdx.x == 0) s_occ[kCells] = 0;
+    }
     __syncthreads();
-    for (int k = threadIdx.x; k < TN; k += blockDim.x) tile[k] = 0;
+    static_assert(TN % 4 == 0, "tile rows are 16-byte multiples");
+    for (int k = threadIdx.x; k < TN / 4; k += blockDim.x) reinterpret_cast<int4*>(tile)[k] = make_int4(0, 0, 0, 0);
     int rounds;
     if constexpr (RES)
       rounds = stage_resident<S, TAB, D, TXB, T::SH, NT>(res, b, cnt, g, bk, pd, n_points, ta, inv_vcell, rho,
@@ -274,12 +277,15 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
       // with the 1.5*2^52 magic number (B200 fp64 runs at half the fp32 rate):
       // the low word of the result is the integer modulo 2^32, for any
       // contribution size, so the scale is limited by the cell bound alone.
-      int e_sum = 0;
+      // (frexp / ldexp through the exponent bits: the bound is a normal float
+      // and sc stays far inside the normal range; the 1.01 margin covers the
+      // per-contribution rounding)
       const int m = s_occ[kCells];
-      frexpf(qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f, &e_sum);
+      const float bound = qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f;
+      const int e_sum = ((__float_as_int(bound) >> 23) & 0xff) - 126;  // bound < 2^e_sum
       const int sc = 31 - e_sum;
-      scale = ldexpf(1.f, sc);
-      inv_scale = ldexpf(1.f, -sc) * inv_vcell;
+      scale = __int_as_float((127 + sc) << 23);
+      inv_scale = __int_as_float((127 - sc) << 23) * inv_vcell;
     }
     for (int rr = warp; rr < rounds; rr += nwarp) {
       if (rr >= bsize[lane]) continue;
@@ -325,16 +331,22 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
     }
     __syncthreads();
     if (FIX)
-      for (int k = threadIdx.x; k < TN; k += blockDim.x) ftile[k] = (float)tile[k] * inv_scale;
+      for (int k = threadIdx.x; k < TN / 4; k += blockDim.x) {
+        const int4 v = reinterpret_cast<const int4*>(tile)[k];
+        reinterpret_cast<float4*>(ftile)[k] =
+            make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
+      }
     fence_proxy_async_smem();
     if (bk.sched && threadIdx.x == 0) s_brick = gridDim.x + atomicAdd(bk.sched + 32, 1);  // next brick
     __syncthreads();
     prefetched = bk.sched != nullptr;
+#ifndef PPPM_PROBE_NO_REDUCE  // A/B probe only (wrong mesh): cost of the tile reduce-adds
     if (threadIdx.x == 0) {
       const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
       tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
       bulk_commit();
     }
+#endif
     ++issued;
   }
   if (threadIdx.x == 0) bulk_wait_read<0>();
