@@ -265,6 +265,38 @@ int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* 
   return launch_status();
 }
 
+// fp64 residents in brick order: forces back to the caller's order, new
+// caller-order positions into brick order
+__global__ void k_unpermute_forces64(const double* __restrict__ f, const int* __restrict__ orig, int64_t n,
+                                     double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = orig[i];
+    out[3 * o] = f[3 * i];
+    out[3 * o + 1] = f[3 * i + 1];
+    out[3 * o + 2] = f[3 * i + 2];
+  }
+}
+
+__global__ void k_permute_rows64(const double* __restrict__ src, const int* __restrict__ orig, int64_t n,
+                                 double* __restrict__ dst) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = orig[k];
+    dst[3 * k] = src[3 * i];
+    dst[3 * k + 1] = src[3 * i + 1];
+    dst[3 * k + 2] = src[3 * i + 2];
+  }
+}
+
+int launch_unpermute_forces64(const double* f, const int* orig, int64_t n, double* out, cudaStream_t s) {
+  k_unpermute_forces64<<<grid_for(n), kThreads, 0, s>>>(f, orig, n, out);
+  return launch_status();
+}
+
+int launch_permute_rows64(const double* src, const int* orig, int64_t n, double* dst, cudaStream_t s) {
+  k_permute_rows64<<<grid_for(n), kThreads, 0, s>>>(src, orig, n, dst);
+  return launch_status();
+}
+
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
                             void* q_out, int* orig_out, cudaStream_t s) {

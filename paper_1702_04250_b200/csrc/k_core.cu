@@ -163,7 +163,12 @@ __global__ void k_fix_scale(const unsigned long long* __restrict__ qmax_bits, in
   inv_scale[0] = ldexp(1.0, -s);
 }
 
-template <int S, bool TAB, typename TIn, bool R32>
+// MAGIC (n >= 2^11 atoms): every contribution is below 2^51 in fixed point
+// (|q w| <= max|q| and the scale is 2^(62 - ceil(log2(n max|q|)))), so the
+// rounding to an integer is one DFMA with the 1.5*2^52 magic number - the same
+// round-to-nearest-even of the exact product as __double2ll_rn (the scale is a
+// power of two), without the slow 64-bit F2I
+template <int S, bool TAB, typename TIn, bool R32, bool MAGIC>
 __global__ void __launch_bounds__(kThreads) k_spread_fix64(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g,
     const double* __restrict__ ta, int n_points, const double* __restrict__ scale_p,
@@ -204,7 +209,9 @@ __global__ void __launch_bounds__(kThreads) k_spread_fix64(
 #pragma unroll
         for (int c = 0; c < S; ++c) {
           const double contrib = __dmul_rn(qab, wx[c]);
-          const long long f = __double2ll_rn(__dmul_rn(contrib, scale));
+          const long long f = MAGIC ? __double_as_longlong(__fma_rn(contrib, scale, 6755399441055744.0)) -
+                                          __double_as_longlong(6755399441055744.0)
+                                    : __double2ll_rn(__dmul_rn(contrib, scale));
           if (f != 0) atomicAdd(row + ix[c], (unsigned long long)f);
         }
       }
@@ -533,13 +540,16 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
-      if (!a.f32)
-        k_spread_fix64<S, TAB, double, false><<<grid, kThreads, 0, s>>>(
-            (const double*)a.pos, (const double*)a.q, a.n, g, ta, n_points, scal + 1, acc, err);
-      else
-        k_spread_fix64<S, TAB, float, false><<<grid, kThreads, 0, s>>>(
-            (const float*)a.pos, (const float*)a.q, a.n, g, ta, n_points, scal + 1, acc, err);
-      return 0;
+      return with_bool(a.n >= 2048, [&](auto M_) -> int {
+        constexpr bool MAGIC = decltype(M_)::value;
+        if (!a.f32)
+          k_spread_fix64<S, TAB, double, false, MAGIC><<<grid, kThreads, 0, s>>>(
+              (const double*)a.pos, (const double*)a.q, a.n, g, ta, n_points, scal + 1, acc, err);
+        else
+          k_spread_fix64<S, TAB, float, false, MAGIC><<<grid, kThreads, 0, s>>>(
+              (const float*)a.pos, (const float*)a.q, a.n, g, ta, n_points, scal + 1, acc, err);
+        return 0;
+      });
     });
   });
   if (st) return st;

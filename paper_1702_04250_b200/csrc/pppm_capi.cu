@@ -1434,7 +1434,9 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   c->res_sorted = false;
   c->res_maxcnt = 0;
   c->novf_clean = false;
-  if (!c->fp64() && c->sort_resident) {
+  // brick order for every precision: the mixed path's kernels rely on it, the
+  // fp64 (thread-per-atom) kernels gain locality from it
+  if (c->sort_resident) {
     // keep the resident atoms in brick order (as an MD engine sorts its atoms):
     // bin once, then gather positions / charges into bucket order
     TRY(run_bin(c, c->res_pos.p, c->res_q.p, n, dtype, nullptr));
@@ -1448,7 +1450,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
     std::swap(c->res_pos, c->res_tmp_pos);
     std::swap(c->res_q, c->res_tmp_q);
     c->res_sorted = true;
-    if (dtype == PPPM_F64) {
+    if (dtype == PPPM_F64 && !c->fp64()) {
       // mixed precision maps fp32-rounded positions anyway: keep fp32 residents
       TRY(c->res_tmp_pos.ensure(3 * n * sizeof(float)));
       TRY(c->res_tmp_q.ensure(n * sizeof(float)));
@@ -1699,6 +1701,16 @@ int pppm_ctx_synchronize(pppm_ctx* c) {
 static int update_positions(pppm_ctx* c, const void* pos, int dtype, int mem, bool sync) {
   TRY(activate(c));
   if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
+  if (c->res_sorted && c->fp64()) {
+    // fp64 residents in brick order: caller-order positions gathered into it
+    if (dtype != PPPM_F64) return fail(PPPM_ERR_VALUE, "positions dtype differs from the resident atoms");
+    TRY(c->pos_stage.ensure(3 * c->n_res * 8));
+    CU(cudaMemcpyAsync(c->pos_stage.p, pos, 3 * c->n_res * 8, cudaMemcpyDefault, c->stream));
+    TRY(launch_permute_rows64(c->pos_stage.as<double>(), c->res_orig.as<int>(), c->n_res, c->res_pos.as<double>(),
+                              c->stream));
+    if (sync) CU(cudaStreamSynchronize(c->stream));
+    return PPPM_OK;
+  }
   if (!c->res_sorted || c->res_dtype != PPPM_F32) {
     // unsorted residents: plain copy in the caller's order
     const size_t es = c->res_dtype == PPPM_F64 ? 8 : 4;
@@ -1774,7 +1786,14 @@ int pppm_ctx_get_forces(pppm_ctx* c, double* forces) {
   TRY(activate(c));
   const int64_t cnt = 3 * c->n_res;
   if (c->fp64()) {
-    CU(cudaMemcpyAsync(forces, c->res_force.p, 8 * cnt, cudaMemcpyDeviceToHost, c->stream));
+    if (c->res_sorted) {
+      TRY(c->out_stage.ensure(sizeof(double) * cnt));
+      TRY(launch_unpermute_forces64(c->res_force.as<double>(), c->res_orig.as<int>(), c->n_res,
+                                    c->out_stage.as<double>(), c->stream));
+      CU(cudaMemcpyAsync(forces, c->out_stage.p, 8 * cnt, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+      CU(cudaMemcpyAsync(forces, c->res_force.p, 8 * cnt, cudaMemcpyDeviceToHost, c->stream));
+    }
     CU(cudaStreamSynchronize(c->stream));
     return PPPM_OK;
   }

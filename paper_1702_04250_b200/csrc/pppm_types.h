@@ -130,6 +130,8 @@ int launch_slot_bricks(const int* start, int nb, int64_t n, int* res_brick, cuda
 int launch_compose(const int* orig_old, const int* perm, int64_t n, int* orig_new, cudaStream_t s);
 int launch_round_positions(const double* pos, int64_t n, const Geom& g, float* out, cudaStream_t s);
 int launch_unpermute_forces(const float* f, const int* orig, int64_t n, double* out, cudaStream_t s);
+int launch_unpermute_forces64(const double* f, const int* orig, int64_t n, double* out, cudaStream_t s);
+int launch_permute_rows64(const double* src, const int* orig, int64_t n, double* dst, cudaStream_t s);
 int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* rec, const int* counts, int* start,
                             const int* ovf_perm, int64_t n, const void* pos, const void* q, void* pos_out,
                             void* q_out, int* orig_out, cudaStream_t s);
