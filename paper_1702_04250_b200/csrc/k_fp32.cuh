@@ -464,7 +464,7 @@ __device__ __forceinline__ void occ_publish(int* occ, int m) {
 template <bool PERM, int D, int TXB, int SH, int NT = kThreads>
 __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, const int* __restrict__ rcell,
                                             const int* __restrict__ perm, int64_t base, int cnt, BankSmem sm,
-                                            bool skip_movers = false) {
+                                            bool skip_movers = false, const float* __restrict__ rq = nullptr) {
   constexpr int PER = kCapMax / NT;
   if (threadIdx.x < 32) sm.bsize[threadIdx.x] = 0;
   __syncthreads();
@@ -475,10 +475,17 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
   for (int k = 0; k < PER; ++k) {
     const int j = threadIdx.x + k * NT;
     if (j < cnt) {
-      r[k] = rec[2 * (base + j)];
-      const int4 m = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
-      c[k] = m.x;
-      if (PERM) p[k] = m.y;
+      if (rq) {  // resident 16-byte records {tx, ty, tz, cell bits}; charge and index from the residents
+        r[k] = rec[base + j];
+        c[k] = __float_as_int(r[k].w);
+        r[k].w = rq[base + j];
+        if (PERM) p[k] = (int)(base + j);
+      } else {
+        r[k] = rec[2 * (base + j)];
+        const int4 m = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1];
+        c[k] = m.x;
+        if (PERM) p[k] = m.y;
+      }
       if (skip_movers && c[k] < 0) {
         bank[k] = -1;  // moved out of the brick: handled from the overflow list
       } else {

@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(NT, (S >= 4 ? (PPPM_GATHER_MINB > 2 ? PPPM_GAT
     }
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
     const int rounds =
-        (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm, rstart != nullptr) : 0;
+        (sort && cnt > 0) ? stage_banked<true, D, TXB, T::SH, NT>(rec, rcell, perm, base, cnt, sm, rstart != nullptr,
+                                                                  rstart ? bk.rq : nullptr) : 0;
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     // sort: bank-conflict-free rounds (lane = bank bucket); else bucket order
@@ -180,8 +181,19 @@ __global__ void __launch_bounds__(NT, (S >= 4 ? (PPPM_GATHER_MINB > 2 ? PPPM_GAT
         if (rr >= bsize[lane]) continue;
         j = bstart[lane] + rr;
       }
-      const float4 r = sort ? s_r[j] : rec[2 * (base + j)];
-      const int cc = sort ? s_c[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].x;
+      float4 r;
+      int cc;
+      if (sort) {
+        r = s_r[j];
+        cc = s_c[j];
+      } else if (rstart) {  // resident 16-byte records {tx, ty, tz, cell bits}
+        r = rec[base + j];
+        cc = __float_as_int(r.w);
+        r.w = bk.rq[base + j];
+      } else {
+        r = rec[2 * (base + j)];
+        cc = reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].x;
+      }
       if (cc < 0) continue;  // resident atom that left the brick: overflow list
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(NT, (S >= 4 ? (PPPM_GATHER_MINB > 2 ? PPPM_GAT
         s2 = fmaf(MODE == 0 ? az[a] : dz[a], r2, s2);
       }
       const float sc = cscale * r.w;
-      const int64_t i = sort ? s_p[j] : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].y;
+      const int64_t i = sort ? s_p[j] : (rstart ? base + j : reinterpret_cast<const int4*>(rec)[2 * (base + j) + 1].y);
       if (MODE == 0) store_force<S, MODE>(force, out_f64, i, sc * s0, sc * s1, sc * s2);
       else store_force<S, MODE>(force, out_f64, i, -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
     }
@@ -308,7 +320,9 @@ __global__ void __launch_bounds__(NT, PPPM_GATHER_MINB) k_gather_split(
       base = (int64_t)b * cap;
     }
     BankSmem sm{s_r, s_c, s_p, bsize, bstart};
-    if (cnt > 0) stage_banked<true, DY, TXB, T::SH, NT>(rec, nullptr, nullptr, base, cnt, sm, rstart != nullptr);
+    if (cnt > 0)
+      stage_banked<true, DY, TXB, T::SH, NT>(rec, nullptr, nullptr, base, cnt, sm, rstart != nullptr,
+                                             rstart ? bk.rq : nullptr);
     mbar_wait(&bar[buf], (it >> 1) & 1);
     const float* tile = tiles + buf * BUF;
     int seg0 = 0, seg1 = 0, seg2 = 0;
@@ -505,7 +519,9 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
 #pragma unroll
         for (int u = 0; u < kWsU1; ++u) {
           const int j = j0 + u * 32 * NPW + pt;
-          cc[u] = j < cnt ? __ldg(&meta[2 * (base + j) + 1].x) : -1;
+          // resident: 16-byte records {tx, ty, tz, cell bits}; binned: 32-byte slots
+          cc[u] = j < cnt ? (rstart ? __float_as_int(__ldg(&rec[base + j].w)) : __ldg(&meta[2 * (base + j) + 1].x))
+                          : -1;
         }
 #pragma unroll
         for (int u = 0; u < kWsU1; ++u) {
@@ -539,8 +555,15 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
           const int j = j0 + u * 32 * NPW + pt;
           m[u].x = -1;
           if (j < cnt) {
-            m[u] = __ldg(&meta[2 * (base + j) + 1]);
-            r[u] = __ldg(&rec[2 * (base + j)]);
+            if (rstart) {
+              r[u] = __ldg(&rec[base + j]);
+              m[u].x = __float_as_int(r[u].w);
+              m[u].y = (int)(base + j);
+              r[u].w = __ldg(&bk.rq[base + j]);
+            } else {
+              m[u] = __ldg(&meta[2 * (base + j) + 1]);
+              r[u] = __ldg(&rec[2 * (base + j)]);
+            }
           }
         }
 #pragma unroll
@@ -766,7 +789,9 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsProducerWarps), 3)
 #pragma unroll
         for (int u = 0; u < kWsU1; ++u) {
           const int j = j0 + u * 32 * NPW + pt;
-          cc[u] = j < cnt ? __ldg(&meta[2 * (base + j) + 1].x) : -1;
+          // resident: 16-byte records {tx, ty, tz, cell bits}; binned: 32-byte slots
+          cc[u] = j < cnt ? (rstart ? __float_as_int(__ldg(&rec[base + j].w)) : __ldg(&meta[2 * (base + j) + 1].x))
+                          : -1;
         }
 #pragma unroll
         for (int u = 0; u < kWsU1; ++u) {

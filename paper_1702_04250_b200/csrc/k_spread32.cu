@@ -133,9 +133,10 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
       float4 r;
       int lc, pk;
       const int ab = atom_record<S, TAB>(res, i, g, bk, n_points, r, lc, pk);
-      rec[2 * i] = r;
+      // 16-byte slot record for fieldforce: offsets + brick-local cell (-1:
+      // mover); the charge and the index are the resident arrays' own
+      rec[i] = make_float4(r.x, r.y, r.z, __int_as_float(ab == b ? lc : -1));
       if (ab == b) {
-        reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(lc, (int)i, 0, 0);
         t_r[j] = r;  // unsorted copy in shared memory for pass 2
         t_c[j] = lc;
         if (sm.occ) occ_max = max(occ_max, occ_count(sm.occ, lc));
@@ -143,7 +144,6 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
         bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
       } else {
-        reinterpret_cast<int4*>(rec)[2 * i + 1] = make_int4(-1, (int)i, 0, 0);
         const int o = atomicAdd(res.novf, 1);
         ovf_rec[o] = r;
         ovf_cell[o] = pk;

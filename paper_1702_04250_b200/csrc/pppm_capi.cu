@@ -357,6 +357,9 @@ static int gather_eff(const pppm_ctx* c) {
     return gather_split_ok(c->order, c->pd.hx) && c->mode == 0 ? GATHER_WS : GATHER_SORTED;
   }
   if (c->mode == 1 && c->gather_variant == GATHER_WS) return GATHER_WS;  // warp-specialized fieldforce_ad
+  // the tensor-core and atom-pair A/B kernels read 32-byte binned slots only
+  if ((c->gather_variant == GATHER_MMA || c->gather_variant == GATHER_WSP) && c->res_sorted && c->res_direct)
+    return gather_split_ok(c->order, c->pd.hx) && c->mode == 0 ? GATHER_WS : GATHER_SORTED;
   if ((c->gather_variant == GATHER_SPLIT || c->gather_variant == GATHER_WS || c->gather_variant == GATHER_WSP) &&
       !(c->mode == 0 && gather_split_ok(c->order, c->pd.hx)))
     return GATHER_SORTED;
@@ -673,6 +676,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     else {
     // the warp-specialized fieldforce takes bricks from a counter (zeroed here, inside the graph)
     Bricks bkg = c->bk;
+    if (resident) bkg.rq = c->res_q.as<float>();  // resident 16-byte records take the charges from here
     if (c->dyn_sched && gather_eff(c) == GATHER_WS) {
       TRY(ensure_sched(c));
       bkg.sched = c->sched.as<int>();

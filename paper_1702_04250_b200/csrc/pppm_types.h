@@ -27,6 +27,8 @@ struct Bricks {
   int nbx, nby, nbz;
   int* sched = nullptr;  // optional brick-scheduling counter (zeroed before the launch): persistent CTAs
                          // take bricks dynamically instead of striding by gridDim.x
+  const float* rq = nullptr;  // fieldforce on brick-ordered residents: their charges (the resident
+                              // slot records are 16 bytes {tx, ty, tz, cell bits}, cell -1 = mover)
   __host__ __device__ __forceinline__ int count() const { return nbx * nby * nbz; }
 };
 
