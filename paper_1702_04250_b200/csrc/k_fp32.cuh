@@ -455,10 +455,10 @@ struct BankSmem {
 // occ[kBrick^3] = the largest count
 __device__ __forceinline__ int occ_count(int* occ, int cell) { return atomicAdd(occ + cell, 1) + 1; }
 
-__device__ __forceinline__ void occ_publish(int* occ, int m) {
+__device__ __forceinline__ void occ_publish(int* max_slot, int m) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(occ + kBrick * kBrick * kBrick, m);
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(max_slot, m);
 }
 
 template <bool PERM, int D, int TXB, int SH, int NT = kThreads>
@@ -496,7 +496,7 @@ __device__ __forceinline__ int stage_banked(const float4* __restrict__ rec, cons
       }
     }
   }
-  if (sm.occ) occ_publish(sm.occ, occ_max);
+  if (sm.occ) occ_publish(sm.occ + kBrick * kBrick * kBrick, occ_max);
   __syncthreads();
   if (threadIdx.x < 32) {
     const int v = sm.bsize[threadIdx.x];

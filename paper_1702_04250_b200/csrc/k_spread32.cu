@@ -110,14 +110,19 @@ constexpr int kMoverQueue = 256;  // movers queued per CTA for the warp-cooperat
 // resident mode: stage brick b's atoms from their positions (the binning
 // pass folded into make_rho), write their slot records at the resident index
 // for fieldforce, send movers down the direct path; returns the rounds
-template <int S, bool TAB, int D, int TXB, int SH, int NT>
-__device__ __forceinline__ int stage_resident(const Resident& res, int b, int cnt, const Geom& g, const Bricks& bk,
-                                              const Pad& pd, int n_points, const float* __restrict__ ta,
-                                              float inv_vcell, float* __restrict__ rho, float4* __restrict__ rec,
-                                              float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
-                                              int* __restrict__ ovf_perm, BankSmem sm, float4* __restrict__ t_r,
-                                              int* __restrict__ t_c, int* __restrict__ mq, int* __restrict__ nmq) {
-  constexpr int PER = kCapMax / NT;
+// (a work item is KB consecutive bricks b, b + 1, ...: atom j belongs to brick
+// b + (j >= cnt0); its staged cell code carries the tile index in bit 9, and
+// its occupancy is counted in that brick's half of sm.occ)
+template <int S, bool TAB, int D, int TXB, int SH, int NT, int KB>
+__device__ __forceinline__ int stage_resident(const Resident& res, int b, int cnt0, int cnt, const Geom& g,
+                                              const Bricks& bk, const Pad& pd, int n_points,
+                                              const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
+                                              float4* __restrict__ rec, float4* __restrict__ ovf_rec,
+                                              int* __restrict__ ovf_cell, int* __restrict__ ovf_perm, BankSmem sm,
+                                              float4* __restrict__ t_r, int* __restrict__ t_c, int* __restrict__ mq,
+                                              int* __restrict__ nmq) {
+  constexpr int PER = KB * kCapMax / NT;
+  constexpr int kCells = kBrick * kBrick * kBrick;
   // (bsize was reset by the caller before its brick barrier)
   // pass 1: map positions, write the slot records (fieldforce reads them at
   // the resident index), bank histogram; only bank / rank stay in registers
@@ -133,13 +138,14 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
       float4 r;
       int lc, pk;
       const int ab = atom_record<S, TAB>(res, i, g, bk, n_points, r, lc, pk);
+      const int kt = (KB > 1 && j >= cnt0) ? 1 : 0;  // tile (brick) of the item
       // 16-byte slot record for fieldforce: offsets + brick-local cell (-1:
       // mover); the charge and the index are the resident arrays' own
-      rec[i] = make_float4(r.x, r.y, r.z, __int_as_float(ab == b ? lc : -1));
-      if (ab == b) {
+      rec[i] = make_float4(r.x, r.y, r.z, __int_as_float(ab == b + kt ? lc : -1));
+      if (ab == b + kt) {
         t_r[j] = r;  // unsorted copy in shared memory for pass 2
-        t_c[j] = lc;
-        if (sm.occ) occ_max = max(occ_max, occ_count(sm.occ, lc));
+        t_c[j] = lc | (kt << 9);
+        if (sm.occ) occ_max = max(occ_max, occ_count(sm.occ, kt * kCells + lc));
         const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
         bank[k] = ((lz * D + ly) * TXB + lx + SH) & 31;
         rk[k] = atomicAdd(sm.bsize + bank[k], 1);
@@ -155,7 +161,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
       }
     }
   }
-  if (sm.occ) occ_publish(sm.occ, occ_max);
+  if (sm.occ) occ_publish(sm.occ + KB * kCells, occ_max);
   __syncthreads();
   if (threadIdx.x < 32) {
     const int v = sm.bsize[threadIdx.x];
@@ -202,19 +208,26 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
   using T = TmaTile<S>;
   constexpr int D = T::D, TXB = T::TXB, TN = T::N, lo = Stencil<S>::lo;
   constexpr bool resident = RES;  // resident brick-ordered atoms (Resident), else binned slots
-  // dynamic smem: [tile 0 | tile 1 | staged atoms]; double-buffered tiles (one
-  // may still be read by its TMA reduce), 128-byte aligned for the bulk copy
+  // bricks per work item: the resident path stages / deposits kSpreadPair
+  // consecutive bricks together (their atoms are one contiguous range), which
+  // halves the CTA barriers and staging passes per atom and fills the bank
+  // rounds from twice as many atoms
+  constexpr int KB = RES ? kSpreadPair : 1;
+  // dynamic smem: [KB tiles x 2 | staged atoms]; double-buffered tiles (one
+  // set may still be read by its TMA reduces), 128-byte aligned for the bulk copy
   extern __shared__ __align__(16) unsigned char dyn_raw[];
   int* dyn_i = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));
   int* tiles0 = dyn_i;
-  float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * T::NP);
+  float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * KB * T::NP);
   __shared__ int bsize[32], bstart[33];
   constexpr int kCells = kBrick * kBrick * kBrick;
-  __shared__ __align__(16) int s_occ[kCells + 4];  // per-cell atom counts of the staged brick, [kCells] = max (FIX scale)
+  // per-cell atom counts of the staged bricks, [KB * kCells] = max (FIX scale)
+  __shared__ __align__(16) int s_occ[KB * kCells + 4];
   // staged atoms: s_r[cap] | (resident: t_r[cap]) | s_c[cap] | (resident: t_c[cap])
   BankSmem sm{s_r, reinterpret_cast<int*>(s_r + (RES ? 2 * cap : cap)), nullptr, bsize, bstart,
               FIX ? s_occ : nullptr};
   const int nb = bk.count();
+  const int nitems = (nb + KB - 1) / KB;
   const float qmax = resident ? res.qmax : __int_as_float(counts[((int64_t)nb + 1) * kCountStride]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   int issued = 0;
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
       b = s_brick;
     }
     prefetched = false;
-    if (b >= nb) {
+    if (b >= nitems) {
       // the last CTA done claiming resets the counters for the next launch (no memset node)
       if (bk.sched && threadIdx.x == 0 && atomicAdd(bk.sched + 33, 1) == (int)gridDim.x - 1) {
         atomicExch(bk.sched + 32, 0);
@@ -239,32 +252,38 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
       }
       break;
     }
-    int cnt;
+    // work item b: bricks b0 .. b0 + kb - 1
+    const int b0 = b * KB, kb = nb - b0 < KB ? nb - b0 : KB;
+    int cnt, cnt0;
     if (resident) {
-      cnt = res.start[b + 1] - res.start[b];
+      cnt0 = res.start[b0 + 1] - res.start[b0];
+      cnt = res.start[b0 + kb] - res.start[b0];
     } else {
-      cnt = counts[(int64_t)b * kCountStride];
+      cnt = counts[(int64_t)b0 * kCountStride];
       cnt = cnt < cap ? cnt : cap;
+      cnt0 = cnt;
     }
     if (cnt == 0) continue;
-    int* tile = tiles0 + (issued & 1) * T::NP;
+    int* tile = tiles0 + (issued & 1) * KB * T::NP;
     float* ftile = reinterpret_cast<float*>(tile);
     // all reduces but the most recent (other buffer) have finished reading
     if (threadIdx.x == 0) bulk_wait_read<1>();
     if (RES && threadIdx.x < 32) bsize[threadIdx.x] = 0;  // stage_resident's histogram
     if (FIX) {
-      for (int k = threadIdx.x; k < kCells / 4; k += blockDim.x) reinterpret_cast<int4*>(s_occ)[k] = make_int4(0, 0, 0, 0);
-      if (threadIdx.x == 0) s_occ[kCells] = 0;
+      for (int k = threadIdx.x; k < KB * kCells / 4; k += blockDim.x)
+        reinterpret_cast<int4*>(s_occ)[k] = make_int4(0, 0, 0, 0);
+      if (threadIdx.x == 0) s_occ[KB * kCells] = 0;
     }
     __syncthreads();
-    static_assert(TN % 4 == 0, "tile rows are 16-byte multiples");
-    for (int k = threadIdx.x; k < TN / 4; k += blockDim.x) reinterpret_cast<int4*>(tile)[k] = make_int4(0, 0, 0, 0);
+    static_assert(T::NP % 4 == 0, "tile rows are 16-byte multiples");
+    for (int k = threadIdx.x; k < KB * T::NP / 4; k += blockDim.x)
+      reinterpret_cast<int4*>(tile)[k] = make_int4(0, 0, 0, 0);
     int rounds;
     if constexpr (RES)
-      rounds = stage_resident<S, TAB, D, TXB, T::SH, NT>(res, b, cnt, g, bk, pd, n_points, ta, inv_vcell, rho,
-                                                            rec_out, ovf_rec, ovf_cell, ovf_perm, sm,
-                                                            s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap,
-                                                            s_mq, &s_nmq);
+      rounds = stage_resident<S, TAB, D, TXB, T::SH, NT, KB>(res, b0, cnt0, cnt, g, bk, pd, n_points, ta, inv_vcell,
+                                                                rho, rec_out, ovf_rec, ovf_cell, ovf_perm, sm,
+                                                                s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap,
+                                                                s_mq, &s_nmq);
     else
       rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
     float scale = inv_vcell, inv_scale = 1.f;
@@ -280,7 +299,7 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
       // (frexp / ldexp through the exponent bits: the bound is a normal float
       // and sc stays far inside the normal range; the 1.01 margin covers the
       // per-contribution rounding)
-      const int m = s_occ[kCells];
+      const int m = s_occ[KB * kCells];
       const float bound = qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f;
       const int e_sum = ((__float_as_int(bound) >> 23) & 0xff) - 126;  // bound < 2^e_sum
       const int sc = 31 - e_sum;
@@ -291,7 +310,9 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
       if (rr >= bsize[lane]) continue;
       const int j = bstart[lane] + rr;
       const float4 r = sm.r[j];
-      const int cc = sm.c[j];
+      const int c9 = sm.c[j];
+      const int cc = KB > 1 ? c9 & (kCells - 1) : c9;
+      int* tl = KB > 1 ? tile + (c9 >> 9) * T::NP : tile;
       const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
       float wx[S], wy[S], wz[S], dd[S];
       rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
             const double qab = qa * (double)wy[bb];
             const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
 #pragma unroll
-            for (int c = 0; c < S; ++c) atomicAdd(tile + row + c, __double2loint(fma(qab, dx[c], kMagic52)));
+            for (int c = 0; c < S; ++c) atomicAdd(tl + row + c, __double2loint(fma(qab, dx[c], kMagic52)));
           }
         }
       } else {
@@ -324,14 +345,14 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
             const float qab = qa * wy[bb];
             const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
 #pragma unroll
-            for (int c = 0; c < S; ++c) atomicAdd(ftile + row + c, qab * wx[c]);
+            for (int c = 0; c < S; ++c) atomicAdd(reinterpret_cast<float*>(tl) + row + c, qab * wx[c]);
           }
         }
       }
     }
     __syncthreads();
     if (FIX)
-      for (int k = threadIdx.x; k < TN / 4; k += blockDim.x) {
+      for (int k = threadIdx.x; k < KB * T::NP / 4; k += blockDim.x) {
         const int4 v = reinterpret_cast<const int4*>(tile)[k];
         reinterpret_cast<float4*>(ftile)[k] =
             make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
@@ -342,8 +363,12 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
     prefetched = bk.sched != nullptr;
 #ifndef PPPM_PROBE_NO_REDUCE  // A/B probe only (wrong mesh): cost of the tile reduce-adds
     if (threadIdx.x == 0) {
-      const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
-      tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H, bz * kBrick - lo + pd.H);
+      for (int k = 0; k < kb; ++k) {
+        const int bb_ = b0 + k;
+        const int bx = bb_ % bk.nbx, by = (bb_ / bk.nbx) % bk.nby, bz = bb_ / (bk.nbx * bk.nby);
+        tma_reduce_add_3d(&rmap, tile + k * T::NP, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H,
+                          bz * kBrick - lo + pd.H);
+      }
       bulk_commit();
     }
 #endif
@@ -574,10 +599,13 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
 #endif
         constexpr int NT = kSpreadThreads;
         auto k = res.pos ? k_spread_tma<S, TAB, FIX, NT, true> : k_spread_tma<S, TAB, FIX, NT, false>;
-        const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) +
-                           (res.pos ? 2 : 1) * (size_t)cap * (sizeof(float4) + sizeof(int));
-        const int grid = persistent_grid(k, NT, dyn, bk.count());
-        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, cap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
+        // resident: kSpreadPair tiles per buffer, staging sized for a work item
+        const int kbt = res.pos ? kSpreadPair : 1;
+        const int scap = res.pos ? res.scap : cap;
+        const size_t dyn = 128 + 2 * (size_t)kbt * TmaTile<S>::NP * sizeof(int) +
+                           (res.pos ? 2 : 1) * (size_t)scap * (sizeof(float4) + sizeof(int));
+        const int grid = persistent_grid(k, NT, dyn, (bk.count() + kbt - 1) / kbt);
+        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, scap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
                                 ovf_perm, res, n_points, rec_out);
         if (getenv("PPPM_B200_DEBUG")) {
           const cudaError_t e = cudaPeekAtLastError();

@@ -498,6 +498,9 @@ static Resident resident_of(pppm_ctx* c) {
   r.n = c->n_res;
   r.qmax = c->res_qmax;
   r.novf = c->res_novf.as<int>();
+  // staging capacity of a make_rho work item (kSpreadPair bricks)
+  const int per = std::min(std::max(c->res_maxcnt, 1), c->cap);
+  r.scap = (kSpreadPair * per + 31) / 32 * 32;
   return r;
 }
 
