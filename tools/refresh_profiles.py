@@ -1,5 +1,5 @@
-"""Regenerate profiles/ from the latest gpurun_out/ captures:
-bench_r01.json, launches_r01.csv, sweep.jsonl, md.jsonl, r01_full_*.ncu-rep.
+"""Regenerate profiles/ from the latest gpurun_out/ captures of tools/final_run.sh TAG:
+bench_TAG.json, launches_TAG.csv, sweep.jsonl, md.jsonl, TAG_full_*.ncu-rep.
 
     python tools/refresh_profiles.py [round tag, default r01]
 """
@@ -20,9 +20,13 @@ def cp(src, dst):
         shutil.copy(os.path.join(G, src), os.path.join(P, dst))
 
 
-cp("bench_r01.json", f"{TAG}_bench.json")
-cp("bench_r01_ref.json", f"{TAG}_bench_reference.json")
-cp("launches_r01.csv", f"{TAG}_launches.csv")
+cp(f"bench_{TAG}.json", f"{TAG}_bench.json")
+cp(f"bench_{TAG}_ref.json", f"{TAG}_bench_reference.json")
+cp(f"launches_{TAG}.csv", f"{TAG}_launches.csv")
+cp(f"launches_{TAG}_config5.csv", f"{TAG}_launches_config5.csv")
+cp(f"density_{TAG}.jsonl", f"{TAG}_density.jsonl")
+cp(f"refsuite_{TAG}_fp64.json", f"{TAG}_reference_suite_fp64.json")
+cp(f"refsuite_{TAG}_mixed.json", f"{TAG}_reference_suite_mixed.json")
 cp("sweep.jsonl", f"{TAG}_sweep.jsonl")
 cp("md.jsonl", f"{TAG}_md.jsonl")
 subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"), os.path.join(P, f"{TAG}_launches.csv"),
@@ -57,10 +61,9 @@ for d in lines:
     s.append(f"| {c['workload'].replace(' point charges per GPU', '')} | {d['value']:.3g} | "
              f"{d['whole_step_atom_steps_per_s']:.3g} | {ph['bin'] * 1e3:.1f} | {ph['spread'] * 1e3:.1f} | "
              f"{ph['poisson'] * 1e3:.1f} | {ph['gather'] * 1e3:.1f} |")
-s += ["", "Orders 3-5 run the split (per-component) warp-specialized fieldforce_ik; orders 6-7 have a 16-float tile row",
-      "(TXB = 16) whose component row shift would alias banks, so they use the bank-round kernel with one task per atom",
-      "(and S³ = 216 / 343 stencil points). Power-of-two meshes run the fused Poisson (plane FFT kernels for nx, ny ≤ 128,",
-      "the z kernel); config 2 (40³) the 3D cuFFT path.", "",
+s += ["", "All orders run the split (per-component) warp-specialized fieldforce_ik (orders 6-7 with 20-wide field boxes).",
+      "Power-of-two meshes run the fused Poisson (plane FFT kernels for nx, ny ≤ 128, the z kernel; cuFFT 2D planes at",
+      "256²); config 2 (40³) the 3D cuFFT path.", "",
       "# Force driver either side of the mesh path (SURVEY §8f)", "",
       "`python tools/bench_md.py --config C --precision P` (B200) and `--reference` (the reference's own `pppm.compute_forces`,",
       "one CPU worker, run in the build container — the reference cannot travel to the GPU box). compute_forces = cell list +",
