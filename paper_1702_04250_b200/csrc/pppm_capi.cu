@@ -9,6 +9,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cufft.h>
+#include <nvtx3/nvToolsExt.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -206,6 +207,16 @@ struct pppm_ctx {
 
 // ---------------------------------------------------------------------------
 // internal helpers
+
+// NVTX ranges around the host-side phases (header-only NVTX v3: no-ops unless
+// a profiler is attached), so an nsys / ncu timeline shows make_rho / Poisson /
+// fieldforce / exchanges / re-sorts by name
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 static void drop_graphs(pppm_ctx* c) {
   for (int k = 0; k < SP_COUNT; ++k) {
@@ -1333,6 +1344,7 @@ int pppm_compute(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dty
 // independently into the same buckets)
 int pppm_compute_ex(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, int mem, void* forces,
                     int forces_dtype, double* energy) {
+  NvtxRange r_("pppm compute");
   TRY(activate(c));
   if (forces_dtype != PPPM_F64 && forces_dtype != PPPM_F32) return fail(PPPM_ERR_VALUE, "unknown forces dtype");
   if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
@@ -1406,6 +1418,7 @@ static int after_sort(pppm_ctx* c) {
 // reorder into the scratch arrays, copy back (the captured graphs keep their
 // pointers) and compose the caller-index map
 static int resort_residents(pppm_ctx* c) {
+  NvtxRange r_("pppm resort");
   const int64_t n = c->n_res;
   TRY(run_bin(c, c->res_pos.p, c->res_q.p, n, PPPM_F32, nullptr));
   TRY(c->res_tmp_pos.ensure(3 * n * sizeof(float)));
@@ -1426,6 +1439,7 @@ static int resort_residents(pppm_ctx* c) {
 }
 
 int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype) {
+  NvtxRange r_("pppm load_atoms");
   TRY(activate(c));
   drop_graphs(c);
   if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
@@ -1519,6 +1533,7 @@ static int grouped(const NcclApi* nc, const std::function<int()>& body) {
 // its RECV_HI), my upper ghosts to the slab above (into its RECV_LO); then
 // the received planes are added into the first / last H owned planes
 static int slab_ghost_sum(pppm_ctx* c) {
+  NvtxRange r_("pppm slab ghost reverse sum");
   const NcclApi* nc = slab_nccl(c);
   if (!nc) return PPPM_ERR_NCCL;
   const size_t plane = (size_t)c->pd.py * c->pd.px, n = plane * c->pd.H;
@@ -1576,6 +1591,7 @@ static int slab_fft_bwd(pppm_ctx* c);
 // the distributed Poisson solve: planes R2C -> transpose -> z FFT / Green / ik /
 // energy -> energy all-reduce + transpose back -> planes C2R -> field ghosts
 static int slab_poisson(pppm_ctx* c) {
+  NvtxRange r_("pppm slab poisson (transposes)");
   const NcclApi* nc = slab_nccl(c);
   if (!nc) return PPPM_ERR_NCCL;
   const size_t a2a = (size_t)c->half * 2;  // floats per field
@@ -1665,6 +1681,7 @@ static int launch_subphase(pppm_ctx* c, int sp) {
 
 static int step_phases(pppm_ctx* c, int phases, bool timing) {
   if (phases & PPPM_PHASE_MAKE_RHO) {
+    NvtxRange r_("pppm make_rho");
     if (resident_step(c) && c->use_graphs) {
       // no binning pass: no bin interval (time_steps reports 0; an extra event
       // record would add its own ~2.6 us to the measured intervals)
@@ -1677,10 +1694,12 @@ static int step_phases(pppm_ctx* c, int phases, bool timing) {
     TRY(launch_subphase(c, SP_SPREAD));
   }
   if (phases & PPPM_PHASE_POISSON) {
+    NvtxRange r_("pppm poisson");
     rec_event(c, SP_POISSON, timing);
     TRY(launch_subphase(c, SP_POISSON));
   }
   if (phases & PPPM_PHASE_FIELDFORCE) {
+    NvtxRange r_("pppm fieldforce");
     rec_event(c, SP_GATHER, timing);
     TRY(launch_subphase(c, SP_GATHER));
   }
@@ -1706,6 +1725,7 @@ int pppm_ctx_synchronize(pppm_ctx* c) {
 // async: nothing waits - errors surface at the next synchronize, and the mover
 // count of the previous update decides the re-sort.
 static int update_positions(pppm_ctx* c, const void* pos, int dtype, int mem, bool sync) {
+  NvtxRange r_("pppm update_positions");
   TRY(activate(c));
   if (c->n_res < 1) return fail(PPPM_ERR_STATE, "no resident atoms");
   if (c->res_sorted && c->fp64()) {
