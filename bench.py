@@ -220,6 +220,23 @@ def cpu_sample_rate(pos, q, lengths, dims, order, mode, sample, workers, reps=1)
     return sample * reps / sum(times), times
 
 
+class stdout_to_stderr:
+    """Route file descriptor 1 to stderr inside the block: libraries (NCCL's
+    version banner) must not add lines to the one-JSON-line stdout contract."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -360,8 +377,9 @@ def run_slabs(args, cfg, rank, local, world, pg):
         raise SystemExit(f"bench: launched with {world} ranks but --gpus {args.gpus}")
     mode = args.mode or cfg.mode
     uid = _bcast_unique_id(pg, rank, local)
-    slab, n_total, n_local, launches = slab_timing(cfg, mode, world, rank, local, args.steps, args.warmup,
-                                                   unique_id=uid)
+    with stdout_to_stderr():
+        slab, n_total, n_local, launches = slab_timing(cfg, mode, world, rank, local, args.steps, args.warmup,
+                                                       unique_id=uid)
     barrier(pg)
     sampler = ClockSampler(local)
     sampler.start()
@@ -414,8 +432,9 @@ def run_slabs(args, cfg, rank, local, world, pg):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    slab.close()
-    pg.destroy_process_group()
+    with stdout_to_stderr():
+        slab.close()
+        pg.destroy_process_group()
 
 
 def config5_record(args, device):
@@ -673,7 +692,7 @@ def main():
     achieved = per_kernel[dom]["gbs"]
     mf_bytes = alg["spread"] + alg["gather"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(args.config, mode, dom), "kernel": kernel_name(dom, mode),
+                "traffic": load_traffic(cfg.index, mode, dom), "kernel": kernel_name(dom, mode),
                 "peak_kind": peak_kind,
                 "make_rho_fieldforce_gbs": mf_bytes / (t_mf / k) / 1e9,
                 "make_rho_fieldforce_frac": mf_bytes / (t_mf / k) / 1e9 / peak}
@@ -749,7 +768,8 @@ def main():
         line["value_fp64"] = extra["fp64"]["value"]
         line["extra"] = extra
     if rank == 0 and world == 1 and not args.no_config5 and args.config is None:
-        line["config5"] = config5_record(args, local)
+        with stdout_to_stderr():
+            line["config5"] = config5_record(args, local)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))

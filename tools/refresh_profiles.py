@@ -20,8 +20,17 @@ def cp(src, dst):
         shutil.copy(os.path.join(G, src), os.path.join(P, dst))
 
 
-cp(f"bench_{TAG}.json", f"{TAG}_bench.json")
-cp(f"bench_{TAG}_ref.json", f"{TAG}_bench_reference.json")
+def cp_json_line(src, dst):
+    """The bench's one JSON line (anything a library printed before it dropped)."""
+    path = os.path.join(G, src)
+    if os.path.exists(path):
+        lines = [l for l in open(path).read().splitlines() if l.startswith("{")]
+        if lines:
+            open(os.path.join(P, dst), "w").write(lines[-1] + "\n")
+
+
+cp_json_line(f"bench_{TAG}.json", f"{TAG}_bench.json")
+cp_json_line(f"bench_{TAG}_ref.json", f"{TAG}_bench_reference.json")
 cp(f"launches_{TAG}.csv", f"{TAG}_launches.csv")
 cp(f"launches_{TAG}_config5.csv", f"{TAG}_launches_config5.csv")
 cp(f"density_{TAG}.jsonl", f"{TAG}_density.jsonl")
