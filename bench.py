@@ -383,9 +383,10 @@ def run_slabs(args, cfg, rank, local, world, pg):
     barrier(pg)
     sampler = ClockSampler(local)
     sampler.start()
-    t_load = time.perf_counter()
-    while time.perf_counter() - t_load < 1.5:
-        slab.time_steps(5, 0)
+    # load the GPUs ~1 s for the clock samples: a FIXED number of steps on every
+    # rank (a wall-clock loop could run different counts per rank and leave the
+    # NCCL exchanges unmatched)
+    slab.time_steps(400, 0)
     barrier(pg)
     t_wall = time.perf_counter()
     ms = slab.time_steps(args.steps, args.warmup)
