@@ -20,7 +20,23 @@ __device__ __forceinline__ float2 rot90(float2 a) {
   return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
 }
 
-// in-register DFT of R = 2, 4, 8 points (forward: exp(-2 pi i jk / R))
+// exp(-+ 2 pi i j / 16) for the j = n2 k1 products of the 4 x 4 DFT (j in 1..9)
+template <bool INV>
+__device__ __forceinline__ float2 w16(int j) {
+  constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f, h = 0.70710678118654752f;
+  float2 w;
+  switch (j) {
+    case 1: w = make_float2(c1, s1); break;
+    case 2: w = make_float2(h, h); break;
+    case 3: w = make_float2(s1, c1); break;
+    case 4: w = make_float2(0.f, 1.f); break;
+    case 6: w = make_float2(-h, h); break;
+    default: w = make_float2(-c1, -s1); break;  // 9
+  }
+  return INV ? w : make_float2(w.x, -w.y);
+}
+
+// in-register DFT of R = 2, 4, 8, 16 points (forward: exp(-2 pi i jk / R))
 template <int R, bool INV>
 __device__ __forceinline__ void dft(float2 (&v)[R]) {
   if constexpr (R == 2) {
@@ -34,7 +50,25 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     v[2] = csub(t0, t2);
     v[1] = cadd(t1, t3);
     v[3] = csub(t1, t3);
+  } else if constexpr (R == 16) {
+    // 4 x 4: n = n2 + 4 n1, k = k1 + 4 k2 (natural order out)
+    float2 y[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      float2 a[4] = {v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]};
+      dft<4, INV>(a);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) y[n2][k1] = n2 * k1 == 0 ? a[k1] : cmul(a[k1], w16<INV>(n2 * k1));
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      float2 b[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+      dft<4, INV>(b);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = b[k2];
+    }
   } else {
+    static_assert(R == 8, "dft: R in {2, 4, 8, 16}");
     float2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
     dft<4, INV>(e);
     dft<4, INV>(o);
@@ -55,6 +89,23 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     v[7] = csub(e[3], o3);
   }
 }
+
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+// Two-pass register FFT of N = R1 * R2 points (the plane and z kernels):
+//   pass A: a thread with fixed n2 < R2 takes x[n2 + R2 n1], n1 < R1, does the
+//           R1-point DFT and multiplies output k1 by W_N^(n2 k1);
+//   pass B: a thread with fixed k1 < R1 takes those R2 values (one per n2),
+//           does the R2-point DFT: X[k1 + R1 k2], k2 < R2.
+// One shared-memory round trip (store after A, load before B) per transform.
+template <int N> struct Radix;
+template <> struct Radix<4> { static constexpr int R1 = 2, R2 = 2; };
+template <> struct Radix<8> { static constexpr int R1 = 4, R2 = 2; };
+template <> struct Radix<16> { static constexpr int R1 = 4, R2 = 4; };
+template <> struct Radix<32> { static constexpr int R1 = 8, R2 = 4; };
+template <> struct Radix<64> { static constexpr int R1 = 8, R2 = 8; };
+template <> struct Radix<128> { static constexpr int R1 = 16, R2 = 8; };
+template <> struct Radix<256> { static constexpr int R1 = 16, R2 = 16; };
 
 // One mixed-radix Stockham autosort pass over B sequences of N points, element
 // (b, n) at x[b * BS + n * ES], x -> y, then the remaining passes (radix 8

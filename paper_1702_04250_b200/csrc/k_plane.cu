@@ -1,5 +1,5 @@
-// Poisson step, fp32 path, one GPU: the (y, x) plane transforms around
-// k_zfft_green, one CTA per plane with the whole plane in shared memory
+// Poisson step, fp32 path: the (y, x) plane transforms around k_zfft_green,
+// one CTA per plane (or per half plane, below) with the plane in shared memory
 // (replaces cuFFT's R2C + y-FFT and y-IFFT + C2R pairs and the halo fill):
 //
 //   k_plane_r2c  rho plane (padded, real, NY x NX) -> spectrum plane
@@ -10,6 +10,23 @@
 //                x / y halo and, for the planes within H of a z face, into the
 //                periodic z-halo plane as well (no separate halo fill).
 //
+// Every 1D transform is the two-pass register FFT of fft_smem.cuh (Radix<N>):
+// one shared-memory round trip per transform, the first pass of the column
+// transform loading straight from global memory and the last pass of the r2c
+// column transform storing straight to it.  Shared layout [row][RS] with
+// RS = NX / 2 + 1 complex (odd): column passes put consecutive columns on
+// consecutive lanes, row passes consecutive rows (odd stride), so every
+// shared access is conflict-free.
+//
+// Planes whose half spectrum does not fit one CTA (256 x 256: 264 KB) are
+// split over S CTAs by one radix-S step along y done on load: CTA h holds
+//   r2c (S = 2): b_h[y] = a[y] + (-1)^h a[y + NY/2], times W_NY^(h y) after the
+//        row R2C, whose NY/2-point column FFT gives spectrum rows 2k + h;
+//   c2r (S = 4): u_h[k] = W_NY^(-h k) sum_j X[k + j NY/S] exp(2 pi i h j / S),
+//        whose NY/S-point column IFFT gives the real rows S m + h.
+// Each CTA reads the whole input plane (the repeat reads mostly from L2) and
+// writes only its part.
+//
 // Both are unnormalised like cuFFT (the 1/M of the inverse lives in the Green
 // multiply).  Real-to-complex split (M = NX / 2, W = exp(-2 pi i / NX)):
 //   z[n] = x[2n] + i x[2n+1],  Z = DFT_M(z)
@@ -17,361 +34,399 @@
 // and its inverse Z[k] = (X[k] + conj X[M-k]) + i W^-k (X[k] - conj X[M-k]),
 // IDFT_M(Z) = NX (x_even + i x_odd) = the unnormalised C2R of X.
 #include <cstdlib>
+#include <type_traits>
 
 #include "fft_smem.cuh"
 #include "pppm_device.cuh"
 
 namespace pppm {
 
-#ifndef PPPM_PLANE_THREADS
-#define PPPM_PLANE_THREADS 1024
-#endif
-constexpr int kPlaneThreads = PPPM_PLANE_THREADS;
+bool smem_raise(const void* kernel, size_t dyn);  // k_core.cu
 
-template <int NX, int NY>
-struct PlaneDims {
-  static constexpr int M = NX / 2;       // complex row length of the half-length FFT
-  static constexpr int RS = M + 1;       // row stride (complex): the M + 1 half-spectrum columns
-  static constexpr int BUF = NY * RS;    // one plane buffer (complex)
-  // twiddle tables (complex): rows exp(-2 pi i m / M), columns exp(-2 pi i m / NY), split exp(-2 pi i k / NX)
+constexpr bool plane_split(int nx, int ny) { return (size_t)ny * (nx / 2 + 1) * sizeof(float2) > 160 * 1024; }
+
+// CTAs per plane of the split planes: r2c 2 (the real-row pair trick needs a
+// real butterfly), c2r PPPM_PLANE_C2R_SPLIT (2 or 4: radix-4 on load holds
+// 66 KB, three CTAs per SM, but reads every plane four times)
+#ifndef PPPM_PLANE_C2R_SPLIT
+#define PPPM_PLANE_C2R_SPLIT 2  // 4 measured slower on config 5 (Poisson 393 -> 483 us: 4x L2 reads)
+#endif
+#ifndef PPPM_PLANE_S4_MINB
+#define PPPM_PLANE_S4_MINB 3
+#endif
+constexpr int r2c_split(int nx, int ny) { return plane_split(nx, ny) ? 2 : 1; }
+constexpr int c2r_split(int nx, int ny) { return plane_split(nx, ny) ? PPPM_PLANE_C2R_SPLIT : 1; }
+
+template <int NX, int NY, int S_>
+struct PlaneCfg {
+  static constexpr int M = NX / 2, RS = M + 1, S = S_;
+  static constexpr int NC = NY / S;  // rows held by one CTA (column transform length)
+  static constexpr int C1 = Radix<NC>::R1, C2 = Radix<NC>::R2, X1 = Radix<M>::R1, X2 = Radix<M>::R2;
+  // threads: one column pass-A task each (RS * C2), halved while above the cap
+  static constexpr int NTMAX = S == 4 ? 320 : 1024;
+  static constexpr int NT0 = RS * C2;
+  static constexpr int NT = NT0 <= NTMAX ? NT0 : (NT0 / 2 <= NTMAX ? NT0 / 2 : (NT0 / 4 <= NTMAX ? NT0 / 4 : NT0 / 8));
+  // twiddles (plane_twiddles): W_M^j (j < M), W_NY^j (j < NY; W_NC^j = W_NY^(S j)), W_NX^k (k <= M)
   static constexpr int TW = M + NY + RS;
-  static constexpr size_t smem = sizeof(float2) * (2 * BUF + TW);
+  static constexpr size_t smem = sizeof(float2) * ((size_t)NC * RS + TW);
+  static constexpr int MINB_S = (int)((227u * 1024u) / (smem + 1024u));
+  static constexpr int MINB_R = S == 4 ? PPPM_PLANE_S4_MINB : (NT > 256 ? 2 : 4);
+  static constexpr int MINB = MINB_S < 1 ? 1 : (MINB_S < MINB_R ? MINB_S : MINB_R);
 };
 
-template <int NX, int NY>
-__device__ __forceinline__ void load_twiddles(const float2* __restrict__ tw, float2* s_tw) {
-  constexpr int TW = PlaneDims<NX, NY>::TW;
-  for (int i = threadIdx.x; i < TW; i += blockDim.x) s_tw[i] = tw[i];
+// bulk prefetch of [p, p + bytes) into L2 in 16 KB pieces, one per thread
+// (widened to 16-byte alignment)
+__device__ __forceinline__ void prefetch_l2(const void* p0, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p0);
+  const char* p = reinterpret_cast<const char*>(a & ~(uintptr_t)15);
+  bytes = (uint32_t)((bytes + (a & 15) + 15) & ~(uintptr_t)15);
+  const uint32_t off = threadIdx.x * 16384u;
+  if (off < bytes) {
+    const uint32_t n = bytes - off < 16384u ? bytes - off : 16384u;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
+  }
 }
 
-template <int NX, int NY>
-__global__ void __launch_bounds__(kPlaneThreads) k_plane_r2c(const float* __restrict__ rho, Pad pd,
-                                                            float2* __restrict__ spec,
-                                                            const float2* __restrict__ tw) {
-  using P = PlaneDims<NX, NY>;
-  constexpr int M = P::M, RS = P::RS;
+// a * i^q
+__device__ __forceinline__ float2 rot_i(float2 a, int q) {
+  q &= 3;
+  return q == 0 ? a : (q == 1 ? make_float2(-a.y, a.x) : (q == 2 ? make_float2(-a.x, -a.y) : make_float2(a.y, -a.x)));
+}
+
+// task loop of a pass: COUNT tasks over NT threads, `it` a compile-time index
+// after unrolling (so per-task register arrays stay in registers)
+#define PLANE_TASKS(COUNT, NT, ...)                                           \
+  _Pragma("unroll") for (int it = 0; it < ((COUNT) + (NT)-1) / (NT); ++it) { \
+    const int i = threadIdx.x + it * (NT);                                    \
+    if ((COUNT) % (NT) == 0 || i < (COUNT)) { __VA_ARGS__ }                   \
+  }
+
+template <int NX, int NY, int S_>
+__global__ void __launch_bounds__(PlaneCfg<NX, NY, S_>::NT, PlaneCfg<NX, NY, S_>::MINB)
+    k_plane_r2c(const float* __restrict__ rho, Pad pd, float2* __restrict__ spec, const float2* __restrict__ tw,
+                int ahead) {
+  using P = PlaneCfg<NX, NY, S_>;
+  static_assert(S_ <= 2, "r2c: split over at most two CTAs");
+  constexpr int M = P::M, RS = P::RS, NC = P::NC, NT = P::NT, S = P::S;
+  constexpr int C1 = P::C1, C2 = P::C2, X1 = P::X1, X2 = P::X2;
   extern __shared__ __align__(16) float2 psm[];
   float2* A = psm;
-  float2* B = A + P::BUF;
-  float2* Wr = B + P::BUF;
-  float2* Wc = Wr + M;
-  float2* Ws = Wc + NY;
-  load_twiddles<NX, NY>(tw, Wr);
-  const int z = blockIdx.x;
+  float2* Wr = A + NC * RS;
+  float2* Wn = Wr + M;
+  float2* Ws = Wn + NY;
+  const int h = S == 2 ? (int)(blockIdx.x & 1) : 0;
+  const int z = blockIdx.x / S;
   const float* plane = rho + pd.interior() + (int64_t)z * pd.py * pd.px;
-  // rows as M complex (even, odd) pairs; rows start 8-byte aligned (hx, px even)
-  for (int i = threadIdx.x; i < NY * M; i += blockDim.x) {
-    const int y = i / M, n = i - y * M;
-    A[y * RS + n] = *reinterpret_cast<const float2*>(plane + (int64_t)y * pd.px + 2 * n);
+  if (ahead > 0 && h == 0 && z + ahead < (int)gridDim.x / S)  // padded plane z + ahead into L2 (see k_plane_c2r)
+    prefetch_l2(rho + (int64_t)(pd.H + z + ahead) * pd.py * pd.px,
+                (uint32_t)(sizeof(float) * pd.py * pd.px));
+  // rows as M complex (even, odd) pairs (rows start 8-byte aligned: hx, px even);
+  // split: the y butterfly a[y] +- a[y + NC] on load.  Loads in batches of 8
+  // per thread, all in flight before the shared stores.
+  {
+    constexpr int TL = NC * M, ITL = (TL + NT - 1) / NT, BATCH = 8;
+#pragma unroll
+    for (int b0 = 0; b0 < ITL; b0 += BATCH) {
+      float2 v[BATCH];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int i = threadIdx.x + (b0 + u) * NT;
+        if (b0 + u < ITL && (TL % NT == 0 || i < TL)) {
+          const int m = i / M, n = i % M;
+          v[u] = __ldg(reinterpret_cast<const float2*>(plane + (int64_t)m * pd.px + 2 * n));
+          if constexpr (S == 2) {
+            const float2 w = __ldg(reinterpret_cast<const float2*>(plane + (int64_t)(m + NC) * pd.px + 2 * n));
+            v[u] = h ? csub(v[u], w) : cadd(v[u], w);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int i = threadIdx.x + (b0 + u) * NT;
+        if (b0 + u < ITL && (TL % NT == 0 || i < TL)) A[(i / M) * RS + i % M] = v[u];
+      }
+    }
   }
+  for (int i = threadIdx.x; i < P::TW; i += NT) Wr[i] = tw[i];
   __syncthreads();
-  float2* Z = fft_batch<M, NY, RS, 1, false>(A, B, Wr);
-  float2* X = Z == A ? B : A;
-  // split step: the M + 1 half-spectrum values of each row
-  for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) {
-    const int y = i / RS, k = i - y * RS;
-    const float2 zk = Z[y * RS + (k == M ? 0 : k)];
-    const float2 zc = Z[y * RS + (k == 0 ? 0 : M - k)];
-    const float2 e = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y - zc.y));  // (Z[k] + conj Z[M-k]) / 2
-    const float2 o = make_float2(0.5f * (zk.y + zc.y), -0.5f * (zk.x - zc.x));  // -i (Z[k] - conj Z[M-k]) / 2
-    X[y * RS + k] = cadd(e, cmul(Ws[k], o));
+  // row pass A (M-point forward): task (y, n2), lanes along y
+  {
+    constexpr int T = NC * X2, IT = (T + NT - 1) / NT;
+    float2 v[IT][X1];
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, n2 = i / NC;
+#pragma unroll
+      for (int n1 = 0; n1 < X1; ++n1) v[it][n1] = A[y * RS + n2 + X2 * n1];
+      dft<X1, false>(v[it]);
+#pragma unroll
+      for (int k1 = 1; k1 < X1; ++k1) v[it][k1] = cmul(v[it][k1], Wr[n2 * k1]);
+    })
+    __syncthreads();
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, n2 = i / NC;
+#pragma unroll
+      for (int k1 = 0; k1 < X1; ++k1) A[y * RS + n2 * X1 + k1] = v[it][k1];
+    })
+    __syncthreads();
   }
-  __syncthreads();
-  float2* S = X == A ? B : A;
-  float2* R = fft_batch<NY, RS, 1, RS, false>(X, S, Wc);
-  float2* out = spec + (int64_t)z * NY * RS;
-  for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) out[i] = R[i];
+  // row pass B: task (y, k1) -> Z[k1 + X1 k2] in natural order
+  {
+    constexpr int T = NC * X1, IT = (T + NT - 1) / NT;
+    float2 v[IT][X2];
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, k1 = i / NC;
+#pragma unroll
+      for (int n2 = 0; n2 < X2; ++n2) v[it][n2] = A[y * RS + n2 * X1 + k1];
+      dft<X2, false>(v[it]);
+    })
+    __syncthreads();
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, k1 = i / NC;
+#pragma unroll
+      for (int k2 = 0; k2 < X2; ++k2) A[y * RS + k1 + X1 * k2] = v[it][k2];
+    })
+    __syncthreads();
+  }
+  // column pass A (NC-point forward) with the split step on load: task (c, n2), lanes along c
+  {
+    constexpr int T = RS * C2, IT = (T + NT - 1) / NT;
+    float2 v[IT][C1];
+    PLANE_TASKS(T, NT, {
+      const int c = i % RS, n2 = i / RS;
+      const float2 ws = Ws[c];
+#pragma unroll
+      for (int n1 = 0; n1 < C1; ++n1) {
+        const int y = n2 + C2 * n1;
+        const float2 zk = A[y * RS + (c == M ? 0 : c)];
+        const float2 zc = A[y * RS + (c == 0 ? 0 : M - c)];
+        const float2 e = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y - zc.y));  // (Z[k] + conj Z[M-k]) / 2
+        const float2 o = make_float2(0.5f * (zk.y + zc.y), -0.5f * (zk.x - zc.x));  // -i (Z[k] - conj Z[M-k]) / 2
+        float2 x = cadd(e, cmul(ws, o));
+        if constexpr (S == 2) {
+          if (h) x = cmul(x, Wn[y]);
+        }
+        v[it][n1] = x;
+      }
+      dft<C1, false>(v[it]);
+#pragma unroll
+      for (int k1 = 1; k1 < C1; ++k1) v[it][k1] = cmul(v[it][k1], Wn[S * n2 * k1]);
+    })
+    __syncthreads();
+    PLANE_TASKS(T, NT, {
+      const int c = i % RS, n2 = i / RS;
+#pragma unroll
+      for (int k1 = 0; k1 < C1; ++k1) A[(n2 * C1 + k1) * RS + c] = v[it][k1];
+    })
+    __syncthreads();
+  }
+  // column pass B: task (c, k1) -> spectrum rows k1 + C1 k2 (split: 2 (k1 + C1 k2) + h), straight to global
+  {
+    constexpr int T = RS * C1;
+    float2* out = spec + (int64_t)z * NY * RS;
+    PLANE_TASKS(T, NT, {
+      const int c = i % RS, k1 = i / RS;
+      float2 v[C2];
+#pragma unroll
+      for (int n2 = 0; n2 < C2; ++n2) v[n2] = A[(n2 * C1 + k1) * RS + c];
+      dft<C2, false>(v);
+#pragma unroll
+      for (int k2 = 0; k2 < C2; ++k2) out[(S * (k1 + C1 * k2) + h) * RS + c] = v[k2];
+    })
+  }
 }
 
 // field f's spectrum plane z: (f * spec_fplanes + spec_z0 + z) * NY * RS in
 // `spec`; writes the padded field plane with its x / y halo and, when the z
 // halo is periodic (one GPU), the periodic z-halo copy
-template <int NX, int NY>
-__global__ void __launch_bounds__(kPlaneThreads) k_plane_c2r(const float2* __restrict__ spec, int64_t spec_fplanes,
-                                                            int spec_z0, Pad pd, int nz, float* __restrict__ fields,
-                                                            const float2* __restrict__ tw) {
-  using P = PlaneDims<NX, NY>;
-  constexpr int M = P::M, RS = P::RS;
+template <int NX, int NY, int S_>
+__global__ void __launch_bounds__(PlaneCfg<NX, NY, S_>::NT, PlaneCfg<NX, NY, S_>::MINB)
+    k_plane_c2r(const float2* __restrict__ spec, int64_t spec_fplanes, int spec_z0, Pad pd, int nz,
+                float* __restrict__ fields, const float2* __restrict__ tw, int ahead) {
+  using P = PlaneCfg<NX, NY, S_>;
+  constexpr int M = P::M, RS = P::RS, NC = P::NC, NT = P::NT, S = P::S;
+  constexpr int C1 = P::C1, C2 = P::C2, X1 = P::X1, X2 = P::X2;
   extern __shared__ __align__(16) float2 psm[];
   float2* A = psm;
-  float2* B = A + P::BUF;
-  float2* Wr = B + P::BUF;
-  float2* Wc = Wr + M;
-  float2* Ws = Wc + NY;
-  load_twiddles<NX, NY>(tw, Wr);
-  const int z = blockIdx.x % nz, f = blockIdx.x / nz;
-  const int H = pd.H;
+  float2* Wr = A + NC * RS;
+  float2* Wn = Wr + M;
+  float2* Ws = Wn + NY;
+  const int h = S > 1 ? (int)(blockIdx.x % S) : 0;
+  const int pl = blockIdx.x / S;
+  const int z = pl % nz, f = pl / nz;
   const float2* in = spec + ((int64_t)f * spec_fplanes + spec_z0 + z) * NY * RS;
-  for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) A[i] = in[i];
-  __syncthreads();
-  float2* X = fft_batch<NY, RS, 1, RS, true>(A, B, Wc);
-  float2* Z = X == A ? B : A;
-  // inverse split step: Z[k] = (X[k] + conj X[M-k]) + i W^-k (X[k] - conj X[M-k]), k < M
-  for (int i = threadIdx.x; i < NY * M; i += blockDim.x) {
-    const int y = i / M, k = i - y * M;
-    const float2 xk = X[y * RS + k];
-    const float2 xc = X[y * RS + M - k];
-    const float2 e = make_float2(xk.x + xc.x, xk.y - xc.y);
-    const float2 d = make_float2(xk.x - xc.x, xk.y + xc.y);
-    const float2 w = make_float2(Ws[k].x, -Ws[k].y);  // W^-k
-    const float2 o = cmul(w, d);
-    Z[y * RS + k] = make_float2(e.x - o.y, e.y + o.x);  // e + i o
+  if (ahead > 0 && h == 0 && pl + ahead < (int)gridDim.x / S) {
+    // the plane a CTA about `ahead` planes later works on (likely the next one on this SM) into L2
+    const int pn = pl + ahead, zn = pn % nz, fn = pn / nz;
+    prefetch_l2(spec + ((int64_t)fn * spec_fplanes + spec_z0 + zn) * NY * RS, (uint32_t)(sizeof(float2) * NY * RS));
   }
-  __syncthreads();
-  float2* T = Z == A ? B : A;
-  float2* R = fft_batch<M, NY, RS, 1, true>(Z, T, Wr);
-  // row y of the real plane: float view of R's row (x = 2n, 2n+1 interleaved)
+  // column pass A (NC-point inverse) straight from global: task (c, n2), lanes along c;
+  // split: the radix-S inverse y butterfly of rows k + NC j on load
+  {
+    constexpr int T = RS * C2, IT = (T + NT - 1) / NT;
+    auto load = [&](int i, float2(&v)[C1]) {
+      const int c = i % RS, n2 = i / RS;
+#pragma unroll
+      for (int n1 = 0; n1 < C1; ++n1) {
+        const int k = n2 + C2 * n1;
+        v[n1] = __ldg(in + k * RS + c);
+#pragma unroll
+        for (int j = 1; j < S; ++j)  // X[k + NC j] exp(2 pi i h j / S)
+          v[n1] = cadd(v[n1], rot_i(__ldg(in + (k + NC * j) * RS + c), h * j * (4 / S)));
+      }
+    };
+    auto transform = [&](int i, float2(&v)[C1]) {
+      const int c = i % RS, n2 = i / RS;
+      if constexpr (S > 1) {
+        if (h) {
+#pragma unroll
+          for (int n1 = 0; n1 < C1; ++n1) v[n1] = cmul(v[n1], conjf2(Wn[h * (n2 + C2 * n1)]));
+        }
+      }
+      dft<C1, true>(v);
+#pragma unroll
+      for (int k1 = 0; k1 < C1; ++k1) A[(n2 * C1 + k1) * RS + c] = k1 == 0 ? v[0] : cmul(v[k1], conjf2(Wn[S * n2 * k1]));
+    };
+    if constexpr (IT == 1) {
+      // all of the thread's loads in flight at once, overlapping the twiddle load
+      float2 v[IT][C1];
+      PLANE_TASKS(T, NT, load(i, v[it]);)
+      for (int j = threadIdx.x; j < P::TW; j += NT) Wr[j] = tw[j];
+      __syncthreads();
+      PLANE_TASKS(T, NT, transform(i, v[it]);)
+    } else {
+      // several tasks per thread (split planes): load and transform task by task
+      for (int j = threadIdx.x; j < P::TW; j += NT) Wr[j] = tw[j];
+      __syncthreads();
+      PLANE_TASKS(T, NT, {
+        float2 v[C1];
+        load(i, v);
+        transform(i, v);
+      })
+    }
+    __syncthreads();
+  }
+  // column pass B: task (c, k1) -> rows k1 + C1 k2
+  {
+    constexpr int T = RS * C1, IT = (T + NT - 1) / NT;
+    float2 v[IT][C2];
+    PLANE_TASKS(T, NT, {
+      const int c = i % RS, k1 = i / RS;
+#pragma unroll
+      for (int n2 = 0; n2 < C2; ++n2) v[it][n2] = A[(n2 * C1 + k1) * RS + c];
+      dft<C2, true>(v[it]);
+    })
+    __syncthreads();
+    PLANE_TASKS(T, NT, {
+      const int c = i % RS, k1 = i / RS;
+#pragma unroll
+      for (int k2 = 0; k2 < C2; ++k2) A[(k1 + C1 * k2) * RS + c] = v[it][k2];
+    })
+    __syncthreads();
+  }
+  // row pass A (M-point inverse) with the inverse split step on load: task (y, n2), lanes along y
+  {
+    constexpr int T = NC * X2, IT = (T + NT - 1) / NT;
+    float2 v[IT][X1];
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, n2 = i / NC;
+#pragma unroll
+      for (int n1 = 0; n1 < X1; ++n1) {
+        const int k = n2 + X2 * n1;
+        const float2 xk = A[y * RS + k];
+        const float2 xc = A[y * RS + M - k];
+        const float2 e = make_float2(xk.x + xc.x, xk.y - xc.y);
+        const float2 d = make_float2(xk.x - xc.x, xk.y + xc.y);
+        const float2 o = cmul(conjf2(Ws[k]), d);             // W^-k (X[k] - conj X[M-k])
+        v[it][n1] = make_float2(e.x - o.y, e.y + o.x);      // e + i o
+      }
+      dft<X1, true>(v[it]);
+#pragma unroll
+      for (int k1 = 1; k1 < X1; ++k1) v[it][k1] = cmul(v[it][k1], conjf2(Wr[n2 * k1]));
+    })
+    __syncthreads();
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, n2 = i / NC;
+#pragma unroll
+      for (int k1 = 0; k1 < X1; ++k1) A[y * RS + n2 * X1 + k1] = v[it][k1];
+    })
+    __syncthreads();
+  }
+  // row pass B: task (y, k1) -> real pairs (x[2n], x[2n+1]), n = k1 + X1 k2, staged as
+  // real rows of NX + 2 floats in the same buffer
+  {
+    constexpr int T = NC * X1, IT = (T + NT - 1) / NT;
+    float2 v[IT][X2];
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, k1 = i / NC;
+#pragma unroll
+      for (int n2 = 0; n2 < X2; ++n2) v[it][n2] = A[y * RS + n2 * X1 + k1];
+      dft<X2, true>(v[it]);
+    })
+    __syncthreads();
+    PLANE_TASKS(T, NT, {
+      const int y = i % NC, k1 = i / NC;
+#pragma unroll
+      for (int k2 = 0; k2 < X2; ++k2) A[y * RS + k1 + X1 * k2] = v[it][k2];
+    })
+    __syncthreads();
+  }
+  // write-out: local row m is plane row y = S m + h, written at padded row H + y
+  // and, within H of a y face, at its periodic image; interior x as float2
+  // (padded rows are 8-byte aligned at hx), the x halo by wrapping
   const int64_t mesh = pd.count();
   const int64_t plane = (int64_t)pd.py * pd.px;
   float* fbase = fields + (int64_t)f * mesh;
-  const int xs = pd.hx - H;         // first padded x written (halo)
-  const int ex = NX + 2 * H, ey = NY + 2 * H;
-  // interior plane and, near a z face, its periodic image in the z halo
-  const int zi = H + z;
-  const int zh = !pd.zper ? -1 : (z < H ? H + z + nz : (z >= nz - H ? H + z - nz : -1));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  for (int yy = warp; yy < ey; yy += nwarp) {
-    int sy = yy - H;
-    sy = sy < 0 ? sy + NY : (sy >= NY ? sy - NY : sy);
-    const float* src = reinterpret_cast<const float*>(R + sy * RS);
-    float* d0 = fbase + zi * plane + (int64_t)yy * pd.px + xs;
-    float* d1 = zh >= 0 ? fbase + zh * plane + (int64_t)yy * pd.px + xs : nullptr;
-    for (int xx = lane; xx < ex; xx += 32) {
-      int sx = xx - H;
-      sx = sx < 0 ? sx + NX : (sx >= NX ? sx - NX : sx);
-      const float v = src[sx];
-      d0[xx] = v;
-      if (d1) d1[xx] = v;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-register variant: every 1D transform of a plane is done by one warp in
-// registers (N = 32 P points, lane l holding x[32 p + l]: a P-point DFT per
-// lane, twiddles W_N^(l k1), then a 32-point radix-2 DIF across the lanes with
-// shuffles), in place in ONE shared plane buffer - 67 KB instead of 135 KB, so
-// three CTAs share an SM (the Stockham kernels above fit one).  Needs
-// NX / 2 >= 32 and NY >= 32.
-
-__device__ __forceinline__ int brev5(int l) { return (int)(__brev((unsigned)l) >> 27); }
-
-// per-lane twiddles: tn[k1] = W_N^(l k1), ts[s] = W_(2h)^(l mod h) for h = 16 >> s (conjugated for INV)
-template <int P, bool INV>
-__device__ __forceinline__ void warp_fft_twiddles(int lane, float2 (&tn)[P], float2 (&ts)[5]) {
-  const float sg = INV ? 2.f : -2.f;
-#pragma unroll
-  for (int k1 = 0; k1 < P; ++k1) {
-    float sn, cs;
-    sincospif(sg * (float)(lane * k1) / (float)(32 * P), &sn, &cs);
-    tn[k1] = make_float2(cs, sn);
-  }
-#pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int h = 16 >> st;
-    float sn, cs;
-    sincospif(sg * 0.5f * (float)(lane & (h - 1)) / (float)h, &sn, &cs);
-    ts[st] = make_float2(cs, sn);
-  }
-}
-
-// N = 32 P point DFT of v (lane l: v[p] = x[32 p + l]); on return v[k1] = X[k1 + P brev5(l)]
-template <int P, bool INV>
-__device__ __forceinline__ void warp_fft(float2 (&v)[P], const float2 (&tn)[P], const float2 (&ts)[5], int lane) {
-  if constexpr (P > 1) {
-    dft<P, INV>(v);
-#pragma unroll
-    for (int k1 = 1; k1 < P; ++k1) v[k1] = cmul(v[k1], tn[k1]);
-  }
-#pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int h = 16 >> st;
-    const bool up = (lane & h) != 0;
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) {
-      float2 o;
-      o.x = __shfl_xor_sync(0xffffffffu, v[k1].x, h);
-      o.y = __shfl_xor_sync(0xffffffffu, v[k1].y, h);
-      v[k1] = up ? cmul(csub(o, v[k1]), ts[st]) : cadd(v[k1], o);
-    }
-  }
-}
-
-#ifdef PPPM_AB_VARIANTS  // warp-register plane FFTs: A/B variant (measured slower)
-constexpr int kPlaneWThreads = 512;
-
-template <int NX, int NY>
-struct PlaneWDims {
-  static constexpr int M = NX / 2, RS = M + 1, PR = M / 32, PC = NY / 32;
-  static constexpr size_t smem = sizeof(float2) * ((size_t)NY * RS + RS);
-};
-
-template <int NX, int NY>
-__global__ void __launch_bounds__(kPlaneWThreads, 3) k_plane_r2c_w(const float* __restrict__ rho, Pad pd,
-                                                                  float2* __restrict__ spec,
-                                                                  const float2* __restrict__ tw) {
-  using P = PlaneWDims<NX, NY>;
-  constexpr int M = P::M, RS = P::RS, PR = P::PR, PC = P::PC;
-  extern __shared__ __align__(16) float2 wsm[];
-  float2* A = wsm;
-  float2* Ws = A + NY * RS;
-  for (int i = threadIdx.x; i < RS; i += blockDim.x) Ws[i] = tw[M + NY + i];
-  const int z = blockIdx.x;
-  const float* plane = rho + pd.interior() + (int64_t)z * pd.py * pd.px;
-  for (int i = threadIdx.x; i < NY * M; i += blockDim.x) {
-    const int y = i / M, n = i - y * M;
-    A[y * RS + n] = *reinterpret_cast<const float2*>(plane + (int64_t)y * pd.px + 2 * n);
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  __syncthreads();
-  // row FFTs (M-point complex of the even / odd pairs)
-  {
-  float2 tnr[PR], tsr[5];
-  warp_fft_twiddles<PR, false>(lane, tnr, tsr);
-  for (int y = warp; y < NY; y += nwarp) {
-    float2 v[PR];
-#pragma unroll
-    for (int p = 0; p < PR; ++p) v[p] = A[y * RS + 32 * p + lane];
-    warp_fft<PR, false>(v, tnr, tsr, lane);
-#pragma unroll
-    for (int k1 = 0; k1 < PR; ++k1) A[y * RS + k1 + PR * brev5(lane)] = v[k1];
-  }
-  }
-  __syncthreads();
-  // split step in place: X[k], X[M-k] from Z[k], Z[M-k] (k <= M / 2; X[M] from Z[0])
-  constexpr int HK = M / 2 + 1;
-  for (int i = threadIdx.x; i < NY * HK; i += blockDim.x) {
-    const int y = i / HK, k = i - y * HK;
-    float2* row = A + y * RS;
-    const float2 zk = row[k];
-    const float2 zc = row[k == 0 ? 0 : M - k];
-    auto split = [&](float2 a, float2 b, int kk) {  // (a + conj b) / 2 - i W^kk (a - conj b) / 2
-      const float2 e = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
-      const float2 o = make_float2(0.5f * (a.y + b.y), -0.5f * (a.x - b.x));
-      return cadd(e, cmul(Ws[kk], o));
-    };
-    const float2 xk = split(zk, zc, k);
-    const float2 xc = split(zc, zk, M - k);
-    row[k] = xk;
-    if (k != M / 2) row[M - k] = xc;  // k = 0: X[M]
-  }
-  __syncthreads();
-  // column FFTs (NY points) over the M + 1 half-spectrum columns
-  float2 tnc[PC], tsc[5];
-  warp_fft_twiddles<PC, false>(lane, tnc, tsc);
-  for (int c = warp; c < RS; c += nwarp) {
-    float2 v[PC];
-#pragma unroll
-    for (int p = 0; p < PC; ++p) v[p] = A[(32 * p + lane) * RS + c];
-    warp_fft<PC, false>(v, tnc, tsc, lane);
-#pragma unroll
-    for (int k1 = 0; k1 < PC; ++k1) A[(k1 + PC * brev5(lane)) * RS + c] = v[k1];
-  }
-  __syncthreads();
-  float2* out = spec + (int64_t)z * NY * RS;
-  for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) out[i] = A[i];
-}
-
-template <int NX, int NY>
-__global__ void __launch_bounds__(kPlaneWThreads, 3) k_plane_c2r_w(const float2* __restrict__ spec,
-                                                                  int64_t spec_fplanes, int spec_z0, Pad pd, int nz,
-                                                                  float* __restrict__ fields,
-                                                                  const float2* __restrict__ tw) {
-  using P = PlaneWDims<NX, NY>;
-  constexpr int M = P::M, RS = P::RS, PR = P::PR, PC = P::PC;
-  extern __shared__ __align__(16) float2 wsm[];
-  float2* A = wsm;
-  float2* Ws = A + NY * RS;
-  for (int i = threadIdx.x; i < RS; i += blockDim.x) Ws[i] = tw[M + NY + i];
-  const int z = blockIdx.x % nz, f = blockIdx.x / nz;
   const int H = pd.H;
-  const float2* in = spec + ((int64_t)f * spec_fplanes + spec_z0 + z) * NY * RS;
-  for (int i = threadIdx.x; i < NY * RS; i += blockDim.x) A[i] = in[i];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  __syncthreads();
-  // column IFFTs
-  {
-  float2 tnc[PC], tsc[5];
-  warp_fft_twiddles<PC, true>(lane, tnc, tsc);
-  for (int c = warp; c < RS; c += nwarp) {
-    float2 v[PC];
-#pragma unroll
-    for (int p = 0; p < PC; ++p) v[p] = A[(32 * p + lane) * RS + c];
-    warp_fft<PC, true>(v, tnc, tsc, lane);
-#pragma unroll
-    for (int k1 = 0; k1 < PC; ++k1) A[(k1 + PC * brev5(lane)) * RS + c] = v[k1];
-  }
-  }
-  __syncthreads();
-  // inverse split in place: Z[k] = (X[k] + conj X[M-k]) + i W^-k (X[k] - conj X[M-k]), k < M
-  constexpr int HK = M / 2 + 1;
-  for (int i = threadIdx.x; i < NY * HK; i += blockDim.x) {
-    const int y = i / HK, k = i - y * HK;
-    float2* row = A + y * RS;
-    const float2 xk = row[k], xc = row[M - k];
-    auto isplit = [&](float2 a, float2 b, int kk) {
-      const float2 e = make_float2(a.x + b.x, a.y - b.y);
-      const float2 d = make_float2(a.x - b.x, a.y + b.y);
-      const float2 o = cmul(make_float2(Ws[kk].x, -Ws[kk].y), d);
-      return make_float2(e.x - o.y, e.y + o.x);
-    };
-    const float2 zk = isplit(xk, xc, k);
-    row[k] = zk;
-    if (k != 0 && k != M / 2) row[M - k] = isplit(xc, xk, M - k);
-  }
-  __syncthreads();
-  // row IFFTs (M-point complex -> the real row as interleaved even / odd)
-  {
-  float2 tnr[PR], tsr[5];
-  warp_fft_twiddles<PR, true>(lane, tnr, tsr);
-  for (int y = warp; y < NY; y += nwarp) {
-    float2 v[PR];
-#pragma unroll
-    for (int p = 0; p < PR; ++p) v[p] = A[y * RS + 32 * p + lane];
-    warp_fft<PR, true>(v, tnr, tsr, lane);
-#pragma unroll
-    for (int k1 = 0; k1 < PR; ++k1) A[y * RS + k1 + PR * brev5(lane)] = v[k1];
-  }
-  }
-  __syncthreads();
-  const int64_t mesh = pd.count();
-  const int64_t plane = (int64_t)pd.py * pd.px;
-  float* fbase = fields + (int64_t)f * mesh;
-  const int xs = pd.hx - H;
-  const int ex = NX + 2 * H, ey = NY + 2 * H;
   const int zi = H + z;
   const int zh = !pd.zper ? -1 : (z < H ? H + z + nz : (z >= nz - H ? H + z - nz : -1));
-  for (int yy = warp; yy < ey; yy += nwarp) {
-    int sy = yy - H;
-    sy = sy < 0 ? sy + NY : (sy >= NY ? sy - NY : sy);
-    const float* src = reinterpret_cast<const float*>(A + sy * RS);
-    float* d0 = fbase + zi * plane + (int64_t)yy * pd.px + xs;
-    float* d1 = zh >= 0 ? fbase + zh * plane + (int64_t)yy * pd.px + xs : nullptr;
-    for (int xx = lane; xx < ex; xx += 32) {
-      int sx = xx - H;
-      sx = sx < 0 ? sx + NX : (sx >= NX ? sx - NX : sx);
-      const float v = src[sx];
-      d0[xx] = v;
-      if (d1) d1[xx] = v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NFW = NT / 32;  // full warps (a partial last warp idles here)
+  if (warp >= NFW) return;
+  // halo lanes: lane < H -> padded x hx - H + lane from x = NX - H + lane; H <= lane < 2H -> hx + NX + (lane - H) from lane - H
+  const bool hl = lane < 2 * H;
+  const int hsrc = lane < H ? NX - H + lane : lane - H;
+  const int hdst = lane < H ? pd.hx - H + lane : pd.hx + NX + lane - H;
+  for (int m = warp; m < NC; m += NFW) {
+    const int y = S * m + h;
+    const int yi = y < H ? H + y + NY : (y >= NY - H ? H + y - NY : -1);
+    const float2* src = A + m * RS;
+    // destinations: interior row; y image; z-halo plane copies of both (null when absent)
+    float* r0 = fbase + zi * plane + (int64_t)(H + y) * pd.px;
+    float* r1 = yi >= 0 ? fbase + zi * plane + (int64_t)yi * pd.px : nullptr;
+    float* r2 = zh >= 0 ? fbase + zh * plane + (int64_t)(H + y) * pd.px : nullptr;
+    float* r3 = zh >= 0 && yi >= 0 ? fbase + zh * plane + (int64_t)yi * pd.px : nullptr;
+#pragma unroll
+    for (int n0 = 0; n0 < M; n0 += 32) {
+      const int n = n0 + lane;
+      if (M % 32 == 0 || n < M) {
+        const float2 v = src[n];
+        const int o = pd.hx + 2 * n;
+        *reinterpret_cast<float2*>(r0 + o) = v;
+        if (r1) *reinterpret_cast<float2*>(r1 + o) = v;
+        if (r2) *reinterpret_cast<float2*>(r2 + o) = v;
+        if (r3) *reinterpret_cast<float2*>(r3 + o) = v;
+      }
+    }
+    if (hl) {
+      const float v = reinterpret_cast<const float*>(src)[hsrc];
+      r0[hdst] = v;
+      if (r1) r1[hdst] = v;
+      if (r2) r2[hdst] = v;
+      if (r3) r3[hdst] = v;
     }
   }
 }
 
-// PPPM_B200_PLANEW (A/B; default 0 = off: measured slower, Poisson 67.9 -> 84.0 us on config 3):
-// 1 both, 2 C2R only, 3 R2C only
-static bool plane_w_ok(int nx, int ny, bool c2r) {
-  const char* v = getenv("PPPM_B200_PLANEW");
-  const int m = v ? atoi(v) : 0;
-  return nx >= 64 && ny >= 32 && (m == 1 || (m == 2 && c2r) || (m == 3 && !c2r));
-}
-#endif
+#undef PLANE_TASKS
 
 bool plane_supported(int nx, int ny) {
-  auto p2 = [](int v) { return v >= 16 && v <= 128 && (v & (v - 1)) == 0; };
+  auto p2 = [](int v) { return v >= 16 && v <= 256 && (v & (v - 1)) == 0; };
   return p2(nx) && p2(ny);
 }
 
-// twiddles of PlaneDims<nx, ny>, fp64 host computation (nx / 2 + ny + nx / 2 + 1 complex)
+int plane_twiddle_count(int nx, int ny) { return nx / 2 + ny + nx / 2 + 1; }
+
+// twiddles of PlaneCfg<nx, ny, S> (any S), fp64 host computation (plane_twiddle_count complex)
 void plane_twiddles(int nx, int ny, float* out) {
   const int m = nx / 2;
   int k = 0;
@@ -385,6 +440,15 @@ void plane_twiddles(int nx, int ny, float* out) {
   for (int i = 0; i <= m; ++i) put(-2.0 * M_PI * i / nx);
 }
 
+// L2 prefetch distance in planes for the split (one CTA per SM) kernels: about
+// one wave of CTAs ahead; 0 (off) otherwise.  PPPM_B200_PLANE_PREFETCH=0 disables.
+int device_sm_count();
+static int plane_ahead(int S, int minb) {
+  static const int on = getenv("PPPM_B200_PLANE_PREFETCH") ? atoi(getenv("PPPM_B200_PLANE_PREFETCH")) : 1;
+  if (!on || S == 1) return 0;
+  return device_sm_count() * minb / S;
+}
+
 template <typename F>
 static int with_plane(int nx, int ny, F&& f) {
   auto by_y = [&](auto NX_) -> int {
@@ -393,7 +457,8 @@ static int with_plane(int nx, int ny, F&& f) {
       case 32: return f(NX_, std::integral_constant<int, 32>{});
       case 64: return f(NX_, std::integral_constant<int, 64>{});
       case 128: return f(NX_, std::integral_constant<int, 128>{});
-      default: set_error(1, "plane FFT: ny must be a power of two in [16, 128]"); return 1;
+      case 256: return f(NX_, std::integral_constant<int, 256>{});
+      default: set_error(1, "plane FFT: ny must be a power of two in [16, 256]"); return 1;
     }
   };
   switch (nx) {
@@ -401,7 +466,8 @@ static int with_plane(int nx, int ny, F&& f) {
     case 32: return by_y(std::integral_constant<int, 32>{});
     case 64: return by_y(std::integral_constant<int, 64>{});
     case 128: return by_y(std::integral_constant<int, 128>{});
-    default: set_error(1, "plane FFT: nx must be a power of two in [16, 128]"); return 1;
+    case 256: return by_y(std::integral_constant<int, 256>{});
+    default: set_error(1, "plane FFT: nx must be a power of two in [16, 256]"); return 1;
   }
 }
 
@@ -409,21 +475,12 @@ int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, fl
                      cudaStream_t s) {
   int st = with_plane(nx, ny, [&](auto NX_, auto NY_) -> int {
     constexpr int NX = decltype(NX_)::value, NY = decltype(NY_)::value;
-#ifdef PPPM_AB_VARIANTS
-    if constexpr (NX >= 64 && NY >= 32) {
-      if (plane_w_ok(nx, ny, false)) {
-        auto kw = k_plane_r2c_w<NX, NY>;
-        constexpr size_t dw = PlaneWDims<NX, NY>::smem;
-        if (dw > 48 * 1024) cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dw);
-        kw<<<nz, kPlaneWThreads, dw, s>>>(rho, pd, spec, tw);
-        return 0;
-      }
-    }
-#endif
-    auto k = k_plane_r2c<NX, NY>;
-    constexpr size_t dyn = PlaneDims<NX, NY>::smem;
-    if (dyn > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k<<<nz, kPlaneThreads, dyn, s>>>(rho, pd, spec, tw);
+    constexpr int S = r2c_split(NX, NY);
+    using P = PlaneCfg<NX, NY, S>;
+    auto k = k_plane_r2c<NX, NY, S>;
+    if (P::smem > 48 * 1024 && smem_raise((const void*)k, P::smem))
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::smem);
+    k<<<nz * P::S, P::NT, P::smem, s>>>(rho, pd, spec, tw, plane_ahead(P::S, P::MINB));
     return 0;
   });
   return st ? st : launch_status();
@@ -431,23 +488,19 @@ int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, fl
 
 int launch_plane_c2r(int nx, int ny, int nz, int nfields, const float2* spec, int64_t spec_fplanes, int spec_z0,
                      const Pad& pd, float* fields, const float2* tw, cudaStream_t s) {
+  if (2 * pd.H > ny) {
+    set_error(1, "plane FFT: the y halo must not exceed half the plane");
+    return 1;
+  }
   int st = with_plane(nx, ny, [&](auto NX_, auto NY_) -> int {
     constexpr int NX = decltype(NX_)::value, NY = decltype(NY_)::value;
-#ifdef PPPM_AB_VARIANTS
-    if constexpr (NX >= 64 && NY >= 32) {
-      if (plane_w_ok(nx, ny, true)) {
-        auto kw = k_plane_c2r_w<NX, NY>;
-        constexpr size_t dw = PlaneWDims<NX, NY>::smem;
-        if (dw > 48 * 1024) cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dw);
-        kw<<<nz * nfields, kPlaneWThreads, dw, s>>>(spec, spec_fplanes, spec_z0, pd, nz, fields, tw);
-        return 0;
-      }
-    }
-#endif
-    auto k = k_plane_c2r<NX, NY>;
-    constexpr size_t dyn = PlaneDims<NX, NY>::smem;
-    if (dyn > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    k<<<nz * nfields, kPlaneThreads, dyn, s>>>(spec, spec_fplanes, spec_z0, pd, nz, fields, tw);
+    constexpr int S = c2r_split(NX, NY);
+    using P = PlaneCfg<NX, NY, S>;
+    auto k = k_plane_c2r<NX, NY, S>;
+    if (P::smem > 48 * 1024 && smem_raise((const void*)k, P::smem))
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::smem);
+    k<<<nz * nfields * P::S, P::NT, P::smem, s>>>(spec, spec_fplanes, spec_z0, pd, nz, fields, tw,
+                                                  plane_ahead(P::S, P::MINB));
     return 0;
   });
   return st ? st : launch_status();

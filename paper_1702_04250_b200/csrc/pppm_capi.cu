@@ -331,7 +331,7 @@ static int ensure_plans(pppm_ctx* c) {
     CU(cudaMemset(c->ework.p, 0, ez));
     c->plane = c->use_plane && plane_supported(c->g.nx, c->g.ny);
     if (c->plane) {
-      const int ntw = c->g.nx / 2 + c->g.ny + c->g.nx / 2 + 1;
+      const int ntw = plane_twiddle_count(c->g.nx, c->g.ny);
       std::vector<float> ptw(2 * ntw);
       plane_twiddles(c->g.nx, c->g.ny, ptw.data());
       TRY(c->ptw.ensure(sizeof(float) * 2 * ntw));
@@ -1904,7 +1904,7 @@ static int ensure_slab_plans(pppm_ctx* c) {
   c->plane = c->use_plane && plane_supported(nx, ny);
   c->zfft = c->use_zfft && zfft_supported(c->g.nz);
   if (c->plane) {
-    const int ntw = nx / 2 + ny + nx / 2 + 1;
+    const int ntw = plane_twiddle_count(nx, ny);
     std::vector<float> ptw(2 * ntw);
     plane_twiddles(nx, ny, ptw.data());
     TRY(c->ptw.ensure(sizeof(float) * 2 * ntw));

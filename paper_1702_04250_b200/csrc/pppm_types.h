@@ -123,6 +123,7 @@ int launch_series_row(const double* v, const double* m, int64_t n, double* tmp4,
 int py_floordiv_int(double a, double b);  // Python's float a // b (k_pair.cu)
 bool zfft_supported(int nz);
 bool plane_supported(int nx, int ny);
+int plane_twiddle_count(int nx, int ny);
 void plane_twiddles(int nx, int ny, float* out);
 int launch_plane_r2c(int nx, int ny, int nz, const float* rho, const Pad& pd, float2* spec, const float2* tw,
                      cudaStream_t s);
