@@ -306,9 +306,9 @@ __device__ __forceinline__ void rows_f32(float v, const float* __restrict__ ta, 
 // the slot record of resident atom i, exactly as k_bin_fixed computes it;
 // returns the atom's brick (pk: wrapped node packed 10+10+10 bits)
 template <int S, bool TAB>
-__device__ __forceinline__ int atom_record(const Resident& res, int64_t i, const Geom& g, const Bricks& bk,
-                                           int n_points, float4& r, int& lc, int& pk) {
-  const double x = (double)res.pos[3 * i], y = (double)res.pos[3 * i + 1], z = (double)res.pos[3 * i + 2];
+__device__ __forceinline__ int atom_record_xyz(float xf, float yf, float zf, float q, const Geom& g, const Bricks& bk,
+                                               int n_points, float4& r, int& lc, int& pk) {
+  const double x = (double)xf, y = (double)yf, z = (double)zf;
   int n0, n1, n2;
   double tx, ty, tz;
   particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
@@ -332,8 +332,15 @@ __device__ __forceinline__ int atom_record(const Resident& res, int64_t i, const
     r.y = (float)ty;
     r.z = (float)tz;
   }
-  r.w = res.q[i];
+  r.w = q;
   return ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);
+}
+
+template <int S, bool TAB>
+__device__ __forceinline__ int atom_record(const Resident& res, int64_t i, const Geom& g, const Bricks& bk,
+                                           int n_points, float4& r, int& lc, int& pk) {
+  return atom_record_xyz<S, TAB>(res.pos[3 * i], res.pos[3 * i + 1], res.pos[3 * i + 2], res.q[i], g, bk, n_points, r,
+                                 lc, pk);
 }
 
 // ---------------------------------------------------------------------------

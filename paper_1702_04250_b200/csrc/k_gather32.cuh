@@ -407,6 +407,10 @@ template <int S> constexpr int kWsXl = PPPM_WS_XL < S ? PPPM_WS_XL : S;
 #define PPPM_WS_U2 4
 #endif
 constexpr int kWsU1 = PPPM_WS_U1, kWsU2 = PPPM_WS_U2;
+#ifndef PPPM_WS_UR
+#define PPPM_WS_UR 4
+#endif
+constexpr int kWsUr = PPPM_WS_UR;  // ranked records loaded per batch (registers shared with the consumers)
 
 // producer warps / staging batch of the warp-specialized gather: fieldforce_ad's
 // consumers are ~3x faster per brick, so its staging runs on two warps
@@ -441,6 +445,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
   __shared__ int bsize[2][32], bstart[2][32], cursor[32], sbrick[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = bk.count();
+  const bool ranked = bk.gbs != nullptr && rstart != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], kWsPw<MODE>);
@@ -511,6 +516,50 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
         base = (int64_t)b * cap;
       }
       const int4* meta = reinterpret_cast<const int4*>(rec);
+      if (ranked) {
+        // make_rho ranked the records (Bricks::gbs): bucket sizes from its histogram, every
+        // record straight to bucket start + rank - one memory round trip, no atomics
+        if (warp == 0) {
+          const int v = cnt > 0 ? __ldg(bk.gbs + (int64_t)b * 32 + lane) : 0;
+          int x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          bsize[s][lane] = v;
+          bstart[s][lane] = x - v;
+        }
+        pbar();
+        float4* sr = s_r + s * cap;
+        int* sc = s_c + s * cap;
+        int* sp = s_p + s * cap;
+        for (int j0 = 0; j0 < cnt; j0 += 32 * NPW * kWsUr) {
+          float4 r[kWsUr];
+          float qq[kWsUr];
+#pragma unroll
+          for (int u = 0; u < kWsUr; ++u) {
+            const int j = j0 + u * 32 * NPW + pt;
+            r[u].w = __int_as_float(-1);
+            if (j < cnt) {
+              r[u] = __ldg(&rec[base + j]);
+              qq[u] = __ldg(&bk.rq[base + j]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kWsUr; ++u) {
+            const int code = __float_as_int(r[u].w);
+            if (code < 0) continue;  // left the brick: overflow list
+            const int dst = bstart[s][(code >> kRecBankShift) & 31] + ((code >> kRecRankShift) & kRecRankMask);
+            sr[dst] = make_float4(r[u].x, r[u].y, r[u].z, qq[u]);
+            sc[dst] = (code & kRecHoleBit) ? -1 : (code & kRecCellMask);  // hole: reserved slot, atom on the list
+            sp[dst] = (int)(base + j0 + u * 32 * NPW + pt);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        continue;
+      }
       if (warp == 0) bsize[s][lane] = 0;
       pbar();
       // pass 1: bank histogram (loads batched: one memory round trip per kWsU1 x 32 records)
@@ -611,6 +660,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
         const int j = bstart[s][(lane - f * TXB) & 31] + rk;
         const float4 r = sr[j];
         const int cc = sc[j];
+        if (cc < 0) continue;  // hole (ranked records): the atom is on the overflow list
         const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
         if constexpr (MODE == 1) {
           // fieldforce_ad (gridmap.py:299-310): split-atom derivative sums over one potential tile

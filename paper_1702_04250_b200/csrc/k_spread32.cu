@@ -3,6 +3,7 @@
 // per-brick power-of-two scale, or float CAS atomics), the tile added to the
 // halo-padded mesh with one TMA reduce-add, then the halo folded back.
 #include <algorithm>
+#include <cmath>
 
 #include "k_fp32.cuh"
 #include "tma.cuh"
@@ -103,6 +104,13 @@ __device__ __forceinline__ void spread_direct_warp(const float4& r, int cc, cons
     // same product order as spread_direct: ((q wz) wy) wx
     atomicAdd(rho + pd.at(n0 - lo + c, n1 - lo + bb, n2 - lo + a), q * pick_w(wz, a) * pick_w(wy, bb) * pick_w(wx, c));
   }
+}
+
+// out-of-line copy for rare paths inside unrolled staging loops
+template <int S, bool TAB>
+__device__ __noinline__ void spread_direct_cold(float4 r, int cc, Pad pd, const float* __restrict__ ta,
+                                                float inv_vcell, float* __restrict__ rho) {
+  spread_direct<S, TAB>(r, cc, pd, ta, inv_vcell, rho);
 }
 
 constexpr int kMoverQueue = 256;  // movers queued per CTA for the warp-cooperative direct spread
@@ -401,6 +409,249 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
 }
 
 
+// make_rho on brick-ordered residents, software-pipelined (default resident
+// path).  Per CTA, work item k (one brick) goes through three stages that
+// overlap across items:
+//   prefetch: one bulk copy (TMA, mbarrier) of the brick's contiguous positions
+//             and charges into shared memory, issued one item ahead, so the
+//             mapping never waits on HBM;
+//   map:      particle_map + slot record (written for fieldforce) + the atom
+//             straight into its bank bucket, stored round-major
+//             (slot = rank * 32 + bank: a round's record loads are contiguous)
+//             with a fixed bucket capacity `bcap` - one pass, no scan, no
+//             scatter pass (bucket overflow: the movers' direct path);
+//   deposit:  bank rounds of int32 fixed-point shared atomics into the tile
+//             (same arithmetic as k_spread_tma), then fp32 conversion and one
+//             TMA reduce-add.
+// Item k + 1 is mapped in the same barrier interval in which item k's tile is
+// converted, so an item costs two CTA barriers (k_spread_tma: six) and no
+// exposed global-memory latency.
+template <int S, bool TAB, int NT>
+__global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPREAD_MINB)) k_spread_res(
+    Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
+    const __grid_constant__ CUtensorMap rmap, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
+    int* __restrict__ ovf_perm, Resident res, int n_points, float4* __restrict__ rec_out, int cap, int bcap) {
+  using T = TmaTile<S>;
+  constexpr int D = T::D, TXB = T::TXB, lo = Stencil<S>::lo;
+  constexpr int kCells = kBrick * kBrick * kBrick;
+  constexpr int PER = kCapMax / NT;
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  int* tiles = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][NP]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * T::NP);                                    // [bcap][32]
+  float* pre_pos = reinterpret_cast<float*>(s_r + 32 * bcap);                                     // 3 cap + 8
+  float* pre_q = pre_pos + (3 * cap + 8 + 3) / 4 * 4;                                             // cap + 8
+  int* s_c = reinterpret_cast<int*>(pre_q + (cap + 8 + 3) / 4 * 4);                               // [bcap][32]
+  __shared__ int bsize[2][32], gsize[2][32];
+  __shared__ __align__(16) int s_occ[2][kCells + 4];
+  __shared__ int s_item[2], s_s0[2], s_cnt[2], s_mq[kMoverQueue], s_nmq;
+  __shared__ __align__(8) uint64_t pbar;
+  const int nb = bk.count();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = NT / 32;
+  const float qmax = res.qmax;
+
+  // claim the CTA's next brick (dynamic after the first; static stride without the counter)
+  int nclaimed = 1;
+  auto claim = [&]() -> int {
+    const int b = bk.sched ? (int)gridDim.x + atomicAdd(bk.sched + 32, 1) : (int)(blockIdx.x + nclaimed * gridDim.x);
+    ++nclaimed;
+    return b;
+  };
+  // thread 0: bulk-copy brick b's positions / charges (16-byte granules around the range)
+  // and publish its range (slot = the item's parity; read after the next barrier)
+  auto prefetch = [&](int b, int slot) {
+    const int s0 = res.start[b], s1 = res.start[b + 1];
+    s_s0[slot] = s0;
+    s_cnt[slot] = s1 - s0;
+    if (s1 <= s0) return;
+    const uint32_t pb0 = (uint32_t)((12ll * s0) & 15), pbytes = (pb0 + 12u * (uint32_t)(s1 - s0) + 15u) & ~15u;
+    const uint32_t qb0 = (uint32_t)((4ll * s0) & 15), qbytes = (qb0 + 4u * (uint32_t)(s1 - s0) + 15u) & ~15u;
+    mbar_arrive_expect_tx(&pbar, pbytes + qbytes);
+    bulk_load_1d(pre_pos, reinterpret_cast<const char*>(res.pos) + 12ll * s0 - pb0, pbytes, &pbar);
+    bulk_load_1d(pre_q, reinterpret_cast<const char*>(res.q) + 4ll * s0 - qb0, qbytes, &pbar);
+  };
+  // map brick b's atoms (prefetched) into the bank buckets of parity p
+  auto map_item = [&](int b, int p, uint32_t phase) {
+    const int s0 = s_s0[p], cnt = s_cnt[p];
+    if (cnt <= 0) return;
+    mbar_wait(&pbar, phase);
+    const float* pp = pre_pos + ((12ll * s0) & 15) / 4;
+    const float* pq = pre_q + ((4ll * s0) & 15) / 4;
+    int occ_max = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j = threadIdx.x + k * NT;
+      if (j < cnt) {
+        const int64_t i = (int64_t)s0 + j;
+        float4 r;
+        int lc, pk;
+        const int ab = atom_record_xyz<S, TAB>(pp[3 * j], pp[3 * j + 1], pp[3 * j + 2], pq[j], g, bk, n_points, r, lc, pk);
+        bool direct = ab != b;
+        int code = -1;
+        if (!direct) {
+          const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
+          const int bank = ((lz * D + ly) * TXB + lx + T::SH) & 31;
+          const int rk = atomicAdd(&bsize[p][bank], 1);
+          code = lc;
+          if (bk.gbs) {  // bank and rank in fieldforce's tile, for its staging
+            const int gb = ((lz * bk.gdy + ly) * bk.gtxb + lx + T::SH) & 31;
+            const int grk = atomicAdd(&gsize[p][gb], 1);
+            code |= (gb << kRecBankShift) | (grk << kRecRankShift);
+          }
+          if (rk < bcap) {
+            occ_max = max(occ_max, occ_count(s_occ[p], lc));
+            s_r[rk * 32 + bank] = r;
+            s_c[rk * 32 + bank] = lc;
+          } else {
+            direct = true;  // bucket full: the movers' path (make_rho here, fieldforce through the list)
+            code = bk.gbs ? (code | kRecHoleBit) : -1;  // its fieldforce slot stays reserved
+          }
+        }
+        // 16-byte slot record for fieldforce: offsets + cell word (-1 / hole: direct path)
+        rec_out[i] = make_float4(r.x, r.y, r.z, __int_as_float(code));
+        if (direct) {
+          const int o = atomicAdd(res.novf, 1);
+          ovf_rec[o] = r;
+          ovf_cell[o] = pk;
+          ovf_perm[o] = (int)i;
+          const int slot = atomicAdd(&s_nmq, 1);
+          if (slot < kMoverQueue) s_mq[slot] = o;
+          else spread_direct_cold<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
+        }
+      }
+    }
+    occ_publish(&s_occ[p][kCells], occ_max);
+  };
+
+  // ---- prologue: buffers cleared, brick 0 prefetched; iteration -1 only maps it
+  for (int k = threadIdx.x; k < 2 * (kCells + 4); k += NT) (&s_occ[0][0])[k] = 0;
+  if (threadIdx.x < 64) (&bsize[0][0])[threadIdx.x] = 0;
+  if (threadIdx.x >= 64 && threadIdx.x < 128) (&gsize[0][0])[threadIdx.x - 64] = 0;
+  if (threadIdx.x == 0) {
+    s_nmq = 0;
+    mbar_init(&pbar, 1);
+    fence_mbar_init();
+    s_item[0] = blockIdx.x;
+    s_item[1] = nb;
+    s_cnt[0] = s_cnt[1] = 0;
+    if ((int)blockIdx.x < nb) prefetch(blockIdx.x, 0);
+  }
+  __syncthreads();
+  uint32_t nfetch = 0;  // prefetch phases consumed so far (uniform)
+  for (int k = -1;; ++k) {
+    const int p = k & 1;
+    const int b = k < 0 ? -1 : s_item[p];
+    if (b >= nb) break;
+    const int cnt = k < 0 ? 0 : s_cnt[p];
+    const int nxt = s_item[p ^ 1];
+    int* tile = tiles + p * T::NP;
+    float* ftile = reinterpret_cast<float*>(tile);
+    float inv_scale = 1.f;
+    if (cnt > 0) {
+      // int32 fixed point, power-of-two scale from the brick's largest cell occupancy (see k_spread_tma)
+      const int m = s_occ[p][kCells];
+      const float bound = qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f;
+      const int e_sum = ((__float_as_int(bound) >> 23) & 0xff) - 126;  // bound < 2^e_sum
+      const int sc = 31 - e_sum;
+      const float scale = __int_as_float((127 + sc) << 23);
+      inv_scale = __int_as_float((127 - sc) << 23) * inv_vcell;
+      int mine = bsize[p][lane];
+      mine = mine < bcap ? mine : bcap;
+      int rounds = mine;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+      constexpr double kMagic52 = 6755399441055744.0;  // 1.5 * 2^52
+      for (int rr = warp; rr < rounds; rr += nwarp) {
+        if (rr >= mine) continue;
+        const float4 r = s_r[rr * 32 + lane];
+        const int cc = s_c[rr * 32 + lane];
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        float wx[S], wy[S], wz[S], dd[S];
+        rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+        rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+        rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+        double dx[S];
+#pragma unroll
+        for (int c = 0; c < S; ++c) dx[c] = (double)wx[c];
+        const double qs = (double)r.w * (double)scale;
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          const double qa = qs * (double)wz[a];
+#pragma unroll
+          for (int bb = 0; bb < S; ++bb) {
+            const double qab = qa * (double)wy[bb];
+            const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+#pragma unroll
+            for (int c = 0; c < S; ++c) atomicAdd(tile + row + c, __double2loint(fma(qab, dx[c], kMagic52)));
+          }
+        }
+      }
+    }
+    int n2 = nb;
+    if (threadIdx.x == 0) {
+      bulk_wait_read<0>();            // the other tile's reduce (previous item) has read it
+      if (nxt < nb) n2 = claim();     // the brick after next (its latency hides behind the barrier)
+    }
+    __syncthreads();
+    // ---- item k: tile -> fp32; item k + 1: mapped; buffers of item k + 2 cleared
+    if (cnt > 0)
+      for (int t = threadIdx.x; t < T::NP / 4; t += NT) {
+        const int4 v = reinterpret_cast<const int4*>(tile)[t];
+        reinterpret_cast<float4*>(ftile)[t] =
+            make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
+      }
+    for (int t = threadIdx.x; t < T::NP / 4; t += NT)
+      reinterpret_cast<int4*>(tiles + (p ^ 1) * T::NP)[t] = make_int4(0, 0, 0, 0);
+    for (int t = threadIdx.x; t < (kCells + 4) / 4; t += NT) reinterpret_cast<int4*>(s_occ[p])[t] = make_int4(0, 0, 0, 0);
+    if (threadIdx.x < 32) bsize[p][threadIdx.x] = 0;
+    if (threadIdx.x >= 32 && threadIdx.x < 64) gsize[p][threadIdx.x - 32] = 0;
+    if (nxt < nb && s_cnt[p ^ 1] > 0) {
+      map_item(nxt, p ^ 1, nfetch & 1);
+      ++nfetch;
+    }
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) s_item[p] = n2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (cnt > 0) {
+        const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+        tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H,
+                          bz * kBrick - lo + pd.H);
+        bulk_commit();
+      }
+      if (n2 < nb) prefetch(n2, p);
+    }
+    // the mapped brick's fieldforce bucket sizes (gsize[p ^ 1] is cleared after the next barrier)
+    if (bk.gbs && warp == 1 && nxt < nb) bk.gbs[(int64_t)nxt * 32 + lane] = gsize[p ^ 1][lane];
+  }
+  if (threadIdx.x == 0) {
+    bulk_wait_read<0>();
+    // the last CTA done claiming resets the counters for the next launch (no memset node)
+    if (bk.sched && atomicAdd(bk.sched + 33, 1) == (int)gridDim.x - 1) {
+      atomicExch(bk.sched + 32, 0);
+      atomicExch(bk.sched + 33, 0);
+    }
+  }
+  // this CTA's movers (atoms outside their sorted brick, full buckets), one warp each
+  __syncthreads();
+  const int nmq = s_nmq < kMoverQueue ? s_nmq : kMoverQueue;
+  for (int m = warp; m < nmq; m += nwarp) {
+    const int o = s_mq[m];
+    spread_direct_warp<S, TAB>(ovf_rec[o], ovf_cell[o], pd, ta, inv_vcell, rho);
+  }
+  // atoms that overflowed their bucket at load: direct path, and on the list for fieldforce
+  for (int64_t i = res.start[nb] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < res.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 r;
+    int lc, pk;
+    atom_record<S, TAB>(res, i, g, bk, n_points, r, lc, pk);
+    spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
+    const int o = atomicAdd(res.novf, 1);
+    ovf_rec[o] = r;
+    ovf_cell[o] = pk;
+    ovf_perm[o] = (int)i;
+  }
+}
+
 #ifdef PPPM_AB_VARIANTS  // A/B variant (measured slower)
 // make_rho, warp-specialized: warp 0 stages brick i+1 (two-pass bank-bucketed
 // counting sort of its slots into one of two stage slots) and finishes brick
@@ -572,7 +823,8 @@ __global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, const Resident& res,
-                        int n_points, float4* rec_out, cudaStream_t s) {
+                        int n_points, float4* rec_out, cudaStream_t s, bool* ranked) {
+  if (ranked) *ranked = false;
   if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
   int st = with_order(order, [&](auto S_) -> int {
@@ -598,6 +850,26 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         (void)F_;
 #endif
         constexpr int NT = kSpreadThreads;
+        static const bool pipelined = !getenv("PPPM_B200_SPREAD_RES") || atoi(getenv("PPPM_B200_SPREAD_RES")) != 0;
+        if (res.pos && FIX && pipelined && kSpreadPair == 1) {
+          // software-pipelined resident make_rho: bucket capacity from the largest brick
+          // (mean + ~4.5 sigma of its bank buckets; fuller buckets spill to the direct path)
+          auto kr = k_spread_res<S, TAB, NT>;
+          const int rcap = (res.scap + 31) / 32 * 32;
+          const int bmean = rcap / 32;
+          const int bcap = std::min(64, std::max(16, bmean + (int)(4.5f * sqrtf((float)bmean)) + 2));
+          const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)bcap * 32 * (sizeof(float4) + sizeof(int)) +
+                             sizeof(float) * ((3 * (size_t)rcap + 8 + 3) / 4 * 4 + ((size_t)rcap + 8 + 3) / 4 * 4);
+          const int grid = persistent_grid(kr, NT, dyn, bk.count());
+          // worth it only when a CTA works through several bricks (config 4's 512 bricks are one
+          // per CTA: nothing to overlap, and the larger staging lowers the CTAs per SM)
+          if (bk.count() >= 2 * grid) {
+            kr<<<grid, NT, dyn, s>>>(g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell, ovf_perm, res, n_points,
+                                     rec_out, rcap, bcap);
+            if (ranked) *ranked = bk.gbs != nullptr;
+            return 0;
+          }
+        }
         auto k = res.pos ? k_spread_tma<S, TAB, FIX, NT, true> : k_spread_tma<S, TAB, FIX, NT, false>;
         // resident: kSpreadPair tiles per buffer, staging sized for a work item
         const int kbt = res.pos ? kSpreadPair : 1;

@@ -93,7 +93,7 @@ struct DevBuf {
     p = nullptr;
     bytes = 0;
     if (b == 0) return PPPM_OK;
-    CU(cudaMalloc(&p, b));
+    CU(cudaMalloc(&p, b + 64));  // slack: 16-byte-granular bulk loads may read past the last element
     bytes = b;
     return PPPM_OK;
   }
@@ -146,11 +146,14 @@ struct pppm_ctx {
   int spread_variant = SPREAD_FIX32, gather_variant = GATHER_WS;
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
+  DevBuf gbs;               // per-brick fieldforce bank-bucket sizes written by the pipelined make_rho
+  bool rec_ranked = false;  // the slot records carry fieldforce bank + rank (Bricks::gbs)
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
   int res_maxcnt = 0;       // largest resident brick (staging capacity of the resident fieldforce)
   DevBuf sched;             // brick-scheduling counters of the persistent fieldforce / make_rho
   bool novf_clean = false;  // the resident mover counter is zero (cleared by the last fieldforce CTA)
   bool dyn_sched = true;
+  bool rank_handoff = true;  // PPPM_B200_RANKS=0: fieldforce staging sorts the records itself (A/B)
   // resident step without a binning pass: make_rho maps the brick-ordered fp32
   // positions itself (Resident in pppm_types.h); bstart = per-brick ranges
   bool res_direct = true;
@@ -498,6 +501,7 @@ static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int d
                  c->stream));
   c->launches += 1;
   c->binned = true;
+  c->rec_ranked = false;
   return PPPM_OK;
 }
 
@@ -539,11 +543,22 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
       TRY(ensure_sched(c));
       bks.sched = c->sched.as<int>();
     }
+    c->rec_ranked = false;
+    if (resident && gather_eff(c) == GATHER_WS && c->rank_handoff) {
+      // records carry the bank / rank of the warp-specialized fieldforce's tile (ik: component
+      // tiles of split_txb columns and D + 2 rows; ad: the brick tile)
+      const int D = kBrick + c->order - 1, lo = (c->order - 1) / 2;
+      const int sh = ((c->pd.hx - lo) % 4 + 4) % 4;
+      TRY(c->gbs.ensure(sizeof(int) * 32 * (size_t)c->bk.count()));
+      bks.gbs = c->gbs.as<int>();
+      bks.gtxb = c->mode == 0 ? split_txb(c->order, c->pd.hx) : (D + sh + 3) / 4 * 4;
+      bks.gdy = c->mode == 0 ? D + 2 : D;
+    }
     TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(),
                             c->ovf_perm.as<int>(), c->g, bks, c->pd, c->rho_map, c->tab.as<float>(),
                             c->rho.as<float>(), resident ? resident_of(c) : Resident{}, c->n_points,
-                            c->rec.as<float4>(), c->stream));
+                            c->rec.as<float4>(), c->stream, &c->rec_ranked));
     c->launches += 1 + fold_launches(c->g, c->pd);  // spread + halo fold
   }
   c->have_rho = true;
@@ -691,6 +706,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     // the warp-specialized fieldforce takes bricks from a counter (zeroed here, inside the graph)
     Bricks bkg = c->bk;
     if (resident) bkg.rq = c->res_q.as<float>();  // resident 16-byte records take the charges from here
+    if (resident && c->rec_ranked) bkg.gbs = c->gbs.as<int>();  // ... and are placed by make_rho's ranks
     if (c->dyn_sched && gather_eff(c) == GATHER_WS) {
       TRY(ensure_sched(c));
       bkg.sched = c->sched.as<int>();
@@ -983,6 +999,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_PLANE")) c->use_plane = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_RANKS")) c->rank_handoff = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RESORT")) c->resort_frac = atof(v);
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;
@@ -1048,7 +1065,7 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   DevBuf* bufs[] = {&c->spec2d, &c->a2a_send, &c->a2a_recv, &c->ghost_lo, &c->ghost_hi, &c->rho, &c->rho_fix, &c->rho_hat, &c->ework, &c->fields, &c->green, &c->ikc,
                     &c->ik64, &c->tab, &c->pos_stage, &c->q_stage, &c->out_stage, &c->node_stage,
                     &c->counts, &c->rec, &c->rcell, &c->perm, &c->ovf_rec, &c->ovf_cell, &c->ovf_perm, &c->partial,
-                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->ztw, &c->zdone, &c->res_novf, &c->ptw,
+                    &c->scal, &c->err, &c->flush, &c->res_pos, &c->res_q, &c->res_force, &c->res_orig, &c->res_tmp_pos, &c->res_tmp_q, &c->bstart, &c->gbs, &c->ztw, &c->zdone, &c->res_novf, &c->ptw,
                     &c->pr_cell, &c->pr_count, &c->pr_start, &c->pr_cursor, &c->pr_order, &c->pr_tmp, &c->pr_force,
                     &c->pr_e, &c->pr_cnt, &c->pr_rmin, &c->pr_ij, &c->pr_part, &c->pr_pos, &c->pr_q, &c->pr_scal, &c->pr_sp,
                     &c->md_pos, &c->md_vel, &c->md_m, &c->md_q, &c->md_f, &c->md_tmp, &c->md_series,

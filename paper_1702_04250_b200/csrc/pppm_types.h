@@ -29,8 +29,19 @@ struct Bricks {
                          // take bricks dynamically instead of striding by gridDim.x
   const float* rq = nullptr;  // fieldforce on brick-ordered residents: their charges (the resident
                               // slot records are 16 bytes {tx, ty, tz, cell bits}, cell -1 = mover)
+  // make_rho -> fieldforce hand-off on brick-ordered residents (pipelined make_rho only): every
+  // slot record carries the atom's bank and rank in fieldforce's shared field tile (rows of gtxb,
+  // gdy rows per plane) and gbs holds each brick's 32 bank-bucket sizes, so that fieldforce's
+  // staging places the records without its own counting sort (kRecBank / kRecRank / kRecHole)
+  int* gbs = nullptr;
+  int gdy = 0, gtxb = 0;
   __host__ __device__ __forceinline__ int count() const { return nbx * nby * nbz; }
 };
+
+// resident slot record word (rec.w as int): brick-local cell, then - ranked records only - the
+// fieldforce bank, the rank inside that bank's bucket, and the hole flag (slot reserved, but the
+// atom takes the direct path in both kernels); -1: the atom left its brick (direct path)
+constexpr int kRecCellMask = 511, kRecBankShift = 9, kRecRankShift = 14, kRecRankMask = 1023, kRecHoleBit = 1 << 24;
 
 struct GreenSpec {
   int nx, ny, nz, order;
@@ -149,7 +160,8 @@ int launch_reorder_resident(bool f32, const Bricks& bk, int cap, const float4* r
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad,
-                        const Resident& res, int n_points, float4* rec_out, cudaStream_t s);
+                        const Resident& res, int n_points, float4* rec_out, cudaStream_t s,
+                        bool* ranked = nullptr);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s);
