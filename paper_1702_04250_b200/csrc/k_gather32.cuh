@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
   int* s_c = reinterpret_cast<int*>(s_r + 2 * cap);          // [2][cap]
   int* s_p = s_c + 2 * cap;                                  // [2][cap]
   __shared__ __align__(8) uint64_t full[2], tmaf[2], empty[2];
-  __shared__ int bsize[2][32], bstart[2][32], cursor[32], sbrick[2];
+  __shared__ int bsize[2][32], bstart[2][32], cursor[32], sbrick[2], sbase[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = bk.count();
   const bool ranked = bk.gbs != nullptr && rstart != nullptr;
@@ -516,6 +516,9 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
         base = (int64_t)b * cap;
       }
       const int4* meta = reinterpret_cast<const int4*>(rec);
+      // residents: a staged cell word also carries the atom's index within the brick (bits 9..),
+      // the force index is sbase + that (one shared-memory load less per task than a slot index)
+      if (pt == 0) sbase[s] = (int)base;
       if (ranked) {
         // make_rho ranked the records (Bricks::gbs): bucket sizes from its histogram, every
         // record straight to bucket start + rank - one memory round trip, no atomics
@@ -552,8 +555,8 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
             if (code < 0) continue;  // left the brick: overflow list
             const int dst = bstart[s][(code >> kRecBankShift) & 31] + ((code >> kRecRankShift) & kRecRankMask);
             sr[dst] = make_float4(r[u].x, r[u].y, r[u].z, qq[u]);
-            sc[dst] = (code & kRecHoleBit) ? -1 : (code & kRecCellMask);  // hole: reserved slot, atom on the list
-            sp[dst] = (int)(base + j0 + u * 32 * NPW + pt);
+            // hole: reserved slot, atom on the list
+            sc[dst] = (code & kRecHoleBit) ? -1 : ((code & kRecCellMask) | ((j0 + u * 32 * NPW + pt) << 9));
           }
         }
         __syncwarp();
@@ -621,8 +624,12 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
           const int lx = m[u].x & (kBrick - 1), ly = (m[u].x >> 3) & (kBrick - 1), lz = m[u].x >> 6;
           const int dst = atomicAdd(&cursor[((lz * DY + ly) * TXB + lx + T::SH) & 31], 1);
           sr[dst] = r[u];
-          sc[dst] = m[u].x;
-          sp[dst] = m[u].y;
+          if (rstart) {
+            sc[dst] = m[u].x | ((m[u].y - (int)base) << 9);
+          } else {
+            sc[dst] = m[u].x;
+            sp[dst] = m[u].y;
+          }
         }
       }
       __syncwarp();
@@ -640,28 +647,26 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
       const float4* sr = s_r + s * cap;
       const int* sc = s_c + s * cap;
       const int* sp = s_p + s * cap;
+      const int sb = sbase[s];
       const int seg0 = bsize[s][lane];
       const int seg1 = MODE == 0 ? bsize[s][(lane - TXB) & 31] : 0, seg2 = MODE == 0 ? bsize[s][(lane - 2 * TXB) & 31] : 0;
       const int tot = seg0 + seg1 + seg2;
       int trounds = tot;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) trounds = max(trounds, __shfl_xor_sync(0xffffffffu, trounds, o));
+      // the lane's task list: its three bank buckets back to back (slot = segment start + round)
+      const int e1 = seg0 + seg1;
+      const int st0 = bstart[s][lane];
+      const int st1 = MODE == 0 ? bstart[s][(lane - TXB) & 31] - seg0 : 0;
+      const int st2 = MODE == 0 ? bstart[s][(lane - 2 * TXB) & 31] - e1 : 0;
       for (int rr = cw; rr < trounds; rr += NCW) {
         if (rr >= tot) continue;
-        int f = 0, rk = rr;
-        if (rk >= seg0) {
-          rk -= seg0;
-          f = 1;
-          if (rk >= seg1) {
-            rk -= seg1;
-            f = 2;
-          }
-        }
-        const int j = bstart[s][(lane - f * TXB) & 31] + rk;
+        const int f = MODE == 0 ? (rr >= seg0) + (rr >= e1) : 0;
+        const int j = (f == 0 ? st0 : (f == 1 ? st1 : st2)) + rr;
         const float4 r = sr[j];
         const int cc = sc[j];
         if (cc < 0) continue;  // hole (ranked records): the atom is on the overflow list
-        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = (cc >> 6) & (kBrick - 1);
         if constexpr (MODE == 1) {
           // fieldforce_ad (gridmap.py:299-310): split-atom derivative sums over one potential tile
           float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
@@ -691,7 +696,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
             s2 = fmaf(dz[a], r2, s2);
           }
           const float sc = cscale * r.w;
-          const int64_t i = sp[j];
+          const int64_t i = rstart ? (int64_t)(sb + (cc >> 9)) : (int64_t)sp[j];
           store_force<S, 1>(force, out_f64, i, -sc * s0 * (float)g.ihx, -sc * s1 * (float)g.ihy,
                             -sc * s2 * (float)g.ihz);
           continue;
@@ -716,7 +721,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
           acc = fmaf(az[a], ra, acc);
         }
         const float v = cscale * r.w * acc;
-        const int64_t i = sp[j];
+        const int64_t i = rstart ? (int64_t)(sb + (cc >> 9)) : (int64_t)sp[j];
         if (out_f64) static_cast<double*>(force)[3 * i + f] = v;
         else static_cast<float*>(force)[3 * i + f] = v;
       }
