@@ -308,12 +308,20 @@ __device__ __forceinline__ void rows_f32(float v, const float* __restrict__ ta, 
 template <int S, bool TAB>
 __device__ __forceinline__ int atom_record_xyz(float xf, float yf, float zf, float q, const Geom& g, const Bricks& bk,
                                                int n_points, float4& r, int& lc, int& pk) {
-  const double x = (double)xf, y = (double)yf, z = (double)zf;
   int n0, n1, n2;
   double tx, ty, tz;
-  particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
-  particle_map_fast<S>(y, g.hy, g.ihy, n1, ty);
-  particle_map_fast<S>(z, g.hz, g.ihz, n2, tz);
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  if (TAB) {  // table bins are taken from the fp64 offsets, as the reference takes them
+    const double x = (double)xf, y = (double)yf, z = (double)zf;
+    particle_map_fast<S>(x, g.hx, g.ihx, n0, tx);
+    particle_map_fast<S>(y, g.hy, g.ihy, n1, ty);
+    particle_map_fast<S>(z, g.hz, g.ihz, n2, tz);
+  } else {    // fp32 arithmetic, bit-exact nodes (particle_map_f32)
+    const float hxh = (float)g.ihx, hyh = (float)g.ihy, hzh = (float)g.ihz;
+    particle_map_f32<S>(xf, hxh, (float)(g.ihx - (double)hxh), g.hx, n0, fx);
+    particle_map_f32<S>(yf, hyh, (float)(g.ihy - (double)hyh), g.hy, n1, fy);
+    particle_map_f32<S>(zf, hzh, (float)(g.ihz - (double)hzh), g.hz, n2, fz);
+  }
   n0 = n0 >= g.nx ? n0 - g.nx : n0;
   n1 = n1 >= g.ny ? n1 - g.ny : n1;
   n2 = n2 >= g.nz ? n2 - g.nz : n2;
@@ -328,9 +336,9 @@ __device__ __forceinline__ int atom_record_xyz(float xf, float yf, float zf, flo
     r.y = __int_as_float(table_bin(ty, n_points));
     r.z = __int_as_float(table_bin(tz, n_points));
   } else {
-    r.x = (float)tx;
-    r.y = (float)ty;
-    r.z = (float)tz;
+    r.x = fx;
+    r.y = fy;
+    r.z = fz;
   }
   r.w = q;
   return ((n2 / kBrick) * bk.nby + (n1 / kBrick)) * bk.nbx + (n0 / kBrick);

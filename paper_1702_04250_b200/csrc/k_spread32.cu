@@ -652,6 +652,259 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
   }
 }
 
+#ifdef PPPM_AB_VARIANTS  // A/B variant (measured: 67.6 us vs 65.7 us for k_spread_res on config 3 - its two
+// producer warps map a brick more slowly than eight consumer warps deposit one)
+// make_rho on brick-ordered residents, warp-specialized: kSprPw producer warps
+// map brick k + 1 (bulk-copy prefetch two bricks ahead, particle_map, slot
+// records for fieldforce, bank buckets stored round-major) while kSprCw
+// consumer warps deposit brick k (bank rounds of int32 shared atomics), convert
+// its tile and issue the TMA reduce-add.  Stage slots (records, bucket sizes,
+// occupancy) are handed over with mbarriers; the consumers synchronise among
+// themselves with a named barrier, so the mapping is off their critical path.
+#ifndef PPPM_SPR_PW
+#define PPPM_SPR_PW 2
+#endif
+#ifndef PPPM_SPR_CW
+#define PPPM_SPR_CW 8
+#endif
+constexpr int kSprPw = PPPM_SPR_PW, kSprCw = PPPM_SPR_CW;
+
+template <int S, bool TAB>
+__global__ void __launch_bounds__(32 * (kSprPw + kSprCw), (S >= 7 ? 2 : 3)) k_spread_wsr(
+    Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
+    const __grid_constant__ CUtensorMap rmap, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
+    int* __restrict__ ovf_perm, Resident res, int n_points, float4* __restrict__ rec_out, int cap, int bcap) {
+  using T = TmaTile<S>;
+  constexpr int D = T::D, TXB = T::TXB, lo = Stencil<S>::lo;
+  constexpr int kCells = kBrick * kBrick * kBrick;
+  constexpr int NP_T = 32 * kSprPw, NC_T = 32 * kSprCw;
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  int* tiles = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][NP]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * T::NP);                                    // [2][bcap][32]
+  const int prep = (3 * cap + 8 + 3) / 4 * 4, preq = (cap + 8 + 3) / 4 * 4;
+  float* pre_pos = reinterpret_cast<float*>(s_r + 2 * 32 * bcap);                                 // [2][prep]
+  float* pre_q = pre_pos + 2 * prep;                                                              // [2][preq]
+  int* s_c = reinterpret_cast<int*>(pre_q + 2 * preq);                                            // [2][bcap][32]
+  __shared__ int bsize[2][32], gsize[2][32];
+  __shared__ __align__(16) int s_occ[2][kCells + 4];
+  __shared__ int s_item[2], s_cnt[2], p_s0[2], p_cnt[2], s_next, s_mq[kMoverQueue], s_nmq;
+  __shared__ __align__(8) uint64_t full[2], empty[2], pfull[2];
+  const int nb = bk.count();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float qmax = res.qmax;
+  for (int k = threadIdx.x; k < T::NP / 4; k += blockDim.x) reinterpret_cast<int4*>(tiles)[k] = make_int4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    s_nmq = 0;
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], kSprPw);
+      mbar_init(&empty[s], kSprCw);
+      mbar_init(&pfull[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp < kSprPw) {
+    // ---------------- producers
+    const int pt = threadIdx.x;
+    auto pbar = [&]() { asm volatile("bar.sync 2, %0;" ::"n"(NP_T) : "memory"); };
+    // thread 0: bulk-copy brick b's positions / charges into prefetch buffer pb (16-byte granules)
+    auto prefetch = [&](int b, int pb) {
+      const int s0 = res.start[b], s1 = res.start[b + 1];
+      p_s0[pb] = s0;  // (producer-side: the consumers read s_cnt, set when the slot is theirs)
+      p_cnt[pb] = s1 - s0;
+      const uint32_t n = (uint32_t)(s1 > s0 ? s1 - s0 : 0);
+      const uint32_t pb0 = (uint32_t)((12ll * s0) & 15), pbytes = n ? (pb0 + 12u * n + 15u) & ~15u : 0u;
+      const uint32_t qb0 = (uint32_t)((4ll * s0) & 15), qbytes = n ? (qb0 + 4u * n + 15u) & ~15u : 0u;
+      mbar_arrive_expect_tx(&pfull[pb], pbytes + qbytes);
+      if (n) {
+        bulk_load_1d(pre_pos + pb * prep, reinterpret_cast<const char*>(res.pos) + 12ll * s0 - pb0, pbytes, &pfull[pb]);
+        bulk_load_1d(pre_q + pb * preq, reinterpret_cast<const char*>(res.q) + 4ll * s0 - qb0, qbytes, &pfull[pb]);
+      }
+    };
+    int b = blockIdx.x;
+    if (pt == 0 && b < nb) prefetch(b, 0);
+    for (int k = 0;; ++k) {
+      const int s = k & 1;
+      // claim the brick after this one and start its prefetch (its buffer was consumed at k - 1)
+      if (pt == 0) {
+        int bn = nb;
+        if (b < nb) bn = bk.sched ? (int)gridDim.x + atomicAdd(bk.sched + 32, 1) : (int)(blockIdx.x + (k + 1) * gridDim.x);
+        if (bn < nb) prefetch(bn, s ^ 1);
+        s_next = bn;
+      }
+      if (k >= 2) mbar_wait(&empty[s], ((k >> 1) - 1) & 1);
+      if (b >= nb) {
+        if (pt == 0) s_item[s] = -1;
+        pbar();
+        if (lane == 0) mbar_arrive(&full[s]);
+        break;
+      }
+      // clear the slot's histograms
+      for (int t = pt; t < (kCells + 4) / 4; t += NP_T) reinterpret_cast<int4*>(s_occ[s])[t] = make_int4(0, 0, 0, 0);
+      if (pt < 32) bsize[s][pt] = 0;
+      else if (pt < 64) gsize[s][pt - 32] = 0;
+      if (pt == 0) {
+        s_item[s] = b;
+        s_cnt[s] = p_cnt[s];
+      }
+      pbar();
+      const int bnext = s_next;
+      mbar_wait(&pfull[s], (k >> 1) & 1);
+      const int s0 = p_s0[s], cnt = p_cnt[s];
+      const float* pp = pre_pos + s * prep + ((12ll * s0) & 15) / 4;
+      const float* pq = pre_q + s * preq + ((4ll * s0) & 15) / 4;
+      float4* sr = s_r + s * 32 * bcap;
+      int* sc = s_c + s * 32 * bcap;
+      int occ_max = 0;
+#pragma unroll 2
+      for (int j = pt; j < cnt; j += NP_T) {
+        const int64_t i = (int64_t)s0 + j;
+        float4 r;
+        int lc, pk;
+        const int ab = atom_record_xyz<S, TAB>(pp[3 * j], pp[3 * j + 1], pp[3 * j + 2], pq[j], g, bk, n_points, r, lc, pk);
+        bool direct = ab != b;
+        int code = -1;
+        if (!direct) {
+          const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
+          const int bank = ((lz * D + ly) * TXB + lx + T::SH) & 31;
+          const int rk = atomicAdd(&bsize[s][bank], 1);
+          code = lc;
+          if (bk.gbs) {  // bank and rank in fieldforce's tile, for its staging
+            const int gb = ((lz * bk.gdy + ly) * bk.gtxb + lx + T::SH) & 31;
+            const int grk = atomicAdd(&gsize[s][gb], 1);
+            code |= (gb << kRecBankShift) | (grk << kRecRankShift);
+          }
+          if (rk < bcap) {
+            occ_max = max(occ_max, occ_count(s_occ[s], lc));
+            sr[rk * 32 + bank] = r;
+            sc[rk * 32 + bank] = lc;
+          } else {
+            direct = true;  // bucket full: the movers' path
+            code = bk.gbs ? (code | kRecHoleBit) : -1;
+          }
+        }
+        rec_out[i] = make_float4(r.x, r.y, r.z, __int_as_float(code));
+        if (direct) {
+          const int o = atomicAdd(res.novf, 1);
+          ovf_rec[o] = r;
+          ovf_cell[o] = pk;
+          ovf_perm[o] = (int)i;
+          const int slot = atomicAdd(&s_nmq, 1);
+          if (slot < kMoverQueue) s_mq[slot] = o;
+          else spread_direct_cold<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
+        }
+      }
+      occ_publish(&s_occ[s][kCells], occ_max);
+      pbar();
+      if (bk.gbs && warp == kSprPw - 1) bk.gbs[(int64_t)b * 32 + lane] = gsize[s][lane];
+      if (lane == 0) mbar_arrive(&full[s]);
+      b = bnext;
+    }
+    if (pt == 0 && bk.sched && atomicAdd(bk.sched + 33, 1) == (int)gridDim.x - 1) {
+      atomicExch(bk.sched + 32, 0);
+      atomicExch(bk.sched + 33, 0);
+    }
+  } else {
+    // ---------------- consumers
+    const int cw = warp - kSprPw, ct = threadIdx.x - NP_T;
+    auto cbar = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NC_T) : "memory"); };
+    for (int k = 0;; ++k) {
+      const int s = k & 1;
+      mbar_wait(&full[s], (k >> 1) & 1);
+      const int b = s_item[s];
+      if (b < 0) break;
+      const int cnt = s_cnt[s];
+      int* tile = tiles + s * T::NP;
+      float* ftile = reinterpret_cast<float*>(tile);
+      float inv_scale = 1.f;
+      if (cnt > 0) {
+        // int32 fixed point, power-of-two scale from the brick's largest cell occupancy (see k_spread_tma)
+        const int m = s_occ[s][kCells];
+        const float bound = qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f;
+        const int e_sum = ((__float_as_int(bound) >> 23) & 0xff) - 126;  // bound < 2^e_sum
+        const int sc = 31 - e_sum;
+        const float scale = __int_as_float((127 + sc) << 23);
+        inv_scale = __int_as_float((127 - sc) << 23) * inv_vcell;
+        int mine = bsize[s][lane];
+        mine = mine < bcap ? mine : bcap;
+        int rounds = mine;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+        constexpr double kMagic52 = 6755399441055744.0;  // 1.5 * 2^52
+        const float4* sr = s_r + s * 32 * bcap;
+        const int* scs = s_c + s * 32 * bcap;
+        for (int rr = cw; rr < rounds; rr += kSprCw) {
+          if (rr >= mine) continue;
+          const float4 r = sr[rr * 32 + lane];
+          const int cc = scs[rr * 32 + lane];
+          const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+          float wx[S], wy[S], wz[S], dd[S];
+          rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
+          rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
+          rows_f32<S, TAB, false>(r.z, ta, ta, wz, dd);
+          double dx[S];
+#pragma unroll
+          for (int c = 0; c < S; ++c) dx[c] = (double)wx[c];
+          const double qs = (double)r.w * (double)scale;
+#pragma unroll
+          for (int a = 0; a < S; ++a) {
+            const double qa = qs * (double)wz[a];
+#pragma unroll
+            for (int bb = 0; bb < S; ++bb) {
+              const double qab = qa * (double)wy[bb];
+              const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+#pragma unroll
+              for (int c = 0; c < S; ++c) atomicAdd(tile + row + c, __double2loint(fma(qab, dx[c], kMagic52)));
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // records, bucket sizes, occupancy of slot s are free
+      if (ct == 0) bulk_wait_read<0>();       // the other tile's reduce (previous brick) has read it
+      cbar();
+      if (cnt > 0)
+        for (int t = ct; t < T::NP / 4; t += NC_T) {
+          const int4 v = reinterpret_cast<const int4*>(tile)[t];
+          reinterpret_cast<float4*>(ftile)[t] =
+              make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
+        }
+      for (int t = ct; t < T::NP / 4; t += NC_T)
+        reinterpret_cast<int4*>(tiles + (s ^ 1) * T::NP)[t] = make_int4(0, 0, 0, 0);
+      fence_proxy_async_smem();
+      cbar();
+      if (ct == 0 && cnt > 0) {
+        const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+        tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H,
+                          bz * kBrick - lo + pd.H);
+        bulk_commit();
+      }
+    }
+    if (ct == 0) bulk_wait_read<0>();
+  }
+  // this CTA's movers (atoms outside their sorted brick, full buckets), one warp each
+  __syncthreads();
+  const int nwarp = kSprPw + kSprCw;
+  const int nmq = s_nmq < kMoverQueue ? s_nmq : kMoverQueue;
+  for (int m = warp; m < nmq; m += nwarp) {
+    const int o = s_mq[m];
+    spread_direct_warp<S, TAB>(ovf_rec[o], ovf_cell[o], pd, ta, inv_vcell, rho);
+  }
+  // atoms that overflowed their bucket at load: direct path, and on the list for fieldforce
+  for (int64_t i = res.start[nb] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < res.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 r;
+    int lc, pk;
+    atom_record<S, TAB>(res, i, g, bk, n_points, r, lc, pk);
+    spread_direct<S, TAB>(r, pk, pd, ta, inv_vcell, rho);
+    const int o = atomicAdd(res.novf, 1);
+    ovf_rec[o] = r;
+    ovf_cell[o] = pk;
+    ovf_perm[o] = (int)i;
+  }
+}
+#endif
+
 #ifdef PPPM_AB_VARIANTS  // A/B variant (measured slower)
 // make_rho, warp-specialized: warp 0 stages brick i+1 (two-pass bank-bucketed
 // counting sort of its slots into one of two stage slots) and finishes brick
@@ -850,7 +1103,28 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         (void)F_;
 #endif
         constexpr int NT = kSpreadThreads;
-        static const bool pipelined = !getenv("PPPM_B200_SPREAD_RES") || atoi(getenv("PPPM_B200_SPREAD_RES")) != 0;
+        static const int res_mode = getenv("PPPM_B200_SPREAD_RES") ? atoi(getenv("PPPM_B200_SPREAD_RES")) : 1;
+        const bool pipelined = res_mode != 0;
+#ifdef PPPM_AB_VARIANTS
+        if (res.pos && FIX && res_mode == 2 && kSpreadPair == 1) {
+          // warp-specialized resident make_rho (two stage slots, two prefetch buffers)
+          auto kw = k_spread_wsr<S, TAB>;
+          constexpr int NTW = 32 * (kSprPw + kSprCw);
+          const int rcap = (res.scap + 31) / 32 * 32;
+          const int bmean = rcap / 32;
+          const int bcap = std::min(64, std::max(16, bmean + (int)(4.5f * sqrtf((float)bmean)) + 2));
+          const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) +
+                             2 * (size_t)bcap * 32 * (sizeof(float4) + sizeof(int)) +
+                             2 * sizeof(float) * ((3 * (size_t)rcap + 8 + 3) / 4 * 4 + ((size_t)rcap + 8 + 3) / 4 * 4);
+          const int grid = persistent_grid(kw, NTW, dyn, bk.count());
+          if (bk.count() >= 2 * grid) {
+            kw<<<grid, NTW, dyn, s>>>(g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell, ovf_perm, res, n_points,
+                                      rec_out, rcap, bcap);
+            if (ranked) *ranked = bk.gbs != nullptr;
+            return 0;
+          }
+        }
+#endif
         if (res.pos && FIX && pipelined && kSpreadPair == 1) {
           // software-pipelined resident make_rho: bucket capacity from the largest brick
           // (mean + ~4.5 sigma of its bank buckets; fuller buckets spill to the direct path)

@@ -199,6 +199,38 @@ __device__ __forceinline__ void particle_map_fast(double x, double h, double inv
   t = fmin(fmax(t, -0.5), kHalfBelow);
 }
 
+// particle_map for fp32-representable coordinates in fp32 arithmetic, nodes
+// still bit-exact: the candidate node comes from x * (1/h) rounded to fp32 (1/h
+// split into two floats); the offset t = fma(x, ih_hi, -node) + x * ih_lo is
+// one rounding of an exact product minus an integer plus a tiny correction,
+// good to ~1e-7 of a cell.  The candidate can only be wrong when the true u
+// lies within ~2e-5 of the rounding boundary, and then |t| shows it: inside
+// 1e-4 of the boundary the exact fp64 division (particle_map_1d) decides.
+template <int S>
+__device__ __forceinline__ void particle_map_f32(float x, float ih_hi, float ih_lo, double h, int& node, float& t) {
+  const float u = __fmul_rn(x, ih_hi);
+  float nd, tt;
+  bool near;
+  if (S & 1) {
+    nd = rintf(u);
+    tt = __fmaf_rn(x, ih_lo, __fmaf_rn(x, ih_hi, -nd));
+    near = fabsf(tt) > 0.5f - 1e-4f;
+  } else {
+    nd = floorf(u);
+    const float fr = __fmaf_rn(x, ih_lo, __fmaf_rn(x, ih_hi, -nd));
+    near = fr < 1e-4f || fr > 1.f - 1e-4f;
+    tt = fr - 0.5f;
+  }
+  if (near) {
+    double td;
+    particle_map_1d<S>((double)x, h, node, td);
+    t = (float)td;
+    return;
+  }
+  node = (int)nd;
+  t = tt;
+}
+
 // per-dimension weights for one coordinate, exact recurrence or table lookup
 template <typename P, int S, bool TAB, bool DERIV>
 __device__ __forceinline__ void weights_1d(double t, const typename P::T* __restrict__ ta,

@@ -573,6 +573,50 @@ def test_resident_direct_movers_and_overflow(pb, mode):
     ref.close()
 
 
+@pytest.mark.parametrize("order", [4, 5])
+def test_resident_map_on_cell_boundaries(pb, order):
+    """The resident make_rho maps positions itself in fp32 arithmetic with an exact
+    fp64 fallback near rounding boundaries (particle_map_f32): atoms placed on the
+    node-rounding boundaries of their order (half-cell points for odd, cell edges for
+    even orders), a few fp32 ulps either side, must land in the reference's cells -
+    one wrong node shifts a whole stencil and breaks the mesh at the 1e-2 level.
+    128^3 so that the pipelined kernel (several bricks per CTA) is the one running."""
+    from paper_1702_04250_b200 import scenarios
+
+    rng = np.random.default_rng(77)
+    dims, edge, n = (128, 128, 128), 96.0, 300000
+    lengths = np.array([edge, edge * 1.03125, edge * 0.96875])
+    h = lengths / np.array(dims)
+    cells = rng.integers(0, 128, (n, 3))
+    frac = np.where(order & 1, 0.5, 0.0)
+    pos = (cells + frac) * h
+    # two thirds of the coordinates sit on a boundary (+- 0..3 ulps), the rest anywhere
+    free = rng.random((n, 3)) < 1.0 / 3.0
+    pos = np.where(free, rng.uniform(0, 1, (n, 3)) * lengths, pos)
+    p32 = scenarios.round_to_f32(np.mod(pos, lengths), lengths)
+    for _ in range(3):
+        step = rng.integers(-1, 2, p32.shape)
+        p32 = np.where(step > 0, np.nextafter(p32, np.float32(np.inf)),
+                       np.where(step < 0, np.nextafter(p32, np.float32(-np.inf)), p32)).astype(np.float32)
+    p32 = scenarios.round_to_f32(np.mod(p32.astype(np.float64), lengths), lengths)
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    ctx = pb.PppmContext(dims, lengths, order=order, mode="ik", precision="mixed", alpha=0.3)
+    ctx.load_atoms(p32, q.astype(np.float32))
+    for _ in range(2):
+        ctx.step()
+    ctx.synchronize()
+    rho, forces = ctx.rho(), ctx.forces()
+    ctx.close()
+    pos64 = p32.astype(np.float64)
+    rho_ref = orc.map_charge(pos64, q, lengths, dims, order)
+    assert rel_rms(rho, rho_ref) <= MIXED_TOL
+    g = orc.influence_pme(dims, lengths, 0.3, order)
+    fields = orc.poisson_ik(rho_ref, g, orc.ik_vectors(dims, lengths))
+    sub = rng.choice(n, 4096, replace=False)
+    f_ref = orc.fieldforce_ik(fields, pos64[sub], q[sub], lengths, dims, order)
+    assert rel_rms(forces[sub], f_ref) <= MIXED_TOL
+
+
 @pytest.mark.parametrize("dims,order", [((64, 32, 16), 5), ((16, 128, 32), 3), ((128, 16, 64), 7),
                                         ((32, 32, 256), 4), ((48, 64, 32), 5)])
 def test_mixed_fused_poisson_shapes(pb, dims, order):
