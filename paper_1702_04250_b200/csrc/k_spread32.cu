@@ -4,6 +4,7 @@
 // halo-padded mesh with one TMA reduce-add, then the halo folded back.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "k_fp32.cuh"
 #include "tma.cuh"
@@ -16,6 +17,9 @@ namespace pppm {
 constexpr int kSpreadThreads = PPPM_SPREAD_THREADS;
 #ifndef PPPM_SPREAD_MINB
 #define PPPM_SPREAD_MINB 4
+#endif
+#ifndef PPPM_SPREAD_THREADS2
+#define PPPM_SPREAD_THREADS2 320  // CTA size of the two-brick resident make_rho (three CTAs per SM)
 #endif
 
 // overflow atoms (full buckets): straight into the padded interior
@@ -426,26 +430,29 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
 // Item k + 1 is mapped in the same barrier interval in which item k's tile is
 // converted, so an item costs two CTA barriers (k_spread_tma: six) and no
 // exposed global-memory latency.
-template <int S, bool TAB, int NT>
-__global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPREAD_MINB)) k_spread_res(
+template <int S, bool TAB, int NT, int KX>
+__global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPREAD_MINB))) k_spread_res(
     Geom g, Bricks bk, Pad pd, const float* __restrict__ ta, float inv_vcell, float* __restrict__ rho,
     const __grid_constant__ CUtensorMap rmap, float4* __restrict__ ovf_rec, int* __restrict__ ovf_cell,
     int* __restrict__ ovf_perm, Resident res, int n_points, float4* __restrict__ rec_out, int cap, int bcap) {
   using T = TmaTile<S>;
-  constexpr int D = T::D, TXB = T::TXB, lo = Stencil<S>::lo;
+  // KX x-adjacent bricks per work item (their atoms are one contiguous range): one tile of
+  // KX * 8 + S - 1 columns, one reduce-add, fuller bank rounds, half the barriers per atom
+  constexpr int D = T::D, TXB = KX == 1 ? T::TXB : (D + kBrick * (KX - 1) + T::SH + 3) / 4 * 4, lo = Stencil<S>::lo;
+  constexpr int NPX = KX == 1 ? T::NP : (TXB * D * D + 31) / 32 * 32;
   constexpr int kCells = kBrick * kBrick * kBrick;
-  constexpr int PER = kCapMax / NT;
+  constexpr int PER = (KX * kCapMax + NT - 1) / NT;
   extern __shared__ __align__(16) unsigned char dyn_raw[];
   int* tiles = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][NP]
-  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * T::NP);                                    // [bcap][32]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * NPX);                                    // [bcap][32]
   float* pre_pos = reinterpret_cast<float*>(s_r + 32 * bcap);                                     // 3 cap + 8
   float* pre_q = pre_pos + (3 * cap + 8 + 3) / 4 * 4;                                             // cap + 8
   int* s_c = reinterpret_cast<int*>(pre_q + (cap + 8 + 3) / 4 * 4);                               // [bcap][32]
-  __shared__ int bsize[2][32], gsize[2][32];
-  __shared__ __align__(16) int s_occ[2][kCells + 4];
-  __shared__ int s_item[2], s_s0[2], s_cnt[2], s_mq[kMoverQueue], s_nmq;
+  __shared__ int bsize[2][32], gsize[2][KX][32];
+  __shared__ __align__(16) int s_occ[2][KX * kCells + 4];
+  __shared__ int s_item[2], s_s0[2], s_cnt[2], s_cnt0[2], s_mq[kMoverQueue], s_nmq;
   __shared__ __align__(8) uint64_t pbar;
-  const int nb = bk.count();
+  const int nb = bk.count(), nitems = nb / KX;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = NT / 32;
   const float qmax = res.qmax;
 
@@ -459,9 +466,10 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
   // thread 0: bulk-copy brick b's positions / charges (16-byte granules around the range)
   // and publish its range (slot = the item's parity; read after the next barrier)
   auto prefetch = [&](int b, int slot) {
-    const int s0 = res.start[b], s1 = res.start[b + 1];
+    const int s0 = res.start[KX * b], s1 = res.start[KX * b + KX];
     s_s0[slot] = s0;
     s_cnt[slot] = s1 - s0;
+    s_cnt0[slot] = KX > 1 ? res.start[KX * b + 1] - s0 : s1 - s0;
     if (s1 <= s0) return;
     const uint32_t pb0 = (uint32_t)((12ll * s0) & 15), pbytes = (pb0 + 12u * (uint32_t)(s1 - s0) + 15u) & ~15u;
     const uint32_t qb0 = (uint32_t)((4ll * s0) & 15), qbytes = (qb0 + 4u * (uint32_t)(s1 - s0) + 15u) & ~15u;
@@ -471,7 +479,7 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
   };
   // map brick b's atoms (prefetched) into the bank buckets of parity p
   auto map_item = [&](int b, int p, uint32_t phase) {
-    const int s0 = s_s0[p], cnt = s_cnt[p];
+    const int s0 = s_s0[p], cnt = s_cnt[p], cnt0 = s_cnt0[p];
     if (cnt <= 0) return;
     mbar_wait(&pbar, phase);
     const float* pp = pre_pos + ((12ll * s0) & 15) / 4;
@@ -482,25 +490,26 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
       const int j = threadIdx.x + k * NT;
       if (j < cnt) {
         const int64_t i = (int64_t)s0 + j;
+        const int kt = (KX > 1 && j >= cnt0) ? 1 : 0;  // the atom's brick within the item
         float4 r;
         int lc, pk;
         const int ab = atom_record_xyz<S, TAB>(pp[3 * j], pp[3 * j + 1], pp[3 * j + 2], pq[j], g, bk, n_points, r, lc, pk);
-        bool direct = ab != b;
+        bool direct = ab != KX * b + kt;
         int code = -1;
         if (!direct) {
           const int lx = lc & (kBrick - 1), ly = (lc >> 3) & (kBrick - 1), lz = lc >> 6;
-          const int bank = ((lz * D + ly) * TXB + lx + T::SH) & 31;
+          const int bank = ((lz * D + ly) * TXB + lx + kBrick * kt + T::SH) & 31;
           const int rk = atomicAdd(&bsize[p][bank], 1);
           code = lc;
           if (bk.gbs) {  // bank and rank in fieldforce's tile, for its staging
             const int gb = ((lz * bk.gdy + ly) * bk.gtxb + lx + T::SH) & 31;
-            const int grk = atomicAdd(&gsize[p][gb], 1);
+            const int grk = atomicAdd(&gsize[p][kt][gb], 1);
             code |= (gb << kRecBankShift) | (grk << kRecRankShift);
           }
           if (rk < bcap) {
-            occ_max = max(occ_max, occ_count(s_occ[p], lc));
+            occ_max = max(occ_max, occ_count(s_occ[p], kt * kCells + lc));
             s_r[rk * 32 + bank] = r;
-            s_c[rk * 32 + bank] = lc;
+            s_c[rk * 32 + bank] = lc | (kt << 9);
           } else {
             direct = true;  // bucket full: the movers' path (make_rho here, fieldforce through the list)
             code = bk.gbs ? (code | kRecHoleBit) : -1;  // its fieldforce slot stays reserved
@@ -519,36 +528,36 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
         }
       }
     }
-    occ_publish(&s_occ[p][kCells], occ_max);
+    occ_publish(&s_occ[p][KX * kCells], occ_max);
   };
 
   // ---- prologue: buffers cleared, brick 0 prefetched; iteration -1 only maps it
-  for (int k = threadIdx.x; k < 2 * (kCells + 4); k += NT) (&s_occ[0][0])[k] = 0;
+  for (int k = threadIdx.x; k < 2 * (KX * kCells + 4); k += NT) (&s_occ[0][0])[k] = 0;
   if (threadIdx.x < 64) (&bsize[0][0])[threadIdx.x] = 0;
-  if (threadIdx.x >= 64 && threadIdx.x < 128) (&gsize[0][0])[threadIdx.x - 64] = 0;
+  for (int k = threadIdx.x; k < 2 * KX * 32; k += NT) (&gsize[0][0][0])[k] = 0;
   if (threadIdx.x == 0) {
     s_nmq = 0;
     mbar_init(&pbar, 1);
     fence_mbar_init();
     s_item[0] = blockIdx.x;
-    s_item[1] = nb;
+    s_item[1] = nitems;
     s_cnt[0] = s_cnt[1] = 0;
-    if ((int)blockIdx.x < nb) prefetch(blockIdx.x, 0);
+    if ((int)blockIdx.x < nitems) prefetch(blockIdx.x, 0);
   }
   __syncthreads();
   uint32_t nfetch = 0;  // prefetch phases consumed so far (uniform)
   for (int k = -1;; ++k) {
     const int p = k & 1;
     const int b = k < 0 ? -1 : s_item[p];
-    if (b >= nb) break;
+    if (b >= nitems) break;
     const int cnt = k < 0 ? 0 : s_cnt[p];
     const int nxt = s_item[p ^ 1];
-    int* tile = tiles + p * T::NP;
+    int* tile = tiles + p * NPX;
     float* ftile = reinterpret_cast<float*>(tile);
     float inv_scale = 1.f;
     if (cnt > 0) {
-      // int32 fixed point, power-of-two scale from the brick's largest cell occupancy (see k_spread_tma)
-      const int m = s_occ[p][kCells];
+      // int32 fixed point, power-of-two scale from the item's largest cell occupancy (see k_spread_tma)
+      const int m = s_occ[p][KX * kCells];
       const float bound = qmax > 0.f ? (float)(m > 0 ? m : 1) * qmax * WSum3<S>::v * 1.01f : 1.f;
       const int e_sum = ((__float_as_int(bound) >> 23) & 0xff) - 126;  // bound < 2^e_sum
       const int sc = 31 - e_sum;
@@ -564,7 +573,8 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
         if (rr >= mine) continue;
         const float4 r = s_r[rr * 32 + lane];
         const int cc = s_c[rr * 32 + lane];
-        const int lx = cc & (kBrick - 1), ly = (cc >> 3) & (kBrick - 1), lz = cc >> 6;
+        const int lx = (cc & (kBrick - 1)) + (KX > 1 ? (cc >> 9) * kBrick : 0), ly = (cc >> 3) & (kBrick - 1),
+                  lz = (cc >> 6) & (kBrick - 1);
         float wx[S], wy[S], wz[S], dd[S];
         rows_f32<S, TAB, false>(r.x, ta, ta, wx, dd);
         rows_f32<S, TAB, false>(r.y, ta, ta, wy, dd);
@@ -586,25 +596,25 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
         }
       }
     }
-    int n2 = nb;
+    int n2 = nitems;
     if (threadIdx.x == 0) {
       bulk_wait_read<0>();            // the other tile's reduce (previous item) has read it
-      if (nxt < nb) n2 = claim();     // the brick after next (its latency hides behind the barrier)
+      if (nxt < nitems) n2 = claim();     // the brick after next (its latency hides behind the barrier)
     }
     __syncthreads();
     // ---- item k: tile -> fp32; item k + 1: mapped; buffers of item k + 2 cleared
     if (cnt > 0)
-      for (int t = threadIdx.x; t < T::NP / 4; t += NT) {
+      for (int t = threadIdx.x; t < NPX / 4; t += NT) {
         const int4 v = reinterpret_cast<const int4*>(tile)[t];
         reinterpret_cast<float4*>(ftile)[t] =
             make_float4((float)v.x * inv_scale, (float)v.y * inv_scale, (float)v.z * inv_scale, (float)v.w * inv_scale);
       }
-    for (int t = threadIdx.x; t < T::NP / 4; t += NT)
-      reinterpret_cast<int4*>(tiles + (p ^ 1) * T::NP)[t] = make_int4(0, 0, 0, 0);
-    for (int t = threadIdx.x; t < (kCells + 4) / 4; t += NT) reinterpret_cast<int4*>(s_occ[p])[t] = make_int4(0, 0, 0, 0);
+    for (int t = threadIdx.x; t < NPX / 4; t += NT)
+      reinterpret_cast<int4*>(tiles + (p ^ 1) * NPX)[t] = make_int4(0, 0, 0, 0);
+    for (int t = threadIdx.x; t < (KX * kCells + 4) / 4; t += NT) reinterpret_cast<int4*>(s_occ[p])[t] = make_int4(0, 0, 0, 0);
     if (threadIdx.x < 32) bsize[p][threadIdx.x] = 0;
-    if (threadIdx.x >= 32 && threadIdx.x < 64) gsize[p][threadIdx.x - 32] = 0;
-    if (nxt < nb && s_cnt[p ^ 1] > 0) {
+    if (threadIdx.x >= 32 && threadIdx.x < 32 + 32 * KX) (&gsize[p][0][0])[threadIdx.x - 32] = 0;
+    if (nxt < nitems && s_cnt[p ^ 1] > 0) {
       map_item(nxt, p ^ 1, nfetch & 1);
       ++nfetch;
     }
@@ -613,15 +623,17 @@ __global__ void __launch_bounds__(NT, (S >= 7 ? PPPM_SPREAD_MINB - 1 : PPPM_SPRE
     __syncthreads();
     if (threadIdx.x == 0) {
       if (cnt > 0) {
-        const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+        const int b0 = KX * b;  // the item's first brick (bricks b0 .. b0 + KX - 1 are x-neighbours)
+        const int bx = b0 % bk.nbx, by = (b0 / bk.nbx) % bk.nby, bz = b0 / (bk.nbx * bk.nby);
         tma_reduce_add_3d(&rmap, tile, bx * kBrick - lo + pd.hx - T::SH, by * kBrick - lo + pd.H,
                           bz * kBrick - lo + pd.H);
         bulk_commit();
       }
-      if (n2 < nb) prefetch(n2, p);
+      if (n2 < nitems) prefetch(n2, p);
     }
     // the mapped brick's fieldforce bucket sizes (gsize[p ^ 1] is cleared after the next barrier)
-    if (bk.gbs && warp == 1 && nxt < nb) bk.gbs[(int64_t)nxt * 32 + lane] = gsize[p ^ 1][lane];
+    if (bk.gbs && warp >= 1 && warp <= KX && nxt < nitems)
+      bk.gbs[((int64_t)KX * nxt + (warp - 1)) * 32 + lane] = gsize[p ^ 1][warp - 1][lane];
   }
   if (threadIdx.x == 0) {
     bulk_wait_read<0>();
@@ -1076,7 +1088,7 @@ __global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, const Resident& res,
-                        int n_points, float4* rec_out, cudaStream_t s, bool* ranked) {
+                        int n_points, float4* rec_out, cudaStream_t s, bool* ranked, const CUtensorMap* rmap2) {
   if (ranked) *ranked = false;
   if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
@@ -1126,23 +1138,36 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         }
 #endif
         if (res.pos && FIX && pipelined && kSpreadPair == 1) {
-          // software-pipelined resident make_rho: bucket capacity from the largest brick
+          // software-pipelined resident make_rho: bucket capacity from the largest item
           // (mean + ~4.5 sigma of its bank buckets; fuller buckets spill to the direct path)
-          auto kr = k_spread_res<S, TAB, NT>;
-          const int rcap = (res.scap + 31) / 32 * 32;
-          const int bmean = rcap / 32;
-          const int bcap = std::min(64, std::max(16, bmean + (int)(4.5f * sqrtf((float)bmean)) + 2));
-          const size_t dyn = 128 + 2 * (size_t)TmaTile<S>::NP * sizeof(int) + (size_t)bcap * 32 * (sizeof(float4) + sizeof(int)) +
-                             sizeof(float) * ((3 * (size_t)rcap + 8 + 3) / 4 * 4 + ((size_t)rcap + 8 + 3) / 4 * 4);
-          const int grid = persistent_grid(kr, NT, dyn, bk.count());
-          // worth it only when a CTA works through several bricks (config 4's 512 bricks are one
-          // per CTA: nothing to overlap, and the larger staging lowers the CTAs per SM)
-          if (bk.count() >= 2 * grid) {
-            kr<<<grid, NT, dyn, s>>>(g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell, ovf_perm, res, n_points,
-                                     rec_out, rcap, bcap);
+          static const int kx_env = getenv("PPPM_SPREAD_KX") ? atoi(getenv("PPPM_SPREAD_KX")) : 2;
+          const int rcap1 = (res.scap + 31) / 32 * 32;
+          auto launch_res = [&](auto KX_, const CUtensorMap& map) -> bool {
+            constexpr int KX = decltype(KX_)::value;
+            constexpr int NTX = KX == 1 ? NT : PPPM_SPREAD_THREADS2;
+            auto kr = k_spread_res<S, TAB, NTX, KX>;
+            const int rcap = KX * rcap1;
+            const int bmean = rcap / 32;
+            const int bcap = std::min(64, std::max(16, bmean + (int)(4.5f * sqrtf((float)bmean)) + 2));
+            constexpr int D = TmaTile<S>::D;
+            constexpr int TXB = KX == 1 ? TmaTile<S>::TXB : (D + kBrick * (KX - 1) + TmaTile<S>::SH + 3) / 4 * 4;
+            constexpr int NPX = KX == 1 ? TmaTile<S>::NP : (TXB * D * D + 31) / 32 * 32;
+            const size_t dyn = 128 + 2 * (size_t)NPX * sizeof(int) + (size_t)bcap * 32 * (sizeof(float4) + sizeof(int)) +
+                               sizeof(float) * ((3 * (size_t)rcap + 8 + 3) / 4 * 4 + ((size_t)rcap + 8 + 3) / 4 * 4);
+            const int items = bk.count() / KX;
+            const int grid = persistent_grid(kr, NTX, dyn, items);
+            // worth it only when a CTA works through several items (config 4's 512 bricks are one
+            // per CTA: nothing to overlap, and the larger staging lowers the CTAs per SM)
+            if (items < 2 * grid) return false;
+            kr<<<grid, NTX, dyn, s>>>(g, bk, pd, ta, inv_vcell, rho, map, ovf_rec, ovf_cell, ovf_perm, res, n_points,
+                                      rec_out, rcap, bcap);
             if (ranked) *ranked = bk.gbs != nullptr;
+            return true;
+          };
+          if (kx_env == 2 && rmap2 && bk.nbx % 2 == 0 && 2 * rcap1 <= kCapMax * 2 &&
+              launch_res(std::integral_constant<int, 2>{}, *rmap2))
             return 0;
-          }
+          if (launch_res(std::integral_constant<int, 1>{}, rmap)) return 0;
         }
         auto k = res.pos ? k_spread_tma<S, TAB, FIX, NT, true> : k_spread_tma<S, TAB, FIX, NT, false>;
         // resident: kSpreadPair tiles per buffer, staging sized for a work item

@@ -122,6 +122,7 @@ struct pppm_ctx {
   int64_t M = 0, half = 0, Ml = 0;  // global mesh, spectrum held here, local (slab) mesh
   Pad pd{};                          // fp32: halo-padded meshes; fp64: H = 0 (dense)
   CUtensorMap rho_map{}, field_map{};  // TMA descriptors of the padded fp32 meshes
+  CUtensorMap rho_map2{};              // rho boxes of two x-adjacent bricks (resident make_rho work items)
   int nxh = 0;
   cudaStream_t stream = nullptr;
   cufftHandle fwd = 0, bwd = 0;
@@ -407,6 +408,11 @@ static int encode_maps(pppm_ctx* c) {
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (rho) failed");
+    cuuint32_t box2[3] = {(cuuint32_t)((D + kBrick + sh + 3) / 4 * 4), (cuuint32_t)D, (cuuint32_t)D};
+    r = fn(&c->rho_map2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->rho.p, dims, strides, box2, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (rho, two bricks) failed");
   }
   {
     cuuint64_t dims[4] = {(cuuint64_t)c->pd.px, (cuuint64_t)c->pd.py, (cuuint64_t)c->pd.pz,
@@ -558,7 +564,7 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(),
                             c->ovf_perm.as<int>(), c->g, bks, c->pd, c->rho_map, c->tab.as<float>(),
                             c->rho.as<float>(), resident ? resident_of(c) : Resident{}, c->n_points,
-                            c->rec.as<float4>(), c->stream, &c->rec_ranked));
+                            c->rec.as<float4>(), c->stream, &c->rec_ranked, &c->rho_map2));
     c->launches += 1 + fold_launches(c->g, c->pd);  // spread + halo fold
   }
   c->have_rho = true;
