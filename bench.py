@@ -178,7 +178,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-KERNEL_NAMES = {"spread": "k_spread_tma", "gather": "k_gather_tma", "bin": "k_bin_fixed"}
+KERNEL_NAMES = {"spread": "k_spread_res", "gather": "k_gather_tma", "bin": "k_bin_fixed"}
 
 
 def kernel_name(kernel, mode):

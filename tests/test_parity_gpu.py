@@ -573,6 +573,44 @@ def test_resident_direct_movers_and_overflow(pb, mode):
     ref.close()
 
 
+@pytest.mark.parametrize("mode", ["ik", "ad"])
+def test_resident_pipelined_movers_holes_overflow(pb, mode):
+    """The pipelined resident make_rho (several bricks per CTA: 128 x 128 x 64 mesh) and
+    the ranked record hand-off to fieldforce, on their rare paths: a cell so full that
+    its bank bucket overflows (atoms take the direct path, their fieldforce slots stay
+    reserved as holes), a brick so full that it overflows at load, and atoms moved
+    across bricks with update_positions - against the one-shot binned path."""
+    from paper_1702_04250_b200 import scenarios
+
+    rng = np.random.default_rng(33)
+    dims, n = (128, 128, 64), 500000
+    lengths = np.array([192.0, 192.0, 96.0])
+    pos, q, _ = scenarios.random_gas(n, 11, 192.0)
+    pos[:, 2] *= 0.5
+    pos[:300] = np.array([50.2, 60.3, 40.4]) + rng.uniform(0, 0.8, (300, 3))       # one cell: one bank bucket
+    pos[300:3300] = np.array([120.0, 30.0, 20.0]) + rng.uniform(0, 6.0, (3000, 3))  # bricks beyond the slot capacity
+    p32 = scenarios.round_to_f32(np.mod(pos, lengths), lengths)
+    q32 = q.astype(np.float32)
+    ctx = pb.PppmContext(dims, lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
+    ref = pb.PppmContext(dims, lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
+    ctx.load_atoms(p32, q32)
+    for trial in range(3):
+        for _ in range(2):  # eager, then graph replay
+            ctx.step()
+        ctx.synchronize()
+        f, e = ctx.forces(), ctx.energy()
+        fr, er = ref.compute(p32, q32)
+        assert rel_rms(f, fr) <= 3e-6
+        assert abs(e - er) <= 3e-6 * abs(er)
+        # ~1 cell rms displacement: a good fraction of the atoms leaves its brick
+        p32 = scenarios.round_to_f32(np.mod(p32.astype(np.float64) + rng.uniform(-1.5, 1.5, p32.shape), lengths),
+                                     lengths)
+        ctx.set_resort(1.0)  # keep the movers on the direct path (no automatic re-sort)
+        ctx.update_positions(p32)
+    ctx.close()
+    ref.close()
+
+
 @pytest.mark.parametrize("order", [4, 5])
 def test_resident_map_on_cell_boundaries(pb, order):
     """The resident make_rho maps positions itself in fp32 arithmetic with an exact

@@ -24,7 +24,7 @@ B="--config 5 --steps 2 --warmup 2 --no-e2e --no-cpu-baseline --no-extra --no-co
 timeout 300 python bench.py $B > /dev/null 2>&1 && \
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv \
   --log-file gpurun_out/launches_${T}_config5.csv python bench.py $B > gpurun_out/ncu_launch5.log 2>&1; echo "launches5=$?"
-for k in k_gather_ws k_spread_tma k_zfft_green k_plane_c2r; do
+for k in k_gather_ws k_spread_res k_zfft_green k_plane_c2r; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/${T}_full_$k \
     python bench.py $A > gpurun_out/ncu_$k.log 2>&1; echo "ncu $k=$?"
 done
