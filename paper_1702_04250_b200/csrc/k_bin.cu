@@ -157,11 +157,14 @@ __global__ void k_update_resident(const TIn* __restrict__ pos, const int* __rest
       // they were sorted into take make_rho's / fieldforce's direct path;
       // their count drives the automatic re-sort (atoms that overflowed their
       // bucket at the sort, brick -1, are on the direct path anyway)
+      // (fp32 arithmetic with the exact division as the fallback near node-rounding
+      // boundaries: particle_map_f32, the same nodes as particle_map_1d)
       int n0, n1, n2;
-      double t;
-      particle_map_1d<S>((double)x, g.hx, n0, t);
-      particle_map_1d<S>((double)y, g.hy, n1, t);
-      particle_map_1d<S>((double)z, g.hz, n2, t);
+      float t;
+      const float hxh = (float)g.ihx, hyh = (float)g.ihy, hzh = (float)g.ihz;
+      particle_map_f32<S>(x, hxh, (float)(g.ihx - (double)hxh), g.hx, n0, t);
+      particle_map_f32<S>(y, hyh, (float)(g.ihy - (double)hyh), g.hy, n1, t);
+      particle_map_f32<S>(z, hzh, (float)(g.ihz - (double)hzh), g.hz, n2, t);
       n0 = n0 >= g.nx ? n0 - g.nx : n0;
       n1 = n1 >= g.ny ? n1 - g.ny : n1;
       n2 = n2 >= g.nz ? n2 - g.nz : n2;
