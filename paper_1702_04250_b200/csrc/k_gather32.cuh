@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
             const int code = __float_as_int(r[u].w);
             if (code < 0) continue;  // left the brick: overflow list
             const int dst = bstart[s][(code >> kRecBankShift) & 31] + ((code >> kRecRankShift) & kRecRankMask);
+            PPPM_CHECK(dst >= 0 && dst < cap && dst < cnt);  // make_rho's ranks fill [0, atoms that stayed)
             sr[dst] = make_float4(r[u].x, r[u].y, r[u].z, qq[u]);
             // hole: reserved slot, atom on the list
             sc[dst] = (code & kRecHoleBit) ? -1 : ((code & kRecCellMask) | ((j0 + u * 32 * NPW + pt) << 9));
@@ -663,6 +664,7 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
         if (rr >= tot) continue;
         const int f = MODE == 0 ? (rr >= seg0) + (rr >= e1) : 0;
         const int j = (f == 0 ? st0 : (f == 1 ? st1 : st2)) + rr;
+        PPPM_CHECK(j >= 0 && j < cap);
         const float4 r = sr[j];
         const int cc = sc[j];
         if (cc < 0) continue;  // hole (ranked records): the atom is on the overflow list

@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB -
     s_s0[slot] = s0;
     s_cnt[slot] = s1 - s0;
     s_cnt0[slot] = KX > 1 ? res.start[KX * b + 1] - s0 : s1 - s0;
+    PPPM_CHECK(s1 - s0 <= cap && s1 - s0 <= PER * NT);  // prefetch buffers / mapping passes hold the item
     if (s1 <= s0) return;
     const uint32_t pb0 = (uint32_t)((12ll * s0) & 15), pbytes = (pb0 + 12u * (uint32_t)(s1 - s0) + 15u) & ~15u;
     const uint32_t qb0 = (uint32_t)((4ll * s0) & 15), qbytes = (qb0 + 4u * (uint32_t)(s1 - s0) + 15u) & ~15u;
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB -
             code |= (gb << kRecBankShift) | (grk << kRecRankShift);
           }
           if (rk < bcap) {
+            PPPM_CHECK(rk >= 0 && bank >= 0 && bank < 32 && lc >= 0 && lc < kCells);
             occ_max = max(occ_max, occ_count(s_occ[p], kt * kCells + lc));
             s_r[rk * 32 + bank] = r;
             s_c[rk * 32 + bank] = lc | (kt << 9);
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB -
         rec_out[i] = make_float4(r.x, r.y, r.z, __int_as_float(code));
         if (direct) {
           const int o = atomicAdd(res.novf, 1);
+          PPPM_CHECK(o >= 0 && o < res.n);
           ovf_rec[o] = r;
           ovf_cell[o] = pk;
           ovf_perm[o] = (int)i;
@@ -590,6 +593,7 @@ __global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB -
           for (int bb = 0; bb < S; ++bb) {
             const double qab = qa * (double)wy[bb];
             const int row = ((lz + a) * D + (ly + bb)) * TXB + lx + T::SH;
+            PPPM_CHECK(row >= 0 && row + S <= NPX);
 #pragma unroll
             for (int c = 0; c < S; ++c) atomicAdd(tile + row + c, __double2loint(fma(qab, dx[c], kMagic52)));
           }

@@ -20,6 +20,22 @@
 namespace pppm {
 
 constexpr int kMaxOrder = 7;
+// -DPPPM_BOUNDS_CHECK builds (tools/build_variant.py): index / capacity assertions in the
+// shared-memory staging of the mapping kernels (compute-sanitizer is not available on the GPU
+// pool); a failed check prints its location and traps
+#ifdef PPPM_BOUNDS_CHECK
+#include <cstdio>
+#define PPPM_CHECK(cond)                                                         \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      printf("pppm bounds check failed: %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define PPPM_CHECK(cond) ((void)0)
+#endif
+
 constexpr double kHalfBelow = 0.49999999999999994;  // nextafter(0.5, 0)
 
 // ---------------------------------------------------------------------------
