@@ -719,7 +719,14 @@ def main():
                                f"{mode}, {cfg.precision}", "n_atoms_per_gpu": n, "mesh": list(cfg.dims),
                    "order": cfg.order, "mode": mode, "precision": cfg.precision,
                    "l2": "flushed before every step (256 MiB memset, outside the phase intervals)",
-                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "determinism": ("fp64: bitwise run to run (64-bit fixed-point make_rho, fixed-order sums)"
+                                   if not fp32 else
+                                   "mixed: run-to-run differences ~1e-7 relative (fp32 TMA reduce-adds of brick "
+                                   "tiles meet in halo cells in no fixed order); parity bar 1e-5"),
+                   **({"parity_note": "orders 4 and 6 are an extension (the reference accepts 3, 5, 7 only): "
+                                      "parity unpinned by the reference, checked against the oracle's own extension"}
+                      if cfg.order in (4, 6) else {})},
         "phases_ms_per_step": {kk: v / k for kk, v in ms.items()},
         "whole_step_atom_steps_per_s": atoms_total * k / t_step_max,
         "kernels": per_kernel, "roofline": roofline, "onchip_roofline": onchip, "clocks": clocks,

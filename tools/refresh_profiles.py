@@ -70,9 +70,13 @@ for d in lines:
     s.append(f"| {c['workload'].replace(' point charges per GPU', '')} | {d['value']:.3g} | "
              f"{d['whole_step_atom_steps_per_s']:.3g} | {ph['bin'] * 1e3:.1f} | {ph['spread'] * 1e3:.1f} | "
              f"{ph['poisson'] * 1e3:.1f} | {ph['gather'] * 1e3:.1f} |")
-s += ["", "All orders run the split (per-component) warp-specialized fieldforce_ik (orders 6-7 with 20-wide field boxes).",
-      "Power-of-two meshes run the fused Poisson (plane FFT kernels for nx, ny ≤ 128, the z kernel; cuFFT 2D planes at",
-      "256²); config 2 (40³) the 3D cuFFT path.", "",
+s += ["", "Orders 4 and 6 are an extension (the reference accepts 3, 5 and 7 only): their parity is **unpinned by the reference**,",
+      "checked against the oracle's own extension and the spline invariants. Mixed precision is not bitwise run-to-run",
+      "(~1e-7 relative: unordered fp32 reduce-adds in halo cells); fp64 is.",
+      "", "All orders run the split (per-component) warp-specialized fieldforce_ik (orders 6-7 with 20-wide field boxes).",
+      "Power-of-two meshes run the fused Poisson (plane FFT kernels for nx, ny ≤ 256 and the z kernel); config 2 (40³)",
+      "the 3D cuFFT path. Configs 3 and 5 run the pipelined two-brick make_rho (`k_spread_res`) with ranked records for",
+      "fieldforce; config 4 (512 bricks, about one per CTA) the per-brick `k_spread_tma`.", "",
       "# Force driver either side of the mesh path (SURVEY §8f)", "",
       "`python tools/bench_md.py --config C --precision P` (B200) and `--reference` (the reference's own `pppm.compute_forces`,",
       "one CPU worker, run in the build container — the reference cannot travel to the GPU box). compute_forces = cell list +",
