@@ -219,6 +219,149 @@ __global__ void __launch_bounds__(kThreads) k_spread_fix64(
   }
 }
 
+// fp64 make_rho on brick-ordered residents: the same 64-bit fixed-point
+// contributions as k_spread_fix64 (so the mesh is bitwise the same: integer
+// adds are associative), accumulated per brick in a shared (8 + S - 1)^3 tile
+// and added to the global mesh once per tile cell - S^3 shared instead of S^3
+// global 64-bit atomics per atom.  Shared 64-bit atomics are CAS loops on
+// sm_100a, so a tile cell is three 32-bit limbs of 21 + 21 + 22 bits (two's
+// complement split of the contribution, each limb summed with a native 32-bit
+// shared atomic: a brick deposits at most `cap` <= 1024 contributions per
+// cell, so no limb sum overflows).  Atoms that moved out of the brick they
+// were sorted into, and those that overflowed their bucket at load, keep the
+// direct global path.
+template <int S, bool TAB, typename TIn>
+__device__ __forceinline__ void fix64_atom(const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t i,
+                                           const Geom& g, const double* __restrict__ ta, int n_points, double scale,
+                                           int* __restrict__ err, int& n0, int& n1, int& n2, double& q,
+                                           double (&wx)[S], double (&wy)[S], double (&wz)[S], bool& ok) {
+  const double x = load_pos<TIn, false>(pos, 3 * i + 0, g.lx);
+  const double y = load_pos<TIn, false>(pos, 3 * i + 1, g.ly);
+  const double z = load_pos<TIn, false>(pos, 3 * i + 2, g.lz);
+  q = load_real<TIn, false>(qv, i);
+  ok = !(outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz));
+  if (!ok) {
+    atomicOr(err, 1);
+    return;
+  }
+  double tx, ty, tz, dd[S];
+  particle_map_1d<S>(x, g.hx, n0, tx);
+  particle_map_1d<S>(y, g.hy, n1, ty);
+  particle_map_1d<S>(z, g.hz, n2, tz);
+  weights_1d<ExactF64, S, TAB, false>(tx, ta, ta, n_points, wx, dd);
+  weights_1d<ExactF64, S, TAB, false>(ty, ta, ta, n_points, wy, dd);
+  weights_1d<ExactF64, S, TAB, false>(tz, ta, ta, n_points, wz, dd);
+}
+
+// the fixed-point value of one contribution, exactly as k_spread_fix64<MAGIC> forms it
+__device__ __forceinline__ long long fix64_value(double qab, double w, double scale) {
+  const double contrib = __dmul_rn(qab, w);
+  return __double_as_longlong(__fma_rn(contrib, scale, 6755399441055744.0)) - __double_as_longlong(6755399441055744.0);
+}
+
+template <int S, bool TAB, typename TIn>
+__global__ void __launch_bounds__(kThreads, 3) k_spread_fix64_tile(
+    const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk,
+    const int* __restrict__ bstart, const double* __restrict__ ta, int n_points, const double* __restrict__ scale_p,
+    unsigned long long* __restrict__ acc, int* __restrict__ err) {
+  constexpr int lo = Stencil<S>::lo, D = kBrick + S - 1, N = D * D * D;
+  extern __shared__ unsigned tile64[];  // [3][N] limbs
+  unsigned* l0 = tile64;
+  unsigned* l1 = tile64 + N;
+  int* l2 = reinterpret_cast<int*>(tile64 + 2 * N);
+  const double scale = *scale_p;
+  const int nb = bk.count();
+  // an atom straight into the global mesh (k_spread_fix64's inner loops)
+  auto direct = [&](int n0, int n1, int n2, double q, const double (&wx)[S], const double (&wy)[S],
+                    const double (&wz)[S]) {
+    int ix[S];
+#pragma unroll
+    for (int c = 0; c < S; ++c) ix[c] = wrap_index(n0 - lo + c, g.nx);
+#pragma unroll 1
+    for (int a = 0; a < S; ++a) {
+      const int iz = wrap_index(n2 - lo + a, g.nz);
+      const double qa = __dmul_rn(q, wz[a]);
+#pragma unroll 1
+      for (int b = 0; b < S; ++b) {
+        const int iy = wrap_index(n1 - lo + b, g.ny);
+        const double qab = __dmul_rn(qa, wy[b]);
+        unsigned long long* row = acc + ((int64_t)iz * g.ny + iy) * g.nx;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+          const long long f = fix64_value(qab, wx[c], scale);
+          if (f != 0) atomicAdd(row + ix[c], (unsigned long long)f);
+        }
+      }
+    }
+  };
+  for (int k = threadIdx.x; k < 3 * N; k += blockDim.x) tile64[k] = 0u;
+  __syncthreads();
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int s0 = bstart[b], cnt = bstart[b + 1] - s0;
+    if (cnt <= 0) continue;
+    const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+      int n0, n1, n2;
+      double q, wx[S], wy[S], wz[S];
+      bool ok;
+      fix64_atom<S, TAB, TIn>(pos, qv, (int64_t)s0 + j, g, ta, n_points, scale, err, n0, n1, n2, q, wx, wy, wz, ok);
+      if (!ok) continue;
+      n0 = n0 >= g.nx ? n0 - g.nx : n0;
+      n1 = n1 >= g.ny ? n1 - g.ny : n1;
+      n2 = n2 >= g.nz ? n2 - g.nz : n2;
+      const int lx = n0 - bx * kBrick, ly = n1 - by * kBrick, lz = n2 - bz * kBrick;
+      if ((unsigned)lx >= (unsigned)kBrick || (unsigned)ly >= (unsigned)kBrick || (unsigned)lz >= (unsigned)kBrick) {
+        direct(n0, n1, n2, q, wx, wy, wz);  // left the brick it was sorted into
+        continue;
+      }
+#pragma unroll 1
+      for (int a = 0; a < S; ++a) {
+        const double qa = __dmul_rn(q, wz[a]);
+#pragma unroll
+        for (int bb = 0; bb < S; ++bb) {
+          const double qab = __dmul_rn(qa, wy[bb]);
+          const int row = ((lz + a) * D + (ly + bb)) * D + lx;
+#pragma unroll
+          for (int c = 0; c < S; ++c) {
+            const long long f = fix64_value(qab, wx[c], scale);
+            if (f != 0) {
+              atomicAdd(l0 + row + c, (unsigned)f & 0x1fffffu);
+              atomicAdd(l1 + row + c, (unsigned)(f >> 21) & 0x1fffffu);
+              atomicAdd(l2 + row + c, (int)(f >> 42));
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // tile -> global mesh (periodic wrap), limbs cleared for the next brick
+    for (int t = threadIdx.x; t < N; t += blockDim.x) {
+      const unsigned a0 = l0[t], a1 = l1[t];
+      const int a2 = l2[t];
+      if (a0 | a1 | (unsigned)a2) {
+        l0[t] = 0u;
+        l1[t] = 0u;
+        l2[t] = 0;
+        const long long v = (long long)a2 * (1ll << 42) + ((long long)a1 << 21) + (long long)a0;
+        const int tx = t % D, ty = (t / D) % D, tz = t / (D * D);
+        const int ix = wrap_index(bx * kBrick - lo + tx, g.nx), iy = wrap_index(by * kBrick - lo + ty, g.ny),
+                  iz = wrap_index(bz * kBrick - lo + tz, g.nz);
+        if (v != 0) atomicAdd(acc + ((int64_t)iz * g.ny + iy) * g.nx + ix, (unsigned long long)v);
+      }
+    }
+    __syncthreads();
+  }
+  // atoms beyond the bricks' slots (bucket overflow at load): direct path
+  for (int64_t i = bstart[nb] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int n0, n1, n2;
+    double q, wx[S], wy[S], wz[S];
+    bool ok;
+    fix64_atom<S, TAB, TIn>(pos, qv, i, g, ta, n_points, scale, err, n0, n1, n2, q, wx, wy, wz, ok);
+    if (ok) direct(n0, n1, n2, q, wx, wy, wz);
+  }
+}
+
 // rho = (fixed * 2^-s) / Vcell   (gridmap.py:209-210 divides by hx*hy*hz)
 template <typename TOut>
 __global__ void k_fix64_to_real(const unsigned long long* __restrict__ acc, int64_t m,
@@ -527,7 +670,8 @@ int launch_weight_rows(int order, const double* t, int64_t n, double* assign, do
 
 // scal: [0] energy, [1] scale, [2] inv_scale, [4] qmax bits
 int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, const double* ta, int n_points,
-                        double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s) {
+                        double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s,
+                        const Bricks* bk, const int* bstart) {
   const int grid = grid_for(a.n);
   const int64_t M = (int64_t)g.nx * g.ny * g.nz;
   unsigned long long* qmax = reinterpret_cast<unsigned long long*>(scal + 4);
@@ -540,6 +684,24 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
     constexpr int S = decltype(S_)::value;
     return with_bool(tab, [&](auto T_) -> int {
       constexpr bool TAB = decltype(T_)::value;
+      // brick-ordered residents (bstart), enough of them for the magic-number rounding: per-brick
+      // shared tiles (the same mesh, bitwise)
+      if (bk && bstart && a.n >= 2048) {
+        constexpr int D = kBrick + S - 1;
+        const size_t dyn = 3 * (size_t)D * D * D * sizeof(unsigned);
+        if (!a.f32) {
+          auto k = k_spread_fix64_tile<S, TAB, double>;
+          const int tg = persistent_grid(k, kThreads, dyn, bk->count());
+          k<<<tg, kThreads, dyn, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, *bk, bstart, ta, n_points,
+                                      scal + 1, acc, err);
+        } else {
+          auto k = k_spread_fix64_tile<S, TAB, float>;
+          const int tg = persistent_grid(k, kThreads, dyn, bk->count());
+          k<<<tg, kThreads, dyn, s>>>((const float*)a.pos, (const float*)a.q, a.n, g, *bk, bstart, ta, n_points,
+                                      scal + 1, acc, err);
+        }
+        return 0;
+      }
       return with_bool(a.n >= 2048, [&](auto M_) -> int {
         constexpr bool MAGIC = decltype(M_)::value;
         if (!a.f32)

@@ -155,6 +155,7 @@ struct pppm_ctx {
   bool novf_clean = false;  // the resident mover counter is zero (cleared by the last fieldforce CTA)
   bool dyn_sched = true;
   bool rank_handoff = true;  // PPPM_B200_RANKS=0: fieldforce staging sorts the records itself (A/B)
+  bool fix64_tiles = true;   // PPPM_B200_FIX64_TILES=0: fp64 make_rho with global atomics only (A/B)
   // resident step without a binning pass: make_rho maps the brick-ordered fp32
   // positions itself (Resident in pppm_types.h); bstart = per-brick ranges
   bool res_direct = true;
@@ -537,9 +538,12 @@ static int ensure_sched(pppm_ctx* c) {
 static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, bool resident = false) {
   const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
+    // brick-ordered residents: per-brick shared tiles (bitwise the same mesh as the direct kernel)
+    const bool tiles = c->fix64_tiles && c->res_sorted && pos == c->res_pos.p && !c->slab && c->bstart.p != nullptr;
     TRY(launch_spread_fix64(c->order, c->n_points > 0, a, c->g, c->tab.as<double>(), c->n_points,
                             c->scal.as<double>(), c->rho_fix.as<unsigned long long>(), c->rho.as<double>(),
-                            c->err.as<int>(), c->stream));
+                            c->err.as<int>(), c->stream, tiles ? &c->bk : nullptr,
+                            tiles ? c->bstart.as<int>() : nullptr));
     c->launches += 4;
   } else {
     if (!c->binned && !resident) return fail(PPPM_ERR_STATE, "atoms not binned");
@@ -1006,6 +1010,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RANKS")) c->rank_handoff = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_FIX64_TILES")) c->fix64_tiles = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RESORT")) c->resort_frac = atof(v);
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;

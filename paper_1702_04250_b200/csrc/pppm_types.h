@@ -113,7 +113,8 @@ int launch_particle_map(int order, bool r32, const AtomsIn& a, const Geom& g, in
 int launch_table_rows(int order, int n_points, double* assign, double* deriv, cudaStream_t s);
 int launch_weight_rows(int order, const double* t, int64_t n, double* assign, double* deriv, cudaStream_t s);
 int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, const double* ta, int n_points,
-                        double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s);
+                        double* scal, unsigned long long* acc, double* rho, int* err, cudaStream_t s,
+                        const Bricks* bk = nullptr, const int* bstart = nullptr);
 int launch_bin(int order, bool tab, const AtomsIn& a, const Geom& g, const Bricks& bk, int cap, int n_points,
                int* counts, float4* rec, int* rcell, int* perm, float4* ovf_rec, int* ovf_cell, int* ovf_perm,
                int* err, const int* orig, cudaStream_t s, int64_t ibase = 0, bool reset = true);

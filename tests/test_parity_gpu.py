@@ -573,6 +573,45 @@ def test_resident_direct_movers_and_overflow(pb, mode):
     ref.close()
 
 
+@pytest.mark.parametrize("order", [5, 7])
+def test_fp64_tile_make_rho_bitwise(pb, order, monkeypatch):
+    """fp64 make_rho on brick-ordered residents accumulates per-brick shared tiles of
+    three 32-bit limbs (k_spread_fix64_tile): the same 64-bit fixed-point contributions
+    as the direct kernel, so the mesh must be bitwise the same - with a brick that
+    overflows its bucket at load and after moving atoms across bricks - and match the
+    oracle at the fp64 bar."""
+    from paper_1702_04250_b200 import scenarios
+
+    rng = np.random.default_rng(8)
+    dims, n = (64, 64, 32), 120000
+    lengths = np.array([96.0, 96.0, 48.0])
+    pos = rng.uniform(0, 1, (n, 3)) * lengths
+    pos[:2500] = np.array([40.0, 50.0, 20.0]) + rng.uniform(0, 3.0, (2500, 3))
+    q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0) * rng.uniform(0.5, 1.5, n)
+    q -= q.mean()
+    moved = np.mod(pos + rng.uniform(-2.0, 2.0, pos.shape), lengths)
+    out = {}
+    for tiles in ("1", "0"):
+        monkeypatch.setenv("PPPM_B200_FIX64_TILES", tiles)
+        ctx = pb.PppmContext(dims, lengths, order=order, mode="ik", precision="fp64", alpha=0.3)
+        ctx.load_atoms(pos, q)
+        ctx.step()
+        ctx.synchronize()
+        r0 = ctx.rho().copy()
+        ctx.set_resort(1.0)
+        ctx.update_positions(moved)
+        for _ in range(2):
+            ctx.step()
+        ctx.synchronize()
+        out[tiles] = (r0, ctx.rho().copy(), ctx.forces().copy())
+        ctx.close()
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert np.array_equal(out["1"][2], out["0"][2])
+    rho_ref = orc.map_charge(moved, q, lengths, dims, order)
+    assert rel_rms(out["1"][1], rho_ref) <= 1e-11  # 64-bit fixed point with the global scale 2^(62 - log2(N max|q|))
+
+
 @pytest.mark.parametrize("mode", ["ik", "ad"])
 def test_resident_pipelined_movers_holes_overflow(pb, mode):
     """The pipelined resident make_rho (several bricks per CTA: 128 x 128 x 64 mesh) and
