@@ -622,6 +622,149 @@ __global__ void __launch_bounds__(kThreads) k_gather_direct(
   }
 }
 
+// fp64 fieldforce on brick-ordered residents: the brick's (8 + S - 1)^3 field
+// tile(s) are copied into shared memory (periodic wrap) and every atom of the
+// brick reads its stencil from there - the same values, the same FMAs in the
+// same order as k_gather_direct, so the forces are bitwise the same; atoms that
+// left their brick or overflowed their bucket at load read the global meshes.
+template <int S, int MODE, typename LD>
+__device__ __forceinline__ void gather_sums_f64(const double (&ax)[S], const double (&ay)[S], const double (&az)[S],
+                                                const double (&dx)[S], const double (&dy)[S], const double (&dz)[S],
+                                                LD ld, double& s0, double& s1, double& s2) {
+  s0 = 0.0;
+  s1 = 0.0;
+  s2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < S; ++a) {
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      if (MODE == 0) {
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+          const double w = ax[c];
+          e0 = fma(w, ld(0, a, b, c), e0);
+          e1 = fma(w, ld(1, a, b, c), e1);
+          e2 = fma(w, ld(2, a, b, c), e2);
+        }
+        r0 = fma(ay[b], e0, r0);
+        r1 = fma(ay[b], e1, r1);
+        r2 = fma(ay[b], e2, r2);
+      } else {
+        double pd = 0.0, pa = 0.0;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+          const double p = ld(0, a, b, c);
+          pd = fma(dx[c], p, pd);
+          pa = fma(ax[c], p, pa);
+        }
+        r0 = fma(ay[b], pd, r0);  // az ay dx
+        r1 = fma(dy[b], pa, r1);  // az dy ax
+        r2 = fma(ay[b], pa, r2);  // dz ay ax (dz applied below)
+      }
+    }
+    s0 = fma(az[a], r0, s0);
+    s1 = fma(az[a], r1, s1);
+    s2 = fma(MODE == 0 ? az[a] : dz[a], r2, s2);
+  }
+}
+
+// the rare path (atoms outside their brick's tile): stencil from the global meshes, out of line
+template <int S, int MODE>
+__device__ __noinline__ void gather_global_f64(int n0, int n1, int n2, int nx, int ny, int nz, const double (&ax)[S],
+                                               const double (&ay)[S], const double (&az)[S], const double (&dx)[S],
+                                               const double (&dy)[S], const double (&dz)[S],
+                                               const double* __restrict__ f0, const double* __restrict__ f1,
+                                               const double* __restrict__ f2, double& s0, double& s1, double& s2) {
+  constexpr int lo = Stencil<S>::lo;
+  int ix[S], iy[S], iz[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) {
+    ix[c] = wrap_index(n0 - lo + c, nx);
+    iy[c] = wrap_index(n1 - lo + c, ny);
+    iz[c] = wrap_index(n2 - lo + c, nz);
+  }
+  gather_sums_f64<S, MODE>(ax, ay, az, dx, dy, dz,
+                           [&](int f, int a, int b, int c) {
+                             const double* fl = f == 0 ? f0 : (f == 1 ? f1 : f2);
+                             return __ldg(fl + ((int64_t)iz[a] * ny + iy[b]) * nx + ix[c]);
+                           },
+                           s0, s1, s2);
+}
+
+template <int S, bool TAB, int MODE, typename TIn>
+__global__ void __launch_bounds__(kThreads, (S >= 6 ? 1 : 2)) k_gather_direct_tile(
+    const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk,
+    const int* __restrict__ bstart, const double* __restrict__ ta, const double* __restrict__ td, int n_points,
+    const double* __restrict__ f0, const double* __restrict__ f1, const double* __restrict__ f2, double cscale,
+    double* __restrict__ force, int* __restrict__ err) {
+  constexpr int lo = Stencil<S>::lo, D = kBrick + S - 1, N = D * D * D, F = MODE == 0 ? 3 : 1;
+  extern __shared__ double ftile[];  // [F][N]
+  const int nb = bk.count();
+  // one atom: the arithmetic of k_gather_direct; its stencil from the tile when the atom is in brick (bx, by, bz)
+  auto one = [&](int64_t i, bool tiled, int bx, int by, int bz) {
+    const double x = load_pos<TIn, false>(pos, 3 * i + 0, g.lx);
+    const double y = load_pos<TIn, false>(pos, 3 * i + 1, g.ly);
+    const double z = load_pos<TIn, false>(pos, 3 * i + 2, g.lz);
+    const double q = load_real<TIn, false>(qv, i);
+    if (outside(x, g.lx) || outside(y, g.ly) || outside(z, g.lz)) {
+      atomicOr(err, 1);
+      return;
+    }
+    int n0, n1, n2;
+    double tx, ty, tz;
+    particle_map_1d<S>(x, g.hx, n0, tx);
+    particle_map_1d<S>(y, g.hy, n1, ty);
+    particle_map_1d<S>(z, g.hz, n2, tz);
+    double ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
+    weights_1d<ExactF64, S, TAB, MODE == 1>(tx, ta, td, n_points, ax, dx);
+    weights_1d<ExactF64, S, TAB, MODE == 1>(ty, ta, td, n_points, ay, dy);
+    weights_1d<ExactF64, S, TAB, MODE == 1>(tz, ta, td, n_points, az, dz);
+    const int w0 = n0 >= g.nx ? n0 - g.nx : n0, w1 = n1 >= g.ny ? n1 - g.ny : n1, w2 = n2 >= g.nz ? n2 - g.nz : n2;
+    const int lx = w0 - bx * kBrick, ly = w1 - by * kBrick, lz = w2 - bz * kBrick;
+    double s0, s1, s2;
+    if (tiled && (unsigned)lx < (unsigned)kBrick && (unsigned)ly < (unsigned)kBrick && (unsigned)lz < (unsigned)kBrick) {
+      const double* corner = ftile + (lz * D + ly) * D + lx;
+      gather_sums_f64<S, MODE>(ax, ay, az, dx, dy, dz,
+                               [&](int f, int a, int b, int c) { return corner[f * N + (a * D + b) * D + c]; }, s0, s1,
+                               s2);
+    } else {
+      gather_global_f64<S, MODE>(n0, n1, n2, g.nx, g.ny, g.nz, ax, ay, az, dx, dy, dz, f0, f1, f2, s0, s1, s2);
+    }
+    const double sc = cscale * q;
+    if (MODE == 0) {
+      force[3 * i + 0] = sc * s0;
+      force[3 * i + 1] = sc * s1;
+      force[3 * i + 2] = sc * s2;
+    } else {
+      force[3 * i + 0] = -sc * s0 / g.hx;
+      force[3 * i + 1] = -sc * s1 / g.hy;
+      force[3 * i + 2] = -sc * s2 / g.hz;
+    }
+  };
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int s0 = bstart[b], cnt = bstart[b + 1] - s0;
+    if (cnt <= 0) continue;
+    const int bx = b % bk.nbx, by = (b / bk.nbx) % bk.nby, bz = b / (bk.nbx * bk.nby);
+    __syncthreads();  // the previous brick's atoms are done with the tile
+    for (int t = threadIdx.x; t < F * N; t += blockDim.x) {
+      const int f = t / N, r = t - f * N;
+      const int tx = r % D, ty = (r / D) % D, tz = r / (D * D);
+      const int ix = wrap_index(bx * kBrick - lo + tx, g.nx), iy = wrap_index(by * kBrick - lo + ty, g.ny),
+                iz = wrap_index(bz * kBrick - lo + tz, g.nz);
+      const double* fl = f == 0 ? f0 : (f == 1 ? f1 : f2);
+      ftile[t] = __ldg(fl + ((int64_t)iz * g.ny + iy) * g.nx + ix);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) one((int64_t)s0 + j, true, bx, by, bz);
+  }
+  // atoms beyond the bricks' slots (bucket overflow at load)
+  for (int64_t i = bstart[nb] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    one(i, false, 0, 0, 0);
+}
+
 // real-mesh conversions for the host boundary
 template <typename TA, typename TB>
 __global__ void k_convert(const TA* __restrict__ a, TB* __restrict__ b, int64_t n) {
@@ -722,7 +865,7 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
 
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* f, int64_t mesh, double cscale,
-                         double* force, int* err, cudaStream_t s) {
+                         double* force, int* err, cudaStream_t s, const Bricks* bk, const int* bstart) {
   const int grid = grid_for(a.n);
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
@@ -730,6 +873,22 @@ int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const 
       constexpr bool TAB = decltype(T_)::value;
       auto go = [&](auto MODE_) {
         constexpr int MODE = decltype(MODE_)::value;
+        if (bk && bstart) {  // brick-ordered residents: field tiles in shared memory (bitwise the same forces)
+          constexpr int D = kBrick + S - 1;
+          const size_t dyn = (MODE == 0 ? 3 : 1) * (size_t)D * D * D * sizeof(double);
+          if (!a.f32) {
+            auto k = k_gather_direct_tile<S, TAB, MODE, double>;
+            const int tg = persistent_grid(k, kThreads, dyn, bk->count());
+            k<<<tg, kThreads, dyn, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, *bk, bstart, ta, td, n_points,
+                                        f, f + mesh, f + 2 * mesh, cscale, force, err);
+          } else {
+            auto k = k_gather_direct_tile<S, TAB, MODE, float>;
+            const int tg = persistent_grid(k, kThreads, dyn, bk->count());
+            k<<<tg, kThreads, dyn, s>>>((const float*)a.pos, (const float*)a.q, a.n, g, *bk, bstart, ta, td, n_points,
+                                        f, f + mesh, f + 2 * mesh, cscale, force, err);
+          }
+          return;
+        }
         if (!a.f32)
           k_gather_direct<S, TAB, MODE, double, false><<<grid, kThreads, 0, s>>>(
               (const double*)a.pos, (const double*)a.q, a.n, g, ta, td, n_points, f, f + mesh, f + 2 * mesh,

@@ -700,8 +700,12 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
   if (c->fp64()) {
     const double* ta = c->tab.as<double>();
     const double* td = ta ? ta + (int64_t)c->n_points * kRowPad : nullptr;
+    // brick-ordered residents writing their own (brick-ordered) force array: field tiles in shared memory
+    const bool tiles = c->fix64_tiles && c->res_sorted && pos == c->res_pos.p && out == c->res_force.p && !c->slab &&
+                       c->bstart.p != nullptr && n >= 2048;
     TRY(launch_gather_direct(c->order, c->n_points > 0, c->mode, a, c->g, ta, td, c->n_points,
-                             c->fields.as<double>(), c->M, c->cscale, (double*)out, c->err.as<int>(), c->stream));
+                             c->fields.as<double>(), c->M, c->cscale, (double*)out, c->err.as<int>(), c->stream,
+                             tiles ? &c->bk : nullptr, tiles ? c->bstart.as<int>() : nullptr));
   } else {
     if (!c->binned && !resident) return fail(PPPM_ERR_STATE, "atoms not binned");
     const float* ta = c->tab.as<float>();

@@ -165,7 +165,8 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
                         bool* ranked = nullptr, const CUtensorMap* rho_map2 = nullptr);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
-                         double* force, int* err, cudaStream_t s);
+                         double* force, int* err, cudaStream_t s, const Bricks* bk = nullptr,
+                         const int* bstart = nullptr);
 int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64, const float4* rec,
                         const int* rcell, const int* perm, const int* counts, int cap, int scap, const float4* ovf_rec,
                         const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
