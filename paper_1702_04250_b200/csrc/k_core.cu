@@ -259,16 +259,18 @@ __device__ __forceinline__ long long fix64_value(double qab, double w, double sc
   return __double_as_longlong(__fma_rn(contrib, scale, 6755399441055744.0)) - __double_as_longlong(6755399441055744.0);
 }
 
-template <int S, bool TAB, typename TIn>
+// (LIMBS = 2 when every contribution is below 2^42, i.e. for n >= 2^20 atoms: limbs of 21 bits and
+// the signed rest, whose sums of <= 1024 terms still fit 32 bits)
+template <int S, bool TAB, typename TIn, int LIMBS>
 __global__ void __launch_bounds__(kThreads, 3) k_spread_fix64_tile(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk,
     const int* __restrict__ bstart, const double* __restrict__ ta, int n_points, const double* __restrict__ scale_p,
     unsigned long long* __restrict__ acc, int* __restrict__ err) {
   constexpr int lo = Stencil<S>::lo, D = kBrick + S - 1, N = D * D * D;
-  extern __shared__ unsigned tile64[];  // [3][N] limbs
+  extern __shared__ unsigned tile64[];  // [LIMBS][N] limbs
   unsigned* l0 = tile64;
   unsigned* l1 = tile64 + N;
-  int* l2 = reinterpret_cast<int*>(tile64 + 2 * N);
+  int* l2 = reinterpret_cast<int*>(tile64 + (LIMBS - 1) * N);  // the signed top limb
   const double scale = *scale_p;
   const int nb = bk.count();
   // an atom straight into the global mesh (k_spread_fix64's inner loops)
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_spread_fix64_tile(
       }
     }
   };
-  for (int k = threadIdx.x; k < 3 * N; k += blockDim.x) tile64[k] = 0u;
+  for (int k = threadIdx.x; k < LIMBS * N; k += blockDim.x) tile64[k] = 0u;
   __syncthreads();
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     const int s0 = bstart[b], cnt = bstart[b + 1] - s0;
@@ -326,8 +328,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_spread_fix64_tile(
             const long long f = fix64_value(qab, wx[c], scale);
             if (f != 0) {
               atomicAdd(l0 + row + c, (unsigned)f & 0x1fffffu);
-              atomicAdd(l1 + row + c, (unsigned)(f >> 21) & 0x1fffffu);
-              atomicAdd(l2 + row + c, (int)(f >> 42));
+              if (LIMBS == 3) {
+                atomicAdd(l1 + row + c, (unsigned)(f >> 21) & 0x1fffffu);
+                atomicAdd(l2 + row + c, (int)(f >> 42));
+              } else {
+                atomicAdd(l2 + row + c, (int)(f >> 21));
+              }
             }
           }
         }
@@ -336,13 +342,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_spread_fix64_tile(
     __syncthreads();
     // tile -> global mesh (periodic wrap), limbs cleared for the next brick
     for (int t = threadIdx.x; t < N; t += blockDim.x) {
-      const unsigned a0 = l0[t], a1 = l1[t];
+      const unsigned a0 = l0[t], a1 = LIMBS == 3 ? l1[t] : 0u;
       const int a2 = l2[t];
       if (a0 | a1 | (unsigned)a2) {
         l0[t] = 0u;
-        l1[t] = 0u;
+        if (LIMBS == 3) l1[t] = 0u;
         l2[t] = 0;
-        const long long v = (long long)a2 * (1ll << 42) + ((long long)a1 << 21) + (long long)a0;
+        const long long v = LIMBS == 3 ? (long long)a2 * (1ll << 42) + ((long long)a1 << 21) + (long long)a0
+                                       : (long long)a2 * (1ll << 21) + (long long)a0;
         const int tx = t % D, ty = (t / D) % D, tz = t / (D * D);
         const int ix = wrap_index(bx * kBrick - lo + tx, g.nx), iy = wrap_index(by * kBrick - lo + ty, g.ny),
                   iz = wrap_index(bz * kBrick - lo + tz, g.nz);
@@ -831,19 +838,23 @@ int launch_spread_fix64(int order, bool tab, const AtomsIn& a, const Geom& g, co
       // shared tiles (the same mesh, bitwise)
       if (bk && bstart && a.n >= 2048) {
         constexpr int D = kBrick + S - 1;
-        const size_t dyn = 3 * (size_t)D * D * D * sizeof(unsigned);
-        if (!a.f32) {
-          auto k = k_spread_fix64_tile<S, TAB, double>;
-          const int tg = persistent_grid(k, kThreads, dyn, bk->count());
-          k<<<tg, kThreads, dyn, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, *bk, bstart, ta, n_points,
-                                      scal + 1, acc, err);
-        } else {
-          auto k = k_spread_fix64_tile<S, TAB, float>;
-          const int tg = persistent_grid(k, kThreads, dyn, bk->count());
-          k<<<tg, kThreads, dyn, s>>>((const float*)a.pos, (const float*)a.q, a.n, g, *bk, bstart, ta, n_points,
-                                      scal + 1, acc, err);
-        }
-        return 0;
+        // |contribution| <= max|q| * scale < 2^62 / n: two limbs from 2^20 atoms on
+        return with_bool(a.n >= (1ll << 20), [&](auto L_) -> int {
+          constexpr int LIMBS = decltype(L_)::value ? 2 : 3;
+          const size_t dyn = LIMBS * (size_t)D * D * D * sizeof(unsigned);
+          if (!a.f32) {
+            auto k = k_spread_fix64_tile<S, TAB, double, LIMBS>;
+            const int tg = persistent_grid(k, kThreads, dyn, bk->count());
+            k<<<tg, kThreads, dyn, s>>>((const double*)a.pos, (const double*)a.q, a.n, g, *bk, bstart, ta, n_points,
+                                        scal + 1, acc, err);
+          } else {
+            auto k = k_spread_fix64_tile<S, TAB, float, LIMBS>;
+            const int tg = persistent_grid(k, kThreads, dyn, bk->count());
+            k<<<tg, kThreads, dyn, s>>>((const float*)a.pos, (const float*)a.q, a.n, g, *bk, bstart, ta, n_points,
+                                        scal + 1, acc, err);
+          }
+          return 0;
+        });
       }
       return with_bool(a.n >= 2048, [&](auto M_) -> int {
         constexpr bool MAGIC = decltype(M_)::value;

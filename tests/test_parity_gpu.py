@@ -573,8 +573,8 @@ def test_resident_direct_movers_and_overflow(pb, mode):
     ref.close()
 
 
-@pytest.mark.parametrize("order", [5, 7])
-def test_fp64_tile_make_rho_bitwise(pb, order, monkeypatch):
+@pytest.mark.parametrize("order,n", [(5, 120000), (7, 120000), (5, 1 << 20)])
+def test_fp64_tile_make_rho_bitwise(pb, order, n, monkeypatch):
     """fp64 make_rho on brick-ordered residents accumulates per-brick shared tiles of
     three 32-bit limbs (k_spread_fix64_tile): the same 64-bit fixed-point contributions
     as the direct kernel, so the mesh must be bitwise the same - with a brick that
@@ -583,8 +583,9 @@ def test_fp64_tile_make_rho_bitwise(pb, order, monkeypatch):
     from paper_1702_04250_b200 import scenarios
 
     rng = np.random.default_rng(8)
-    dims, n = (64, 64, 32), 120000
-    lengths = np.array([96.0, 96.0, 48.0])
+    # (from 2^20 atoms on the tiles hold two limbs per cell instead of three)
+    dims = (64, 64, 32) if n < (1 << 20) else (128, 128, 64)
+    lengths = np.array([96.0, 96.0, 48.0]) * (dims[0] // 64)
     pos = rng.uniform(0, 1, (n, 3)) * lengths
     pos[:2500] = np.array([40.0, 50.0, 20.0]) + rng.uniform(0, 3.0, (2500, 3))
     q = np.where(np.arange(n) % 2 == 0, 1.0, -1.0) * rng.uniform(0.5, 1.5, n)
