@@ -700,8 +700,11 @@ __device__ __noinline__ void gather_global_f64(int n0, int n1, int n2, int nx, i
                            s0, s1, s2);
 }
 
+#ifndef PPPM_G64_MINB
+#define PPPM_G64_MINB 3  // measured on config 3 fp64: 339 us (small spills) vs 377 us at 2
+#endif
 template <int S, bool TAB, int MODE, typename TIn>
-__global__ void __launch_bounds__(kThreads, (S >= 6 ? 1 : 2)) k_gather_direct_tile(
+__global__ void __launch_bounds__(kThreads, (S >= 6 ? 1 : PPPM_G64_MINB)) k_gather_direct_tile(
     const TIn* __restrict__ pos, const TIn* __restrict__ qv, int64_t n, Geom g, Bricks bk,
     const int* __restrict__ bstart, const double* __restrict__ ta, const double* __restrict__ td, int n_points,
     const double* __restrict__ f0, const double* __restrict__ f1, const double* __restrict__ f2, double cscale,
