@@ -744,6 +744,201 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
   }
 }
 
+// fieldforce_ik, warp-specialized, stages of TWO x-adjacent bricks (residents ranked by the
+// two-brick make_rho, Bricks::gpair): one (20, D + 2, D) box per component and stage, the pair's
+// atoms in one set of bank buckets - twice the atoms per lane list, so fuller conflict-free
+// rounds (simulated 78 % vs 71 % lane occupancy) and 17 % less field-tile traffic per atom.
+// Two CTAs per SM (two 40 KB tile sets per stage), kWs2ConsumerWarps consumer warps each.
+// Same tasks and arithmetic as k_gather_ws (bitwise the same forces).
+#ifndef PPPM_WS2_CW
+#define PPPM_WS2_CW 8  // measured on config 3: 84.7 us (8), 90.1 (10), 87.6 (12), 90.0 (14)
+#endif
+constexpr int kWs2ConsumerWarps = PPPM_WS2_CW;
+
+template <int S> struct PairTile {
+  static constexpr int D = TmaTile<S>::D, DY = D + 2;
+  static constexpr int TXB = (D + kBrick + TmaTile<S>::SH + 3) / 4 * 4;  // two bricks + stencil halo
+  static constexpr int FTN = TXB * DY * D;
+  static constexpr int FT = (FTN + 31) / 32 * 32;
+  static constexpr bool ok = (TXB % 32 == 12 || TXB % 32 == 20);
+};
+
+template <int S, bool TAB>
+__global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
+    const float4* __restrict__ rec, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
+    const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,
+    float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell,
+    const int* __restrict__ ovf_perm, const int* __restrict__ rstart, const int* __restrict__ novf_res) {
+  using T = TmaTile<S>;
+  using PT = PairTile<S>;
+  constexpr int TXB = PT::TXB, DY = PT::DY, FT = PT::FT, lo = Stencil<S>::lo;
+  constexpr int BUF = 3 * FT;
+  constexpr int NCW = kWs2ConsumerWarps;
+  constexpr uint32_t kBytes = 3u * PT::FTN * sizeof(float);
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
+  float* tiles = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][BUF]
+  float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);  // [2][cap]
+  int* s_c = reinterpret_cast<int*>(s_r + 2 * cap);          // [2][cap]
+  __shared__ __align__(8) uint64_t full[2], tmaf[2], empty[2];
+  __shared__ int bsize[2][32], bstart[2][32], sbrick[2], sbase[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = bk.count(), nitems = nb / 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&tmaf[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer
+    int k = 0;
+    for (int it = blockIdx.x;; it += gridDim.x, ++k) {
+      const int s = k & 1, use = k >> 1;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      if (bk.sched && k > 0) {  // dynamic after the first (static) item
+        int nbk = 0;
+        if (lane == 0) nbk = gridDim.x + atomicAdd(bk.sched, 1);
+        it = __shfl_sync(0xffffffffu, nbk, 0);
+      }
+      if (it >= nitems) {  // end marker for the consumers
+        if (lane == 0) {
+          sbrick[s] = -1;
+          if (bk.sched && atomicAdd(bk.sched + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(bk.sched, 0);
+            atomicExch(bk.sched + 1, 0);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        break;
+      }
+      const int b0 = 2 * it;  // bricks b0, b0 + 1 (x-neighbours: nbx is even)
+      if (lane == 0) {
+        sbrick[s] = it;
+        const int bx = b0 % bk.nbx, by = (b0 / bk.nbx) % bk.nby, bz = b0 / (bk.nbx * bk.nby);
+        const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&tmaf[s], kBytes);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+      }
+      const int64_t base = rstart[b0];
+      const int cnt0 = rstart[b0 + 1] - rstart[b0], cnt = rstart[b0 + 2] - rstart[b0];
+      if (lane == 0) sbase[s] = (int)base;
+      {
+        const int v = cnt > 0 ? __ldg(bk.gbs + (int64_t)it * 32 + lane) : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        bsize[s][lane] = v;
+        bstart[s][lane] = x - v;
+      }
+      __syncwarp();
+      float4* sr = s_r + s * cap;
+      int* sc = s_c + s * cap;
+      for (int j0 = 0; j0 < cnt; j0 += 32 * kWsUr) {
+        float4 r[kWsUr];
+        float qq[kWsUr];
+#pragma unroll
+        for (int u = 0; u < kWsUr; ++u) {
+          const int j = j0 + u * 32 + lane;
+          r[u].w = __int_as_float(-1);
+          if (j < cnt) {
+            r[u] = __ldg(&rec[base + j]);
+            qq[u] = __ldg(&bk.rq[base + j]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kWsUr; ++u) {
+          const int code = __float_as_int(r[u].w);
+          if (code < 0) continue;  // left its brick: overflow list
+          const int j = j0 + u * 32 + lane;
+          const int dst = bstart[s][(code >> kRecBankShift) & 31] + ((code >> kRecRankShift) & kRecRankMask);
+          PPPM_CHECK(dst >= 0 && dst < cap && dst < cnt);
+          sr[dst] = make_float4(r[u].x, r[u].y, r[u].z, qq[u]);
+          // cell | brick of the pair (bit 9) | index within the pair's range (bits 10..); hole: -1
+          sc[dst] = (code & kRecHoleBit) ? -1 : ((code & kRecCellMask) | ((j >= cnt0 ? 1 : 0) << 9) | (j << 10));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else {
+    // ---------------- consumers
+    const int cw = warp - 1;
+    for (int k = 0;; ++k) {
+      const int s = k & 1, ph = (k >> 1) & 1;
+      mbar_wait(&full[s], ph);
+      if (sbrick[s] < 0) break;
+      mbar_wait(&tmaf[s], ph);
+      const float* tile = tiles + s * BUF;
+      const float4* sr = s_r + s * cap;
+      const int* sc = s_c + s * cap;
+      const int sb = sbase[s];
+      const int seg0 = bsize[s][lane];
+      const int seg1 = bsize[s][(lane - TXB) & 31], seg2 = bsize[s][(lane - 2 * TXB) & 31];
+      const int tot = seg0 + seg1 + seg2;
+      int trounds = tot;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) trounds = max(trounds, __shfl_xor_sync(0xffffffffu, trounds, o));
+      const int e1 = seg0 + seg1;
+      const int st0 = bstart[s][lane];
+      const int st1 = bstart[s][(lane - TXB) & 31] - seg0;
+      const int st2 = bstart[s][(lane - 2 * TXB) & 31] - e1;
+      for (int rr = cw; rr < trounds; rr += NCW) {
+        if (rr >= tot) continue;
+        const int f = (rr >= seg0) + (rr >= e1);
+        const int j = (f == 0 ? st0 : (f == 1 ? st1 : st2)) + rr;
+        const float4 r = sr[j];
+        const int cc = sc[j];
+        if (cc < 0) continue;  // hole: the atom is on the overflow list
+        const int lx = (cc & (kBrick - 1)) + ((cc >> 9) & 1) * kBrick, ly = (cc >> 3) & (kBrick - 1),
+                  lz = (cc >> 6) & (kBrick - 1);
+        float ax[S], ay[S], az[S], dd[S];
+        rows_f32<S, TAB, false>(r.x, ta, td, ax, dd);
+        rows_f32<S, TAB, false>(r.y, ta, td, ay, dd);
+        rows_f32<S, TAB, false>(r.z, ta, td, az, dd);
+        const float* tf = tile + f * FT + (lz * DY + ly + f) * TXB + lx + T::SH;
+        float acc = 0.f;
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          float ra = 0.f;
+#pragma unroll
+          for (int bb = 0; bb < S; ++bb) {
+            const float* row = tf + (a * DY + bb) * TXB;
+            float e = 0.f;
+#pragma unroll
+            for (int c = 0; c < S; ++c) e = fmaf(ax[c], row[c], e);
+            ra = fmaf(ay[bb], e, ra);
+          }
+          acc = fmaf(az[a], ra, acc);
+        }
+        const float v = cscale * r.w * acc;
+        const int64_t i = (int64_t)(sb + (cc >> 10));
+        if (out_f64) static_cast<double*>(force)[3 * i + f] = v;
+        else static_cast<float*>(force)[3 * i + f] = v;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  gather_overflow<S, TAB, 0>(novf_res, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell, ovf_perm);
+  // the last CTA done with the per-step mover list clears it for the next make_rho
+  if (bk.sched) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(bk.sched + 2, 1) == (int)gridDim.x - 1) {
+      atomicExch(const_cast<int*>(novf_res), 0);
+      atomicExch(bk.sched + 2, 0);
+    }
+  }
+}
+
 // fieldforce_ik, warp-specialized split variant with x-adjacent atom pairs:
 // two atoms in the same (y, z) cell row whose cells are 0 or 1 apart in x
 // (consecutive in the cell-ordered resident records) share one task per
@@ -1043,7 +1238,8 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
                        const int* perm, const int* counts, int cap, int scap, const float4* ovf_rec, const int* ovf_cell,
                        const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                        const CUtensorMap& fmap, const float* ta, const float* td, const float* fields, float cscale,
-                       void* force, const int* rstart, const int* novf_res, cudaStream_t s) {
+                       void* force, const int* rstart, const int* novf_res, cudaStream_t s,
+                       const CUtensorMap* fmap2 = nullptr) {
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
     constexpr int F = MODE == 0 ? 3 : 1;
@@ -1066,6 +1262,24 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
         });
       }
 #endif
+      if constexpr (S <= 5 && PairTile<S>::ok) {
+        if (variant == GATHER_WS && fmap2 && bk.gpair && bk.gbs && rstart) {
+          // residents ranked in two-brick buckets by make_rho: stages of two x-adjacent bricks
+          const int cap2 = (2 * scap + 31) / 32 * 32;
+          const size_t dyn = 128 + 2 * 3 * (size_t)PairTile<S>::FT * sizeof(float) +
+                             2 * (size_t)cap2 * (sizeof(float4) + sizeof(int));
+          return with_bool(tab, [&](auto T_) -> int {
+            constexpr bool TAB = decltype(T_)::value;
+            auto k = k_gather_ws2<S, TAB>;
+            constexpr int NT = 32 * (kWs2ConsumerWarps + 1);
+            const int grid = persistent_grid(k, NT, dyn, bk.count() / 2);
+            k<<<grid, NT, dyn, s>>>(rec, cap2, g, bk, pd, ta, td, *fmap2, fields, cscale, force, out_f64, ovf_rec,
+                                    ovf_cell, ovf_perm, rstart, novf_res);
+            debug_launch("gather", grid, NT, dyn);
+            return 0;
+          });
+        }
+      }
       if (variant == GATHER_WS) {
         const size_t dyn = 128 + 2 * 3 * (size_t)SplitTile<S>::FT * sizeof(float) +
                            2 * (size_t)cap * (sizeof(float4) + 2 * sizeof(int));

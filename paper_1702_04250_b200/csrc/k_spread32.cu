@@ -502,9 +502,11 @@ __global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB -
           const int bank = ((lz * D + ly) * TXB + lx + kBrick * kt + T::SH) & 31;
           const int rk = atomicAdd(&bsize[p][bank], 1);
           code = lc;
-          if (bk.gbs) {  // bank and rank in fieldforce's tile, for its staging
-            const int gb = ((lz * bk.gdy + ly) * bk.gtxb + lx + T::SH) & 31;
-            const int grk = atomicAdd(&gsize[p][kt][gb], 1);
+          if (bk.gbs) {  // bank and rank in fieldforce's tile (its two-brick tile with gpair), for its staging
+            const bool gp = KX > 1 && bk.gpair;
+            const int gb = gp ? ((lz * bk.gdy + ly) * bk.gtxb2 + lx + kBrick * kt + T::SH) & 31
+                              : ((lz * bk.gdy + ly) * bk.gtxb + lx + T::SH) & 31;
+            const int grk = atomicAdd(&gsize[p][gp ? 0 : kt][gb], 1);
             code |= (gb << kRecBankShift) | (grk << kRecRankShift);
           }
           if (rk < bcap) {
@@ -636,8 +638,13 @@ __global__ void __launch_bounds__(NT, (KX > 1 ? 3 : (S >= 7 ? PPPM_SPREAD_MINB -
       if (n2 < nitems) prefetch(n2, p);
     }
     // the mapped brick's fieldforce bucket sizes (gsize[p ^ 1] is cleared after the next barrier)
-    if (bk.gbs && warp >= 1 && warp <= KX && nxt < nitems)
-      bk.gbs[((int64_t)KX * nxt + (warp - 1)) * 32 + lane] = gsize[p ^ 1][warp - 1][lane];
+    if (bk.gbs && warp >= 1 && warp <= KX && nxt < nitems) {
+      if (KX > 1 && bk.gpair) {
+        if (warp == 1) bk.gbs[(int64_t)nxt * 32 + lane] = gsize[p ^ 1][0][lane];  // one row per pair
+      } else {
+        bk.gbs[((int64_t)KX * nxt + (warp - 1)) * 32 + lane] = gsize[p ^ 1][warp - 1][lane];
+      }
+    }
   }
   if (threadIdx.x == 0) {
     bulk_wait_read<0>();
@@ -1092,8 +1099,8 @@ __global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, const Resident& res,
-                        int n_points, float4* rec_out, cudaStream_t s, bool* ranked, const CUtensorMap* rmap2) {
-  if (ranked) *ranked = false;
+                        int n_points, float4* rec_out, cudaStream_t s, int* ranked, const CUtensorMap* rmap2) {
+  if (ranked) *ranked = 0;
   if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
   int st = with_order(order, [&](auto S_) -> int {
@@ -1136,7 +1143,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
           if (bk.count() >= 2 * grid) {
             kw<<<grid, NTW, dyn, s>>>(g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell, ovf_perm, res, n_points,
                                       rec_out, rcap, bcap);
-            if (ranked) *ranked = bk.gbs != nullptr;
+            if (ranked) *ranked = bk.gbs ? 1 : 0;
             return 0;
           }
         }
@@ -1165,7 +1172,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
             if (items < 2 * grid) return false;
             kr<<<grid, NTX, dyn, s>>>(g, bk, pd, ta, inv_vcell, rho, map, ovf_rec, ovf_cell, ovf_perm, res, n_points,
                                       rec_out, rcap, bcap);
-            if (ranked) *ranked = bk.gbs != nullptr;
+            if (ranked) *ranked = bk.gbs ? ((KX > 1 && bk.gpair) ? 2 : 1) : 0;  // 2: ranked in two-brick buckets
             return true;
           };
           if (kx_env == 2 && rmap2 && bk.nbx % 2 == 0 && 2 * rcap1 <= kCapMax * 2 &&

@@ -123,6 +123,7 @@ struct pppm_ctx {
   Pad pd{};                          // fp32: halo-padded meshes; fp64: H = 0 (dense)
   CUtensorMap rho_map{}, field_map{};  // TMA descriptors of the padded fp32 meshes
   CUtensorMap rho_map2{};              // rho boxes of two x-adjacent bricks (resident make_rho work items)
+  CUtensorMap field_map2{};            // split field boxes of two x-adjacent bricks (k_gather_ws2)
   int nxh = 0;
   cudaStream_t stream = nullptr;
   cufftHandle fwd = 0, bwd = 0;
@@ -148,7 +149,8 @@ struct pppm_ctx {
   DevBuf partial, scal, err, flush;
   DevBuf res_pos, res_q, res_force, res_orig, res_tmp_pos, res_tmp_q, bstart;
   DevBuf gbs;               // per-brick fieldforce bank-bucket sizes written by the pipelined make_rho
-  bool rec_ranked = false;  // the slot records carry fieldforce bank + rank (Bricks::gbs)
+  int rec_ranked = 0;       // the slot records carry fieldforce bank + rank (Bricks::gbs): 1 per brick, 2 per brick pair
+  bool gather_pairs = true;  // PPPM_B200_GATHER_PAIRS=0: one brick per fieldforce stage (A/B)
   bool res_sorted = false;  // resident atoms kept in brick order (res_orig: caller's index)
   int res_maxcnt = 0;       // largest resident brick (staging capacity of the resident fieldforce)
   DevBuf sched;             // brick-scheduling counters of the persistent fieldforce / make_rho
@@ -432,6 +434,13 @@ static int encode_maps(pppm_ctx* c) {
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (fields) failed");
+    if (split) {  // two x-adjacent bricks per stage (k_gather_ws2)
+      cuuint32_t box2[4] = {(cuuint32_t)((D + kBrick + sh + 3) / 4 * 4), (cuuint32_t)(D + 2), (cuuint32_t)D, 1};
+      r = fn(&c->field_map2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->fields.p, dims, strides, box2, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (fields, two bricks) failed");
+    }
   }
   return PPPM_OK;
 }
@@ -508,7 +517,7 @@ static int run_bin(pppm_ctx* c, const void* pos, const void* q, int64_t n, int d
                  c->stream));
   c->launches += 1;
   c->binned = true;
-  c->rec_ranked = false;
+  c->rec_ranked = 0;
   return PPPM_OK;
 }
 
@@ -553,7 +562,7 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
       TRY(ensure_sched(c));
       bks.sched = c->sched.as<int>();
     }
-    c->rec_ranked = false;
+    c->rec_ranked = 0;
     if (resident && gather_eff(c) == GATHER_WS && c->rank_handoff) {
       // records carry the bank / rank of the warp-specialized fieldforce's tile (ik: component
       // tiles of split_txb columns and D + 2 rows; ad: the brick tile)
@@ -563,6 +572,12 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
       bks.gbs = c->gbs.as<int>();
       bks.gtxb = c->mode == 0 ? split_txb(c->order, c->pd.hx) : (D + sh + 3) / 4 * 4;
       bks.gdy = c->mode == 0 ? D + 2 : D;
+      // fieldforce_ik stages of two x-adjacent bricks (orders 3-5): ranks in the pair's buckets
+      const int txb2 = (D + kBrick + sh + 3) / 4 * 4;
+      if (c->gather_pairs && c->mode == 0 && c->order <= 5 && c->bk.nbx % 2 == 0 && (txb2 % 32 == 12 || txb2 % 32 == 20)) {
+        bks.gpair = 1;
+        bks.gtxb2 = txb2;
+      }
     }
     TRY(launch_spread_brick(c->spread_variant, c->order, c->n_points > 0, c->rec.as<float4>(), c->rcell.as<int>(),
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(),
@@ -721,6 +736,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
     Bricks bkg = c->bk;
     if (resident) bkg.rq = c->res_q.as<float>();  // resident 16-byte records take the charges from here
     if (resident && c->rec_ranked) bkg.gbs = c->gbs.as<int>();  // ... and are placed by make_rho's ranks
+    if (resident && c->rec_ranked == 2) bkg.gpair = 1;          // ... in two-brick buckets
     if (c->dyn_sched && gather_eff(c) == GATHER_WS) {
       TRY(ensure_sched(c));
       bkg.sched = c->sched.as<int>();
@@ -731,7 +747,7 @@ static int run_gather(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
                             c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->g, bkg, c->pd,
                             c->field_map, ta, td, c->fields.as<float>(), (float)c->cscale, out,
                             resident ? c->bstart.as<int>() : nullptr, resident ? c->res_novf.as<int>() : nullptr,
-                            c->stream));
+                            c->stream, &c->field_map2));
     }
   }
   c->launches += 1;
@@ -1015,6 +1031,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RANKS")) c->rank_handoff = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_FIX64_TILES")) c->fix64_tiles = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_GATHER_PAIRS")) c->gather_pairs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RESORT")) c->resort_frac = atof(v);
   if (!c->fp64() && encode_maps(c) != PPPM_OK) return cleanup(PPPM_ERR_CUDA);
   *out = c;

@@ -35,13 +35,16 @@ struct Bricks {
   // staging places the records without its own counting sort (kRecBank / kRecRank / kRecHole)
   int* gbs = nullptr;
   int gdy = 0, gtxb = 0;
+  // gpair: fieldforce stages two x-adjacent bricks at a time (k_gather_ws2: tiles of gtxb2 columns);
+  // make_rho's two-brick items then rank their atoms in the pair's buckets, gbs holds one row per pair
+  int gpair = 0, gtxb2 = 0;
   __host__ __device__ __forceinline__ int count() const { return nbx * nby * nbz; }
 };
 
 // resident slot record word (rec.w as int): brick-local cell, then - ranked records only - the
 // fieldforce bank, the rank inside that bank's bucket, and the hole flag (slot reserved, but the
 // atom takes the direct path in both kernels); -1: the atom left its brick (direct path)
-constexpr int kRecCellMask = 511, kRecBankShift = 9, kRecRankShift = 14, kRecRankMask = 1023, kRecHoleBit = 1 << 24;
+constexpr int kRecCellMask = 511, kRecBankShift = 9, kRecRankShift = 14, kRecRankMask = 2047, kRecHoleBit = 1 << 25;
 
 struct GreenSpec {
   int nx, ny, nz, order;
@@ -162,7 +165,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad,
                         const Resident& res, int n_points, float4* rec_out, cudaStream_t s,
-                        bool* ranked = nullptr, const CUtensorMap* rho_map2 = nullptr);
+                        int* ranked = nullptr, const CUtensorMap* rho_map2 = nullptr);
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s, const Bricks* bk = nullptr,
@@ -171,7 +174,8 @@ int launch_gather_brick(int variant, int order, bool tab, int mode, bool out_f64
                         const int* rcell, const int* perm, const int* counts, int cap, int scap, const float4* ovf_rec,
                         const int* ovf_cell, const int* ovf_perm, const Geom& g, const Bricks& bk, const Pad& pd,
                         const CUtensorMap& field_map, const float* ta, const float* td, const float* fields_pad,
-                        float cscale, void* force, const int* rstart, const int* novf_res, cudaStream_t s);
+                        float cscale, void* force, const int* rstart, const int* novf_res, cudaStream_t s,
+                        const CUtensorMap* field_map2 = nullptr);
 // fieldforce_ik on the tensor cores (k_gather_mma.cu): orders whose 3 field tiles fit TMEM
 bool gather_mma_ok(int order);
 int launch_gather_mma(int order, bool tab, bool out_f64, const float4* rec, const int* counts, int cap,
