@@ -754,6 +754,10 @@ __global__ void __launch_bounds__(32 * (kWsConsumerWarps + kWsPw<MODE>), (S >= 6
 #define PPPM_WS2_CW 8  // measured on config 3: 84.7 us (8), 90.1 (10), 87.6 (12), 90.0 (14)
 #endif
 constexpr int kWs2ConsumerWarps = PPPM_WS2_CW;
+#ifndef PPPM_WS2_UR
+#define PPPM_WS2_UR 4
+#endif
+constexpr int kWs2Ur = PPPM_WS2_UR;  // records per producer lane and batch (two CTAs per SM: registers to spare)
 
 template <int S> struct PairTile {
   static constexpr int D = TmaTile<S>::D, DY = D + 2;
@@ -763,18 +767,21 @@ template <int S> struct PairTile {
   static constexpr bool ok = (TXB % 32 == 12 || TXB % 32 == 20);
 };
 
-template <int S, bool TAB>
-__global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
+template <int S, bool TAB, int MODE = 0>
+__global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), (MODE == 0 ? 2 : 3)) k_gather_ws2(
     const float4* __restrict__ rec, int cap, Geom g, Bricks bk, Pad pd, const float* __restrict__ ta,
     const float* __restrict__ td, const __grid_constant__ CUtensorMap fmap, const float* __restrict__ fields,
     float cscale, void* force, bool out_f64, const float4* __restrict__ ovf_rec, const int* __restrict__ ovf_cell,
     const int* __restrict__ ovf_perm, const int* __restrict__ rstart, const int* __restrict__ novf_res) {
   using T = TmaTile<S>;
   using PT = PairTile<S>;
-  constexpr int TXB = PT::TXB, DY = PT::DY, FT = PT::FT, lo = Stencil<S>::lo;
-  constexpr int BUF = 3 * FT;
+  // ik (MODE 0): three component tiles, rows shifted by the component (DY = D + 2);
+  // ad (MODE 1): one potential tile (DY = D), one task per atom, three derivative sums
+  constexpr int TXB = PT::TXB, DY = MODE == 0 ? PT::DY : PT::D, lo = Stencil<S>::lo;
+  constexpr int FTN = TXB * DY * PT::D, FT = (FTN + 31) / 32 * 32;
+  constexpr int BUF = MODE == 0 ? 3 * FT : FT;
   constexpr int NCW = kWs2ConsumerWarps;
-  constexpr uint32_t kBytes = 3u * PT::FTN * sizeof(float);
+  constexpr uint32_t kBytes = (MODE == 0 ? 3u : 1u) * FTN * sizeof(float);
   extern __shared__ __align__(16) unsigned char dyn_raw[];
   float* tiles = reinterpret_cast<float*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));  // [2][BUF]
   float4* s_r = reinterpret_cast<float4*>(tiles + 2 * BUF);  // [2][cap]
@@ -822,8 +829,12 @@ __global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
         const int x = bx * kBrick - lo + pd.hx - T::SH, y = by * kBrick - lo + pd.H, z = bz * kBrick - lo + pd.H;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&tmaf[s], kBytes);
+        if constexpr (MODE == 0) {
 #pragma unroll
-        for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+          for (int f = 0; f < 3; ++f) tma_load_4d(tiles + s * BUF + f * FT, &fmap, &tmaf[s], x, y - f, z, f);
+        } else {
+          tma_load_4d(tiles + s * BUF, &fmap, &tmaf[s], x, y, z, 0);
+        }
       }
       const int64_t base = rstart[b0];
       const int cnt0 = rstart[b0 + 1] - rstart[b0], cnt = rstart[b0 + 2] - rstart[b0];
@@ -842,11 +853,11 @@ __global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
       __syncwarp();
       float4* sr = s_r + s * cap;
       int* sc = s_c + s * cap;
-      for (int j0 = 0; j0 < cnt; j0 += 32 * kWsUr) {
-        float4 r[kWsUr];
-        float qq[kWsUr];
+      for (int j0 = 0; j0 < cnt; j0 += 32 * kWs2Ur) {
+        float4 r[kWs2Ur];
+        float qq[kWs2Ur];
 #pragma unroll
-        for (int u = 0; u < kWsUr; ++u) {
+        for (int u = 0; u < kWs2Ur; ++u) {
           const int j = j0 + u * 32 + lane;
           r[u].w = __int_as_float(-1);
           if (j < cnt) {
@@ -855,7 +866,7 @@ __global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
           }
         }
 #pragma unroll
-        for (int u = 0; u < kWsUr; ++u) {
+        for (int u = 0; u < kWs2Ur; ++u) {
           const int code = __float_as_int(r[u].w);
           if (code < 0) continue;  // left its brick: overflow list
           const int j = j0 + u * 32 + lane;
@@ -882,24 +893,57 @@ __global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
       const int* sc = s_c + s * cap;
       const int sb = sbase[s];
       const int seg0 = bsize[s][lane];
-      const int seg1 = bsize[s][(lane - TXB) & 31], seg2 = bsize[s][(lane - 2 * TXB) & 31];
+      const int seg1 = MODE == 0 ? bsize[s][(lane - TXB) & 31] : 0, seg2 = MODE == 0 ? bsize[s][(lane - 2 * TXB) & 31] : 0;
       const int tot = seg0 + seg1 + seg2;
       int trounds = tot;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) trounds = max(trounds, __shfl_xor_sync(0xffffffffu, trounds, o));
       const int e1 = seg0 + seg1;
       const int st0 = bstart[s][lane];
-      const int st1 = bstart[s][(lane - TXB) & 31] - seg0;
-      const int st2 = bstart[s][(lane - 2 * TXB) & 31] - e1;
+      const int st1 = MODE == 0 ? bstart[s][(lane - TXB) & 31] - seg0 : 0;
+      const int st2 = MODE == 0 ? bstart[s][(lane - 2 * TXB) & 31] - e1 : 0;
       for (int rr = cw; rr < trounds; rr += NCW) {
         if (rr >= tot) continue;
-        const int f = (rr >= seg0) + (rr >= e1);
+        const int f = MODE == 0 ? (rr >= seg0) + (rr >= e1) : 0;
         const int j = (f == 0 ? st0 : (f == 1 ? st1 : st2)) + rr;
         const float4 r = sr[j];
         const int cc = sc[j];
         if (cc < 0) continue;  // hole: the atom is on the overflow list
         const int lx = (cc & (kBrick - 1)) + ((cc >> 9) & 1) * kBrick, ly = (cc >> 3) & (kBrick - 1),
                   lz = (cc >> 6) & (kBrick - 1);
+        if constexpr (MODE == 1) {
+          // fieldforce_ad (gridmap.py:299-310): split-atom derivative sums over one potential tile
+          float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
+          rows_f32<S, TAB, true>(r.x, ta, td, ax, dx);
+          rows_f32<S, TAB, true>(r.y, ta, td, ay, dy);
+          rows_f32<S, TAB, true>(r.z, ta, td, az, dz);
+          const float* tf = tile + (lz * DY + ly) * TXB + lx + T::SH;
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int a = 0; a < S; ++a) {
+            float r0 = 0.f, r1 = 0.f, r2 = 0.f;
+#pragma unroll
+            for (int bb = 0; bb < S; ++bb) {
+              const float* row = tf + (a * DY + bb) * TXB;
+              float pdv = 0.f, pa = 0.f;
+#pragma unroll
+              for (int c = 0; c < S; ++c) {
+                pdv = fmaf(dx[c], row[c], pdv);
+                pa = fmaf(ax[c], row[c], pa);
+              }
+              r0 = fmaf(ay[bb], pdv, r0);
+              r1 = fmaf(dy[bb], pa, r1);
+              r2 = fmaf(ay[bb], pa, r2);
+            }
+            s0 = fmaf(az[a], r0, s0);
+            s1 = fmaf(az[a], r1, s1);
+            s2 = fmaf(dz[a], r2, s2);
+          }
+          const float scq = cscale * r.w;
+          store_force<S, 1>(force, out_f64, (int64_t)(sb + (cc >> 10)), -scq * s0 * (float)g.ihx,
+                            -scq * s1 * (float)g.ihy, -scq * s2 * (float)g.ihz);
+          continue;
+        }
         float ax[S], ay[S], az[S], dd[S];
         rows_f32<S, TAB, false>(r.x, ta, td, ax, dd);
         rows_f32<S, TAB, false>(r.y, ta, td, ay, dd);
@@ -928,7 +972,7 @@ __global__ void __launch_bounds__(32 * (kWs2ConsumerWarps + 1), 2) k_gather_ws2(
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
-  gather_overflow<S, TAB, 0>(novf_res, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell, ovf_perm);
+  gather_overflow<S, TAB, MODE>(novf_res, g, pd, ta, td, fields, cscale, force, out_f64, ovf_rec, ovf_cell, ovf_perm);
   // the last CTA done with the per-step mover list clears it for the next make_rho
   if (bk.sched) {
     __syncthreads();
@@ -1310,6 +1354,24 @@ int launch_gather_mode(int variant, int order, bool tab, bool out_f64, const flo
         });
       }
 #endif
+    }
+    if constexpr (MODE == 1 && S <= 5 && PairTile<S>::ok) {
+      if (variant == GATHER_WS && fmap2 && bk.gpair && bk.gbs && rstart) {
+        // residents ranked in two-brick buckets by make_rho: stages of two x-adjacent bricks
+        const int cap2 = (2 * scap + 31) / 32 * 32;
+        constexpr int FT1 = (PairTile<S>::TXB * TmaTile<S>::D * TmaTile<S>::D + 31) / 32 * 32;
+        const size_t dyn = 128 + 2 * (size_t)FT1 * sizeof(float) + 2 * (size_t)cap2 * (sizeof(float4) + sizeof(int));
+        return with_bool(tab, [&](auto T_) -> int {
+          constexpr bool TAB = decltype(T_)::value;
+          auto k = k_gather_ws2<S, TAB, 1>;
+          constexpr int NT = 32 * (kWs2ConsumerWarps + 1);
+          const int grid = persistent_grid(k, NT, dyn, bk.count() / 2);
+          k<<<grid, NT, dyn, s>>>(rec, cap2, g, bk, pd, ta, td, *fmap2, fields, cscale, force, out_f64, ovf_rec,
+                                  ovf_cell, ovf_perm, rstart, novf_res);
+          debug_launch("gather", grid, NT, dyn);
+          return 0;
+        });
+      }
     }
     if constexpr (MODE == 1) {
       if (variant == GATHER_WS) {  // warp-specialized fieldforce_ad

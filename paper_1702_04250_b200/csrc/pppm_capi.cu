@@ -434,8 +434,8 @@ static int encode_maps(pppm_ctx* c) {
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PPPM_ERR_CUDA, "cuTensorMapEncodeTiled (fields) failed");
-    if (split) {  // two x-adjacent bricks per stage (k_gather_ws2)
-      cuuint32_t box2[4] = {(cuuint32_t)((D + kBrick + sh + 3) / 4 * 4), (cuuint32_t)(D + 2), (cuuint32_t)D, 1};
+    if (split || (c->mode == 1 && gather_eff(c) == GATHER_WS)) {  // two x-adjacent bricks per stage (k_gather_ws2)
+      cuuint32_t box2[4] = {(cuuint32_t)((D + kBrick + sh + 3) / 4 * 4), (cuuint32_t)(split ? D + 2 : D), (cuuint32_t)D, 1};
       r = fn(&c->field_map2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->fields.p, dims, strides, box2, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -572,9 +572,9 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
       bks.gbs = c->gbs.as<int>();
       bks.gtxb = c->mode == 0 ? split_txb(c->order, c->pd.hx) : (D + sh + 3) / 4 * 4;
       bks.gdy = c->mode == 0 ? D + 2 : D;
-      // fieldforce_ik stages of two x-adjacent bricks (orders 3-5): ranks in the pair's buckets
+      // fieldforce stages of two x-adjacent bricks (orders 3-5): ranks in the pair's buckets
       const int txb2 = (D + kBrick + sh + 3) / 4 * 4;
-      if (c->gather_pairs && c->mode == 0 && c->order <= 5 && c->bk.nbx % 2 == 0 && (txb2 % 32 == 12 || txb2 % 32 == 20)) {
+      if (c->gather_pairs && c->order <= 5 && c->bk.nbx % 2 == 0 && (txb2 % 32 == 12 || txb2 % 32 == 20)) {
         bks.gpair = 1;
         bks.gtxb2 = txb2;
       }
