@@ -132,7 +132,7 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
                                               float4* __restrict__ rec, float4* __restrict__ ovf_rec,
                                               int* __restrict__ ovf_cell, int* __restrict__ ovf_perm, BankSmem sm,
                                               float4* __restrict__ t_r, int* __restrict__ t_c, int* __restrict__ mq,
-                                              int* __restrict__ nmq) {
+                                              int* __restrict__ nmq, int* __restrict__ gsize) {
   constexpr int PER = KB * kCapMax / NT;
   constexpr int kCells = kBrick * kBrick * kBrick;
   // (bsize was reset by the caller before its brick barrier)
@@ -153,7 +153,13 @@ __device__ __forceinline__ int stage_resident(const Resident& res, int b, int cn
       const int kt = (KB > 1 && j >= cnt0) ? 1 : 0;  // tile (brick) of the item
       // 16-byte slot record for fieldforce: offsets + brick-local cell (-1:
       // mover); the charge and the index are the resident arrays' own
-      rec[i] = make_float4(r.x, r.y, r.z, __int_as_float(ab == b + kt ? lc : -1));
+      int code = ab == b + kt ? lc : -1;
+      if (code >= 0 && KB == 1 && bk.gbs) {  // bank and rank in fieldforce's tile, for its staging (ranked records)
+        const int glx = lc & (kBrick - 1), gly = (lc >> 3) & (kBrick - 1), glz = lc >> 6;
+        const int gb = ((glz * bk.gdy + gly) * bk.gtxb + glx + SH) & 31;
+        code |= (gb << kRecBankShift) | (atomicAdd(gsize + gb, 1) << kRecRankShift);
+      }
+      rec[i] = make_float4(r.x, r.y, r.z, __int_as_float(code));
       if (ab == b + kt) {
         t_r[j] = r;  // unsorted copy in shared memory for pass 2
         t_c[j] = lc | (kt << 9);
@@ -231,7 +237,7 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
   int* dyn_i = reinterpret_cast<int*>(dyn_raw + ((128u - (smem_u32(dyn_raw) & 127u)) & 127u));
   int* tiles0 = dyn_i;
   float4* s_r = reinterpret_cast<float4*>(dyn_i + 2 * KB * T::NP);
-  __shared__ int bsize[32], bstart[33];
+  __shared__ int bsize[32], bstart[33], gsize[32];
   constexpr int kCells = kBrick * kBrick * kBrick;
   // per-cell atom counts of the staged bricks, [KB * kCells] = max (FIX scale)
   __shared__ __align__(16) int s_occ[KB * kCells + 4];
@@ -281,6 +287,7 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
     // all reduces but the most recent (other buffer) have finished reading
     if (threadIdx.x == 0) bulk_wait_read<1>();
     if (RES && threadIdx.x < 32) bsize[threadIdx.x] = 0;  // stage_resident's histogram
+    if (RES && threadIdx.x >= 32 && threadIdx.x < 64) gsize[threadIdx.x - 32] = 0;
     if (FIX) {
       for (int k = threadIdx.x; k < KB * kCells / 4; k += blockDim.x)
         reinterpret_cast<int4*>(s_occ)[k] = make_int4(0, 0, 0, 0);
@@ -295,9 +302,10 @@ __global__ void __launch_bounds__(NT, (!RES && S >= 6 ? 2 : (S >= 7 || !RES ? PP
       rounds = stage_resident<S, TAB, D, TXB, T::SH, NT, KB>(res, b0, cnt0, cnt, g, bk, pd, n_points, ta, inv_vcell,
                                                                 rho, rec_out, ovf_rec, ovf_cell, ovf_perm, sm,
                                                                 s_r + cap, reinterpret_cast<int*>(s_r + 2 * cap) + cap,
-                                                                s_mq, &s_nmq);
+                                                                s_mq, &s_nmq, gsize);
     else
       rounds = stage_banked<false, D, TXB, T::SH, NT>(rec, rcell, nullptr, (int64_t)b * cap, cnt, sm);
+    if (RES && KB == 1 && bk.gbs && threadIdx.x < 32) bk.gbs[(int64_t)b0 * 32 + threadIdx.x] = gsize[threadIdx.x];
     float scale = inv_vcell, inv_scale = 1.f;
     if (FIX) {
       // int32 fixed point, power-of-two scale 2^sc.  Integer adds wrap, so only
@@ -1187,8 +1195,12 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
         const size_t dyn = 128 + 2 * (size_t)kbt * TmaTile<S>::NP * sizeof(int) +
                            (res.pos ? 2 : 1) * (size_t)scap * (sizeof(float4) + sizeof(int));
         const int grid = persistent_grid(k, NT, dyn, (bk.count() + kbt - 1) / kbt);
-        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, scap, g, bk, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
+        Bricks bk1 = bk;
+        bk1.gpair = 0;  // one brick per work item here: per-brick ranks
+        if (kSpreadPair != 1) bk1.gbs = nullptr;
+        k<<<grid, NT, dyn, s>>>(rec, rcell, counts, scap, g, bk1, pd, ta, inv_vcell, rho, rmap, ovf_rec, ovf_cell,
                                 ovf_perm, res, n_points, rec_out);
+        if (ranked && res.pos && bk1.gbs) *ranked = 1;
         if (getenv("PPPM_B200_DEBUG")) {
           const cudaError_t e = cudaPeekAtLastError();
           if (e != cudaSuccess)
