@@ -184,7 +184,7 @@ KERNEL_NAMES = {"spread": "k_spread_res", "gather": "k_gather_tma", "bin": "k_bi
 def kernel_name(kernel, mode):
     """Name of the kernel behind a phase (fieldforce_ik: the warp-specialized split kernel)."""
     if kernel == "gather" and mode == "ik":
-        return "k_gather_ws"
+        return "k_gather_ws2"  # residents ranked by the two-brick make_rho (config 3 / 5); else k_gather_ws
     return KERNEL_NAMES[kernel]
 
 
