@@ -613,8 +613,9 @@ def test_fp64_tile_make_rho_bitwise(pb, order, n, monkeypatch):
     assert rel_rms(out["1"][1], rho_ref) <= 1e-11  # 64-bit fixed point with the global scale 2^(62 - log2(N max|q|))
 
 
-@pytest.mark.parametrize("mode", ["ik", "ad"])
-def test_resident_pipelined_movers_holes_overflow(pb, mode):
+@pytest.mark.parametrize("mode,order,table", [("ik", 5, 0), ("ad", 5, 0), ("ik", 3, 5000), ("ad", 4, 0),
+                                              ("ik", 7, 0)])
+def test_resident_pipelined_movers_holes_overflow(pb, mode, order, table):
     """The pipelined resident make_rho (several bricks per CTA: 128 x 128 x 64 mesh) and
     the ranked record hand-off to fieldforce, on their rare paths: a cell so full that
     its bank bucket overflows (atoms take the direct path, their fieldforce slots stay
@@ -631,8 +632,10 @@ def test_resident_pipelined_movers_holes_overflow(pb, mode):
     pos[300:3300] = np.array([120.0, 30.0, 20.0]) + rng.uniform(0, 6.0, (3000, 3))  # bricks beyond the slot capacity
     p32 = scenarios.round_to_f32(np.mod(pos, lengths), lengths)
     q32 = q.astype(np.float32)
-    ctx = pb.PppmContext(dims, lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
-    ref = pb.PppmContext(dims, lengths, order=5, mode=mode, precision="mixed", alpha=0.3)
+    # (orders 3-5: two-brick make_rho items and fieldforce stages, exact and table weights;
+    # order 7: two-brick make_rho items, per-brick ranked fieldforce stages)
+    ctx = pb.PppmContext(dims, lengths, order=order, mode=mode, precision="mixed", alpha=0.3, table_points=table)
+    ref = pb.PppmContext(dims, lengths, order=order, mode=mode, precision="mixed", alpha=0.3, table_points=table)
     ctx.load_atoms(p32, q32)
     for trial in range(3):
         for _ in range(2):  # eager, then graph replay
