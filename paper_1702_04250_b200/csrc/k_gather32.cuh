@@ -58,6 +58,7 @@ __device__ __forceinline__ void gather_overflow(const int* __restrict__ novf_ptr
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < novf; k += nwarps) {
     const float4 r = ovf_rec[k];
     const int cc = ovf_cell[k];
+    const int64_t iperm = ovf_perm[k];  // (loaded with the record: one memory round trip less per atom)
     const int n0 = cc & 1023, n1 = (cc >> 10) & 1023, n2 = cc >> 20;
     float ax[S], ay[S], az[S], dx[S], dy[S], dz[S];
     rows_f32<S, TAB, MODE == 1>(r.x, ta, td, ax, dx);
@@ -91,8 +92,8 @@ __device__ __forceinline__ void gather_overflow(const int* __restrict__ novf_ptr
     }
     if (lane == 0) {
       const float sc = cscale * r.w;
-      if (MODE == 0) store_force<S, MODE>(force, out_f64, ovf_perm[k], sc * s0, sc * s1, sc * s2);
-      else store_force<S, MODE>(force, out_f64, ovf_perm[k], -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
+      if (MODE == 0) store_force<S, MODE>(force, out_f64, iperm, sc * s0, sc * s1, sc * s2);
+      else store_force<S, MODE>(force, out_f64, iperm, -sc * s0 * ihx, -sc * s1 * ihy, -sc * s2 * ihz);
     }
   }
 }
