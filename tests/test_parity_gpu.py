@@ -613,9 +613,10 @@ def test_fp64_tile_make_rho_bitwise(pb, order, n, monkeypatch):
     assert rel_rms(out["1"][1], rho_ref) <= 1e-11  # 64-bit fixed point with the global scale 2^(62 - log2(N max|q|))
 
 
-@pytest.mark.parametrize("mode,order,table", [("ik", 5, 0), ("ad", 5, 0), ("ik", 3, 5000), ("ad", 4, 0),
-                                              ("ik", 7, 0)])
-def test_resident_pipelined_movers_holes_overflow(pb, mode, order, table):
+@pytest.mark.parametrize("mode,order,table,nx", [("ik", 5, 0, 128), ("ad", 5, 0, 128), ("ik", 3, 5000, 128),
+                                                 ("ad", 4, 0, 128), ("ik", 7, 0, 128), ("ik", 5, 0, 136),
+                                                 ("ad", 5, 0, 136)])
+def test_resident_pipelined_movers_holes_overflow(pb, mode, order, table, nx):
     """The pipelined resident make_rho (several bricks per CTA: 128 x 128 x 64 mesh) and
     the ranked record hand-off to fieldforce, on their rare paths: a cell so full that
     its bank bucket overflows (atoms take the direct path, their fieldforce slots stay
@@ -624,9 +625,12 @@ def test_resident_pipelined_movers_holes_overflow(pb, mode, order, table):
     from paper_1702_04250_b200 import scenarios
 
     rng = np.random.default_rng(33)
-    dims, n = (128, 128, 64), 500000
-    lengths = np.array([192.0, 192.0, 96.0])
+    # (nx = 136: an odd number of bricks along x - one-brick make_rho items and fieldforce stages
+    # on the pipelined path, no brick pairs)
+    dims, n = (nx, 128, 64), 500000
+    lengths = np.array([1.5 * nx, 192.0, 96.0])
     pos, q, _ = scenarios.random_gas(n, 11, 192.0)
+    pos[:, 0] *= nx / 128.0
     pos[:, 2] *= 0.5
     pos[:300] = np.array([50.2, 60.3, 40.4]) + rng.uniform(0, 0.8, (300, 3))       # one cell: one bank bucket
     pos[300:3300] = np.array([120.0, 30.0, 20.0]) + rng.uniform(0, 6.0, (3000, 3))  # bricks beyond the slot capacity
