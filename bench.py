@@ -760,9 +760,10 @@ def main():
         line["e2e"] = {"value": e2e[main_dt][0], "unit": UNIT,
                        "h2d_bytes_per_step": int(posd.nbytes + qd.nbytes), "d2h_bytes_per_step": e2e[main_dt][1],
                        "forces_dtype": main_dt,
-                       "what": "PppmContext.compute -> pppm_compute_ex: H2D pos+q from pinned memory (8 chunks on a "
-                               "copy stream, each binned as it lands), make_rho, poisson, fieldforce, D2H forces "
-                               "(pinned) + energy; wall clock per synchronous call"}
+                       "what": "PppmContext.compute -> pppm_compute_ex: H2D pos+q from pinned memory in 4 atom groups "
+                               "on a copy stream, each group binned and spread (make_rho) as it lands, poisson, "
+                               "fieldforce per group with the group's forces going back (D2H, pinned) while the "
+                               "next group's fieldforce runs, + energy; wall clock per synchronous call"}
         if "float64" in e2e and fp32:
             line["e2e"]["value_f64_forces"] = e2e["float64"][0]
             line["e2e"]["d2h_bytes_per_step_f64_forces"] = e2e["float64"][1]

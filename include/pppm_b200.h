@@ -120,8 +120,10 @@ int pppm_compute(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int d
 
 /* pppm_compute with the forces' element type chosen by the caller (PPPM_F64,
  * or PPPM_F32 on a mixed-precision context: the path's own precision, half the
- * device->host bytes).  Host fp32 atoms on the mixed path are copied in chunks
- * on a second stream, each chunk binned as soon as it has landed. */
+ * device->host bytes).  Host atoms on the mixed path travel in groups of the
+ * caller's order on a second stream: each group is binned into its own brick
+ * slots and spread as soon as it has landed, and each group's forces are
+ * copied back while the next group's fieldforce runs. */
 int pppm_compute_ex(pppm_ctx* ctx, const void* pos, const void* q, int64_t n, int dtype, int mem,
                     void* forces, int forces_dtype, double* energy);
 

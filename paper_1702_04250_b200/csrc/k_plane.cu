@@ -54,8 +54,20 @@ constexpr bool plane_split(int nx, int ny) { return (size_t)ny * (nx / 2 + 1) * 
 #ifndef PPPM_PLANE_S4_MINB
 #define PPPM_PLANE_S4_MINB 3
 #endif
-constexpr int r2c_split(int nx, int ny) { return plane_split(nx, ny) ? 2 : 1; }
-constexpr int c2r_split(int nx, int ny) { return plane_split(nx, ny) ? PPPM_PLANE_C2R_SPLIT : 1; }
+// A/B: planes whose half spectrum exceeds these sizes are split as well (0: only the planes that must be)
+#ifndef PPPM_R2C_SPLIT_KB
+#define PPPM_R2C_SPLIT_KB 0
+#endif
+#ifndef PPPM_C2R_SPLIT_KB
+#define PPPM_C2R_SPLIT_KB 0
+#endif
+constexpr bool plane_over(int nx, int ny, int kb) {
+  return kb > 0 && ny >= 32 && (size_t)ny * (nx / 2 + 1) * sizeof(float2) > (size_t)kb * 1024;
+}
+constexpr int r2c_split(int nx, int ny) { return plane_split(nx, ny) || plane_over(nx, ny, PPPM_R2C_SPLIT_KB) ? 2 : 1; }
+constexpr int c2r_split(int nx, int ny) {
+  return plane_split(nx, ny) ? PPPM_PLANE_C2R_SPLIT : (plane_over(nx, ny, PPPM_C2R_SPLIT_KB) ? 2 : 1);
+}
 
 template <int NX, int NY, int S_>
 struct PlaneCfg {

@@ -1107,9 +1107,10 @@ __global__ void __launch_bounds__(32 * (kSpreadWsWarps + 1), 3) k_spread_ws(
 int launch_spread_brick(int variant, int order, bool tab, const float4* rec, const int* rcell, const int* counts,
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rmap, const float* ta, float* rho, const Resident& res,
-                        int n_points, float4* rec_out, cudaStream_t s, int* ranked, const CUtensorMap* rmap2) {
+                        int n_points, float4* rec_out, cudaStream_t s, int* ranked, const CUtensorMap* rmap2,
+                        bool clear, bool fold) {
   if (ranked) *ranked = 0;
-  if (cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
+  if (clear && cudaMemsetAsync(rho, 0, sizeof(float) * pd.count(), s) != cudaSuccess) return launch_status();
   const float inv_vcell = (float)(1.0 / (g.hx * g.hy * g.hz));
   int st = with_order(order, [&](auto S_) -> int {
     constexpr int S = decltype(S_)::value;
@@ -1213,7 +1214,7 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
   });
   if (st) return st;
   st = launch_status();
-  if (st) return st;
+  if (st || !fold) return st;
   return launch_fold_halo(g, pd, rho, s);
 }
 

@@ -201,11 +201,22 @@ struct pppm_ctx {
   int* h_movers = nullptr;
   cudaEvent_t movers_ev = nullptr;
   bool movers_pending = false;
+  int64_t movers_gen = 0;  // c->resorts when the pending count was taken
   double resort_frac = 0.05;
   int64_t resorts = 0, last_movers = 0;
   static constexpr int kChunks = 8;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ev[kChunks] = {};
+  // pppm_compute_ex in atom groups (host fp32 atoms, mixed): every group of the caller's atoms has
+  // its own brick slots, so its make_rho runs while the next group is still on the link and its
+  // forces go back while the next group's fieldforce runs (PPPM_B200_GROUPS, 1: one group)
+  struct BinSet {
+    DevBuf counts, rec, rcell, perm, ovf_rec, ovf_cell, ovf_perm;
+  };
+  BinSet grp[kChunks - 1];
+  cudaEvent_t grp_ev[kChunks] = {};
+  cudaEvent_t d2h_ev = nullptr;
+  int groups = 4;
 
   bool fp64() const { return prec == PPPM_PREC_FP64; }
   size_t real_size() const { return fp64() ? sizeof(double) : sizeof(float); }
@@ -544,7 +555,8 @@ static int ensure_sched(pppm_ctx* c) {
   return PPPM_OK;
 }
 
-static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, bool resident = false) {
+static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, bool resident = false,
+                      bool clear = true, bool fold = true) {
   const AtomsIn a = atoms_in(pos, q, n, dtype);
   if (c->fp64()) {
     // brick-ordered residents: per-brick shared tiles (bitwise the same mesh as the direct kernel)
@@ -583,8 +595,8 @@ static int run_spread(pppm_ctx* c, const void* pos, const void* q, int64_t n, in
                             c->counts.as<int>(), c->cap, c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(),
                             c->ovf_perm.as<int>(), c->g, bks, c->pd, c->rho_map, c->tab.as<float>(),
                             c->rho.as<float>(), resident ? resident_of(c) : Resident{}, c->n_points,
-                            c->rec.as<float4>(), c->stream, &c->rec_ranked, &c->rho_map2));
-    c->launches += 1 + fold_launches(c->g, c->pd);  // spread + halo fold
+                            c->rec.as<float4>(), c->stream, &c->rec_ranked, &c->rho_map2, clear, fold));
+    c->launches += 1 + (fold ? fold_launches(c->g, c->pd) : 0);  // spread + halo fold
   }
   c->have_rho = true;
   return PPPM_OK;
@@ -1030,6 +1042,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RANKS")) c->rank_handoff = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_GROUPS")) c->groups = std::max(1, std::min(atoi(v), (int)pppm_ctx::kChunks));
   if (const char* v = getenv("PPPM_B200_FIX64_TILES")) c->fix64_tiles = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_GATHER_PAIRS")) c->gather_pairs = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RESORT")) c->resort_frac = atof(v);
@@ -1109,6 +1122,11 @@ int pppm_ctx_destroy(pppm_ctx* c) {
   if (c->h_scal) cudaFreeHost(c->h_scal);
   for (auto& e : c->chunk_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->grp_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->d2h_ev) cudaEventDestroy(c->d2h_ev);
+  for (auto& b : c->grp)
+    for (DevBuf* d : {&b.counts, &b.rec, &b.rcell, &b.perm, &b.ovf_rec, &b.ovf_cell, &b.ovf_perm}) d->release();
   if (c->movers_ev) cudaEventDestroy(c->movers_ev);
   if (c->h_movers) cudaFreeHost(c->h_movers);
   c->res_brick.release();
@@ -1386,6 +1404,105 @@ int pppm_compute(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dty
   return PPPM_OK;
 }
 
+static void swap_bins(pppm_ctx* c, pppm_ctx::BinSet& b) {
+  std::swap(c->counts, b.counts);
+  std::swap(c->rec, b.rec);
+  std::swap(c->rcell, b.rcell);
+  std::swap(c->perm, b.perm);
+  std::swap(c->ovf_rec, b.ovf_rec);
+  std::swap(c->ovf_cell, b.ovf_cell);
+  std::swap(c->ovf_perm, b.ovf_perm);
+}
+
+// the context's own slots (group 0) or group g's swapped in for the duration of `body`
+static int with_group(pppm_ctx* c, int g, const std::function<int()>& body) {
+  if (g > 0) swap_bins(c, c->grp[g - 1]);
+  const int st = body();
+  if (g > 0) swap_bins(c, c->grp[g - 1]);
+  return st;
+}
+
+// pppm_compute_ex on host atoms in G groups of the caller's order (mixed precision).  Group g:
+// H2D on the copy stream -> binned into its own slots (records carry the caller's index) ->
+// make_rho of the group added to the mesh (cleared before the first, folded after the last) while
+// group g + 1 is on the link; after Poisson, fieldforce of group g writes the forces of its
+// caller-index range, which go back on the copy stream while group g + 1's fieldforce runs.
+static int compute_grouped(pppm_ctx* c, const void* pos, const void* q, int64_t n, int dtype, void* forces,
+                           bool f64_out, int G) {
+  const size_t es = dtype == PPPM_F64 ? 8 : 4, fs = f64_out ? 8 : 4;
+  TRY(c->pos_stage.ensure(3 * n * es));
+  TRY(c->q_stage.ensure(n * es));
+  TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
+  TRY(ensure_bins(c, n));  // the bucket capacity of the whole system, shared by the groups
+  if (!c->copy_stream) CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : c->chunk_ev)
+    if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : c->grp_ev)
+    if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (!c->d2h_ev) CU(cudaEventCreateWithFlags(&c->d2h_ev, cudaEventDisableTiming));
+  const int64_t per = (n + G - 1) / G;
+  // PPPM_B200_TRACE=1: device timeline of the call on stderr (events on the compute stream)
+  static const bool trace = getenv("PPPM_B200_TRACE") && atoi(getenv("PPPM_B200_TRACE")) != 0;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&]() {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    tev.push_back(e);
+  };
+  mark();
+  for (int g = 0; g < G; ++g) {
+    const int64_t off = g * per, m = std::min(per, n - off);
+    char* dp = (char*)c->pos_stage.p + 3 * off * es;
+    char* dq = (char*)c->q_stage.p + off * es;
+    CU(cudaMemcpyAsync(dp, (const char*)pos + 3 * off * es, 3 * m * es, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaMemcpyAsync(dq, (const char*)q + off * es, m * es, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaEventRecord(c->chunk_ev[g], c->copy_stream));
+    CU(cudaStreamWaitEvent(c->stream, c->chunk_ev[g], 0));
+    TRY(with_group(c, g, [&]() -> int {
+      TRY(ensure_bins(c, m));
+      TRY(launch_bin(c->order, c->n_points > 0, atoms_in(dp, dq, m, dtype), c->g, c->bk, c->cap, c->n_points,
+                     c->counts.as<int>(), c->rec.as<float4>(), c->rcell.as<int>(), c->perm.as<int>(),
+                     c->ovf_rec.as<float4>(), c->ovf_cell.as<int>(), c->ovf_perm.as<int>(), c->err.as<int>(), nullptr,
+                     c->stream, off, true));
+      c->launches += 1;
+      c->binned = true;
+      return run_spread(c, c->pos_stage.p, c->q_stage.p, n, dtype, false, g == 0, g == G - 1);
+    }));
+    mark();
+  }
+  TRY(run_poisson(c));
+  mark();
+  for (int g = 0; g < G; ++g) {
+    const int64_t off = g * per, m = std::min(per, n - off);
+    TRY(with_group(c, g, [&]() -> int {
+      return run_gather(c, c->pos_stage.p, c->q_stage.p, n, dtype, c->out_stage.p, f64_out);
+    }));
+    CU(cudaEventRecord(c->grp_ev[g], c->stream));
+    mark();
+    CU(cudaStreamWaitEvent(c->copy_stream, c->grp_ev[g], 0));
+    CU(cudaMemcpyAsync((char*)forces + 3 * off * fs, (const char*)c->out_stage.p + 3 * off * fs, 3 * m * fs,
+                       cudaMemcpyDeviceToHost, c->copy_stream));
+  }
+  CU(cudaEventRecord(c->d2h_ev, c->copy_stream));
+  CU(cudaStreamWaitEvent(c->stream, c->d2h_ev, 0));
+  mark();
+  c->binned = false;  // the context's own slots hold group 0 only
+  if (trace) {
+    CU(cudaStreamSynchronize(c->stream));
+    fprintf(stderr, "pppm trace (us since the call's first event; %d x bin+make_rho, poisson, %d x fieldforce, d2h):", G, G);
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      fprintf(stderr, " %.0f", ms * 1e3);
+    }
+    fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
+  return PPPM_OK;
+}
+
 // pppm_compute with the output type chosen by the caller, and for host fp32
 // inputs on the mixed path the H2D copy overlapped with binning: the atoms
 // travel in chunks on a copy stream and each chunk is binned as soon as it
@@ -1401,6 +1518,9 @@ int pppm_compute_ex(pppm_ctx* c, const void* pos, const void* q, int64_t n, int 
   const bool f64_out = forces_dtype == PPPM_F64;
   if (c->fp64() && !f64_out) return fail(PPPM_ERR_VALUE, "fp64 contexts return fp64 forces");
   const size_t es = dtype == PPPM_F64 ? 8 : 4;
+  // atom groups: at least 2^17 atoms each (smaller groups leave the brick kernels mostly overhead)
+  const int G = (int)std::min<int64_t>(std::min(c->groups, (int)pppm_ctx::kChunks), n >> 17);
+  const bool in_groups = !(c->fp64() || mem == PPPM_DEVICE || c->slab) && G >= 2;
   if (c->fp64() || mem == PPPM_DEVICE || c->slab) {
     const void *dpos, *dq;
     TRY(stage_atoms(c, pos, q, n, dtype, mem, &dpos, &dq));
@@ -1408,6 +1528,8 @@ int pppm_compute_ex(pppm_ctx* c, const void* pos, const void* q, int64_t n, int 
     TRY(run_poisson(c));
     TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
     TRY(do_fieldforce(c, dpos, dq, n, dtype, false, c->out_stage.p, f64_out));
+  } else if (in_groups) {
+    TRY(compute_grouped(c, pos, q, n, dtype, forces, f64_out, G));
   } else {
     TRY(c->pos_stage.ensure(3 * n * es));
     TRY(c->q_stage.ensure(n * es));
@@ -1438,7 +1560,8 @@ int pppm_compute_ex(pppm_ctx* c, const void* pos, const void* q, int64_t n, int 
     TRY(c->out_stage.ensure(sizeof(double) * 3 * n));
     TRY(run_gather(c, c->pos_stage.p, c->q_stage.p, n, dtype, c->out_stage.p, f64_out));
   }
-  CU(cudaMemcpyAsync(forces, c->out_stage.p, (f64_out ? 8 : 4) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (!in_groups)
+    CU(cudaMemcpyAsync(forces, c->out_stage.p, (f64_out ? 8 : 4) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaMemcpyAsync(c->h_scal, c->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   TRY(check_err_flag(c));
   if (energy) *energy = c->h_scal[0];
@@ -1500,6 +1623,7 @@ int pppm_ctx_load_atoms(pppm_ctx* c, const void* pos, const void* q, int64_t n, 
   CU(cudaMemcpyAsync(c->res_pos.p, pos, 3 * n * es, cudaMemcpyDefault, c->stream));
   CU(cudaMemcpyAsync(c->res_q.p, q, n * es, cudaMemcpyDefault, c->stream));
   c->n_res = n;
+  c->movers_pending = false;  // (a count of the previous residents)
   c->res_dtype = dtype;
   c->res_sorted = false;
   c->res_maxcnt = 0;
@@ -1806,7 +1930,8 @@ static int update_positions(pppm_ctx* c, const void* pos, int dtype, int mem, bo
   if (!sync && c->movers_pending && cudaEventQuery(c->movers_ev) == cudaSuccess) {
     c->movers_pending = false;
     c->last_movers = *c->h_movers;
-    if (c->last_movers > c->resort_frac * (double)c->n_res) TRY(resort_residents(c));
+    // (a count taken before the last re-sort says nothing about the current order)
+    if (c->movers_gen == c->resorts && c->last_movers > c->resort_frac * (double)c->n_res) TRY(resort_residents(c));
   }
   const void* dp = pos;
   if (mem == PPPM_HOST) {
@@ -1819,9 +1944,15 @@ static int update_positions(pppm_ctx* c, const void* pos, int dtype, int mem, bo
   TRY(launch_update_resident(c->order, dtype == PPPM_F32, dp, c->res_orig.as<int>(), c->n_res, c->g, c->bk,
                              c->res_brick.as<int>(), c->res_pos.as<float>(), c->err.as<int>(),
                              c->res_movers.as<int>(), c->stream));
-  CU(cudaMemcpyAsync(c->h_movers, c->res_movers.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaEventRecord(c->movers_ev, c->stream));
   c->launches += 1;
+  // async: a count still in flight is kept (a host that runs ahead of the device would otherwise
+  // re-record the event at every update and never see one complete); movers only grow between
+  // re-sorts, so an older count over the threshold still calls for one
+  if (sync || !c->movers_pending) {
+    CU(cudaMemcpyAsync(c->h_movers, c->res_movers.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaEventRecord(c->movers_ev, c->stream));
+    c->movers_gen = c->resorts;
+  }
   if (!sync) {
     c->movers_pending = true;
     return PPPM_OK;

@@ -165,7 +165,8 @@ int launch_spread_brick(int variant, int order, bool tab, const float4* rec, con
                         int cap, float4* ovf_rec, int* ovf_cell, int* ovf_perm, const Geom& g, const Bricks& bk,
                         const Pad& pd, const CUtensorMap& rho_map, const float* ta, float* rho_pad,
                         const Resident& res, int n_points, float4* rec_out, cudaStream_t s,
-                        int* ranked = nullptr, const CUtensorMap* rho_map2 = nullptr);
+                        int* ranked = nullptr, const CUtensorMap* rho_map2 = nullptr, bool clear = true,
+                        bool fold = true);  // clear / fold: first / last launch of a make_rho done in atom groups
 int launch_gather_direct(int order, bool tab, int mode, const AtomsIn& a, const Geom& g, const double* ta,
                          const double* td, int n_points, const double* fields, int64_t mesh, double cscale,
                          double* force, int* err, cudaStream_t s, const Bricks* bk = nullptr,
