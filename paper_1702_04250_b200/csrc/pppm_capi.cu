@@ -217,6 +217,7 @@ struct pppm_ctx {
   cudaEvent_t grp_ev[kChunks] = {};
   cudaEvent_t d2h_ev = nullptr;
   int groups = 4;
+  double group_last = 1.0;  // PPPM_B200_GROUP_LAST: size of the last group relative to the others (A/B)
 
   bool fp64() const { return prec == PPPM_PREC_FP64; }
   size_t real_size() const { return fp64() ? sizeof(double) : sizeof(float); }
@@ -1042,6 +1043,7 @@ static int ctx_create(pppm_ctx** out, int device, int nx, int ny, int nz, double
   if (const char* v = getenv("PPPM_B200_RES_DIRECT")) c->res_direct = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_DYN")) c->dyn_sched = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_RANKS")) c->rank_handoff = atoi(v) != 0;
+  if (const char* v = getenv("PPPM_B200_GROUP_LAST")) c->group_last = std::max(0.02, std::min(atof(v), 1.0));
   if (const char* v = getenv("PPPM_B200_GROUPS")) c->groups = std::max(1, std::min(atoi(v), (int)pppm_ctx::kChunks));
   if (const char* v = getenv("PPPM_B200_FIX64_TILES")) c->fix64_tiles = atoi(v) != 0;
   if (const char* v = getenv("PPPM_B200_GATHER_PAIRS")) c->gather_pairs = atoi(v) != 0;
@@ -1440,7 +1442,12 @@ static int compute_grouped(pppm_ctx* c, const void* pos, const void* q, int64_t 
   for (auto& e : c->grp_ev)
     if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (!c->d2h_ev) CU(cudaEventCreateWithFlags(&c->d2h_ev, cudaEventDisableTiming));
-  const int64_t per = (n + G - 1) / G;
+  // group sizes: G - 1 equal groups and a last one of group_last times their size.  (The last group's
+  // make_rho is the one the link does not hide, but a smaller last group measured slower - 1.38 /
+  // 1.36 / 1.34 / 1.32e9 at 1 / 0.5 / 0.25 / 0.1: a brick kernel's time hardly falls with the group,
+  // and the larger groups before it lengthen the fieldforce / D2H chain.)
+  int64_t per = (int64_t)std::ceil((double)n / ((double)(G - 1) + c->group_last));
+  per = std::min<int64_t>((per + 127) / 128 * 128, (n - 1) / (G - 1));
   // PPPM_B200_TRACE=1: device timeline of the call on stderr (events on the compute stream)
   static const bool trace = getenv("PPPM_B200_TRACE") && atoi(getenv("PPPM_B200_TRACE")) != 0;
   std::vector<cudaEvent_t> tev;
@@ -1453,7 +1460,7 @@ static int compute_grouped(pppm_ctx* c, const void* pos, const void* q, int64_t 
   };
   mark();
   for (int g = 0; g < G; ++g) {
-    const int64_t off = g * per, m = std::min(per, n - off);
+    const int64_t off = g * per, m = g == G - 1 ? n - off : per;
     char* dp = (char*)c->pos_stage.p + 3 * off * es;
     char* dq = (char*)c->q_stage.p + off * es;
     CU(cudaMemcpyAsync(dp, (const char*)pos + 3 * off * es, 3 * m * es, cudaMemcpyHostToDevice, c->copy_stream));
@@ -1475,7 +1482,7 @@ static int compute_grouped(pppm_ctx* c, const void* pos, const void* q, int64_t 
   TRY(run_poisson(c));
   mark();
   for (int g = 0; g < G; ++g) {
-    const int64_t off = g * per, m = std::min(per, n - off);
+    const int64_t off = g * per, m = g == G - 1 ? n - off : per;
     TRY(with_group(c, g, [&]() -> int {
       return run_gather(c, c->pos_stage.p, c->q_stage.p, n, dtype, c->out_stage.p, f64_out);
     }));

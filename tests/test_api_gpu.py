@@ -172,14 +172,18 @@ def test_mixed_grid_limit(pb):
         pb.PppmContext((2048, 8, 8), (2048.0, 8.0, 8.0), order=5, mode="ik", precision="mixed", alpha=0.3)
 
 
+@pytest.mark.parametrize("groups", ["1", "4"])
 @pytest.mark.parametrize("mode", ["ik", "ad"])
-def test_compute_chunked_h2d_and_fp32_forces(pb, mode):
-    """pppm_compute_ex: host atoms binned chunk by chunk as they land (several
-    chunks of 2^17), forces returned as fp64 or fp32; same result as the
-    resident step and the oracle."""
+def test_compute_chunked_h2d_and_fp32_forces(pb, mode, groups, monkeypatch):
+    """pppm_compute_ex: host atoms in groups of the caller's order (each binned
+    into its own brick slots and spread as it lands, forces copied back group
+    by group; 400,003 atoms -> 3 groups with a ragged last one) or, with
+    PPPM_B200_GROUPS=1, binned chunk by chunk into one set of slots; forces
+    returned as fp64 or fp32; same result as the resident step and the oracle."""
     from paper_1702_04250_b200 import scenarios
 
-    pos, q, lengths = scenarios.random_gas(400000, 41, 160.0)
+    monkeypatch.setenv("PPPM_B200_GROUPS", groups)
+    pos, q, lengths = scenarios.random_gas(400003, 41, 160.0)
     p32 = scenarios.round_to_f32(pos, lengths)
     q32 = q.astype(np.float32)
     ctx = pb.PppmContext((64, 64, 64), lengths, order=5, mode=mode, precision="mixed", alpha=0.25)
