@@ -177,13 +177,13 @@ def test_mixed_grid_limit(pb):
 def test_compute_chunked_h2d_and_fp32_forces(pb, mode, groups, monkeypatch):
     """pppm_compute_ex: host atoms in groups of the caller's order (each binned
     into its own brick slots and spread as it lands, forces copied back group
-    by group; 400,003 atoms -> 3 groups with a ragged last one) or, with
+    by group; 400,006 atoms -> 3 groups with a ragged last one) or, with
     PPPM_B200_GROUPS=1, binned chunk by chunk into one set of slots; forces
     returned as fp64 or fp32; same result as the resident step and the oracle."""
     from paper_1702_04250_b200 import scenarios
 
     monkeypatch.setenv("PPPM_B200_GROUPS", groups)
-    pos, q, lengths = scenarios.random_gas(400003, 41, 160.0)
+    pos, q, lengths = scenarios.random_gas(400006, 41, 160.0)
     p32 = scenarios.round_to_f32(pos, lengths)
     q32 = q.astype(np.float32)
     ctx = pb.PppmContext((64, 64, 64), lengths, order=5, mode=mode, precision="mixed", alpha=0.25)
