@@ -2370,8 +2370,10 @@ static int stage_f64(pppm_ctx* c, const void* pos, const void* q, int64_t n, int
 
 // pair forces into pr_force (n, 3), pair energy into pr_scal[0]; synchronises
 // to report unwrapped positions / overlapping atoms
+// pev (nullable): two events recorded around the device work of the pair phase (after the
+// buffers exist, before the host waits for the counters), the report's `pair` section
 static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double alpha, double rc,
-                       const double* lj, long long* counters) {
+                       const double* lj, long long* counters, cudaEvent_t* pev = nullptr) {
   const int cx = std::max(1, py_floordiv_int(c->g.lx, rc)), cy = std::max(1, py_floordiv_int(c->g.ly, rc)),
             cz = std::max(1, py_floordiv_int(c->g.lz, rc));
   const int64_t ncells = (int64_t)cx * cy * cz;
@@ -2390,6 +2392,7 @@ static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_
   TRY(c->pr_ij.ensure(8));
   TRY(c->pr_part.ensure(8 * 256));
   TRY(c->pr_scal.ensure(8 * 4));
+  if (pev) cudaEventRecord(pev[0], c->stream);
   CU(cudaMemsetAsync(c->pr_cnt.p, 0, 16, c->stream));
   CU(cudaMemsetAsync(c->pr_rmin.p, 0xff, 8, c->stream));
   const double scale = c->cscale;
@@ -2399,6 +2402,7 @@ static int pair_device(pppm_ctx* c, const double* dpos, const double* dq, int64_
                   c->pr_cnt.as<unsigned long long>(), c->pr_rmin.as<unsigned long long>(), c->err.as<int>(),
                   c->stream));
   TRY(launch_sum(c->pr_e.as<double>(), n, c->pr_part.as<double>(), 1.0, c->pr_scal.as<double>(), c->stream));
+  if (pev) cudaEventRecord(pev[1], c->stream);
   c->launches += 8;
   unsigned long long h[3];
   CU(cudaMemcpyAsync(h, c->pr_cnt.p, 16, cudaMemcpyDeviceToHost, c->stream));
@@ -2454,7 +2458,7 @@ int pppm_ctx_pair_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n,
 
 // full force evaluation on device atoms: pair forces + mesh forces -> out (n, 3)
 // fp64, energies -> pr_scal[0] (pair), scal[0] (kspace), pr_scal[1] (self).
-// ev (nullable): 5 events bracketing pair | make_rho | Poisson | fieldforce
+// ev (nullable): 7 events, [0..4] bracketing pair | make_rho | Poisson | fieldforce, [5..6] the pair kernels
 // md_step >= 0 on a mixed-precision context: the mesh part of an MD step on
 // the resident path - the atoms are loaded (and brick-sorted) at step 0 and
 // afterwards only moved (update_positions_async: scatter into brick order,
@@ -2463,7 +2467,7 @@ int pppm_ctx_pair_forces(pppm_ctx* c, const void* pos, const void* q, int64_t n,
 static int forces_device(pppm_ctx* c, const double* dpos, const double* dq, int64_t n, double rc, const double* lj,
                          double* out, long long* counters, cudaEvent_t* ev = nullptr, int md_step = -1) {
   if (ev) cudaEventRecord(ev[0], c->stream);
-  TRY(pair_device(c, dpos, dq, n, c->alpha, rc, lj, counters));
+  TRY(pair_device(c, dpos, dq, n, c->alpha, rc, lj, counters, ev ? ev + 5 : nullptr));
   if (ev) cudaEventRecord(ev[1], c->stream);
   if (!c->fp64() && md_step >= 0 && c->sort_resident && !c->slab) {
     if (md_step == 0 || c->n_res != n) TRY(pppm_ctx_load_atoms(c, dpos, dq, n, PPPM_F64));
@@ -2499,7 +2503,7 @@ int pppm_ctx_compute_forces(pppm_ctx* c, const void* pos, const void* q, int64_t
   TRY(activate(c));
   if (n < 1) return fail(PPPM_ERR_VALUE, "system must contain at least one atom");
   TRY(check_pair_args(c, c->alpha, cutoff));
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t ev[7] = {};  // [5], [6]: the pair phase's device work
   if (sections)
     for (auto& e : ev) CU(cudaEventCreate(&e));
   auto destroy = [&]() {
@@ -2527,6 +2531,7 @@ int pppm_ctx_compute_forces(pppm_ctx* c, const void* pos, const void* q, int64_t
     for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
     sections[0] = 1e-3 * ((double)t[1] + (double)t[3]);
     sections[1] = 1e-3 * (double)t[2];
+    cudaEventElapsedTime(&t[0], ev[5], ev[6]);  // pair: the kernels, not the host's wait for the counters
     sections[2] = 1e-3 * (double)t[0];
   }
   destroy();
@@ -2568,7 +2573,7 @@ int pppm_ctx_integrate_nve(pppm_ctx* c, const double* pos, const double* vel, co
   // per-evaluation section times (CUDA events; driver.REPORT_SECTIONS) and
   // pair counters, accumulated over the steps + 1 force evaluations as the
   // reference's compute_forces calls accumulate them (driver.py:310-376)
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t ev[7] = {};  // [5], [6]: the pair phase's device work
   if (sections) {
     for (auto& e : ev) CU(cudaEventCreate(&e));
     sections[0] = sections[1] = sections[2] = 0.0;
@@ -2595,7 +2600,8 @@ int pppm_ctx_integrate_nve(pppm_ctx* c, const double* pos, const double* vel, co
       for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
       sections[0] += 1e-3 * ((double)t[1] + (double)t[3]);  // pppm_non_fft: make_rho + fieldforce
       sections[1] += 1e-3 * (double)t[2];                   // pppm_fft: Poisson
-      sections[2] += 1e-3 * (double)t[0];                   // pair
+      cudaEventElapsedTime(&t[0], ev[5], ev[6]);
+      sections[2] += 1e-3 * (double)t[0];                   // pair (device work)
     }
     return PPPM_OK;
   };

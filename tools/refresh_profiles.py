@@ -38,6 +38,11 @@ cp(f"refsuite_{TAG}_fp64.json", f"{TAG}_reference_suite_fp64.json")
 cp(f"refsuite_{TAG}_mixed.json", f"{TAG}_reference_suite_mixed.json")
 cp("sweep.jsonl", f"{TAG}_sweep.jsonl")
 cp("md.jsonl", f"{TAG}_md.jsonl")
+# tools/md_resort_sweep.py (--sync, then enqueue-only): steady-state MD step against the re-sort threshold
+parts = [open(os.path.join(G, f)).read() for f in ("md_resort_sync.jsonl", "md_resort_async.jsonl")
+         if os.path.exists(os.path.join(G, f))]
+if parts:
+    open(os.path.join(P, f"{TAG}_md_resort.jsonl"), "w").write("".join(parts))
 subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"), os.path.join(P, f"{TAG}_launches.csv"),
                 "--traffic", "config3_ik"], capture_output=True, cwd=ROOT)
 
