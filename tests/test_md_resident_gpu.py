@@ -60,6 +60,46 @@ def test_moving_residents_with_automatic_resort(pb, mode, sync):
         ref.close()
 
 
+def test_enqueue_only_loop_still_resorts(pb):
+    """A host that only enqueues (device positions, no synchronisation between
+    steps) runs ahead of the device: the mover count of an update is consumed
+    when its event has completed - a count in flight is kept, not re-recorded -
+    so the automatic re-sort still happens, and the forces stay right."""
+    import torch
+
+    from paper_1702_04250_b200 import _native as nat
+    from paper_1702_04250_b200 import scenarios
+
+    rng = np.random.default_rng(5)
+    n, edge, steps = 200000, 96.0, 60
+    pos, q, lengths = scenarios.random_gas(n, 13, edge)
+    q32 = q.astype(np.float32)
+    traj = np.empty((steps, n, 3), dtype=np.float32)
+    cur = pos.copy()
+    for i in range(steps):
+        cur = scenarios.wrap(cur + rng.normal(0.0, 0.25, cur.shape), lengths)
+        traj[i] = scenarios.round_to_f32(cur, lengths)
+    dev = torch.from_numpy(traj).to("cuda:0")
+    ctx = pb.PppmContext((64, 64, 64), lengths, order=5, mode="ik", precision="mixed", alpha=0.3)
+    ref = pb.PppmContext((64, 64, 64), lengths, order=5, mode="ik", precision="mixed", alpha=0.3)
+    try:
+        ctx.set_resort(0.02)
+        ctx.load_atoms(scenarios.round_to_f32(pos, lengths), q32)
+        for i in range(steps):
+            ctx.update_positions_async(dev[i].data_ptr(), mem=nat.DEVICE)
+            ctx.step()
+        ctx.synchronize()
+        info = ctx.resident_info()
+        assert info["resorts"] >= 1
+        f, e = ctx.forces(), ctx.energy()
+        fr, er = ref.compute(traj[-1], q32)
+        assert rel_rms(f, fr) <= 3e-6
+        assert abs(e - er) <= 3e-6 * abs(er)
+    finally:
+        ctx.close()
+        ref.close()
+
+
 def test_mixed_nve_resident_matches_fp64(pb):
     """integrate_nve in mixed precision (resident mesh path) follows the fp64
     (reference arithmetic) trajectory to fp32 accuracy."""
