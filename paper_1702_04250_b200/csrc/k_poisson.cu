@@ -40,7 +40,9 @@ template <int NZ, int T>
 struct ZfftCfg {
   static constexpr int Z1 = Radix<NZ>::R1, Z2 = Radix<NZ>::R2;
   static constexpr int NT = T * Z1;  // one forward pass-B task per thread
-  static constexpr int MINB = NT >= 256 ? PPPM_ZFFT_MINB : 4;
+  // four CTAs per SM up to NZ = 128 (64 registers, no spills): config 3's 520 CTAs are one wave of
+  // 592 slots instead of 1.17 waves of 444 (Poisson 49.4 -> 45.3 us); NZ = 256 would spill
+  static constexpr int MINB = NT >= 256 ? (NZ <= 128 ? 4 : PPPM_ZFFT_MINB) : 4;
 };
 
 template <int NZ, int T, int MODE>
