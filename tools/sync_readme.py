@@ -23,7 +23,8 @@ text = (f"  kernels behind the C ABI in `include/pppm_b200.h`. Config 3 (1M atom
         f"{ad3['value'] / 1e9:.2f}e9; config 5\n"
         f"  (8.4M atoms, 256³): {ik5['value'] / 1e9:.2f}e9; fp64 (the reference's arithmetic, config 3): "
         f"{d['value_fp64'] / 1e9:.2f}e9; MD step with\n"
-        f"  moving atoms: {d['value_md'] / 1e9:.2f}e9 (`profiles/README.md`, `profiles/r02_sweep.md`).\n")
+        f"  moving atoms: {d['value_md'] / 1e9:.2f}e9; end to end from pinned host arrays through the C ABI: "
+        f"{d['e2e']['value'] / 1e9:.2f}e9\n  (`profiles/README.md`, `profiles/r02_sweep.md`).\n")
 p = os.path.join(ROOT, "README.md")
 s = open(p).read()
 a = s.index("  kernels behind the C ABI in `include/pppm_b200.h`. Config 3")
