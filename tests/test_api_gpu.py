@@ -209,3 +209,26 @@ def test_compute_chunked_h2d_and_fp32_forces(pb, mode, groups, monkeypatch):
         phi = orc.poisson_ad(rho_ref, g)
         f_ref = orc.fieldforce_ad(phi, p32[sub].astype(np.float64), q[sub], lengths, (64, 64, 64), 5)
     assert rel_rms(f64[sub], f_ref) <= 1e-5
+
+
+def test_compute_groups_at_config5_size(pb):
+    """pppm_compute_ex in four atom groups at BASELINE config 5's size (8,388,608
+    atoms, 256^3): same forces and energy as the resident step on the same atoms
+    (whose parity against the oracle tests/test_configs_gpu.py checks)."""
+    from paper_1702_04250_b200 import scenarios
+
+    cfg = scenarios.CONFIGS[5]
+    pos, q, lengths = cfg.build()
+    p32 = scenarios.round_to_f32(pos, lengths)
+    q32 = q.astype(np.float32)
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=cfg.mode, precision="mixed", alpha=cfg.alpha)
+    try:
+        f, e = ctx.compute(p32, q32, out=np.empty((q.size, 3), dtype=np.float32))
+        ctx.load_atoms(p32, q32)
+        ctx.step()
+        ctx.synchronize()
+        fr, er = ctx.forces(), ctx.energy()
+    finally:
+        ctx.close()
+    assert rel_rms(f, fr) <= 2e-6
+    assert abs(e - er) <= 2e-6 * abs(er)
