@@ -546,6 +546,13 @@ def extra_records(args, cfg, device, pos, q, lengths):
                          "automatic re-sort at 5 % movers; value = whole MD PPPM step (update, make_rho, "
                          "Poisson, fieldforce)",
                  "resorts": info["resorts"], "movers_last_update": info["movers"], "steps": k}
+    # --- md, sustained: a device random walk long enough for several re-sorts (inside the timed
+    # steps), the host waiting for every step's forces; the walk's own time is measured alone and
+    # taken off (tools/md_resort_sweep.py sweeps the re-sort threshold the same way)
+    try:
+        out["md_sustained"] = md_sustained(pb, nat, torch, cfg, mode, lengths, pos, q32, device, sp_steps=150)
+    except Exception as exc:  # report, do not hide
+        out["md_sustained"] = {"error": str(exc)[:300]}
     # --- binned one-shot path
     ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
                          device=device)
@@ -570,6 +577,57 @@ def extra_records(args, cfg, device, pos, q, lengths):
                    "whole_step_atom_steps_per_s": n * kk4 / (t_mf + ms["poisson"] / 1e3),
                    "phases_ms_per_step": {kx: v / kk4 for kx, v in ms.items()}}
     return out
+
+
+def md_sustained(pb, nat, torch, cfg, mode, lengths, pos, q32, device, sp_steps=150, sigma=0.1):
+    n = pos.shape[0]
+    dev = f"cuda:{device}"
+    L = torch.tensor(np.asarray(lengths, dtype=np.float64), device=dev)
+    L32 = L.to(torch.float32)
+    ctx = pb.PppmContext(cfg.dims, lengths, order=cfg.order, mode=mode, precision="mixed", alpha=cfg.alpha,
+                         device=device)
+    ctx.load_atoms(pos.astype(np.float32), q32)
+    sp = ctypes.c_void_p()
+    ctx.ctx("pppm_ctx_stream", ctypes.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value, device=device)
+    res = {}
+    for what in ("walk", "md"):
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(7)
+        cur = torch.from_numpy(pos.astype(np.float64)).to(dev)
+        p32 = torch.empty((n, 3), dtype=torch.float32, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        warm = 5
+        r0 = 0
+        with torch.cuda.stream(stream):
+            for i in range(sp_steps + warm):
+                if i == warm:
+                    ctx.synchronize()
+                    r0 = ctx.resident_info()["resorts"]
+                    e0.record(stream)
+                cur += torch.randn(cur.shape, generator=gen, device=dev, dtype=torch.float64) * (sigma / 3 ** 0.5)
+                cur -= torch.floor(cur / L) * L
+                p32.copy_(cur)
+                p32.masked_fill_(p32 >= L32, 0.0)
+                p32.masked_fill_(p32 < 0, 0.0)
+                if what == "md":
+                    ctx.update_positions_async(p32.data_ptr(), mem=nat.DEVICE)
+                    ctx.step(nat.PHASE_ALL)
+                    ctx.synchronize()
+            e1.record(stream)
+        ctx.synchronize()
+        res[what] = e0.elapsed_time(e1) / sp_steps
+        if what == "md":
+            info = ctx.resident_info()
+            res["resorts"] = info["resorts"] - r0
+            res["movers_last"] = info["movers"]
+    ctx.close()
+    ms = res["md"] - res["walk"]
+    return {"value": n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": sp_steps, "resorts": res["resorts"],
+            "movers_last_update": res["movers_last"], "ms_random_walk_taken_off": res["walk"],
+            "what": f"{sp_steps} MD steps (update_positions_async from device positions of a {sigma} A rms per step "
+                    "random walk + full step, host synchronised every step), automatic re-sorts at 5 % movers inside "
+                    "the timed region, no L2 flush; the walk's own device time measured alone and taken off"}
 
 
 def probe_launch(args, rank, world, pg):
@@ -773,6 +831,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_extra:
         extra = extra_records(args, cfg, local, pos, q, lengths)
         line["value_md"] = extra["md"]["value"]
+        if "value" in extra.get("md_sustained", {}):
+            line["value_md_sustained"] = extra["md_sustained"]["value"]
         line["value_binned"] = extra["binned"]["value"]
         line["value_fp64"] = extra["fp64"]["value"]
         line["extra"] = extra
