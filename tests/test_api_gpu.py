@@ -139,10 +139,11 @@ def test_nve_report_sections_and_counters(pb):
     assert counters["pairs_within_cutoff"] > 0
 
 
-def test_one_shot_call_regrowing_bins_keeps_resident_step(pb):
-    """A one-shot compute with more atoms regrows the binning buffers; the
-    resident step's captured graphs must be re-captured, not replayed on
-    freed memory."""
+@pytest.mark.parametrize("big_n", [60000, 300000])
+def test_one_shot_call_regrowing_bins_keeps_resident_step(pb, big_n):
+    """A one-shot compute with more atoms regrows the binning buffers (300,000
+    atoms: in two atom groups with their own slots); the resident step's
+    captured graphs must be re-captured, not replayed on freed memory."""
     from paper_1702_04250_b200 import scenarios
 
     pos, q, lengths = scenarios.random_gas(4000, 31, 24.0)
@@ -154,7 +155,7 @@ def test_one_shot_call_regrowing_bins_keeps_resident_step(pb):
             ctx.step()
         ctx.synchronize()
         f0 = ctx.forces()
-        big, qb, _ = scenarios.random_gas(60000, 32, 24.0)
+        big, qb, _ = scenarios.random_gas(big_n, 32, 24.0)
         ctx.compute(scenarios.round_to_f32(big, lengths), qb.astype(np.float32))
         for _ in range(2):
             ctx.step()
